@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark: shared-prefix decode attention tokens/s and HBM GB/s vs roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+A "step" is one engine decode step through the public API (GpuEngine.step:
+plan -> per-layer prefix/private/merge attention kernels for all L layers ->
+one-token growth -> K/V append) for the B forks of one prefix-affinity group.
+Per GPU the workload is fixed (one group per rank, weak scaling); under
+torchrun every rank runs its own engine on its own GPU with no collective
+on the data path.  Rank 0 prints one JSON line.
+
+  value : tokens/s with inputs (Q, new K/V rows) resident in HBM, device
+          timed with CUDA events on the engine stream, max over ranks.
+  e2e   : the same through the engine API with host (pinned) inputs: Q and
+          K/V rows copied H2D and the attention output copied D2H each step.
+  roofline : the per-layer attention (fk_attn_decode) against measured HBM
+          peak with algorithmic bytes = (batch_tokens * H * D * 2 * 2) + Q + out.
+  cpu_baseline : the numpy oracle on the host cores, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[2] (headline): LLaMA-13B shape, 6k prefix x 64 forks, S=256
+    "llama13b_p6000_b64": dict(model="LLaMA-13B", L=40, H=40, P=6000, B=64, S=256),
+    "llama13b_p6000_b128": dict(model="LLaMA-13B", L=40, H=40, P=6000, B=128, S=256),
+    "llama13b_p6000_b256": dict(model="LLaMA-13B", L=40, H=40, P=6000, B=256, S=256),
+    # BASELINE.json configs[1]: LLaMA-7B shape
+    "llama7b_p6000_b64": dict(model="LLaMA-7B", L=32, H=32, P=6000, B=64, S=256),
+    # BASELINE.json configs[3]: map-reduce, 2 groups of 32 forks over 2k prefixes per GPU
+    "mapreduce_13b": dict(model="LLaMA-13B", L=40, H=40, P=2000, B=32, S=None, groups=2),
+    # BASELINE.json configs[4]: nested 4k -> 1k -> 64 users x 256 per GPU
+    "nested_13b": dict(model="LLaMA-13B", L=40, H=40, P=4096, B=64, S=256, app=1024),
+}
+DEFAULT_CONFIG = "llama13b_p6000_b64"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=4096):
+    import paper_2405_19888_b200 as P
+    from paper_2405_19888_b200.workloads import drain_fills, fork_group, nested_forest
+
+    L, H = cfg["L"], cfg["H"]
+    geo = P.ModelGeometry(L, H, 128)
+    eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 30, device=device, geometry=geo,
+                      model=P.SyntheticDecodeModel(seed))
+    if "app" in cfg:
+        nested_forest(eng, cfg["P"], cfg["app"], 1, cfg["S"], cfg["B"], out_len=out_len, seed=seed)
+    elif cfg.get("groups"):
+        import random
+        rng = random.Random(0)
+        for gi in range(cfg["groups"]):
+            fork_group(eng, cfg["P"], [rng.randint(128, 1024) for _ in range(cfg["B"])], out_len=out_len,
+                       tag=f"g{gi}", seed=seed + gi)
+    else:
+        fork_group(eng, cfg["P"], [cfg["S"]] * cfg["B"], out_len=out_len, seed=seed)
+    drain_fills(eng)
+    rows = len(eng.gens)
+    shape = (L, rows, H, 128)
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    q = torch.randn(shape, generator=gen).to(torch.bfloat16)
+    k = torch.randn(shape, generator=gen).to(torch.bfloat16)
+    v = torch.randn(shape, generator=gen).to(torch.bfloat16)
+    if host_inputs:
+        q, k, v = q.pin_memory(), k.pin_memory(), v.pin_memory()
+        eng.model = P.TensorDecodeModel(q, k, v, copy_out=True)
+        eng.model.seed = seed
+    else:
+        dev = torch.device("cuda", device)
+        eng.model = P.TensorDecodeModel(q.to(dev), k.to(dev), v.to(dev))
+        eng.model.seed = seed
+    torch.cuda.synchronize(device)
+    return eng, rows
+
+
+def alg_bytes_per_layer(info, rows, H, D=128):
+    """(_batch_tokens) * H * D * 2 (K,V) * 2 B + Q + out."""
+    return info.batch_tokens * H * D * 2 * 2 + 2 * rows * H * D * 2
+
+
+def time_steps(eng, steps, torch):
+    st = eng.stream
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(st)
+    for _ in range(steps):
+        eng.step()
+    end.record(st)
+    end.synchronize()
+    return start.elapsed_time(end) / 1e3
+
+
+def time_layers(eng, steps, torch):
+    """Device time of the per-layer attention alone (same plan, same inputs)."""
+    from paper_2405_19888_b200 import _lib
+
+    L = eng.geometry.num_layers
+    rows = eng.last_plan.num_rows
+    H = eng.geometry.num_heads
+    q = eng.model.q
+    out = torch.empty_like(q)
+    le = rows * H * 128 * 2
+    st = eng.stream
+    sp = ctypes.c_void_p(st.cuda_stream)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(st)
+    for _ in range(steps):
+        for layer in range(L):
+            _lib.check(_lib.lib.fk_attn_decode(eng._pool.handle, layer, ctypes.c_void_p(q.data_ptr() + layer * le),
+                                               ctypes.c_void_p(out.data_ptr() + layer * le), None, sp))
+    end.record(st)
+    end.synchronize()
+    return start.elapsed_time(end) / 1e3 / (steps * L)
+
+
+def cpu_baseline(cfg, budget_s=12.0, impl_steps=None):
+    """numpy fp32 oracle (matmul form) on the host cores for one layer of the
+    workload; tokens/s extrapolated x L.  Returns (tokens/s, sample, cores, secs)."""
+    import numpy as np
+
+    from oracle import forkattn_oracle as O
+
+    H, P, B = cfg["H"], cfg["P"], cfg["B"]
+    S = cfg["S"] or 576
+    rng = np.random.default_rng(0)
+    q = O.bf16_round(rng.standard_normal((B, H, 128), dtype=np.float32))
+    pk = O.bf16_round(rng.standard_normal((P, H, 128), dtype=np.float32))
+    pv = O.bf16_round(rng.standard_normal((P, H, 128), dtype=np.float32))
+    sk = [O.bf16_round(rng.standard_normal((S, H, 128), dtype=np.float32)) for _ in range(B)]
+    sv = [O.bf16_round(rng.standard_normal((S, H, 128), dtype=np.float32)) for _ in range(B)]
+    O.attend_shared_batch(q, pk, pv, sk, sv)  # warm
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        O.attend_shared_batch(q, pk, pv, sk, sv)
+        times.append(time.perf_counter() - t0)
+        if impl_steps is not None:
+            if len(times) >= impl_steps:
+                break
+        elif time.perf_counter() - t_all > budget_s:
+            break
+    t_layer = statistics.median(times)
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"1 of {cfg['L']} layers ({H} heads, {B} rows, P={P}, S={S}) numpy fp32 matmul form, "
+              f"{len(times)} reps, median, extrapolated x{cfg['L']} layers")
+    return B / (cfg["L"] * t_layer), sample, cores, t_layer
+
+
+# ----------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tc-min-fanout", type=int, default=None)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    workload = dict(workload=args.config, model=cfg["model"], layers=cfg["L"], heads=cfg["H"], head_dim=128,
+                    prefix_tokens=cfg["P"], forks=cfg["B"] * cfg.get("groups", 1),
+                    suffix_tokens=cfg["S"] if cfg["S"] else "U[128,1024]",
+                    per_gpu="one prefix-affinity group set per GPU (weak scaling)",
+                    l2="inputs larger than L2 (KV per layer >> 126 MB; layers stream distinct pages)",
+                    parallelism=f"dp{args.gpus} (independent engines, no collective)")
+    metric = "shared-prefix decode attn tokens/s + HBM GB/s vs roofline, 1/2/4/8 B200"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        rows = cfg["B"] * cfg.get("groups", 1)
+        c = dict(cfg, B=rows)
+        tok_s, sample, cores, t_layer = cpu_baseline(c, impl_steps=max(1, args.steps) + max(0, args.warmup))
+        line = {"metric": metric, "value": tok_s, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_layer * cfg["L"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": workload,
+                "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+                "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = local
+    torch.cuda.set_device(device)
+    from paper_2405_19888_b200 import _lib
+
+    eng, rows = build_engine(cfg, device, torch, out_len=2 * (args.steps + args.warmup) + 64)
+    if args.tc_min_fanout is not None:
+        eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, args.tc_min_fanout)
+    L, H = cfg["L"], cfg["H"]
+    for _ in range(max(args.warmup, 3)):
+        eng.step()
+    torch.cuda.synchronize(device)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=torch.device("cuda", device))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = ClockSampler(device)
+    barrier()
+    clocks.start()
+    t_steps = time_steps(eng, args.steps, torch)
+    barrier()
+    # per-layer attention alone for the roofline (same plan as the last step)
+    t_layer = time_layers(eng, max(args.steps // 2, 3), torch)
+    barrier()
+    clk = clocks.stop()
+    t_steps = max_over_ranks(t_steps)
+    t_layer = max_over_ranks(t_layer)
+    info = eng.last_plan
+    bytes_layer = alg_bytes_per_layer(info, rows, H)
+    peak, peak_kind = load_peaks()
+    achieved = bytes_layer / t_layer / 1e9
+    value = world * rows * args.steps / t_steps
+    launches_per_step = L * (1 + int(info.num_mma_items > 0) + int(info.num_tc_items > 0)) + L
+    batch_tokens = info.batch_tokens
+
+    # ---- e2e: host (pinned) inputs through the engine API
+    e2e = None
+    if not args.no_e2e:
+        eng.close()
+        del eng
+        torch.cuda.empty_cache()
+        eng2, rows2 = build_engine(cfg, device, torch, host_inputs=True,
+                                   out_len=2 * (args.steps + args.warmup) + 64)
+        for _ in range(max(args.warmup, 3)):
+            eng2.step()
+        barrier()
+        t0 = time.perf_counter()
+        t_e2e = time_steps(eng2, args.steps, torch)
+        wall = time.perf_counter() - t0
+        barrier()
+        t_e2e = max_over_ranks(max(t_e2e, wall))
+        bi = 3 * L * rows2 * H * 128 * 2
+        bo = L * rows2 * H * 128 * 2
+        e2e = {"value": world * rows2 * args.steps / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo, "ms_per_step": 1e3 * t_e2e / args.steps}
+        eng2.close()
+    else:
+        eng.close()
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            tok_s, sample, cores, _ = cpu_baseline(dict(cfg, B=rows))
+            cpu = {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
+        line = {
+            "metric": metric,
+            "value": value,
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_steps / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic",
+            "config": workload,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "fk_attn_decode (prefix + private/merge kernels, one layer)",
+                         "alg_bytes_per_layer": bytes_layer, "layer_us": t_layer * 1e6,
+                         "batch_tokens": batch_tokens,
+                         "roofline_tokens_per_s": rows * peak * 1e9 / (L * bytes_layer)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+            "plan": {"rows": info.num_rows, "shared_ctx": info.num_shared_ctx, "prefix_ctas": info.num_prefix_ctas,
+                     "max_slots": info.max_slots, "tc_items": info.num_tc_items, "mma_items": info.num_mma_items},
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+// Device helpers shared by the sm_100a kernels: mbarrier / bulk-copy / TMA
+// PTX wrappers, warp MMA wrappers, the synthetic counter-hash generator and
+// the log-sum-exp merge of per-(row, head) partials.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+#include "fk_internal.h"
+
+namespace fk {
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D bulk copy global -> shared, completion on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 3-D TMA tile load (SASS: UTMALDG).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float bf_lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// ------------------------------------------------- synthetic data generator
+// Counter-hash generator restated by oracle/forkattn_oracle.py (synth_*):
+//   key = MIX(seed ^ tag<<56); key = MIX(key ^ uid); key = MIX(key ^ pos);
+//   key = MIX(key ^ layer); key = MIX(key ^ head); w_j = MIX(key ^ j)
+//   element 4j+i = bf16_rne(((w_j >> 16i) & 0xFFFF) - 32768) * 1.75/32768 [* k_scale])
+constexpr unsigned long long kTagK = 1, kTagV = 2, kTagQ = 3;
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ULL;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBULL;
+  x ^= x >> 31;
+  return x;
+}
+__device__ __forceinline__ unsigned long long synth_key(unsigned long long seed, unsigned long long tag,
+                                                        long long uid, long long pos, int layer, int head) {
+  unsigned long long k = mix64(seed ^ (tag << 56));
+  k = mix64(k ^ (unsigned long long)uid);
+  k = mix64(k ^ (unsigned long long)pos);
+  k = mix64(k ^ (unsigned long long)layer);
+  k = mix64(k ^ (unsigned long long)head);
+  return k;
+}
+// four bf16 values of chunk j packed as uint2
+__device__ __forceinline__ uint2 synth_chunk(unsigned long long key, int j, float scale) {
+  const unsigned long long w = mix64(key ^ (unsigned long long)j);
+  float v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int u = (int)((w >> (16 * i)) & 0xFFFFull);
+    v[i] = (float)(u - 32768) * 5.340576171875e-05f * scale;
+  }
+  return make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
+}
+
+// ------------------------------------------------------ partial bookkeeping
+__device__ __forceinline__ long long part_index(const PlanDev& p, int H, int row, int slot, int head) {
+  return ((long long)row * p.max_slots + slot) * H + head;
+}
+
+// Merge all partials of (row, head) into the bf16 (and optional fp32) output.
+// Called by the CTA that arrived last on counters[row*H + head]; 128 threads,
+// one head-dim element each.  Partials are read with ld.global.cg so another
+// SM's writes (ordered by the release fence + atomic) are observed.
+__device__ __forceinline__ void merge_row_head(const ArenaDev& a, const PlanDev& p, int row, int head,
+                                               __nv_bfloat16* out, float* out_f32, int d) {
+  const int H = a.num_heads;
+  const int ns = p.row_nslots[row] + 1;
+  float M = -INFINITY;
+  for (int k = 0; k < ns; ++k) M = fmaxf(M, __ldcg(&a.part_ml[part_index(p, H, row, k, head)].x));
+  float L = 0.f, acc = 0.f;
+  if (M != -INFINITY) {
+    for (int k = 0; k < ns; ++k) {
+      const long long pi = part_index(p, H, row, k, head);
+      const float2 ml = __ldcg(&a.part_ml[pi]);
+      const float w = ex2(ml.x - M);
+      L += ml.y * w;
+      acc += __ldcg(&a.part_o[pi * kHeadDim + d]) * w;
+    }
+  }
+  const float o = L > 0.f ? acc / L : 0.f;
+  const long long oi = ((long long)row * H + head) * kHeadDim + d;
+  out[oi] = __float2bfloat16_rn(o);
+  if (out_f32) out_f32[oi] = o;
+}
+
+}  // namespace fk

@@ -1,0 +1,84 @@
+// Internal structures shared by the host pool (fk_pool.cpp) and the sm_100a
+// kernels (fk_*.cu).  Not part of the C-ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+namespace fk {
+
+constexpr int kPage = 16;      // tokens per page (Config.block_size, config.py:21)
+constexpr int kHeadDim = 128;  // D; LLaMA-7B/13B
+constexpr int kMmaQBlock = 64; // queries per mma.sync prefix CTA (4 warps x 16 rows)
+constexpr int kTcQBlock = 128; // queries per tcgen05 prefix CTA (M = 128 rows)
+constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
+constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
+
+// Device view of one step plan.  All arrays live in one device buffer.
+struct PlanDev {
+  int num_rows;
+  int max_slots;
+  int num_items;        // prefix work items (context x split x query block)
+  int tc_begin;         // items [0, tc_begin) -> mma.sync kernel, [tc_begin, num_items) -> tcgen05
+  // prefix items (SoA)
+  const int* it_page_off;  // offset into pages[]
+  const int* it_npages;
+  const int* it_ntok;      // valid tokens in this item (contiguous from its first page)
+  const int* it_q_off;     // offset into qrows[]
+  const int* it_nq;
+  const int* it_slot;      // partial slot of these queries
+  const int* qrows;        // request rows
+  // rows
+  const int* row_priv_off;     // offset into pages[] / page_ntok[]
+  const int* row_priv_npages;
+  const int* row_nslots;       // shared slots; the private partial goes to slot row_nslots[r]
+  const int* pages;            // physical page ids
+  const int* page_ntok;        // valid tokens per page entry
+  // synthetic keys per row
+  const long long* row_uid;    // leaf context uid
+  const long long* row_pos;    // leaf tokens at plan time + (rank << 40)
+  // append targets (written by fk_step_commit)
+  const int* app_page;         // physical page or -1
+  const int* app_slot;
+  const long long* app_pos;    // position in the leaf (synthetic key)
+};
+
+// Device view of the KV arena and scratch.
+struct ArenaDev {
+  __nv_bfloat16* kv;      // [L][2][H][num_pages][16][D]
+  long long num_pages;
+  int num_layers;
+  int num_heads;
+  float* part_o;          // [rows][max_slots][H][D]
+  float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
+  int* counters;          // [rows][H] arrivals, reset by the merging CTA
+};
+
+inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {
+  return ((long long)layer * 2 + kv) * H + head;
+}
+
+// Launchers (fk_kernels.cu).  All return cudaError_t of the launch.
+cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer,
+                           const void* q, void* out, float* out_f32,
+                           float scale_log2, cudaStream_t s);
+cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer,
+                              const void* q, void* out, float* out_f32,
+                              float scale_log2, const CUtensorMap* tmap,
+                              cudaStream_t s);
+cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer,
+                             const void* q, void* out, float* out_f32,
+                             float scale_log2, const CUtensorMap* tmap,
+                             cudaStream_t s);
+cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer,
+                          const void* k, const void* v, cudaStream_t s);
+cudaError_t launch_synth_fill(const ArenaDev& a, const int* pages_dev, int npages_first,
+                              long long uid, long long pos0, long long pos1,
+                              unsigned long long seed, float k_scale, cudaStream_t s);
+cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p,
+                                 unsigned long long seed, void* q_all, cudaStream_t s);
+cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p,
+                                unsigned long long seed, float k_scale, cudaStream_t s);
+
+}  // namespace fk

@@ -1,0 +1,896 @@
+// Host side of the fork-attention pool: logical block accounting (bit-exact
+// with PagedKvStore, engine.py:66-106), physical page free stack, context
+// forest topology, per-step work-list planning and the C-ABI entry points of
+// include/forkattn.h.
+#include "forkattn.h"
+#include "fk_internal.h"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+using namespace fk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define FK_CUDA(expr)                                                        \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess)                                                   \
+      return fail(FK_CUDA_ERROR, "%s: %s (%s:%d)", #expr,                    \
+                  cudaGetErrorString(_e), __FILE__, __LINE__);               \
+  } while (0)
+
+struct Ctx {
+  int64_t parent = -1;
+  int64_t tokens = 0;
+  int32_t children = 0;
+  std::vector<int64_t> logical;  // logical block ids (itertools.count order)
+  std::vector<int32_t> phys;     // physical pages backing them
+};
+
+// One plan slot: pinned staging + device copy + the event that guards reuse.
+struct PlanSlot {
+  void* host = nullptr;
+  void* dev = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool armed = false;
+};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct fk_pool {
+  fk_pool_desc desc{};
+  bool on_device = false;
+  std::unordered_map<int64_t, Ctx> ctxs;
+  int64_t next_logical = 0;
+  int64_t used = 0;
+  int64_t peak = 0;
+  int64_t total_blocks = 0;
+  std::vector<int32_t> free_pages;  // stack, back() is the next page
+  int64_t num_pages = 0;
+
+  // device arena
+  __nv_bfloat16* kv = nullptr;
+  size_t arena_bytes = 0;
+  alignas(64) CUtensorMap tmap;
+  bool tmap_ok = false;
+  int num_sms = 148;
+
+  // options
+  int64_t tc_min_fanout = 0;
+  int64_t prefix_target_ctas = 0;  // 0 -> num_sms
+  int64_t launch_order = 0;
+  int64_t min_split_pages = 8;
+
+  // plan (host mirror + device)
+  PlanSlot slots[2];
+  int cur = -1;
+  PlanDev plan{};
+  bool have_plan = false;
+  std::vector<int64_t> plan_leaves;
+  std::vector<int64_t> plan_leaf_tokens;  // leaf tokens at plan time
+  size_t off_app_page = 0, off_app_slot = 0, off_app_pos = 0;
+  bool committed = false;
+
+  // scratch
+  float* part_o = nullptr;
+  float2* part_ml = nullptr;
+  int* counters = nullptr;
+  size_t part_cap = 0;     // entries (rows*slots*H)
+  size_t counter_cap = 0;  // entries (rows*H)
+
+  ArenaDev arena() const {
+    ArenaDev a;
+    a.kv = kv;
+    a.num_pages = num_pages;
+    a.num_layers = desc.num_layers;
+    a.num_heads = desc.num_heads;
+    a.part_o = part_o;
+    a.part_ml = part_ml;
+    a.counters = counters;
+    return a;
+  }
+};
+
+namespace {
+
+int64_t blocks_for(int64_t tokens, int64_t bs) { return (tokens + bs - 1) / bs; }
+
+int encode_tmap(fk_pool* p) {
+  p->tmap_ok = false;
+  if (!p->kv || p->num_pages == 0) return FK_OK;
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* sym = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &sym, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !sym) return fail(FK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)sym;
+  }
+  const int D = p->desc.head_dim;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)(p->num_pages * kPage),
+                        (cuuint64_t)p->desc.num_layers * 2 * p->desc.num_heads};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)p->num_pages * kPage * D * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)kPage, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&p->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p->kv, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FK_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  p->tmap_ok = true;
+  return FK_OK;
+}
+
+// Grow the physical arena to `pages`; live pages keep their ids (plane-wise copy).
+int reserve_pages(fk_pool* p, int64_t pages) {
+  if (pages <= p->num_pages) return FK_OK;
+  if (!p->on_device) return FK_OK;
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  const size_t D = p->desc.head_dim;
+  const size_t planes = (size_t)p->desc.num_layers * 2 * p->desc.num_heads;
+  const size_t new_bytes = planes * (size_t)pages * kPage * D * 2;
+  __nv_bfloat16* nkv = nullptr;
+  cudaError_t e = cudaMalloc(&nkv, new_bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FK_CUDA_ERROR, "KV arena of %zu bytes (%lld pages): %s", new_bytes,
+                (long long)pages, cudaGetErrorString(e));
+  }
+  // zero so every byte a kernel may touch is a finite bf16
+  FK_CUDA(cudaMemset(nkv, 0, new_bytes));
+  if (p->kv) {
+    FK_CUDA(cudaDeviceSynchronize());
+    const size_t old_plane = (size_t)p->num_pages * kPage * D * 2;
+    const size_t new_plane = (size_t)pages * kPage * D * 2;
+    FK_CUDA(cudaMemcpy2D(nkv, new_plane, p->kv, old_plane, old_plane, planes,
+                         cudaMemcpyDeviceToDevice));
+    FK_CUDA(cudaFree(p->kv));
+  }
+  // new physical pages go under the existing free stack so lower ids pop first
+  std::vector<int32_t> fresh;
+  fresh.reserve(pages - p->num_pages);
+  for (int64_t i = pages - 1; i >= p->num_pages; --i) fresh.push_back((int32_t)i);
+  fresh.insert(fresh.end(), p->free_pages.begin(), p->free_pages.end());
+  p->free_pages.swap(fresh);
+  p->kv = nkv;
+  p->arena_bytes = new_bytes;
+  p->num_pages = pages;
+  return encode_tmap(p);
+}
+
+int ensure_scratch(fk_pool* p, int rows, int slots) {
+  const size_t H = p->desc.num_heads, D = p->desc.head_dim;
+  const size_t need = (size_t)std::max(rows, 1) * std::max(slots, 1) * H;
+  if (need > p->part_cap) {
+    size_t cap = std::max(need, p->part_cap * 2);
+    if (p->part_o) FK_CUDA(cudaFree(p->part_o));
+    if (p->part_ml) FK_CUDA(cudaFree(p->part_ml));
+    p->part_o = nullptr;
+    p->part_ml = nullptr;
+    FK_CUDA(cudaMalloc(&p->part_o, cap * D * sizeof(float)));
+    FK_CUDA(cudaMalloc(&p->part_ml, cap * sizeof(float2)));
+    p->part_cap = cap;
+  }
+  const size_t cneed = (size_t)std::max(rows, 1) * H;
+  if (cneed > p->counter_cap) {
+    size_t cap = std::max(cneed, p->counter_cap * 2);
+    if (p->counters) FK_CUDA(cudaFree(p->counters));
+    p->counters = nullptr;
+    FK_CUDA(cudaMalloc(&p->counters, cap * sizeof(int)));
+    FK_CUDA(cudaMemset(p->counters, 0, cap * sizeof(int)));
+    p->counter_cap = cap;
+  }
+  return FK_OK;
+}
+
+int ensure_slot(fk_pool* p, PlanSlot& s, size_t bytes) {
+  if (bytes <= s.cap) return FK_OK;
+  size_t cap = std::max(bytes, s.cap * 2);
+  if (s.armed) FK_CUDA(cudaEventSynchronize(s.done));
+  if (s.host) FK_CUDA(cudaFreeHost(s.host));
+  if (s.dev) FK_CUDA(cudaFree(s.dev));
+  s.host = nullptr;
+  s.dev = nullptr;
+  FK_CUDA(cudaMallocHost(&s.host, cap));
+  FK_CUDA(cudaMalloc(&s.dev, cap));
+  s.cap = cap;
+  return FK_OK;
+}
+
+// Byte layout builder for one plan buffer.
+struct Layout {
+  size_t size = 0;
+  size_t add(size_t bytes) {
+    size_t off = align_up(size, 16);
+    size = off + bytes;
+    return off;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* fk_last_error(void) { return g_last_error.c_str(); }
+
+const char* fk_build_info(void) {
+  return "forkattn sm_100a (" __DATE__ " " __TIME__ "): private paged decode + mma.sync/tcgen05 "
+         "shared-prefix attention + last-arriver LSE merge";
+}
+
+int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
+  if (!desc || !out) return fail(FK_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (desc->block_size != kPage)
+    return fail(FK_INVALID_ARGUMENT, "block_size must be %d (got %d)", kPage, desc->block_size);
+  if (desc->head_dim != kHeadDim)
+    return fail(FK_INVALID_ARGUMENT, "head_dim must be %d (got %d)", kHeadDim, desc->head_dim);
+  if (desc->num_layers < 1 || desc->num_heads < 1 || desc->total_blocks < 0 || desc->num_pages < 0)
+    return fail(FK_INVALID_ARGUMENT, "bad pool geometry");
+  fk_pool* p = new fk_pool();
+  p->desc = *desc;
+  p->total_blocks = desc->total_blocks;
+  p->on_device = desc->device >= 0;
+  if (p->on_device) {
+    cudaError_t e = cudaSetDevice(desc->device);
+    if (e != cudaSuccess) {
+      delete p;
+      return fail(FK_CUDA_ERROR, "cudaSetDevice(%d): %s", desc->device, cudaGetErrorString(e));
+    }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc->device) == cudaSuccess)
+      p->num_sms = sms;
+    for (auto& s : p->slots) {
+      if (cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) {
+        delete p;
+        return fail(FK_CUDA_ERROR, "cudaEventCreate failed");
+      }
+    }
+    int rc = reserve_pages(p, desc->num_pages);
+    if (rc != FK_OK) {
+      fk_pool_destroy(p);
+      return rc;
+    }
+  }
+  *out = p;
+  return FK_OK;
+}
+
+int fk_pool_destroy(fk_pool* p) {
+  if (!p) return FK_OK;
+  if (p->on_device) {
+    cudaSetDevice(p->desc.device);
+    cudaDeviceSynchronize();
+    for (auto& s : p->slots) {
+      if (s.host) cudaFreeHost(s.host);
+      if (s.dev) cudaFree(s.dev);
+      if (s.done) cudaEventDestroy(s.done);
+    }
+    if (p->kv) cudaFree(p->kv);
+    if (p->part_o) cudaFree(p->part_o);
+    if (p->part_ml) cudaFree(p->part_ml);
+    if (p->counters) cudaFree(p->counters);
+  }
+  delete p;
+  return FK_OK;
+}
+
+int fk_pool_set_total_blocks(fk_pool* p, int64_t total) {
+  if (!p || total < 0) return fail(FK_INVALID_ARGUMENT, "bad total_blocks");
+  p->total_blocks = total;
+  return FK_OK;
+}
+
+int fk_pool_reserve_pages(fk_pool* p, int64_t pages) {
+  if (!p || pages < 0) return fail(FK_INVALID_ARGUMENT, "bad page count");
+  return reserve_pages(p, pages);
+}
+
+int fk_pool_stats_get(const fk_pool* p, fk_pool_stats* out) {
+  if (!p || !out) return fail(FK_INVALID_ARGUMENT, "null argument");
+  out->used_blocks = p->used;
+  out->free_blocks = p->total_blocks - p->used;
+  out->peak_used = p->peak;
+  out->total_blocks = p->total_blocks;
+  out->next_block = p->next_logical;
+  out->num_pages = p->num_pages;
+  out->free_pages = (int64_t)p->free_pages.size();
+  out->arena_bytes = (int64_t)p->arena_bytes;
+  return FK_OK;
+}
+
+int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  switch (option) {
+    case FK_OPT_TC_MIN_FANOUT: p->tc_min_fanout = value; break;
+    case FK_OPT_PREFIX_TARGET_CTAS: p->prefix_target_ctas = value; break;
+    case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
+    case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
+    default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
+  }
+  return FK_OK;
+}
+
+// ---- context forest -------------------------------------------------------
+
+int fk_ctx_create(fk_pool* p, int64_t ctx, int64_t parent) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (p->ctxs.count(ctx)) return fail(FK_INVALID_ARGUMENT, "context %lld exists", (long long)ctx);
+  if (parent >= 0) {
+    auto it = p->ctxs.find(parent);
+    if (it == p->ctxs.end())
+      return fail(FK_UNKNOWN_PARENT_CONTEXT, "unknown parent %lld", (long long)parent);
+    it->second.children += 1;
+  }
+  Ctx c;
+  c.parent = parent >= 0 ? parent : -1;
+  p->ctxs.emplace(ctx, std::move(c));
+  return FK_OK;
+}
+
+int fk_ctx_grow(fk_pool* p, int64_t ctx, int64_t new_tokens, int64_t* new_ids, int64_t cap,
+                int64_t* n_new) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (n_new) *n_new = 0;
+  auto it = p->ctxs.find(ctx);
+  if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)ctx);
+  Ctx& c = it->second;
+  if (new_tokens < 0) return fail(FK_INVALID_ARGUMENT, "negative token count");
+  // engine.py:89 — need may be <= 0 (shrinking never releases blocks)
+  const int64_t need = blocks_for(new_tokens, kPage) - (int64_t)c.logical.size();
+  const int64_t free_logical = p->total_blocks - p->used;
+  if (need > free_logical)
+    return fail(FK_OUT_OF_MEMORY, "need %lld blocks, %lld free", (long long)need,
+                (long long)free_logical);
+  if (need > 0 && new_ids && cap < need)
+    return fail(FK_INVALID_ARGUMENT, "id buffer too small (%lld < %lld)", (long long)cap,
+                (long long)need);
+  if (need > 0 && p->on_device && need > (int64_t)p->free_pages.size()) {
+    // the logical pool admits it: back it with more device pages
+    int64_t want = std::max<int64_t>(p->num_pages + need - (int64_t)p->free_pages.size(),
+                                     std::min<int64_t>(p->total_blocks,
+                                                       std::max<int64_t>(64, p->num_pages * 2)));
+    int rc = reserve_pages(p, want);
+    if (rc != FK_OK) return fail(FK_OUT_OF_MEMORY, "device arena: %s", g_last_error.c_str());
+  }
+  for (int64_t i = 0; i < need; ++i) {
+    const int64_t bid = p->next_logical++;
+    c.logical.push_back(bid);
+    if (p->on_device) {
+      c.phys.push_back(p->free_pages.back());
+      p->free_pages.pop_back();
+    } else {
+      c.phys.push_back(-1);
+    }
+    if (new_ids) new_ids[i] = bid;
+  }
+  if (need > 0) p->used += need;
+  c.tokens = new_tokens;
+  if (p->used > p->peak) p->peak = p->used;
+  if (n_new) *n_new = need > 0 ? need : 0;
+  return FK_OK;
+}
+
+int fk_ctx_release(fk_pool* p, int64_t ctx) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  auto it = p->ctxs.find(ctx);
+  if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)ctx);
+  Ctx& c = it->second;
+  if (c.children > 0)
+    return fail(FK_CONTEXT_BUSY, "context %lld has %d children", (long long)ctx, c.children);
+  // physical pages go back to the free stack; logical ids are retired forever
+  for (auto pg = c.phys.rbegin(); pg != c.phys.rend(); ++pg)
+    if (*pg >= 0) p->free_pages.push_back(*pg);
+  p->used -= (int64_t)c.logical.size();
+  if (c.parent >= 0) {
+    auto par = p->ctxs.find(c.parent);
+    if (par != p->ctxs.end()) par->second.children -= 1;
+  }
+  p->ctxs.erase(it);
+  return FK_OK;
+}
+
+int fk_ctx_info(const fk_pool* p, int64_t ctx, int64_t* tokens, int64_t* nblocks,
+                int64_t* parent) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  auto it = p->ctxs.find(ctx);
+  if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)ctx);
+  if (tokens) *tokens = it->second.tokens;
+  if (nblocks) *nblocks = (int64_t)it->second.logical.size();
+  if (parent) *parent = it->second.parent;
+  return FK_OK;
+}
+
+int fk_ctx_blocks(const fk_pool* p, int64_t ctx, int64_t* logical, int32_t* physical, int64_t cap,
+                  int64_t* n) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  auto it = p->ctxs.find(ctx);
+  if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)ctx);
+  const Ctx& c = it->second;
+  const int64_t k = (int64_t)c.logical.size();
+  if (n) *n = k;
+  if (cap < k && (logical || physical))
+    return fail(FK_INVALID_ARGUMENT, "buffer too small (%lld < %lld)", (long long)cap, (long long)k);
+  for (int64_t i = 0; i < k; ++i) {
+    if (logical) logical[i] = c.logical[i];
+    if (physical) physical[i] = c.phys[i];
+  }
+  return FK_OK;
+}
+
+// ---- decode step plan -----------------------------------------------------
+
+int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, void* stream,
+                 fk_plan_info* info) {
+  if (!p || (B > 0 && !leaves) || B < 0) return fail(FK_INVALID_ARGUMENT, "bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t H = p->desc.num_heads;
+
+  // chains leaf -> root, fan-out per context (engine.py:476-482 walk)
+  std::vector<std::vector<int64_t>> chain(B);
+  std::unordered_map<int64_t, int> fan;
+  std::vector<int64_t> order;  // unique contexts, first-seen (row order, leaf->root)
+  for (int r = 0; r < B; ++r) {
+    int64_t cur = leaves[r];
+    auto it = p->ctxs.find(cur);
+    if (it == p->ctxs.end())
+      return fail(FK_UNKNOWN_CONTEXT, "unknown leaf context %lld", (long long)cur);
+    while (cur >= 0) {
+      auto ci = p->ctxs.find(cur);
+      if (ci == p->ctxs.end()) break;  // parent already discarded (engine.py:482 get() -> None)
+      chain[r].push_back(cur);
+      auto f = fan.find(cur);
+      if (f == fan.end()) {
+        fan.emplace(cur, 1);
+        order.push_back(cur);
+      } else {
+        f->second += 1;
+      }
+      cur = ci->second.parent;
+    }
+  }
+  int64_t batch_tokens = 0, shared_tokens = 0, private_tokens = 0;
+  if (dedup) {
+    for (int64_t c : order) batch_tokens += p->ctxs[c].tokens;
+  } else {
+    for (int r = 0; r < B; ++r)
+      for (int64_t c : chain[r]) batch_tokens += p->ctxs[c].tokens;
+  }
+  auto is_shared = [&](int64_t c) {
+    return dedup && fan[c] >= 2 && p->ctxs[c].tokens > 0;
+  };
+
+  // shared contexts: descendant rows (row order) and kernel class
+  struct Shared {
+    int64_t ctx;
+    std::vector<int> rows;
+    bool tc;
+    int splits = 1;
+    int slot_base = 0;
+  };
+  std::vector<Shared> shared;
+  std::unordered_map<int64_t, int> shared_idx;
+  for (int64_t c : order) {
+    if (!is_shared(c)) continue;
+    shared_idx[c] = (int)shared.size();
+    Shared s;
+    s.ctx = c;
+    s.tc = p->tc_min_fanout > 0 && fan[c] >= p->tc_min_fanout;
+    shared.push_back(std::move(s));
+    shared_tokens += p->ctxs[c].tokens;
+  }
+  for (int r = 0; r < B; ++r)
+    for (int64_t c : chain[r]) {
+      auto si = shared_idx.find(c);
+      if (si != shared_idx.end()) shared[si->second].rows.push_back(r);
+    }
+  // split policy: ~one wave of CTAs over all prefix work
+  {
+    int64_t total = 0;
+    for (auto& s : shared) {
+      const int qb = s.tc ? kTcQBlock : kMmaQBlock;
+      const int64_t nqb = ((int64_t)s.rows.size() + qb - 1) / qb;
+      total += (int64_t)p->ctxs[s.ctx].phys.size() * nqb * H;
+    }
+    const int64_t target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
+    int64_t per = std::max<int64_t>(p->min_split_pages, (total + target - 1) / std::max<int64_t>(target, 1));
+    for (auto& s : shared) {
+      const int tile = s.tc ? kTcTilePages : kMmaTilePages;
+      const int64_t ps = (per + tile - 1) / tile * tile;
+      const int64_t np = (int64_t)p->ctxs[s.ctx].phys.size();
+      s.splits = (int)std::max<int64_t>(1, (np + ps - 1) / ps);
+    }
+  }
+  // slot bases: sum of splits of shared proper ancestors (same for every
+  // descendant because the contexts form a forest)
+  std::vector<int> nslots(B, 0);
+  for (auto& s : shared) {
+    int base = 0;
+    int64_t cur = p->ctxs[s.ctx].parent;
+    while (cur >= 0) {
+      auto si = shared_idx.find(cur);
+      if (si != shared_idx.end()) base += shared[si->second].splits;
+      auto ci = p->ctxs.find(cur);
+      if (ci == p->ctxs.end()) break;
+      cur = ci->second.parent;
+    }
+    s.slot_base = base;
+  }
+  for (int r = 0; r < B; ++r)
+    for (int64_t c : chain[r]) {
+      auto si = shared_idx.find(c);
+      if (si != shared_idx.end()) nslots[r] += shared[si->second].splits;
+    }
+  int max_slots = 1;
+  for (int r = 0; r < B; ++r) max_slots = std::max(max_slots, nslots[r] + 1);
+
+  // host arrays
+  std::vector<int32_t> pages, page_ntok, qrows;
+  std::vector<int32_t> it_page_off, it_npages, it_ntok, it_q_off, it_nq, it_slot;
+  int num_tc = 0, num_mma = 0;
+  // shared page lists first
+  std::vector<int32_t> shared_page_off(shared.size());
+  for (size_t i = 0; i < shared.size(); ++i) {
+    const Ctx& c = p->ctxs[shared[i].ctx];
+    shared_page_off[i] = (int32_t)pages.size();
+    for (size_t k = 0; k < c.phys.size(); ++k) {
+      pages.push_back(c.phys[k]);
+      page_ntok.push_back((int32_t)std::min<int64_t>(kPage, c.tokens - (int64_t)k * kPage));
+    }
+  }
+  std::vector<int32_t> q_off(shared.size());
+  for (size_t i = 0; i < shared.size(); ++i) {
+    q_off[i] = (int32_t)qrows.size();
+    for (int r : shared[i].rows) qrows.push_back(r);
+  }
+  for (int pass = 0; pass < 2; ++pass) {  // mma items first, then tcgen05 items
+    for (size_t i = 0; i < shared.size(); ++i) {
+      const Shared& s = shared[i];
+      if ((int)s.tc != pass) continue;
+      const Ctx& c = p->ctxs[s.ctx];
+      const int64_t np = (int64_t)c.phys.size();
+      const int64_t ps = (np + s.splits - 1) / s.splits;
+      const int tile = s.tc ? kTcTilePages : kMmaTilePages;
+      const int64_t psr = (ps + tile - 1) / tile * tile;
+      const int qb = s.tc ? kTcQBlock : kMmaQBlock;
+      const int nq = (int)s.rows.size();
+      for (int sp = 0; sp < s.splits; ++sp) {
+        const int64_t p0 = sp * psr;
+        const int64_t p1 = std::min<int64_t>(np, p0 + psr);
+        const int64_t t0 = p0 * kPage;
+        const int64_t t1 = std::min<int64_t>(c.tokens, p1 * kPage);
+        for (int q0 = 0; q0 < nq; q0 += qb) {
+          it_page_off.push_back(shared_page_off[i] + (int32_t)p0);
+          it_npages.push_back((int32_t)std::max<int64_t>(0, p1 - p0));
+          it_ntok.push_back((int32_t)std::max<int64_t>(0, t1 - t0));
+          it_q_off.push_back(q_off[i] + q0);
+          it_nq.push_back(std::min(qb, nq - q0));
+          it_slot.push_back(s.slot_base + sp);
+          (s.tc ? num_tc : num_mma) += 1;
+        }
+      }
+    }
+  }
+  // private streams
+  std::vector<int32_t> row_priv_off(B), row_priv_np(B);
+  for (int r = 0; r < B; ++r) {
+    row_priv_off[r] = (int32_t)pages.size();
+    for (auto ci = chain[r].rbegin(); ci != chain[r].rend(); ++ci) {  // root -> leaf
+      if (is_shared(*ci)) continue;
+      const Ctx& c = p->ctxs[*ci];
+      if (c.tokens <= 0) continue;
+      private_tokens += c.tokens;
+      for (size_t k = 0; k < c.phys.size(); ++k) {
+        const int64_t nt = std::min<int64_t>(kPage, c.tokens - (int64_t)k * kPage);
+        if (nt <= 0) break;
+        pages.push_back(c.phys[k]);
+        page_ntok.push_back((int32_t)nt);
+      }
+    }
+    row_priv_np[r] = (int32_t)pages.size() - row_priv_off[r];
+  }
+  // synthetic keys: (leaf uid, leaf tokens at plan time + rank << 40)
+  std::vector<int64_t> row_uid(B), row_pos(B);
+  p->plan_leaves.assign(leaves, leaves + B);
+  p->plan_leaf_tokens.resize(B);
+  {
+    std::unordered_map<int64_t, int> rank;
+    for (int r = 0; r < B; ++r) {
+      const int64_t leaf = leaves[r];
+      const int k = rank[leaf]++;
+      row_uid[r] = leaf;
+      p->plan_leaf_tokens[r] = p->ctxs[leaf].tokens;
+      row_pos[r] = p->ctxs[leaf].tokens + ((int64_t)k << 40);
+    }
+  }
+
+  if (info) {
+    info->batch_tokens = batch_tokens;
+    info->shared_tokens = shared_tokens;
+    info->private_tokens = private_tokens;
+    info->num_rows = B;
+    info->num_shared_ctx = (int32_t)shared.size();
+    info->num_prefix_ctas = (int32_t)(it_page_off.size() * H);
+    info->max_slots = max_slots;
+    info->num_tc_items = num_tc;
+    info->num_mma_items = num_mma;
+  }
+  p->committed = false;
+  if (!p->on_device) {
+    p->have_plan = true;
+    return FK_OK;
+  }
+
+  // ---- upload ----
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  int rc = ensure_scratch(p, B, max_slots);
+  if (rc != FK_OK) return rc;
+  const int n_items = (int)it_page_off.size();
+  Layout L;
+  const size_t o_it = L.add(sizeof(int32_t) * 6 * std::max(n_items, 1));
+  const size_t o_q = L.add(sizeof(int32_t) * std::max<size_t>(qrows.size(), 1));
+  const size_t o_rows = L.add(sizeof(int32_t) * 3 * std::max(B, 1));
+  const size_t o_pages = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
+  const size_t o_pnt = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
+  const size_t o_uid = L.add(sizeof(int64_t) * std::max(B, 1));
+  const size_t o_pos = L.add(sizeof(int64_t) * std::max(B, 1));
+  const size_t o_app = L.add(sizeof(int32_t) * 2 * std::max(B, 1));
+  const size_t o_apos = L.add(sizeof(int64_t) * std::max(B, 1));
+  // rotate slots; wait until the GPU finished with the one we reuse
+  if (p->cur >= 0 && p->slots[p->cur].dev) {
+    FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
+    p->slots[p->cur].armed = true;
+  }
+  p->cur = (p->cur + 1) & 1;
+  PlanSlot& slot = p->slots[p->cur];
+  if (slot.armed) FK_CUDA(cudaEventSynchronize(slot.done));
+  rc = ensure_slot(p, slot, L.size);
+  if (rc != FK_OK) return rc;
+  char* h = (char*)slot.host;
+  auto put = [&](size_t off, const void* src, size_t bytes) {
+    if (bytes) memcpy(h + off, src, bytes);
+  };
+  const size_t ni = (size_t)std::max(n_items, 1);
+  int32_t* itb = (int32_t*)(h + o_it);
+  for (int i = 0; i < n_items; ++i) {
+    itb[0 * ni + i] = it_page_off[i];
+    itb[1 * ni + i] = it_npages[i];
+    itb[2 * ni + i] = it_ntok[i];
+    itb[3 * ni + i] = it_q_off[i];
+    itb[4 * ni + i] = it_nq[i];
+    itb[5 * ni + i] = it_slot[i];
+  }
+  put(o_q, qrows.data(), qrows.size() * 4);
+  const size_t nb = (size_t)std::max(B, 1);
+  int32_t* rb = (int32_t*)(h + o_rows);
+  for (int r = 0; r < B; ++r) {
+    rb[0 * nb + r] = row_priv_off[r];
+    rb[1 * nb + r] = row_priv_np[r];
+    rb[2 * nb + r] = nslots[r];
+  }
+  put(o_pages, pages.data(), pages.size() * 4);
+  put(o_pnt, page_ntok.data(), page_ntok.size() * 4);
+  put(o_uid, row_uid.data(), (size_t)B * 8);
+  put(o_pos, row_pos.data(), (size_t)B * 8);
+  int32_t* ab = (int32_t*)(h + o_app);
+  for (int r = 0; r < B; ++r) {
+    ab[r] = -1;
+    ab[nb + r] = 0;
+  }
+  memset(h + o_apos, 0, nb * 8);
+  FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
+
+  const char* d = (const char*)slot.dev;
+  PlanDev& pd = p->plan;
+  pd.num_rows = B;
+  pd.max_slots = max_slots;
+  pd.num_items = n_items;
+  pd.tc_begin = num_mma;
+  const int32_t* ditb = (const int32_t*)(d + o_it);
+  pd.it_page_off = ditb + 0 * ni;
+  pd.it_npages = ditb + 1 * ni;
+  pd.it_ntok = ditb + 2 * ni;
+  pd.it_q_off = ditb + 3 * ni;
+  pd.it_nq = ditb + 4 * ni;
+  pd.it_slot = ditb + 5 * ni;
+  pd.qrows = (const int32_t*)(d + o_q);
+  const int32_t* drb = (const int32_t*)(d + o_rows);
+  pd.row_priv_off = drb;
+  pd.row_priv_npages = drb + nb;
+  pd.row_nslots = drb + 2 * nb;
+  pd.pages = (const int32_t*)(d + o_pages);
+  pd.page_ntok = (const int32_t*)(d + o_pnt);
+  pd.row_uid = (const long long*)(d + o_uid);
+  pd.row_pos = (const long long*)(d + o_pos);
+  pd.app_page = (const int32_t*)(d + o_app);
+  pd.app_slot = (const int32_t*)(d + o_app) + nb;
+  pd.app_pos = (const long long*)(d + o_apos);
+  p->off_app_page = o_app;
+  p->off_app_slot = o_app + nb * 4;
+  p->off_app_pos = o_apos;
+  p->have_plan = true;
+  return FK_OK;
+}
+
+int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* out_f32,
+                   void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan: call fk_step_plan first");
+  if (layer < 0 || layer >= p->desc.num_layers) return fail(FK_INVALID_ARGUMENT, "bad layer %d", layer);
+  if (p->plan.num_rows == 0) return FK_OK;
+  if (!q || !out) return fail(FK_INVALID_ARGUMENT, "null q/out");
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p->desc.head_dim));
+  ArenaDev a = p->arena();
+  const bool has_mma = p->plan.tc_begin > 0;
+  const bool has_tc = p->plan.num_items > p->plan.tc_begin;
+  if ((has_mma || has_tc) && !p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
+  auto run_prefix = [&]() -> int {
+    if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, out, out_f32, scale_log2, &p->tmap, st));
+    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, out, out_f32, scale_log2, &p->tmap, st));
+    return FK_OK;
+  };
+  if (p->launch_order == 0) {
+    int rc = run_prefix();
+    if (rc != FK_OK) return rc;
+    FK_CUDA(launch_private(a, p->plan, layer, q, out, out_f32, scale_log2, st));
+  } else {
+    FK_CUDA(launch_private(a, p->plan, layer, q, out, out_f32, scale_log2, st));
+    int rc = run_prefix();
+    if (rc != FK_OK) return rc;
+  }
+  return FK_OK;
+}
+
+int fk_step_commit(fk_pool* p, const int64_t* positions, void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
+  const int B = (int)p->plan_leaves.size();
+  if (B > 0 && !positions) return fail(FK_INVALID_ARGUMENT, "null positions");
+  // validate against the forest first (no partial effects)
+  std::vector<int32_t> pg(B, -1), sl(B, 0);
+  std::vector<int64_t> ps(B, 0);
+  for (int r = 0; r < B; ++r) {
+    if (positions[r] < 0) continue;
+    auto it = p->ctxs.find(p->plan_leaves[r]);
+    if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "leaf of row %d vanished", r);
+    const Ctx& c = it->second;
+    const int64_t pos = positions[r];
+    if (pos >= c.tokens || pos / kPage >= (int64_t)c.phys.size())
+      return fail(FK_INVALID_ARGUMENT, "row %d position %lld outside leaf (%lld tokens)", r,
+                  (long long)pos, (long long)c.tokens);
+    pg[r] = c.phys[pos / kPage];
+    sl[r] = (int32_t)(pos % kPage);
+    ps[r] = pos;
+  }
+  p->committed = true;
+  if (!p->on_device || B == 0) return FK_OK;
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  PlanSlot& slot = p->slots[p->cur];
+  char* h = (char*)slot.host;
+  const size_t nb = (size_t)std::max(B, 1);
+  int32_t* ab = (int32_t*)(h + p->off_app_page);
+  memcpy(ab, pg.data(), B * 4);
+  memcpy(ab + nb, sl.data(), B * 4);
+  memcpy(h + p->off_app_pos, ps.data(), B * 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  FK_CUDA(cudaMemcpyAsync((char*)slot.dev + p->off_app_page, h + p->off_app_page, nb * 8,
+                          cudaMemcpyHostToDevice, st));
+  FK_CUDA(cudaMemcpyAsync((char*)slot.dev + p->off_app_pos, h + p->off_app_pos, nb * 8,
+                          cudaMemcpyHostToDevice, st));
+  return FK_OK;
+}
+
+int fk_append_kv(fk_pool* p, int32_t layer, const void* k, const void* v, void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  if (!p->committed) return fail(FK_INVALID_ARGUMENT, "fk_step_commit not called for this plan");
+  if (layer < 0 || layer >= p->desc.num_layers) return fail(FK_INVALID_ARGUMENT, "bad layer %d", layer);
+  if (p->plan.num_rows == 0) return FK_OK;
+  if (!k || !v) return fail(FK_INVALID_ARGUMENT, "null k/v");
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_CUDA(launch_append(p->arena(), p->plan, layer, k, v, (cudaStream_t)stream));
+  return FK_OK;
+}
+
+int fk_synth_fill(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, uint64_t seed,
+                  float k_scale, void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  auto it = p->ctxs.find(ctx);
+  if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)ctx);
+  const Ctx& c = it->second;
+  if (pos0 < 0 || pos1 < pos0 || pos1 > c.tokens)
+    return fail(FK_INVALID_ARGUMENT, "bad range [%lld, %lld) of %lld", (long long)pos0,
+                (long long)pos1, (long long)c.tokens);
+  if (pos1 == pos0) return FK_OK;
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t first = pos0 / kPage, last = (pos1 - 1) / kPage;
+  const int n = (int)(last - first + 1);
+  int* dpages = nullptr;
+  FK_CUDA(cudaMallocAsync(&dpages, sizeof(int) * n, st));
+  FK_CUDA(cudaMemcpyAsync(dpages, c.phys.data() + first, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  FK_CUDA(launch_synth_fill(p->arena(), dpages, (int)first, ctx, pos0, pos1, seed, k_scale, st));
+  FK_CUDA(cudaFreeAsync(dpages, st));
+  return FK_OK;
+}
+
+int fk_synth_queries(fk_pool* p, uint64_t seed, void* q_all, void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
+  if (p->plan.num_rows == 0) return FK_OK;
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_CUDA(launch_synth_queries(p->arena(), p->plan, seed, q_all, (cudaStream_t)stream));
+  return FK_OK;
+}
+
+int fk_synth_append(fk_pool* p, uint64_t seed, float k_scale, void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  if (!p->committed) return fail(FK_INVALID_ARGUMENT, "fk_step_commit not called for this plan");
+  if (p->plan.num_rows == 0) return FK_OK;
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_CUDA(launch_synth_append(p->arena(), p->plan, seed, k_scale, (cudaStream_t)stream));
+  return FK_OK;
+}
+
+// ---- hashing (tokenizer.py:36-49) -------------------------------------------
+
+uint64_t fk_fnv1a64_u32(const uint32_t* ids, size_t n, uint64_t seed) {
+  uint64_t h = seed;
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t t = ids[i];
+    for (int b = 0; b < 4; ++b) {
+      h ^= (uint64_t)((t >> (8 * b)) & 0xFFu);
+      h *= 0x00000100000001B3ULL;
+    }
+  }
+  return h;
+}
+
+int fk_fnv1a64_chain(const uint32_t* ids, const int64_t* seg_off, int32_t nseg, uint64_t seed,
+                     uint64_t* out) {
+  if (nseg < 0 || (nseg > 0 && (!seg_off || !out))) return fail(FK_INVALID_ARGUMENT, "bad arguments");
+  uint64_t h = seed;
+  for (int32_t i = 0; i < nseg; ++i) {
+    const int64_t a = seg_off[i], b = seg_off[i + 1];
+    if (b < a) return fail(FK_INVALID_ARGUMENT, "segment %d has negative length", i);
+    h = fk_fnv1a64_u32(ids + a, (size_t)(b - a), h);
+    out[i] = h;
+  }
+  return FK_OK;
+}
+
+}  // extern "C"

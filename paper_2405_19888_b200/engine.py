@@ -1,0 +1,773 @@
+"""GPU-backed engine behind the reference's Fill/Generate/FreeContext surface.
+
+`GpuEngine` is a drop-in for `semflow.engine.Engine`
+(/root/reference/pkg/src/semflow/engine.py:157-538): same constructor, same
+methods, same live attributes the manager, scheduler and report builder read
+(SURVEY.md §8b).  Bookkeeping that the reference keeps in Python dicts is
+split as follows:
+
+* block accounting, the context forest topology and the per-step work list
+  live in the C++ pool of libforkattn.so (PagedKvStore, engine.py:66-106,
+  and the `_batch_tokens` walk, engine.py:470-484);
+* refcounts, the dropped flag, the hash registry, the fill queue and the
+  generation tasks stay here, because the manager and the scheduler read
+  and write them directly;
+* with a device, every decode step runs the shared-prefix attention kernels
+  for all layers over the running batch before the
+  one-token growth, exactly where the reference charges `batch_tokens`.
+
+Without a device (``device=None``) the engine is the same native block
+manager with no attention — the integer twin the CPU parity suites drive.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Any, Deque, Dict, List, Optional, Sequence, Set, Tuple
+
+from . import _lib
+from .errors import ContextBusy, OutOfMemory, UnknownContext, UnknownParentContext
+
+MS = 1_000_000  # ns per millisecond
+FNV64_EMPTY = 0xCBF29CE484222325
+
+
+def hash_token_ids(token_ids: Sequence[int], seed: int = FNV64_EMPTY) -> int:
+    """tokenizer.hash_token_ids (tokenizer.py:47-49) via the C-ABI."""
+    return _lib.fnv1a64_u32(list(token_ids), seed)
+
+
+def format_ms(ns: int) -> str:
+    """engine.format_ms (engine.py:541-545): ms with <= 3 decimals, zeros trimmed."""
+    text = "%.3f" % (ns / MS)
+    if "." in text:
+        text = text.rstrip("0").rstrip(".")
+    return text
+
+
+@dataclass
+class CostModel:
+    """Virtual clock of the reference (engine.py:25-50); kept so reports and
+    traces stay byte-identical.  Any object with the same attributes works."""
+
+    c0_ms: float = 2.0
+    c1_ms: float = 0.0062
+    c2_ms: float = 5.0
+    c3_ms: float = 0.002
+    shared_kernel: bool = True
+    block_size: int = 16
+
+    def __post_init__(self) -> None:
+        self.c0_ns = round(self.c0_ms * MS)
+        self.c1_ns = round(self.c1_ms * MS)
+        self.c2_ns = round(self.c2_ms * MS)
+        self.c3_ns = round(self.c3_ms * MS)
+
+    def iteration_ns(self, batch_tokens: int) -> int:
+        return self.c0_ns + self.c1_ns * batch_tokens
+
+    def fill_ns(self, fill_tokens: int) -> int:
+        return self.c2_ns + self.c3_ns * fill_tokens
+
+    def latency_threshold_ms(self, capacity: int) -> float:
+        return self.iteration_ns(capacity) / MS
+
+
+@dataclass
+class Context:
+    """Forest node (engine.py:53-63) plus the pool uid that keys it in C++."""
+
+    context_id: str
+    engine_id: str
+    parent_id: Optional[str]
+    token_count: int = 0
+    block_ids: List[int] = field(default_factory=list)
+    refcount: int = 0
+    dropped: bool = False
+    chain_hashes: List[int] = field(default_factory=list)
+    registered_hashes: List[int] = field(default_factory=list)
+    uid: int = -1
+
+
+@dataclass
+class FillTask:
+    request_id: Optional[str]
+    context_id: str
+    token_ids: List[int]
+
+
+@dataclass
+class GenerationTask:
+    request_id: str
+    context_id: str
+    token_ids: List[int]
+    value_text: str
+    emitted: int = 0
+    started: bool = False
+    done: bool = False
+
+    @property
+    def remaining(self) -> int:
+        return len(self.token_ids) - self.emitted
+
+
+@dataclass
+class StepReport:
+    engine_id: str
+    started_ns: int
+    elapsed_ns: int
+    fill_tokens: int
+    batch_tokens: int
+    emitted: Dict[str, int]
+    finished: List[str]
+    failed: List[Tuple[str, str]]
+    fill_completed: List[str]
+
+
+@dataclass
+class ContextPlan:
+    reuse_context_id: Optional[str]
+    reused_tokens: int
+    fill_segments: List[Tuple[List[int], int]]
+    marginal_tokens: int
+    adopted_tokens: int = 0
+
+
+@dataclass(frozen=True)
+class ModelGeometry:
+    """Attention shape of the served model (new ctor args: Config rejects
+    unknown keys, config.py:39-42, so they cannot live there)."""
+
+    num_layers: int
+    num_heads: int
+    head_dim: int = 128
+
+
+LLAMA_7B = ModelGeometry(32, 32, 128)
+LLAMA_13B = ModelGeometry(40, 40, 128)
+TINY = ModelGeometry(1, 32, 128)
+
+
+class GpuKvStore:
+    """PagedKvStore (engine.py:66-106) over the C++ pool.
+
+    `owner` stays a live dict (the reference's conservation oracle reads it,
+    tests/oracles.py:543-553); logical ids come from the pool's monotonic
+    counter and are never recycled, physical pages are.
+    """
+
+    def __init__(self, pool: "_Pool", block_size: int):
+        self._pool = pool
+        self.block_size = block_size
+        self.owner: Dict[int, str] = {}
+
+    @property
+    def total_blocks(self) -> int:
+        return self._pool.stats().total_blocks
+
+    @total_blocks.setter
+    def total_blocks(self, value: int) -> None:  # manager.py:138 writes this
+        _lib.check(_lib.lib.fk_pool_set_total_blocks(self._pool.handle, int(value)))
+
+    @property
+    def peak_used(self) -> int:
+        return self._pool.stats().peak_used
+
+    @property
+    def used_blocks(self) -> int:
+        return self._pool.stats().used_blocks
+
+    @property
+    def free_blocks(self) -> int:
+        return self._pool.stats().free_blocks
+
+    def blocks_for(self, tokens: int) -> int:
+        return -(-tokens // self.block_size)
+
+    def grow(self, ctx: Context, new_token_count: int) -> None:
+        need = self.blocks_for(new_token_count) - len(ctx.block_ids)
+        buf = self._pool.id_buffer(max(need, 0))
+        n = ctypes.c_int64(0)
+        status = _lib.lib.fk_ctx_grow(
+            self._pool.handle, ctx.uid, int(new_token_count), buf, max(need, 0), ctypes.byref(n)
+        )
+        if status == _lib.FK_OUT_OF_MEMORY:
+            raise OutOfMemory(f"engine {ctx.engine_id}: need {need} blocks, {self.free_blocks} free")
+        _lib.check(status)
+        for i in range(n.value):
+            bid = int(buf[i])
+            self.owner[bid] = ctx.context_id
+            ctx.block_ids.append(bid)
+        ctx.token_count = new_token_count
+
+    def release(self, ctx: Context) -> None:
+        _lib.check(_lib.lib.fk_ctx_release(self._pool.handle, ctx.uid))
+        for bid in ctx.block_ids:
+            del self.owner[bid]
+        ctx.block_ids = []
+        ctx.token_count = 0
+
+
+class _Pool:
+    """Owns one fk_pool* (one per engine / GPU)."""
+
+    def __init__(self, geometry: ModelGeometry, block_size: int, total_blocks: int, device: Optional[int],
+                 num_pages: int = 0):
+        desc = _lib.PoolDesc(
+            num_layers=geometry.num_layers,
+            num_heads=geometry.num_heads,
+            head_dim=geometry.head_dim,
+            block_size=block_size,
+            total_blocks=total_blocks,
+            num_pages=num_pages if device is not None else 0,
+            device=-1 if device is None else int(device),
+            reserved=0,
+        )
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.fk_pool_create(ctypes.byref(desc), ctypes.byref(h)))
+        self.handle = h
+        self._ids = (ctypes.c_int64 * 64)()
+        self._stats = _lib.PoolStats()
+
+    def id_buffer(self, n: int):
+        if n > len(self._ids):
+            self._ids = (ctypes.c_int64 * max(n, 2 * len(self._ids)))()
+        return self._ids
+
+    def stats(self) -> _lib.PoolStats:
+        _lib.check(_lib.lib.fk_pool_stats_get(self.handle, ctypes.byref(self._stats)))
+        return self._stats
+
+    def set_option(self, option: int, value: int) -> None:
+        _lib.check(_lib.lib.fk_pool_set_option(self.handle, option, int(value)))
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.lib.fk_pool_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SyntheticDecodeModel:
+    """Deterministic stand-in for the QKV projection: Q rows and the step's
+    new K/V rows come from the counter-hash generator on the device
+    (oracle/forkattn_oracle.py restates it).  Fills use the same generator."""
+
+    def __init__(self, seed: int = 0x5EED, k_scale: float = 1.0):
+        self.seed = seed
+        self.k_scale = k_scale
+
+
+class TensorDecodeModel:
+    """Caller-supplied rows: q[L][B][H][D] and k/v[L][B][H][D] bf16, device
+    resident or host (pinned) — host tensors are copied in the step, and the
+    output is copied back, which is the end-to-end path of bench.py."""
+
+    def __init__(self, q, k=None, v=None, copy_out: bool = False):
+        self.q, self.k, self.v = q, k, v
+        self.copy_out = copy_out
+        self.host_out = None
+
+
+class GpuEngine:
+    """Drop-in `Engine` (engine.py:157-538) with a B200 decode path."""
+
+    def __init__(
+        self,
+        engine_id: str,
+        cost: Any,
+        kv_tokens: int = 120_000,
+        token_capacity: int = 64_000,
+        *,
+        device: Optional[int] = None,
+        geometry: ModelGeometry = TINY,
+        model: Any = None,
+        num_pages: int = 0,
+        capture_f32: bool = False,
+        keep_history: bool = False,
+    ):
+        self.engine_id = engine_id
+        self.cost = cost
+        self.token_capacity = token_capacity
+        self.latency_threshold_ms = cost.latency_threshold_ms(token_capacity)
+        block_size = getattr(cost, "block_size", 16)
+        self.geometry = geometry
+        self.device = device
+        self._pool = _Pool(geometry, block_size, -(-kv_tokens // block_size), device, num_pages)
+        self.store = GpuKvStore(self._pool, block_size)
+        self.clock_ns = 0
+        self.contexts: Dict[str, Context] = {}
+        self.registry: Dict[int, str] = {}
+        self.fill_queue: Deque[FillTask] = deque()
+        self.gens: Dict[str, GenerationTask] = {}
+        self.pending_fills: Dict[str, int] = {}
+        self.charges: Dict[str, int] = {}
+        self.holder_class: Dict[str, str] = {}
+        self.request_leaf: Dict[str, str] = {}
+        self.trace: List[str] = []
+        self.reports: List[StepReport] = []
+        self.reuse_enabled = True
+        self.busy_ns = 0
+        self.fill_ns_total = 0
+        self.decode_ns_total = 0
+        self.total_emitted = 0
+        self._ctx_counter = itertools.count()
+        self._uid_counter = itertools.count()
+        # device state
+        self.model = model if model is not None else SyntheticDecodeModel()
+        self.capture_f32 = capture_f32
+        self.keep_history = keep_history
+        self.history: List[Dict[str, Any]] = []
+        self.last_output = None
+        self.last_output_f32 = None
+        self.last_rows: List[str] = []
+        self.last_plan = _lib.PlanInfo()
+        self.kv_tokens_streamed = 0  # sum of batch_tokens over decode steps (per layer)
+        self._stream = None
+        self._leaf_buf = (ctypes.c_int64 * 64)()
+        self._pos_buf = (ctypes.c_int64 * 64)()
+        if device is not None:
+            import torch
+
+            self._torch = torch
+            self._dev = torch.device("cuda", device)
+            with torch.cuda.device(self._dev):
+                self._stream = torch.cuda.Stream(self._dev)
+
+    # -- device plumbing ------------------------------------------------------
+
+    @property
+    def stream(self):
+        return self._stream
+
+    def _sp(self):
+        return ctypes.c_void_p(self._stream.cuda_stream) if self._stream is not None else None
+
+    def set_option(self, option: int, value: int) -> None:
+        self._pool.set_option(option, value)
+
+    def pool_stats(self) -> _lib.PoolStats:
+        return self._pool.stats()
+
+    def context_pages(self, context_id: str) -> Tuple[List[int], List[int]]:
+        """(logical ids, physical pages) of a context, read back from C++."""
+        ctx = self.get_context(context_id)
+        n = ctypes.c_int64(0)
+        _lib.check(_lib.lib.fk_ctx_blocks(self._pool.handle, ctx.uid, None, None, 0, ctypes.byref(n)))
+        lg = (ctypes.c_int64 * max(n.value, 1))()
+        ph = (ctypes.c_int32 * max(n.value, 1))()
+        _lib.check(_lib.lib.fk_ctx_blocks(self._pool.handle, ctx.uid, lg, ph, n.value, ctypes.byref(n)))
+        return [int(lg[i]) for i in range(n.value)], [int(ph[i]) for i in range(n.value)]
+
+    def close(self) -> None:
+        if self._stream is not None:
+            self._stream.synchronize()
+        self._pool.close()
+
+    # -- context primitives (engine.py:192-300) --------------------------------
+
+    def new_context_id(self) -> str:
+        return f"{self.engine_id}.c{next(self._ctx_counter)}"
+
+    def get_context(self, context_id: str) -> Context:
+        ctx = self.contexts.get(context_id)
+        if ctx is None:
+            raise UnknownContext(f"unknown context {context_id}")
+        return ctx
+
+    def create_context(self, context_id: str, parent_context_id: Optional[str], request_id: Optional[str] = None) -> Context:
+        inherited: List[int] = []
+        parent_uid = -1
+        if parent_context_id is not None:
+            parent = self.contexts.get(parent_context_id)
+            if parent is None:
+                raise UnknownParentContext(f"unknown parent {parent_context_id}")
+            parent.refcount += 1
+            inherited = list(parent.chain_hashes)
+            parent_uid = parent.uid
+        ctx = Context(context_id, self.engine_id, parent_context_id, chain_hashes=inherited,
+                      uid=next(self._uid_counter))
+        _lib.check(_lib.lib.fk_ctx_create(self._pool.handle, ctx.uid, parent_uid))
+        self.contexts[context_id] = ctx
+        if request_id is not None:
+            self.request_leaf[request_id] = context_id
+        return ctx
+
+    def fill(self, token_ids: Sequence[int], context_id: str, parent_context_id: Optional[str] = None,
+             request_id: Optional[str] = None, boundary_hash: Optional[int] = None) -> int:
+        """Allocate pages for the new tokens, write their KV (synthetic
+        prefill stand-in) and queue the fill work; atomic on OutOfMemory."""
+        fresh = context_id not in self.contexts
+        ctx = self.create_context(context_id, parent_context_id) if fresh else self.get_context(context_id)
+        before = ctx.token_count
+        try:
+            self.store.grow(ctx, before + len(token_ids))
+        except OutOfMemory:
+            if fresh:
+                self._discard_context(ctx)
+            raise
+        if self.device is not None and len(token_ids) > 0:
+            _lib.check(_lib.lib.fk_synth_fill(self._pool.handle, ctx.uid, before, ctx.token_count,
+                                              self.model_seed, self.model_k_scale, self._sp()))
+        if boundary_hash is not None:
+            ctx.chain_hashes.append(boundary_hash)
+            if boundary_hash not in self.registry:
+                self.registry[boundary_hash] = context_id
+                ctx.registered_hashes.append(boundary_hash)
+        self.fill_queue.append(FillTask(request_id, context_id, list(token_ids)))
+        if request_id is not None:
+            self.pending_fills[request_id] = self.pending_fills.get(request_id, 0) + 1
+            self.request_leaf[request_id] = context_id
+        return len(token_ids)
+
+    @property
+    def model_seed(self) -> int:
+        return int(getattr(self.model, "seed", 0x5EED))
+
+    @property
+    def model_k_scale(self) -> float:
+        return float(getattr(self.model, "k_scale", 1.0))
+
+    def generate(self, request_id: str, context_id: str, token_ids: Sequence[int], value_text: str) -> GenerationTask:
+        ctx = self.get_context(context_id)
+        ctx.refcount += 1  # the active generation holds its leaf
+        self.request_leaf[request_id] = context_id
+        task = GenerationTask(request_id, context_id, list(token_ids), value_text)
+        task.started = self.pending_fills.get(request_id, 0) == 0
+        self.gens[request_id] = task
+        return task
+
+    def _discard_context(self, ctx: Context) -> None:
+        while ctx is not None:
+            self.store.release(ctx)
+            for h in ctx.registered_hashes:
+                if self.registry.get(h) == ctx.context_id:
+                    del self.registry[h]
+            ctx.registered_hashes = []
+            del self.contexts[ctx.context_id]
+            parent = self.contexts.get(ctx.parent_id) if ctx.parent_id is not None else None
+            ctx = None
+            if parent is not None:
+                parent.refcount -= 1
+                if parent.refcount == 0 and parent.dropped:
+                    ctx = parent  # cascade (engine.py:280-285)
+
+    def free_context(self, context_id: str) -> None:
+        ctx = self.get_context(context_id)
+        if ctx.refcount > 0:
+            raise ContextBusy(f"context {context_id} has refcount {ctx.refcount}")
+        self._discard_context(ctx)
+
+    def mark_dropped(self, context_id: str) -> None:
+        ctx = self.get_context(context_id)
+        ctx.dropped = True
+        if ctx.refcount == 0:
+            self._discard_context(ctx)
+
+    # -- planning (engine.py:304-382) -------------------------------------------
+
+    def plan_prefix(self, chain_hashes: Sequence[int], segment_tokens: Sequence[Sequence[int]],
+                    overlay: Optional[Dict[int, str]] = None) -> ContextPlan:
+        """Deepest chain boundary held by the registry (or the overlay of
+        this scheduling pass) -> context to fork from; see engine.py:304-363."""
+        n = len(chain_hashes)
+        cumulative: List[int] = []
+        acc = 0
+        for i in range(n):
+            if i < len(segment_tokens):
+                acc += len(segment_tokens[i])
+            cumulative.append(acc)
+        reuse_id: Optional[str] = None
+        depth = credited = 0
+        if self.reuse_enabled:
+            live: Optional[Set[str]] = None
+            for i in reversed(range(n)):
+                if cumulative[i] == 0:
+                    break
+                h = chain_hashes[i]
+                holder = self.registry.get(h)
+                planned = overlay is not None and h in overlay
+                if holder is None and not planned:
+                    continue
+                if reuse_id is None:
+                    reuse_id = holder if holder is not None else overlay[h]
+                    depth = i + 1
+                if planned:
+                    credited = i + 1
+                    break
+                if live is None:
+                    live = self._live_context_ids()
+                if holder in live:
+                    credited = i + 1
+                    break
+        fills: List[Tuple[List[int], int]] = []
+        marginal = 0
+        for i in range(depth, len(segment_tokens)):
+            seg = list(segment_tokens[i])
+            if seg:
+                fills.append((seg, chain_hashes[i]))
+                marginal += len(seg)
+        reused = 0
+        if reuse_id is not None and reuse_id in self.contexts:
+            reused = self._chain_tokens(self.contexts[reuse_id])
+        adopted = 0
+        if depth > credited:
+            adopted = cumulative[depth - 1] - (cumulative[credited - 1] if credited else 0)
+        return ContextPlan(reuse_id, reused, fills, marginal, adopted)
+
+    def _ancestors(self, ctx: Optional[Context]):
+        while ctx is not None:
+            yield ctx
+            ctx = self.contexts.get(ctx.parent_id) if ctx.parent_id else None
+
+    def _live_context_ids(self) -> Set[str]:
+        live: Set[str] = set()
+        for leaf in self.request_leaf.values():
+            for c in self._ancestors(self.contexts.get(leaf)):
+                if c.context_id in live:
+                    break
+                live.add(c.context_id)
+        return live
+
+    def _chain_tokens(self, ctx: Context) -> int:
+        return sum(c.token_count for c in self._ancestors(ctx))
+
+    # -- stepping (engine.py:386-484) ---------------------------------------------
+
+    def has_work(self) -> bool:
+        return bool(self.fill_queue) or any(not g.done for g in self.gens.values())
+
+    def _batch_tokens(self, running: List[GenerationTask]) -> int:
+        """Host restatement of the dedup walk; the step itself takes the
+        number from the C++ planner (they are asserted equal in tests)."""
+        if not running:
+            return 0
+        if self.cost.shared_kernel:
+            seen: Set[str] = set()
+            total = 0
+            for g in running:
+                for c in self._ancestors(self.contexts.get(g.context_id)):
+                    if c.context_id not in seen:
+                        seen.add(c.context_id)
+                        total += c.token_count
+            return total
+        return sum(self._chain_tokens(self.contexts[g.context_id]) for g in running)
+
+    def _plan(self, running: List[GenerationTask]) -> int:
+        B = len(running)
+        if B > len(self._leaf_buf):
+            self._leaf_buf = (ctypes.c_int64 * (2 * B))()
+            self._pos_buf = (ctypes.c_int64 * (2 * B))()
+        for i, g in enumerate(running):
+            self._leaf_buf[i] = self.contexts[g.context_id].uid
+        _lib.check(_lib.lib.fk_step_plan(self._pool.handle, self._leaf_buf, B,
+                                         1 if self.cost.shared_kernel else 0, self._sp(),
+                                         ctypes.byref(self.last_plan)))
+        return int(self.last_plan.batch_tokens)
+
+    def _decode_attention(self, running: List[GenerationTask]) -> None:
+        torch = self._torch
+        geo = self.geometry
+        B = len(running)
+        shape = (geo.num_layers, B, geo.num_heads, geo.head_dim)
+        with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
+            model = self.model
+            if isinstance(model, TensorDecodeModel):
+                q = model.q
+                if q.device.type != "cuda":
+                    q = q.to(self._dev, non_blocking=True)
+            else:
+                q = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
+                _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed,
+                                                     ctypes.c_void_p(q.data_ptr()), self._sp()))
+            out = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
+            f32 = torch.empty(shape, dtype=torch.float32, device=self._dev) if self.capture_f32 else None
+            layer_elems = B * geo.num_heads * geo.head_dim
+            for layer in range(geo.num_layers):
+                qp = q.data_ptr() + layer * layer_elems * 2
+                op = out.data_ptr() + layer * layer_elems * 2
+                fp = ctypes.c_void_p(f32.data_ptr() + layer * layer_elems * 4) if f32 is not None else None
+                _lib.check(_lib.lib.fk_attn_decode(self._pool.handle, layer, ctypes.c_void_p(qp),
+                                                   ctypes.c_void_p(op), fp, self._sp()))
+            self.last_output = out
+            self.last_output_f32 = f32
+            if isinstance(model, TensorDecodeModel) and model.copy_out:
+                if model.host_out is None or tuple(model.host_out.shape) != shape:
+                    model.host_out = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
+                model.host_out.copy_(out, non_blocking=True)
+        self.last_rows = [g.request_id for g in running]
+
+    def _append(self, running: List[GenerationTask], positions: List[int]) -> None:
+        torch = self._torch
+        for i, pos in enumerate(positions):
+            self._pos_buf[i] = pos
+        _lib.check(_lib.lib.fk_step_commit(self._pool.handle, self._pos_buf, self._sp()))
+        model = self.model
+        if isinstance(model, TensorDecodeModel) and model.k is not None:
+            geo = self.geometry
+            with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
+                k, v = model.k, model.v
+                if k.device.type != "cuda":
+                    k = k.to(self._dev, non_blocking=True)
+                    v = v.to(self._dev, non_blocking=True)
+                layer_bytes = len(running) * geo.num_heads * geo.head_dim * 2
+                for layer in range(geo.num_layers):
+                    _lib.check(_lib.lib.fk_append_kv(
+                        self._pool.handle, layer, ctypes.c_void_p(k.data_ptr() + layer * layer_bytes),
+                        ctypes.c_void_p(v.data_ptr() + layer * layer_bytes), self._sp()))
+        else:
+            _lib.check(_lib.lib.fk_synth_append(self._pool.handle, self.model_seed, self.model_k_scale,
+                                                self._sp()))
+
+    def _snapshot(self, running: List[GenerationTask]) -> List[List[Tuple[int, int]]]:
+        """Per row: [(context uid, tokens)] root -> leaf at plan time."""
+        rows = []
+        for g in running:
+            chain = [(c.uid, c.token_count) for c in self._ancestors(self.contexts.get(g.context_id))]
+            rows.append(list(reversed(chain)))
+        return rows
+
+    def step(self) -> Optional[StepReport]:
+        if not self.has_work():
+            return None
+        started_ns = self.clock_ns
+        emitted: Dict[str, int] = {}
+        finished: List[str] = []
+        failed: List[Tuple[str, str]] = []
+        fill_completed: List[str] = []
+
+        for g in list(self.gens.values()):  # zero-length generations (engine.py:398-402)
+            if g.started and not g.done and not g.token_ids:
+                g.done = True
+                finished.append(g.request_id)
+
+        fill_tokens = 0
+        if self.fill_queue:  # one fill chunk per step, FIFO (engine.py:404-414)
+            task = self.fill_queue.popleft()
+            fill_tokens = len(task.token_ids)
+            if task.request_id is not None:
+                left = self.pending_fills.get(task.request_id, 0) - 1
+                self.pending_fills[task.request_id] = left
+                if left <= 0:
+                    fill_completed.append(task.request_id)
+
+        running = [g for g in self.gens.values() if g.started and not g.done]
+        batch_tokens = self._plan(running) if running else 0
+        snapshot = self._snapshot(running) if (self.keep_history and running) else None
+        if running and self.device is not None:
+            self._decode_attention(running)
+            self.kv_tokens_streamed += batch_tokens
+
+        elapsed = 0
+        if fill_tokens > 0:
+            part = self.cost.fill_ns(fill_tokens)
+            elapsed += part
+            self.fill_ns_total += part
+        if running:
+            part = self.cost.iteration_ns(batch_tokens)
+            elapsed += part
+            self.decode_ns_total += part
+        self.clock_ns += elapsed
+        self.busy_ns += elapsed
+
+        positions: List[int] = []
+        for g in running:  # one token per running generation (engine.py:431-443)
+            ctx = self.contexts[g.context_id]
+            pos = ctx.token_count
+            try:
+                self.store.grow(ctx, pos + 1)
+            except OutOfMemory as exc:
+                g.done = True
+                failed.append((g.request_id, str(exc)))
+                positions.append(-1)
+                continue
+            positions.append(pos)
+            g.emitted += 1
+            emitted[g.request_id] = 1
+            if g.remaining == 0:
+                g.done = True
+                finished.append(g.request_id)
+        if running and self.device is not None:
+            self._append(running, positions)
+
+        for rid in fill_completed:  # fills done this step decode next step
+            g = self.gens.get(rid)
+            if g is not None:
+                g.started = True
+
+        self.total_emitted += len(emitted)
+        self.trace.append("t=%s engine=%s fill=%d batch=%d emitted=%d"
+                          % (format_ms(self.clock_ns), self.engine_id, fill_tokens, batch_tokens, len(emitted)))
+        report = StepReport(self.engine_id, started_ns, elapsed, fill_tokens, batch_tokens, emitted,
+                            finished, failed, fill_completed)
+        self.reports.append(report)
+        if snapshot is not None:
+            self.history.append({
+                "rows": [g.request_id for g in running],
+                "chains": snapshot,
+                "leaf_uid": [self.contexts[g.context_id].uid if g.context_id in self.contexts else -1
+                             for g in running],
+                "batch_tokens": batch_tokens,
+                "output": None if self.last_output is None else self.last_output.detach().to("cpu", copy=True),
+                "output_f32": None if self.last_output_f32 is None else self.last_output_f32.detach().to("cpu", copy=True),
+                "positions": positions,
+            })
+        return report
+
+    # -- request lifecycle (engine.py:488-538) -------------------------------------
+
+    def finish_generation(self, request_id: str) -> Optional[int]:
+        g = self.gens.pop(request_id, None)
+        if g is None:
+            return None
+        for d in (self.pending_fills, self.charges, self.holder_class, self.request_leaf):
+            d.pop(request_id, None)
+        ctx = self.contexts.get(g.context_id)
+        if ctx is None:
+            return None
+        ctx.refcount -= 1
+        if ctx.refcount == 0 and ctx.dropped:
+            self._discard_context(ctx)
+            return None
+        if not g.token_ids:
+            return None
+        seed = ctx.chain_hashes[-1] if ctx.chain_hashes else FNV64_EMPTY
+        end_hash = hash_token_ids(g.token_ids[: g.emitted], seed)
+        ctx.chain_hashes.append(end_hash)
+        if end_hash not in self.registry:
+            self.registry[end_hash] = ctx.context_id
+            ctx.registered_hashes.append(end_hash)
+        return end_hash
+
+    def cancel_request(self, request_id: str) -> None:
+        self.fill_queue = deque(t for t in self.fill_queue if t.request_id != request_id)
+        for d in (self.pending_fills, self.charges, self.holder_class, self.request_leaf):
+            d.pop(request_id, None)
+        g = self.gens.pop(request_id, None)
+        if g is None:
+            return
+        ctx = self.contexts.get(g.context_id)
+        if ctx is not None:
+            ctx.refcount -= 1
+            ctx.dropped = True
+            if ctx.refcount == 0:
+                self._discard_context(ctx)
+
+    @property
+    def charged_tokens(self) -> int:
+        return sum(self.charges.values())
+
+    def admitted_classes(self) -> List[str]:
+        return sorted(set(self.holder_class.values()))
+
+
+# Alias so a maintainer can rebind `semflow.engine.Engine = Engine`.
+Engine = GpuEngine

@@ -1,0 +1,174 @@
+"""GPU parity: decode attention through the C-ABI vs the CPU oracle.
+
+Every case builds a forest through the reference engine surface (fill /
+create_context / generate), runs real engine steps on cuda:0 (plan ->
+per-layer prefix/private/merge kernels -> one-token growth -> append) and
+compares each recorded step with the oracle's un-decomposed softmax.
+Integer side-conditions (batch_tokens == dedup walk, block ids) are
+asserted alongside.
+"""
+
+import random
+
+import numpy as np
+import pytest
+
+import paper_2405_19888_b200 as P
+from paper_2405_19888_b200 import _lib
+from paper_2405_19888_b200.workloads import fork_group, nested_forest
+
+from gpu_check import check_history
+
+pytestmark = pytest.mark.gpu
+
+
+def make_engine(cuda_device, H, L=1, shared=True, k_scale=1.0, seed=0x5EED, kv_tokens=1 << 20, **kw):
+    eng = P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=kv_tokens, device=cuda_device,
+                      geometry=P.ModelGeometry(L, H, 128), model=P.SyntheticDecodeModel(seed, k_scale),
+                      capture_f32=True, keep_history=True, **kw)
+    return eng
+
+
+def run_steps(eng, n):
+    for _ in range(n):
+        rep = eng.step()
+        if rep is None:
+            break
+        running = [g for g in eng.gens.values()]
+        assert rep.batch_tokens >= 0
+    eng.stream.synchronize()
+
+
+def assert_plan_matches_walk(eng):
+    for rec in eng.history:
+        # batch_tokens from the C++ planner == reference dedup walk over the snapshot
+        if eng.cost.shared_kernel:
+            seen = {}
+            for chain in rec["chains"]:
+                for uid, n in chain:
+                    seen[uid] = n
+            assert rec["batch_tokens"] == sum(seen.values())
+        else:
+            assert rec["batch_tokens"] == sum(n for chain in rec["chains"] for uid, n in chain)
+
+
+def test_tiny_config1(cuda_device):
+    """BASELINE config 1: 1 layer, 32x128, 1k prefix, 8 forks x 64 suffix."""
+    eng = make_engine(cuda_device, H=32)
+    fork_group(eng, 1024, [64] * 8, out_len=3)
+    run_steps(eng, 3)
+    assert eng.last_plan.num_shared_ctx == 1 and eng.last_plan.num_rows == 8
+    assert eng.history[0]["batch_tokens"] == 1024 + 8 * 64
+    w = check_history(eng)
+    assert_plan_matches_walk(eng)
+    print("tiny", w)
+
+
+def test_ragged_suffixes_cross_pages(cuda_device):
+    rng = random.Random(1)
+    eng = make_engine(cuda_device, H=4, L=2)
+    lens = [rng.randint(0, 70) for _ in range(13)] + [0, 1, 15, 16, 17]
+    fork_group(eng, 100, lens, out_len=20, seed=3)  # 100 = partial last prefix page
+    run_steps(eng, 20)
+    check_history(eng)
+    assert_plan_matches_walk(eng)
+
+
+def test_nested_three_levels(cuda_device):
+    eng = make_engine(cuda_device, H=8, L=1)
+    nested_forest(eng, root_len=300, app_len=50, n_apps=3, user_len=33, users_per_app=4, out_len=5)
+    run_steps(eng, 5)
+    assert eng.last_plan.num_shared_ctx == 4  # root + 3 apps
+    check_history(eng)
+    assert_plan_matches_walk(eng)
+
+
+def test_unshared_mode_streams_whole_chains(cuda_device):
+    eng = make_engine(cuda_device, H=8, shared=False)
+    fork_group(eng, 500, [40] * 6, out_len=4)
+    run_steps(eng, 4)
+    assert eng.last_plan.num_shared_ctx == 0
+    assert eng.history[0]["batch_tokens"] == 6 * 540
+    check_history(eng)
+
+
+def test_two_generations_on_one_leaf(cuda_device):
+    eng = make_engine(cuda_device, H=4)
+    eng.fill([1] * 200, "root", None, boundary_hash=1)
+    eng.fill([1] * 30, "leaf", "root", boundary_hash=2)
+    eng.generate("a", "leaf", [1] * 4, "")
+    eng.generate("b", "leaf", [1] * 4, "")
+    eng.fill([1] * 20, "solo", "root", boundary_hash=3)
+    eng.generate("c", "solo", [1] * 4, "")
+    run_steps(eng, 4)
+    assert eng.contexts["leaf"].token_count == 30 + 8  # both rows grow the shared leaf
+    check_history(eng)
+
+
+def test_stress_peaky_softmax(cuda_device):
+    eng = make_engine(cuda_device, H=8, k_scale=8.0)
+    fork_group(eng, 700, [50, 90, 3], out_len=3)
+    run_steps(eng, 3)
+    check_history(eng)
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_merge_by_either_kernel(cuda_device, order):
+    """launch order 1 runs the private kernel first, so the prefix kernel's
+    CTAs are the last arrivers and perform the LSE merge."""
+    eng = make_engine(cuda_device, H=4)
+    eng.set_option(_lib.FK_OPT_LAUNCH_ORDER, order)
+    fork_group(eng, 333, [7, 64, 129, 0], out_len=3)
+    run_steps(eng, 3)
+    check_history(eng)
+
+
+def test_large_fanout_multiple_query_blocks(cuda_device):
+    eng = make_engine(cuda_device, H=2)
+    fork_group(eng, 260, [5] * 150, out_len=2)  # 150 queries -> 3 blocks of 64
+    run_steps(eng, 2)
+    check_history(eng)
+
+
+def test_many_splits(cuda_device):
+    eng = make_engine(cuda_device, H=2)
+    eng.set_option(_lib.FK_OPT_MIN_SPLIT_PAGES, 1)
+    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4096)
+    fork_group(eng, 1000, [20, 21], out_len=2)
+    run_steps(eng, 2)
+    assert eng.last_plan.max_slots > 5
+    check_history(eng)
+
+
+def test_single_request_and_empty_chain(cuda_device):
+    eng = make_engine(cuda_device, H=4)
+    eng.fill([1] * 77, "only", None)
+    eng.generate("r", "only", [1] * 3, "")
+    eng.create_context("empty", None)  # zero tokens: output defined as 0
+    eng.generate("z", "empty", [1] * 2, "")
+    run_steps(eng, 3)
+    check_history(eng)
+    first = eng.history[0]
+    z = first["rows"].index("z")
+    assert np.abs(first["output"][:, z].float().numpy()).max() == 0.0
+
+
+def test_decode_oom_skips_append(cuda_device):
+    eng = make_engine(cuda_device, H=4, kv_tokens=16 * 12)
+    eng.fill([1] * 16 * 10, "root", None)
+    eng.fill([1] * 16, "a", "root")
+    eng.fill([1] * 15, "b", "root")
+    eng.generate("ra", "a", [1] * 3, "")
+    eng.generate("rb", "b", [1] * 3, "")
+    reps = [eng.step() for _ in range(3)]
+    eng.stream.synchronize()
+    assert any(r.failed for r in reps)
+    check_history(eng)
+
+
+def test_engine_pages_are_physical_and_logical_ids_monotonic(cuda_device):
+    eng = make_engine(cuda_device, H=2)
+    fork_group(eng, 64, [16, 16], out_len=1)
+    logical, physical = eng.context_pages("e0.c0")
+    assert logical == list(range(4))
+    assert len(set(physical)) == 4
