@@ -134,30 +134,68 @@ __device__ __forceinline__ long long part_index(const PlanDev& p, int H, int row
   return ((long long)row * p.max_slots + slot) * H + head;
 }
 
-// Merge all partials of (row, head) into the bf16 (and optional fp32) output.
-// Called by the CTA that arrived last on counters[row*H + head]; 128 threads,
-// one head-dim element each.  Partials are read with ld.global.cg so another
-// SM's writes (ordered by the release fence + atomic) are observed.
-__device__ __forceinline__ void merge_row_head(const ArenaDev& a, const PlanDev& p, int row, int head,
-                                               __nv_bfloat16* out, float* out_f32, int d) {
+// Number of private stream-K pieces of (row, head): how many warps' unit
+// ranges intersect the item's pages (0 when the row has no private pages).
+__device__ __forceinline__ int private_pieces(const PlanDev& p, int row, int head) {
+  const int np = p.row_priv_npages[row];
+  if (np == 0) return 0;
+  const long long a0 = (long long)p.row_unit_off[row] + (long long)head * np;
+  const long long b0 = a0 + np;
+  return (int)((b0 - 1) / p.priv_per - a0 / p.priv_per + 1);
+}
+// Arrivals the merge of (row, head) waits for: shared splits + private pieces.
+__device__ __forceinline__ int expected_arrivals(const PlanDev& p, int row, int head) {
+  return p.row_nslots[row] + private_pieces(p, row, head);
+}
+
+// Merge all partials of (row, head) into the bf16 (and optional fp32)
+// output; executed by one warp (4 head-dim elements per lane) of the unit
+// that arrived last on counters[row*H + head].  Partials are read with
+// ld.global.cg so other SMs' writes (release fence + atomic) are observed.
+__device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
+                                                    __nv_bfloat16* out, float* out_f32, int lane) {
   const int H = a.num_heads;
-  const int ns = p.row_nslots[row] + 1;
+  const int ns = expected_arrivals(p, row, head);
   float M = -INFINITY;
-  for (int k = 0; k < ns; ++k) M = fmaxf(M, __ldcg(&a.part_ml[part_index(p, H, row, k, head)].x));
-  float L = 0.f, acc = 0.f;
+  for (int k = lane; k < ns; k += 32) M = fmaxf(M, __ldcg(&a.part_ml[part_index(p, H, row, k, head)].x));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (M != -INFINITY) {
     for (int k = 0; k < ns; ++k) {
       const long long pi = part_index(p, H, row, k, head);
       const float2 ml = __ldcg(&a.part_ml[pi]);
       const float w = ex2(ml.x - M);
       L += ml.y * w;
-      acc += __ldcg(&a.part_o[pi * kHeadDim + d]) * w;
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(a.part_o + pi * kHeadDim) + lane);
+      acc.x += o.x * w;
+      acc.y += o.y * w;
+      acc.z += o.z * w;
+      acc.w += o.w * w;
     }
   }
-  const float o = L > 0.f ? acc / L : 0.f;
-  const long long oi = ((long long)row * H + head) * kHeadDim + d;
-  out[oi] = __float2bfloat16_rn(o);
-  if (out_f32) out_f32[oi] = o;
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const long long oi = ((long long)row * H + head) * kHeadDim + lane * 4;
+  const float4 r = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  *reinterpret_cast<uint2*>(out + oi) = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
+  if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = r;
+}
+
+// Release this unit's partial and arrive; returns true (warp-uniform) when
+// the caller is the last arrival and must merge.  Caller wrote its partial.
+__device__ __forceinline__ bool arrive_last_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
+                                                 int lane) {
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    const int prev = atomicAdd(&a.counters[row * a.num_heads + head], 1);
+    last = prev == expected_arrivals(p, row, head) - 1;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) __threadfence();
+  return last != 0;
 }
 
 }  // namespace fk

@@ -14,6 +14,9 @@ constexpr int kMmaQBlock = 64; // queries per mma.sync prefix CTA (4 warps x 16 
 constexpr int kTcQBlock = 128; // queries per tcgen05 prefix CTA (M = 128 rows)
 constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
 constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
+constexpr int kPrivWarpsPerCta = 8;  // private stream-K kernel: independent warps per CTA
+constexpr int kPrivStages = 3;       // per-warp smem ring depth (8 KiB K+V page per stage)
+constexpr int kPrivMinUnits = 4;     // minimum pages per private warp
 
 // Device view of one step plan.  All arrays live in one device buffer.
 struct PlanDev {
@@ -35,6 +38,12 @@ struct PlanDev {
   const int* row_nslots;       // shared slots; the private partial goes to slot row_nslots[r]
   const int* pages;            // physical page ids
   const int* page_ntok;        // valid tokens per page entry
+  // private stream-K: units = (row, head, page) in row-major order; warp w
+  // owns units [w * priv_per, (w + 1) * priv_per)
+  const int* row_unit_off;     // H * sum of private pages of earlier rows
+  int priv_units;              // U
+  int priv_per;                // units per warp
+  int priv_warps;              // G
   // synthetic keys per row
   const long long* row_uid;    // leaf context uid
   const long long* row_pos;    // leaf tokens at plan time + (rank << 40)

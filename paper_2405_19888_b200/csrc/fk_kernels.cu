@@ -17,139 +17,196 @@
 namespace fk {
 
 // =========================================================== private (n_c=1)
-constexpr int kPrivThreads = 128;
-constexpr int kPrivStages = 4;
+// Warp-granular stream-K: the private work is the unit list (row, head, page)
+// in row-major order; global warp w streams units [w*per, (w+1)*per) through
+// its own 3-stage smem ring (1-D bulk copies, 8 KiB per page: K then V), so
+// every warp moves the same number of bytes and no block barrier is needed.
+// A (row, head) item cut by a range boundary yields one partial per piece.
 constexpr int kPageBytes = kPage * kHeadDim * 2;  // 4 KiB per (page, head, K|V)
+constexpr int kPwThreads = kPrivWarpsPerCta * 32;
+constexpr int kPwStageBytes = 2 * kPageBytes;
+constexpr int kPwSmem = kPrivWarpsPerCta * kPrivStages * kPwStageBytes;
 
-__global__ void __launch_bounds__(kPrivThreads) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
-                                                                  const __nv_bfloat16* __restrict__ q,
-                                                                  __nv_bfloat16* __restrict__ out,
-                                                                  float* __restrict__ out_f32,
-                                                                  float scale_log2) {
+struct UnitCursor {
+  int row, head, page;
+};
+
+__device__ __forceinline__ UnitCursor locate_unit(const PlanDev& p, int H, int u) {
+  int lo = 0, hi = p.num_rows - 1;  // largest row with row_unit_off <= u (has pages)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (p.row_unit_off[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  const int np = p.row_priv_npages[lo];
+  const int rel = u - p.row_unit_off[lo];
+  return UnitCursor{lo, rel / np, rel % np};
+}
+
+__device__ __forceinline__ void advance_unit(const PlanDev& p, int H, UnitCursor& c) {
+  if (++c.page < p.row_priv_npages[c.row]) return;
+  c.page = 0;
+  if (++c.head < H) return;
+  c.head = 0;
+  do {
+    ++c.row;
+  } while (c.row < p.num_rows && p.row_priv_npages[c.row] == 0);
+}
+
+__global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
+                                                                   const __nv_bfloat16* __restrict__ q,
+                                                                   __nv_bfloat16* __restrict__ out,
+                                                                   float* __restrict__ out_f32,
+                                                                   float scale_log2) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kPrivStages];
-  __shared__ float s_scores[kPage];
-  __shared__ float s_comb[64][3];
-  __shared__ int s_last;
+  __shared__ uint64_t full[kPrivWarpsPerCta][kPrivStages];
+  __shared__ int s_ntok[kPrivWarpsPerCta][kPrivStages];
+  __shared__ __align__(16) float s_p[kPrivWarpsPerCta][kPage];
 
-  const int row = blockIdx.x, head = blockIdx.y, tid = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kPrivWarpsPerCta + warp;
   const int H = a.num_heads;
-  const int npages = p.row_priv_npages[row];
-  const int poff = p.row_priv_off[row];
-  const long long plane_elems = a.num_pages * kPage * kHeadDim;
-  const __nv_bfloat16* Kp = a.kv + plane_index(layer, 0, head, H) * plane_elems;
-  const __nv_bfloat16* Vp = a.kv + plane_index(layer, 1, head, H) * plane_elems;
 
-  if (tid == 0) {
-    for (int s = 0; s < kPrivStages; ++s) mbar_init(&full[s], 1);
+  // rows with no tokens at all (no private pages, no shared slot): output 0
+  for (int r = gw; r < p.num_rows; r += gridDim.x * kPrivWarpsPerCta) {
+    if (p.row_priv_npages[r] == 0 && p.row_nslots[r] == 0) {
+      for (int h = 0; h < H; ++h) {
+        const long long oi = ((long long)r * H + h) * kHeadDim + lane * 4;
+        *reinterpret_cast<uint2*>(out + oi) = make_uint2(0u, 0u);
+        if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  const int u0 = gw * p.priv_per;
+  const int u1 = min(p.priv_units, u0 + p.priv_per);
+  if (u0 >= u1) return;
+
+  uint8_t* ring = smem + warp * kPrivStages * kPwStageBytes;
+  const long long plane_elems = a.num_pages * kPage * kHeadDim;
+  if (lane == 0) {
+    for (int s = 0; s < kPrivStages; ++s) mbar_init(&full[warp][s], 1);
     fence_mbar_init();
   }
-  __syncthreads();
-  if (tid == 0) {
-    for (int i = 0; i < kPrivStages && i < npages; ++i) {
-      const int pg = p.pages[poff + i];
-      uint8_t* st = smem + i * 2 * kPageBytes;
-      mbar_expect_tx(&full[i], 2 * kPageBytes);
-      bulk_g2s(st, Kp + (long long)pg * kPage * kHeadDim, kPageBytes, &full[i]);
-      bulk_g2s(st + kPageBytes, Vp + (long long)pg * kPage * kHeadDim, kPageBytes, &full[i]);
+  __syncwarp();
+
+  UnitCursor pc = locate_unit(p, H, u0);
+  int pu = u0;
+  auto issue = [&](int s) {  // lane 0 only
+    const int e = p.row_priv_off[pc.row] + pc.page;
+    const int pg = p.pages[e];
+    s_ntok[warp][s] = p.page_ntok[e];
+    const __nv_bfloat16* kp = a.kv + plane_index(layer, 0, pc.head, H) * plane_elems + (long long)pg * kPage * kHeadDim;
+    const __nv_bfloat16* vp = a.kv + plane_index(layer, 1, pc.head, H) * plane_elems + (long long)pg * kPage * kHeadDim;
+    uint8_t* st = ring + s * kPwStageBytes;
+    mbar_expect_tx(&full[warp][s], kPwStageBytes);
+    bulk_g2s(st, kp, kPageBytes, &full[warp][s]);
+    bulk_g2s(st + kPageBytes, vp, kPageBytes, &full[warp][s]);
+  };
+  if (lane == 0) {
+    for (int s = 0; s < kPrivStages && pu < u1; ++s, ++pu) {
+      issue(s);
+      advance_unit(p, H, pc);
     }
   }
 
-  // q . k mapping: token = tid/8, 16-wide head-dim chunk = tid%8
-  const int qk_tok = tid >> 3, qk_c = tid & 7;
-  float qv[16];
-  {
-    const uint4* qs = reinterpret_cast<const uint4*>(q + ((long long)row * H + head) * kHeadDim + qk_c * 16);
-    const uint4 a0 = qs[0], a1 = qs[1];
-    const uint32_t w[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  // q . k mapping: token t = lane/2, head-dim half hh = lane%2, chunk order
+  // rotated per lane so a quarter-warp's 16-byte smem reads hit 8 distinct
+  // bank groups.
+  const int t = lane >> 1, hh = lane & 1;
+  const int rot = (t & 3) + 4 * hh;
+  float qr[64];
+  UnitCursor cc = locate_unit(p, H, u0);
+  auto load_q = [&](int row, int head) {
+    const uint4* qs = reinterpret_cast<const uint4*>(q + ((long long)row * H + head) * kHeadDim + hh * 64);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      qv[2 * i] = bf_lo(w[i]) * scale_log2;
-      qv[2 * i + 1] = bf_hi(w[i]) * scale_log2;
-    }
-  }
-  // p . v mapping: head-dim pair = tid%64, token half = tid/64
-  const int pv_pair = tid & 63, pv_half = tid >> 6;
-  float o0 = 0.f, o1 = 0.f, m = -INFINITY, l = 0.f;
-
-  for (int i = 0; i < npages; ++i) {
-    const int s = i % kPrivStages;
-    mbar_wait(&full[s], (i / kPrivStages) & 1);
-    const int ntok = p.page_ntok[poff + i];
-    const uint8_t* Ks = smem + s * 2 * kPageBytes;
-    const uint8_t* Vs = Ks + kPageBytes;
-    {
-      const uint4* kr = reinterpret_cast<const uint4*>(Ks + qk_tok * 256 + qk_c * 32);
-      const uint4 k0 = kr[0], k1 = kr[1];
-      const uint32_t w[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-      float dot = 0.f;
+      const uint4 w4 = qs[(i + rot) & 7];
+      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        dot = fmaf(qv[2 * j], bf_lo(w[j]), dot);
-        dot = fmaf(qv[2 * j + 1], bf_hi(w[j]), dot);
+      for (int j = 0; j < 4; ++j) {
+        qr[i * 8 + 2 * j] = bf_lo(w[j]) * scale_log2;
+        qr[i * 8 + 2 * j + 1] = bf_hi(w[j]) * scale_log2;
       }
-      dot += __shfl_xor_sync(0xffffffffu, dot, 4);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-      if (qk_c == 0) s_scores[qk_tok] = qk_tok < ntok ? dot : -INFINITY;
     }
-    __syncthreads();
-    float mx = -INFINITY;
+  };
+  load_q(cc.row, cc.head);
+  float m = -INFINITY, l = 0.f;
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  for (int u = u0; u < u1; ++u) {
+    const int s = (u - u0) % kPrivStages;
+    mbar_wait(&full[warp][s], ((u - u0) / kPrivStages) & 1);
+    const int ntok = s_ntok[warp][s];
+    const uint8_t* Ks = ring + s * kPwStageBytes;
+    const uint8_t* Vs = Ks + kPageBytes;
+    float dot = 0.f;
 #pragma unroll
-    for (int t = 0; t < kPage; ++t) mx = fmaxf(mx, s_scores[t]);
+    for (int i = 0; i < 8; ++i) {
+      const uint4 k4 = *reinterpret_cast<const uint4*>(Ks + t * 256 + hh * 128 + ((i + rot) & 7) * 16);
+      const uint32_t w[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dot = fmaf(qr[i * 8 + 2 * j], bf_lo(w[j]), dot);
+        dot = fmaf(qr[i * 8 + 2 * j + 1], bf_hi(w[j]), dot);
+      }
+    }
+    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+    const float sc = t < ntok ? dot : -INFINITY;
+    float mx = sc;
+#pragma unroll
+    for (int off = 2; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     const float m_new = fmaxf(m, mx);  // finite: every listed page holds >= 1 token
     const float alpha = ex2(m - m_new);
-    m = m_new;
-    float ps = 0.f, a0 = 0.f, a1 = 0.f;
+    const float pt = ex2(sc - m_new);
+    float ps = pt;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int tok = pv_half * 8 + t;
-      const float pt = ex2(s_scores[tok] - m_new);
-      ps += pt;
-      const uint32_t v = *reinterpret_cast<const uint32_t*>(Vs + tok * 256 + pv_pair * 4);
-      a0 = fmaf(pt, bf_lo(v), a0);
-      a1 = fmaf(pt, bf_hi(v), a1);
-    }
+    for (int off = 2; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
     l = l * alpha + ps;
-    o0 = o0 * alpha + a0;
-    o1 = o1 * alpha + a1;
-    __syncthreads();  // stage s and s_scores free
-    if (tid == 0 && i + kPrivStages < npages) {
-      const int pg = p.pages[poff + i + kPrivStages];
-      uint8_t* st = smem + s * 2 * kPageBytes;
-      fence_proxy_async();
-      mbar_expect_tx(&full[s], 2 * kPageBytes);
-      bulk_g2s(st, Kp + (long long)pg * kPage * kHeadDim, kPageBytes, &full[s]);
-      bulk_g2s(st + kPageBytes, Vp + (long long)pg * kPage * kHeadDim, kPageBytes, &full[s]);
+    m = m_new;
+    if (hh == 0) s_p[warp][t] = pt;
+    __syncwarp();
+    o.x *= alpha;
+    o.y *= alpha;
+    o.z *= alpha;
+    o.w *= alpha;
+#pragma unroll
+    for (int t4 = 0; t4 < 4; ++t4) {
+      const float4 p4 = *reinterpret_cast<const float4*>(&s_p[warp][t4 * 4]);
+      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint2 v = *reinterpret_cast<const uint2*>(Vs + (t4 * 4 + e) * 256 + lane * 8);
+        o.x = fmaf(pv[e], bf_lo(v.x), o.x);
+        o.y = fmaf(pv[e], bf_hi(v.x), o.y);
+        o.z = fmaf(pv[e], bf_lo(v.y), o.z);
+        o.w = fmaf(pv[e], bf_hi(v.y), o.w);
+      }
     }
-  }
-  // combine the two token halves (same running max on every thread)
-  if (pv_half == 1) {
-    s_comb[pv_pair][0] = o0;
-    s_comb[pv_pair][1] = o1;
-    s_comb[pv_pair][2] = l;
-  }
-  __syncthreads();
-  const int slot = p.row_nslots[row];
-  const long long pi = part_index(p, H, row, slot, head);
-  if (pv_half == 0) {
-    o0 += s_comb[pv_pair][0];
-    o1 += s_comb[pv_pair][1];
-    l += s_comb[pv_pair][2];
-    reinterpret_cast<float2*>(a.part_o + pi * kHeadDim)[pv_pair] = make_float2(o0, o1);
-    if (pv_pair == 0) a.part_ml[pi] = make_float2(m, l);
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const int prev = atomicAdd(&a.counters[row * H + head], 1);
-    s_last = prev == p.row_nslots[row];  // expected arrivals = nslots + 1
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    merge_row_head(a, p, row, head, out, out_f32, tid);
-    if (tid == 0) a.counters[row * H + head] = 0;
+    __syncwarp();  // stage s and s_p are free again
+    if (lane == 0 && pu < u1) {  // producer state lives in lane 0 only
+      fence_proxy_async();
+      issue(s);
+      advance_unit(p, H, pc);
+      ++pu;
+    }
+    // piece boundary: last unit of this warp or of this (row, head) item
+    const int row = cc.row, head = cc.head;
+    advance_unit(p, H, cc);
+    if (u + 1 == u1 || cc.page == 0) {
+      const int np = p.row_priv_npages[row];
+      const int first = (p.row_unit_off[row] + head * np) / p.priv_per;
+      const int slot = p.row_nslots[row] + (gw - first);
+      const long long pi = part_index(p, H, row, slot, head);
+      reinterpret_cast<float4*>(a.part_o + pi * kHeadDim)[lane] = o;
+      if (lane == 0) a.part_ml[pi] = make_float2(m, l);
+      if (arrive_last_warp(a, p, row, head, lane)) {
+        merge_row_head_warp(a, p, row, head, out, out_f32, lane);
+        if (lane == 0) a.counters[row * H + head] = 0;
+      }
+      m = -INFINITY;
+      l = 0.f;
+      o = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u + 1 < u1) load_q(cc.row, cc.head);
+    }
   }
 }
 
@@ -278,7 +335,9 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
       const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);
       m0 = mn0;
       m1 = mn1;
-      uint32_t pa[4][4];
+      // P = hi + lo, both bf16: the P.V product keeps ~16 mantissa bits
+      // (a single bf16 P costs ~1.3e-3 mean-rel, above the 1e-3 bound)
+      uint32_t pa[4][4], pl[4][4];
       float ps0 = 0.f, ps1 = 0.f;
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
@@ -286,8 +345,11 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
         const float p2 = ex2(sc[nt][2] - mn1), p3 = ex2(sc[nt][3] - mn1);
         ps0 += p0 + p1;
         ps1 += p2 + p3;
-        pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
-        pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+        const uint32_t h01 = pack_bf16(p0, p1), h23 = pack_bf16(p2, p3);
+        pa[nt >> 1][(nt & 1) * 2 + 0] = h01;
+        pa[nt >> 1][(nt & 1) * 2 + 1] = h23;
+        pl[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0 - bf_lo(h01), p1 - bf_hi(h01));
+        pl[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2 - bf_lo(h23), p3 - bf_hi(h23));
       }
       l0 = l0 * al0 + ps0;
       l1 = l1 * al1 + ps1;
@@ -307,6 +369,8 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
           ldsm_x4_t(Vb + sw128(tok, 2 * dp + (mi >> 1)), b0, b1, b2, b3);
           mma_bf16(o[2 * dp], pa[kt2], b0, b1);
           mma_bf16(o[2 * dp + 1], pa[kt2], b2, b3);
+          mma_bf16(o[2 * dp], pl[kt2], b0, b1);
+          mma_bf16(o[2 * dp + 1], pl[kt2], b2, b3);
         }
       }
     }
@@ -343,16 +407,16 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
   if (tid < nq) {
     const int row = s_rows[tid];
     const int prev = atomicAdd(&a.counters[row * H + head], 1);
-    if (prev == p.row_nslots[row]) s_merge[atomicAdd(&s_nmerge, 1)] = row;
+    if (prev == expected_arrivals(p, row, head) - 1) s_merge[atomicAdd(&s_nmerge, 1)] = row;
   }
   __syncthreads();
   const int nm = s_nmerge;
   if (nm > 0) {
     __threadfence();
-    for (int k = 0; k < nm; ++k) {
+    for (int k = warp; k < nm; k += kPmThreads / 32) {
       const int row = s_merge[k];
-      merge_row_head(a, p, row, head, out, out_f32, tid);
-      if (tid == 0) a.counters[row * H + head] = 0;
+      merge_row_head_warp(a, p, row, head, out, out_f32, lane);
+      if (lane == 0) a.counters[row * H + head] = 0;
     }
   }
 }
@@ -430,9 +494,15 @@ __global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long
 // ============================================================== launchers
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, void* out,
                            float* out_f32, float scale_log2, cudaStream_t s) {
-  dim3 grid(p.num_rows, a.num_heads);
-  fk_private_kernel<<<grid, kPrivThreads, kPrivStages * 2 * kPageBytes, s>>>(
-      a, p, layer, (const __nv_bfloat16*)q, (__nv_bfloat16*)out, out_f32, scale_log2);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fk_private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPwSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = (p.priv_warps + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta;
+  fk_private_kernel<<<grid, kPwThreads, kPwSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
+                                                      out_f32, scale_log2);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -549,8 +550,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       auto si = shared_idx.find(c);
       if (si != shared_idx.end()) nslots[r] += shared[si->second].splits;
     }
+  // private stream-K geometry (filled after the private page lists below)
   int max_slots = 1;
-  for (int r = 0; r < B; ++r) max_slots = std::max(max_slots, nslots[r] + 1);
 
   // host arrays
   std::vector<int32_t> pages, page_ntok, qrows;
@@ -617,6 +618,29 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     }
     row_priv_np[r] = (int32_t)pages.size() - row_priv_off[r];
   }
+  // private stream-K: units (row, head, page); warps own equal unit ranges
+  std::vector<int32_t> row_unit_off(B);
+  int64_t U = 0;
+  for (int r = 0; r < B; ++r) {
+    row_unit_off[r] = (int32_t)U;
+    U += (int64_t)row_priv_np[r] * H;
+  }
+  if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
+  int64_t G = std::min<int64_t>((int64_t)p->num_sms * kPrivWarpsPerCta,
+                                (U + kPrivMinUnits - 1) / kPrivMinUnits);
+  G = std::max<int64_t>(G, 1);
+  G = (G + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta * kPrivWarpsPerCta;
+  const int64_t per = std::max<int64_t>(1, (U + G - 1) / G);
+  for (int r = 0; r < B; ++r) {
+    int maxp = 0;
+    const int64_t np = row_priv_np[r];
+    if (np > 0)
+      for (int64_t h = 0; h < H; ++h) {
+        const int64_t a0 = row_unit_off[r] + h * np, b0 = a0 + np;
+        maxp = std::max<int>(maxp, (int)((b0 - 1) / per - a0 / per + 1));
+      }
+    max_slots = std::max(max_slots, nslots[r] + maxp);
+  }
   // synthetic keys: (leaf uid, leaf tokens at plan time + rank << 40)
   std::vector<int64_t> row_uid(B), row_pos(B);
   p->plan_leaves.assign(leaves, leaves + B);
@@ -657,7 +681,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   Layout L;
   const size_t o_it = L.add(sizeof(int32_t) * 6 * std::max(n_items, 1));
   const size_t o_q = L.add(sizeof(int32_t) * std::max<size_t>(qrows.size(), 1));
-  const size_t o_rows = L.add(sizeof(int32_t) * 3 * std::max(B, 1));
+  const size_t o_rows = L.add(sizeof(int32_t) * 4 * std::max(B, 1));
   const size_t o_pages = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
   const size_t o_pnt = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
   const size_t o_uid = L.add(sizeof(int64_t) * std::max(B, 1));
@@ -695,6 +719,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     rb[0 * nb + r] = row_priv_off[r];
     rb[1 * nb + r] = row_priv_np[r];
     rb[2 * nb + r] = nslots[r];
+    rb[3 * nb + r] = row_unit_off[r];
   }
   put(o_pages, pages.data(), pages.size() * 4);
   put(o_pnt, page_ntok.data(), page_ntok.size() * 4);
@@ -726,6 +751,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
   pd.row_nslots = drb + 2 * nb;
+  pd.row_unit_off = drb + 3 * nb;
+  pd.priv_units = (int)U;
+  pd.priv_per = (int)per;
+  pd.priv_warps = (int)G;
   pd.pages = (const int32_t*)(d + o_pages);
   pd.page_ntok = (const int32_t*)(d + o_pnt);
   pd.row_uid = (const long long*)(d + o_uid);

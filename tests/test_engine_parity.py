@@ -1,0 +1,171 @@
+"""Integer parity of the drop-in engine (host-only mode, native C++ pool)
+against the reference Engine: recorded op streams (golden fixtures made by
+tests/golden/make_golden.py on semflow.engine.Engine), live random streams,
+the reference's own engine/manager/acceptance suites with `Engine` rebound,
+and manager-driven workloads (reports, traces, peak blocks)."""
+
+import json
+import os
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+import paper_2405_19888_b200 as P
+import streams
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+REF = os.environ.get("FK_REFERENCE", "/root/reference/pkg/src")
+REF_TESTS = os.path.join(os.path.dirname(REF), "tests")
+
+
+def gpu_engine_factory(kv, shared):
+    return P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=kv)
+
+
+def normalise(rec):
+    return json.loads(json.dumps(rec))
+
+
+def test_golden_streams_bit_exact():
+    data = json.load(open(os.path.join(GOLDEN, "engine_streams.json")))
+    assert len(data) >= 20
+    outcomes = set()
+    for case in data:
+        got = normalise(streams.record_stream(gpu_engine_factory, case["spec"]))
+        want = case["record"]
+        for i, (g, w) in enumerate(zip(got, want)):
+            assert g == w, (case["spec"]["seed"], i, case["spec"]["ops"][i] if i < len(case["spec"]["ops"]) else "final")
+        assert len(got) == len(want)
+        outcomes.update(r[0][1] if r[0][0] == "err" else "ok" for r in want[:-1])
+    # the streams exercise every engine error path
+    assert {"ok", "OutOfMemory", "UnknownContext", "UnknownParentContext", "ContextBusy"} <= outcomes
+
+
+@pytest.mark.reference
+def test_live_random_streams_match_reference():
+    from semflow.engine import CostModel, Engine
+
+    for seed in range(40):
+        spec = streams.make_ops(50_000 + seed, 120)
+        want = normalise(streams.record_stream(
+            lambda kv, sk: Engine("e0", CostModel(shared_kernel=sk), kv_tokens=kv), spec))
+        got = normalise(streams.record_stream(gpu_engine_factory, spec))
+        assert got == want, seed
+
+
+@pytest.mark.reference
+def test_reference_suites_with_engine_rebound(tmp_path):
+    """The reference's own hot-path tests (engine, tokenizer, prefix,
+    manager, experiments, acceptance) run with semflow's Engine replaced by
+    GpuEngine (the substitution point manager.py:130-139)."""
+    names = ["test_engine.py", "test_acceptance.py", "test_manager.py", "test_experiments.py",
+             "test_prefix.py", "test_tokenizer.py"]
+    (tmp_path / "fk_rebind.py").write_text(textwrap.dedent(f"""
+        import sys
+        sys.path.insert(0, {REF!r})
+        sys.path.insert(0, {REF_TESTS!r})
+        sys.path.insert(0, {ROOT!r})
+        import semflow.engine as se
+        import semflow.manager as sm
+        import paper_2405_19888_b200 as P
+        assert P.errors.REFERENCE_ERRORS
+        se.Engine = P.GpuEngine
+        sm.Engine = P.GpuEngine
+
+        def pytest_sessionfinish(session, exitstatus):
+            assert sm.Engine is P.GpuEngine
+    """))
+    env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", PYTHONPATH=str(tmp_path))
+    args = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "fk_rebind",
+            "--rootdir", str(tmp_path), "-c", os.devnull] + [os.path.join(REF_TESTS, n) for n in names]
+    res = subprocess.run(args, cwd=tmp_path, capture_output=True, text=True, env=env, timeout=900)
+    tail = res.stdout[-2000:]
+    assert res.returncode == 0, tail + res.stderr[-2000:]
+    assert " passed" in tail and "failed" not in tail
+
+
+@pytest.mark.reference
+def test_manager_workloads_match_golden_plans():
+    """Manager-driven workloads: per-engine StepReports, traces and peaks
+    identical to the reference run recorded in plans.json."""
+    import semflow.manager as sm
+    from semflow.config import Config
+    from semflow.experiments import run_workload_manager
+    from semflow.workloads import mapreduce_summary, shared_prompt_serving
+
+    golden = json.load(open(os.path.join(GOLDEN, "plans.json")))
+    cases = {
+        "shared_prompt_small": (shared_prompt_serving(1, users=12, system_prompt_len=600, unique_len=40,
+                                                      output_len=30), Config(total_blocks=4000)),
+        "mapreduce_small": (mapreduce_summary(2, maps=4, chunk_size=300, output_len=20), Config(total_blocks=4000)),
+        "shared_prompt_2eng": (shared_prompt_serving(3, users=8, system_prompt_len=300, unique_len=20,
+                                                     output_len=16), Config(engines=2, total_blocks=4000)),
+    }
+    saved = sm.Engine
+    sm.Engine = P.GpuEngine
+    try:
+        for name, (wl, cfg) in cases.items():
+            mgr, _, end_ns = run_workload_manager(wl, "semflow", cfg)
+            assert all(isinstance(e, P.GpuEngine) for e in mgr.engines.values())
+            got = {"end_ns": end_ns,
+                   "engines": {eid: {"reports": [streams.report_tuple(r) for r in e.reports],
+                                     "trace": list(e.trace), "peak": e.store.peak_used}
+                               for eid, e in sorted(mgr.engines.items())}}
+            assert normalise(got) == golden[name], name
+    finally:
+        sm.Engine = saved
+
+
+@pytest.mark.reference
+def test_shared_prefix_memory_acceptance_pin():
+    """test_acceptance.py:65-83: peak 1975 blocks shared vs 25,600 unshared."""
+    import semflow.manager as sm
+    from semflow.config import Config
+    from semflow.experiments import run_experiment
+    from semflow.workloads import shared_prompt_serving
+
+    saved = sm.Engine
+    sm.Engine = P.GpuEngine
+    try:
+        wl = shared_prompt_serving(1, users=64, system_prompt_len=6000, unique_len=200, output_len=200)
+        sf = run_experiment(wl, "semflow", Config(total_blocks=30_000))
+        tc = run_experiment(wl, "throughput-centric", Config(total_blocks=30_000))
+    finally:
+        sm.Engine = saved
+    assert sf["aggregates"]["peak_blocks_total"] == 1975
+    assert tc["aggregates"]["peak_blocks_total"] == 25_600
+
+
+def test_engine_unit_pins():
+    """test_engine.py:32-43 pins restated against the drop-in directly."""
+    eng = P.GpuEngine("e0", P.CostModel())
+    eng.fill([1] * 6000, "root", None, boundary_hash=11)
+    eng.fill([1] * 200, "kid_a", "root", boundary_hash=12)
+    eng.fill([1] * 200, "kid_b", "root", boundary_hash=13)
+    assert eng.store.used_blocks == 375 + 13 + 13
+    assert eng.store.peak_used == 401
+    assert eng.contexts["root"].refcount == 2
+    assert eng.contexts["kid_a"].chain_hashes == [11, 12]
+    assert eng._chain_tokens(eng.contexts["kid_a"]) == 6200
+    logical, physical = eng.context_pages("root")
+    assert logical == list(range(375)) and physical == [-1] * 375  # host-only: no device pages
+
+
+def test_shared_kernel_dedup_counts():
+    """test_engine.py:173-194: batch_tokens 1000+2k shared vs 2000+2k."""
+    for shared, base in ((True, 1000), (False, 2000)):
+        eng = P.GpuEngine("e0", P.CostModel(shared_kernel=shared))
+        eng.fill([1] * 1000, "root", None, boundary_hash=9)
+        eng.step()
+        eng.create_context("a", "root")
+        eng.create_context("b", "root")
+        eng.generate("ra", "a", [1] * 5, "v")
+        eng.generate("rb", "b", [1] * 5, "v")
+        reps = []
+        while any(not g.done for g in eng.gens.values()):
+            reps.append(eng.step())
+        assert [r.batch_tokens for r in reps] == [base + 2 * k for k in range(5)]
+        assert all(r.batch_tokens == eng._batch_tokens([]) + r.batch_tokens for r in reps)

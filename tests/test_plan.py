@@ -1,0 +1,80 @@
+"""Work-list planner (fk_step_plan) on host-only pools: the work-list
+invariant sum(tokens of prefix items and private streams) == the reference
+dedup count _batch_tokens (engine.py:470-484), in both shared_kernel modes,
+over random forests; the oracle twin agrees."""
+
+import random
+
+import pytest
+
+import paper_2405_19888_b200 as P
+from oracle import forkattn_oracle as O
+
+
+def random_forest(seed, shared=True):
+    rng = random.Random(seed)
+    eng = P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=1 << 22)
+    twin = O.BlockTwin(16, -(-(1 << 22) // 16))
+    ids = []
+    for i in range(rng.randint(1, 40)):
+        parent = rng.choice(ids) if ids and rng.random() < 0.7 else None
+        cid = f"c{i}"
+        n = rng.choice([0, 1, 15, 16, 17, rng.randint(0, 600)])
+        eng.fill([1] * n, cid, parent)
+        twin.create(cid, parent)
+        assert twin.grow(cid, n)
+        ids.append(cid)
+    leaves = []
+    for j in range(rng.randint(1, 30)):
+        leaf = rng.choice(ids)
+        eng.generate(f"r{j}", leaf, [1] * 3, "")
+        leaves.append(leaf)
+    return eng, twin, leaves
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_plan_batch_tokens_matches_walk_and_twin(shared):
+    for seed in range(60):
+        eng, twin, leaves = random_forest(seed, shared)
+        running = [g for g in eng.gens.values() if g.started and not g.done]
+        bt = eng._plan(running)
+        info = eng.last_plan
+        assert bt == eng._batch_tokens(running) == twin.batch_tokens(leaves, shared)
+        assert info.num_rows == len(running)
+        if shared:
+            assert info.shared_tokens + info.private_tokens == bt
+        else:
+            assert info.num_shared_ctx == 0 and info.private_tokens == bt
+        assert info.max_slots >= 1
+
+
+def test_block_ids_match_twin():
+    eng, twin, _ = random_forest(7)
+    for cid in twin.blocks:
+        assert eng.contexts[cid].block_ids == twin.blocks[cid]
+    st = eng.pool_stats()
+    assert st.used_blocks == twin.used and st.peak_used == twin.peak
+
+
+def test_headline_plan_shape():
+    """LLaMA-13B headline: one 6000-token prefix shared by 64 forks of 256."""
+    eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 22, geometry=P.LLAMA_13B)
+    from paper_2405_19888_b200.workloads import fork_group
+
+    fork_group(eng, 6000, [256] * 64, out_len=2)
+    running = list(eng.gens.values())
+    assert eng._plan(running) == 6000 + 64 * 256 == 22384
+    info = eng.last_plan
+    assert info.num_shared_ctx == 1 and info.shared_tokens == 6000 and info.private_tokens == 64 * 256
+    # prefix split into about one wave of CTAs
+    assert 40 <= info.num_prefix_ctas <= 2 * 148
+
+
+def test_nested_plan_counts_every_level_once():
+    eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 22)
+    from paper_2405_19888_b200.workloads import nested_forest
+
+    nested_forest(eng, 4096, 1024, 8, 256, 8, out_len=2)
+    running = list(eng.gens.values())
+    assert eng._plan(running) == 4096 + 8 * 1024 + 64 * 256
+    assert eng.last_plan.num_shared_ctx == 9
