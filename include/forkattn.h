@@ -141,6 +141,10 @@ int fk_step_commit(fk_pool* pool, const int64_t* positions, void* stream);
  * into their (page, slot) targets; rows with position -1 are skipped. */
 int fk_append_kv(fk_pool* pool, int32_t layer, const void* k, const void* v,
                  void* stream);
+/* Same for layers [layer0, layer0 + nlayers) in one launch: k/v are
+ * [nlayers][num_rows][H][D] bf16. */
+int fk_append_kv_layers(fk_pool* pool, int32_t layer0, int32_t nlayers,
+                        const void* k, const void* v, void* stream);
 
 /* ---- synthetic model (deterministic KV / Q; the oracle restates it) ------ */
 /* Fill tokens [pos0, pos1) of ctx for every layer/head with the counter-hash

@@ -89,6 +89,7 @@ SIGNATURES = [
     ("fk_attn_decode", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("fk_step_commit", c_int32, [c_void_p, POINTER(c_int64), c_void_p]),
     ("fk_append_kv", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    ("fk_append_kv_layers", c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("fk_synth_fill", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_float, c_void_p]),
     ("fk_synth_queries", c_int32, [c_void_p, c_uint64, c_void_p, c_void_p]),
     ("fk_synth_append", c_int32, [c_void_p, c_uint64, c_float, c_void_p]),

@@ -39,8 +39,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Watchdog: a pipeline bug must fail the launch, not hang the GPU.
+constexpr uint64_t kWaitLimitNs = 10ull * 1000 * 1000 * 1000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = global_ns();
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if ((++n & 1023u) == 0 && global_ns() - t0 > kWaitLimitNs) __trap();
   }
 }
 // 1-D bulk copy global -> shared, completion on an mbarrier (SASS: UBLKCP).
@@ -134,28 +145,18 @@ __device__ __forceinline__ long long part_index(const PlanDev& p, int H, int row
   return ((long long)row * p.max_slots + slot) * H + head;
 }
 
-// Number of private stream-K pieces of (row, head): how many warps' unit
-// ranges intersect the item's pages (0 when the row has no private pages).
-__device__ __forceinline__ int private_pieces(const PlanDev& p, int row, int head) {
-  const int np = p.row_priv_npages[row];
-  if (np == 0) return 0;
-  const long long a0 = (long long)p.row_unit_off[row] + (long long)head * np;
-  const long long b0 = a0 + np;
-  return (int)((b0 - 1) / p.priv_per - a0 / p.priv_per + 1);
-}
-// Arrivals the merge of (row, head) waits for: shared splits + private pieces.
-__device__ __forceinline__ int expected_arrivals(const PlanDev& p, int row, int head) {
-  return p.row_nslots[row] + private_pieces(p, row, head);
+// Partials the merge of (row, head) combines (shared pieces + private pieces).
+__device__ __forceinline__ int partial_count(const PlanDev& p, int H, int row, int head) {
+  return p.row_head_count[(long long)row * H + head];
 }
 
 // Merge all partials of (row, head) into the bf16 (and optional fp32)
-// output; executed by one warp (4 head-dim elements per lane) of the unit
-// that arrived last on counters[row*H + head].  Partials are read with
-// ld.global.cg so other SMs' writes (release fence + atomic) are observed.
+// output; one warp, 4 head-dim elements per lane.  Rows with no token at
+// all (no partial) produce zeros.
 __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
                                                     __nv_bfloat16* out, float* out_f32, int lane) {
   const int H = a.num_heads;
-  const int ns = expected_arrivals(p, row, head);
+  const int ns = partial_count(p, H, row, head);
   float M = -INFINITY;
   for (int k = lane; k < ns; k += 32) M = fmaxf(M, __ldcg(&a.part_ml[part_index(p, H, row, k, head)].x));
 #pragma unroll
@@ -180,22 +181,6 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
   const float4 r = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   *reinterpret_cast<uint2*>(out + oi) = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
   if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = r;
-}
-
-// Release this unit's partial and arrive; returns true (warp-uniform) when
-// the caller is the last arrival and must merge.  Caller wrote its partial.
-__device__ __forceinline__ bool arrive_last_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
-                                                 int lane) {
-  __threadfence();
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) {
-    const int prev = atomicAdd(&a.counters[row * a.num_heads + head], 1);
-    last = prev == expected_arrivals(p, row, head) - 1;
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (last) __threadfence();
-  return last != 0;
 }
 
 }  // namespace fk

@@ -19,29 +19,41 @@ constexpr int kPrivStages = 3;       // per-warp smem ring depth (8 KiB K+V page
 constexpr int kPrivMinUnits = 4;     // minimum pages per private warp
 
 // Device view of one step plan.  All arrays live in one device buffer.
+// Partials of (row, head) live at slots [0, row_head_count): shared-prefix
+// pieces first (root -> leaf), then the private pieces from row_head_base.
 struct PlanDev {
   int num_rows;
   int max_slots;
-  int num_items;        // prefix work items (context x split x query block)
+  int num_items;        // prefix items; each is (context, split|-, query block, head)
   int tc_begin;         // items [0, tc_begin) -> mma.sync kernel, [tc_begin, num_items) -> tcgen05
   // prefix items (SoA)
-  const int* it_page_off;  // offset into pages[]
+  const int* it_page_off;  // offset into pages[] of the item's first page
   const int* it_npages;
-  const int* it_ntok;      // valid tokens in this item (contiguous from its first page)
+  const int* it_ntok;      // valid tokens in the item (contiguous from its first page)
   const int* it_q_off;     // offset into qrows[]
   const int* it_nq;
-  const int* it_slot;      // partial slot of these queries
+  const int* it_head;
+  const int* it_unit_off;  // tcgen05 stream-K: first tile unit of the item
+  const int* it_qslot_off; // offset into qslot[]
+  const int* it_units;     // 128-token tiles of the item
   const int* qrows;        // request rows
+  const int* qslot;        // slot of piece 0 for each (item, query)
+  int tc_units, tc_per, tc_ctas;  // tcgen05 stream-K geometry
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;
-  const int* row_nslots;       // shared slots; the private partial goes to slot row_nslots[r]
+  const int* row_unit_off;     // row's first entry in the flat private list
+  const int* row_head_base;    // [rows][H] slot of private piece 0
+  const int* row_head_count;   // [rows][H] partials the merge combines
   const int* pages;            // physical page ids
   const int* page_ntok;        // valid tokens per page entry
-  // private stream-K: units = (row, head, page) in row-major order; warp w
-  // owns units [w * priv_per, (w + 1) * priv_per)
-  const int* row_unit_off;     // H * sum of private pages of earlier rows
-  int priv_units;              // U
+  // private stream-K: units u in [0, H * priv_np) = (head, flat private page
+  // entry e): head = u / priv_np, entry = priv_base + u % priv_np.  Global
+  // warp w owns units [w * priv_per, (w + 1) * priv_per).
+  const int* page_row;         // row of each flat private entry
+  int priv_base;               // offset of the private entries in pages[]
+  int priv_np;                 // number of private page entries (NPT)
+  int priv_units;              // U = H * NPT
   int priv_per;                // units per warp
   int priv_warps;              // G
   // synthetic keys per row
@@ -61,7 +73,6 @@ struct ArenaDev {
   int num_heads;
   float* part_o;          // [rows][max_slots][H][D]
   float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
-  int* counters;          // [rows][H] arrivals, reset by the merging CTA
 };
 
 inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {
@@ -69,18 +80,15 @@ inline __host__ __device__ long long plane_index(int layer, int kv, int head, in
 }
 
 // Launchers (fk_kernels.cu).  All return cudaError_t of the launch.
-cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer,
-                           const void* q, void* out, float* out_f32,
-                           float scale_log2, cudaStream_t s);
-cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer,
-                              const void* q, void* out, float* out_f32,
-                              float scale_log2, const CUtensorMap* tmap,
-                              cudaStream_t s);
-cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer,
-                             const void* q, void* out, float* out_f32,
-                             float scale_log2, const CUtensorMap* tmap,
-                             cudaStream_t s);
-cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer,
+cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
+                           float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
+cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
+                              float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
+cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
+                             float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
+cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32,
+                         cudaStream_t s);
+cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers,
                           const void* k, const void* v, cudaStream_t s);
 cudaError_t launch_synth_fill(const ArenaDev& a, const int* pages_dev, int npages_first,
                               long long uid, long long pos0, long long pos1,

@@ -17,195 +17,227 @@
 namespace fk {
 
 // =========================================================== private (n_c=1)
-// Warp-granular stream-K: the private work is the unit list (row, head, page)
-// in row-major order; global warp w streams units [w*per, (w+1)*per) through
-// its own 3-stage smem ring (1-D bulk copies, 8 KiB per page: K then V), so
-// every warp moves the same number of bytes and no block barrier is needed.
-// A (row, head) item cut by a range boundary yields one partial per piece.
-constexpr int kPageBytes = kPage * kHeadDim * 2;  // 4 KiB per (page, head, K|V)
+// Warp-granular stream-K over units u = (head, flat private page entry):
+// global warp w streams units [w*per, (w+1)*per) through its own smem ring
+// (TMA, SWIZZLE_128B boxes {64 dims, 16 tokens}: K lo/hi, V lo/hi = 8 KiB per
+// page), so every warp moves the same bytes and no block barrier exists.
+// Per page: S = q.K^T and O += P.V on mma.sync m16n8k16 with the single query
+// in row 0 (the tensor pipe replaces ~400 CUDA-core instructions per page),
+// online softmax on the row-0 fragments, P split hi+lo in bf16.
+// An item (row, head) cut by a range boundary yields one partial per piece.
 constexpr int kPwThreads = kPrivWarpsPerCta * 32;
-constexpr int kPwStageBytes = 2 * kPageBytes;
-constexpr int kPwSmem = kPrivWarpsPerCta * kPrivStages * kPwStageBytes;
+constexpr int kPwStageBytes = 8192;
+constexpr int kPwSmem = kPrivWarpsPerCta * kPrivStages * kPwStageBytes + 1024;
 
-struct UnitCursor {
-  int row, head, page;
+// byte offset of (token row 0..15, 16-byte chunk 0..15) in one K or V page
+// held as two SWIZZLE_128B boxes of 16 rows x 128 B
+__device__ __forceinline__ uint32_t sw_page(int row, int c16) {
+  return (uint32_t)((c16 >> 3) * 2048 + row * 128 + (((c16 & 7) ^ (row & 7)) << 4));
+}
+
+struct UnitMeta {
+  int pg, ntok, row, head;
 };
 
-__device__ __forceinline__ UnitCursor locate_unit(const PlanDev& p, int H, int u) {
-  int lo = 0, hi = p.num_rows - 1;  // largest row with row_unit_off <= u (has pages)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (p.row_unit_off[mid] <= u) lo = mid; else hi = mid - 1;
-  }
-  const int np = p.row_priv_npages[lo];
-  const int rel = u - p.row_unit_off[lo];
-  return UnitCursor{lo, rel / np, rel % np};
-}
-
-__device__ __forceinline__ void advance_unit(const PlanDev& p, int H, UnitCursor& c) {
-  if (++c.page < p.row_priv_npages[c.row]) return;
-  c.page = 0;
-  if (++c.head < H) return;
-  c.head = 0;
-  do {
-    ++c.row;
-  } while (c.row < p.num_rows && p.row_priv_npages[c.row] == 0);
-}
-
+// Streaming warps only write partials; fk_merge_kernel combines them.
 __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
-                                                                   __nv_bfloat16* __restrict__ out,
-                                                                   float* __restrict__ out_f32,
-                                                                   float scale_log2) {
-  extern __shared__ __align__(128) uint8_t smem[];
+                                                                   float scale_log2,
+                                                                   const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kPrivWarpsPerCta][kPrivStages];
-  __shared__ int s_ntok[kPrivWarpsPerCta][kPrivStages];
-  __shared__ __align__(16) float s_p[kPrivWarpsPerCta][kPage];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kPrivWarpsPerCta + warp;
   const int H = a.num_heads;
 
-  // rows with no tokens at all (no private pages, no shared slot): output 0
-  for (int r = gw; r < p.num_rows; r += gridDim.x * kPrivWarpsPerCta) {
-    if (p.row_priv_npages[r] == 0 && p.row_nslots[r] == 0) {
-      for (int h = 0; h < H; ++h) {
-        const long long oi = ((long long)r * H + h) * kHeadDim + lane * 4;
-        *reinterpret_cast<uint2*>(out + oi) = make_uint2(0u, 0u);
-        if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-  }
+  // ---------------------------------------------------- streaming warps
+  const int g = lane >> 2, t4 = lane & 3;
+  const int gw = blockIdx.x * kPrivWarpsPerCta + warp;
+  const int NPT = p.priv_np;
   const int u0 = gw * p.priv_per;
   const int u1 = min(p.priv_units, u0 + p.priv_per);
   if (u0 >= u1) return;
 
   uint8_t* ring = smem + warp * kPrivStages * kPwStageBytes;
-  const long long plane_elems = a.num_pages * kPage * kHeadDim;
   if (lane == 0) {
+    prefetch_tmap(&tmap);
     for (int s = 0; s < kPrivStages; ++s) mbar_init(&full[warp][s], 1);
     fence_mbar_init();
   }
   __syncwarp();
 
-  UnitCursor pc = locate_unit(p, H, u0);
-  int pu = u0;
-  auto issue = [&](int s) {  // lane 0 only
-    const int e = p.row_priv_off[pc.row] + pc.page;
-    const int pg = p.pages[e];
-    s_ntok[warp][s] = p.page_ntok[e];
-    const __nv_bfloat16* kp = a.kv + plane_index(layer, 0, pc.head, H) * plane_elems + (long long)pg * kPage * kHeadDim;
-    const __nv_bfloat16* vp = a.kv + plane_index(layer, 1, pc.head, H) * plane_elems + (long long)pg * kPage * kHeadDim;
-    uint8_t* st = ring + s * kPwStageBytes;
-    mbar_expect_tx(&full[warp][s], kPwStageBytes);
-    bulk_g2s(st, kp, kPageBytes, &full[warp][s]);
-    bulk_g2s(st + kPageBytes, vp, kPageBytes, &full[warp][s]);
-  };
-  if (lane == 0) {
-    for (int s = 0; s < kPrivStages && pu < u1; ++s, ++pu) {
-      issue(s);
-      advance_unit(p, H, pc);
+  // unit metadata, 64-unit window held lane-parallel in registers
+  auto load_meta = [&](int ub) {
+    UnitMeta m{0, 0, 0, 0};
+    const int u = ub + lane;
+    if (u < u1) {
+      const int e = u % NPT;
+      m.head = u / NPT;
+      m.pg = p.pages[p.priv_base + e];
+      m.ntok = p.page_ntok[p.priv_base + e];
+      m.row = p.page_row[e];
     }
+    return m;
+  };
+  int wbase = u0;
+  UnitMeta lo = load_meta(wbase), hi = load_meta(wbase + 32);
+  auto meta = [&](int u) {  // warp-uniform u in [wbase, wbase + 64)
+    const int idx = u - wbase;
+    const int src = idx & 31;
+    UnitMeta a0, b0;
+    a0.pg = __shfl_sync(0xffffffffu, lo.pg, src);
+    a0.ntok = __shfl_sync(0xffffffffu, lo.ntok, src);
+    a0.row = __shfl_sync(0xffffffffu, lo.row, src);
+    a0.head = __shfl_sync(0xffffffffu, lo.head, src);
+    b0.pg = __shfl_sync(0xffffffffu, hi.pg, src);
+    b0.ntok = __shfl_sync(0xffffffffu, hi.ntok, src);
+    b0.row = __shfl_sync(0xffffffffu, hi.row, src);
+    b0.head = __shfl_sync(0xffffffffu, hi.head, src);
+    return idx < 32 ? a0 : b0;
+  };
+  auto issue = [&](int s, const UnitMeta& m) {  // lane 0 only
+    uint8_t* st = ring + s * kPwStageBytes;
+    const int pk = (int)plane_index(layer, 0, m.head, H), pv = (int)plane_index(layer, 1, m.head, H);
+    mbar_expect_tx(&full[warp][s], kPwStageBytes);
+    tma_load_3d(st, &tmap, 0, m.pg * kPage, pk, &full[warp][s]);
+    tma_load_3d(st + 2048, &tmap, 64, m.pg * kPage, pk, &full[warp][s]);
+    tma_load_3d(st + 4096, &tmap, 0, m.pg * kPage, pv, &full[warp][s]);
+    tma_load_3d(st + 6144, &tmap, 64, m.pg * kPage, pv, &full[warp][s]);
+  };
+  int pu = u0;
+  for (int s = 0; s < kPrivStages && pu < u1; ++s, ++pu) {
+    const UnitMeta m = meta(pu);
+    if (lane == 0) issue(s, m);
   }
 
-  // q . k mapping: token t = lane/2, head-dim half hh = lane%2, chunk order
-  // rotated per lane so a quarter-warp's 16-byte smem reads hit 8 distinct
-  // bank groups.
-  const int t = lane >> 1, hh = lane & 1;
-  const int rot = (t & 3) + 4 * hh;
-  float qr[64];
-  UnitCursor cc = locate_unit(p, H, u0);
-  auto load_q = [&](int row, int head) {
-    const uint4* qs = reinterpret_cast<const uint4*>(q + ((long long)row * H + head) * kHeadDim + hh * 64);
+  // q as the A operand: row 0 of a 16 x 128 tile (lanes 0-3 hold it);
+  // the next item's q is prefetched one page ahead into qn
+  uint32_t qa[8][2], qn[8][2];
+  auto fetch_q = [&](uint32_t (&dst)[8][2], int row, int head) {
+    const uint32_t* Q = reinterpret_cast<const uint32_t*>(q + ((long long)row * H + head) * kHeadDim);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint4 w4 = qs[(i + rot) & 7];
-      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        qr[i * 8 + 2 * j] = bf_lo(w[j]) * scale_log2;
-        qr[i * 8 + 2 * j + 1] = bf_hi(w[j]) * scale_log2;
-      }
+    for (int kt = 0; kt < 8; ++kt) {
+      dst[kt][0] = g == 0 ? Q[kt * 8 + t4] : 0u;
+      dst[kt][1] = g == 0 ? Q[kt * 8 + 4 + t4] : 0u;
     }
   };
-  load_q(cc.row, cc.head);
+  UnitMeta cur = meta(u0);
+  fetch_q(qa, cur.row, cur.head);
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m = -INFINITY, l = 0.f;
-  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int mi = lane >> 3, ri = lane & 7;
+  int s = 0;
+  uint32_t phase = 0;
 
   for (int u = u0; u < u1; ++u) {
-    const int s = (u - u0) % kPrivStages;
-    mbar_wait(&full[warp][s], ((u - u0) / kPrivStages) & 1);
-    const int ntok = s_ntok[warp][s];
-    const uint8_t* Ks = ring + s * kPwStageBytes;
-    const uint8_t* Vs = Ks + kPageBytes;
-    float dot = 0.f;
+    const bool last = u + 1 == u1;
+    const UnitMeta nxt = last ? cur : meta(u + 1);
+    const bool item_end = last || nxt.row != cur.row || nxt.head != cur.head;
+    if (item_end && !last) fetch_q(qn, nxt.row, nxt.head);
+    mbar_wait(&full[warp][s], phase);
+    const uint32_t Ks = smem_u32(ring + s * kPwStageBytes);
+    const uint32_t Vs = Ks + 4096;
+    float sc[2][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint4 k4 = *reinterpret_cast<const uint4*>(Ks + t * 256 + hh * 128 + ((i + rot) & 7) * 16);
-      const uint32_t w[4] = {k4.x, k4.y, k4.z, k4.w};
+    for (int i = 0; i < 2; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        dot = fmaf(qr[i * 8 + 2 * j], bf_lo(w[j]), dot);
-        dot = fmaf(qr[i * 8 + 2 * j + 1], bf_hi(w[j]), dot);
-      }
+    for (int kt = 0; kt < 8; ++kt) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(Ks + sw_page((mi >> 1) * 8 + ri, 2 * kt + (mi & 1)), b0, b1, b2, b3);
+      const uint32_t af[4] = {qa[kt][0], 0u, qa[kt][1], 0u};
+      mma_bf16(sc[0], af, b0, b1);
+      mma_bf16(sc[1], af, b2, b3);
     }
-    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-    const float sc = t < ntok ? dot : -INFINITY;
-    float mx = sc;
+    // row-0 online softmax (lanes 0-3 carry the 16 scores)
+    float v[4];
+    float mx = -INFINITY;
 #pragma unroll
-    for (int off = 2; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const float m_new = fmaxf(m, mx);  // finite: every listed page holds >= 1 token
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = nt * 8 + 2 * t4 + e;
+        v[nt * 2 + e] = tok < cur.ntok ? sc[nt][e] * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, v[nt * 2 + e]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m, mx);
     const float alpha = ex2(m - m_new);
-    const float pt = ex2(sc - m_new);
-    float ps = pt;
-#pragma unroll
-    for (int off = 2; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-    l = l * alpha + ps;
     m = m_new;
-    if (hh == 0) s_p[warp][t] = pt;
-    __syncwarp();
-    o.x *= alpha;
-    o.y *= alpha;
-    o.z *= alpha;
-    o.w *= alpha;
+    float pr[4];
+    float ps = 0.f;
 #pragma unroll
-    for (int t4 = 0; t4 < 4; ++t4) {
-      const float4 p4 = *reinterpret_cast<const float4*>(&s_p[warp][t4 * 4]);
-      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint2 v = *reinterpret_cast<const uint2*>(Vs + (t4 * 4 + e) * 256 + lane * 8);
-        o.x = fmaf(pv[e], bf_lo(v.x), o.x);
-        o.y = fmaf(pv[e], bf_hi(v.x), o.y);
-        o.z = fmaf(pv[e], bf_lo(v.y), o.z);
-        o.w = fmaf(pv[e], bf_hi(v.y), o.w);
-      }
+    for (int e = 0; e < 4; ++e) {
+      pr[e] = g == 0 ? ex2(v[e] - m_new) : 0.f;
+      ps += pr[e];
     }
-    __syncwarp();  // stage s and s_p are free again
-    if (lane == 0 && pu < u1) {  // producer state lives in lane 0 only
-      fence_proxy_async();
-      issue(s);
-      advance_unit(p, H, pc);
+    l = l * alpha + ps;
+    uint32_t ph[4], pl[4];
+    ph[0] = pack_bf16(pr[0], pr[1]);
+    ph[2] = pack_bf16(pr[2], pr[3]);
+    pl[0] = pack_bf16(pr[0] - bf_lo(ph[0]), pr[1] - bf_hi(ph[0]));
+    pl[2] = pack_bf16(pr[2] - bf_lo(ph[2]), pr[3] - bf_hi(ph[2]));
+    ph[1] = ph[3] = pl[1] = pl[3] = 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] *= alpha;
+      o[i][1] *= alpha;
+    }
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(Vs + sw_page((mi & 1) * 8 + ri, 2 * dp + (mi >> 1)), b0, b1, b2, b3);
+      mma_bf16(o[2 * dp], ph, b0, b1);
+      mma_bf16(o[2 * dp + 1], ph, b2, b3);
+      mma_bf16(o[2 * dp], pl, b0, b1);
+      mma_bf16(o[2 * dp + 1], pl, b2, b3);
+    }
+    __syncwarp();  // every lane is done reading stage s
+    if (pu < u1) {
+      const UnitMeta nm = meta(pu);
+      if (lane == 0) {
+        fence_proxy_async();
+        issue(s, nm);
+      }
       ++pu;
     }
-    // piece boundary: last unit of this warp or of this (row, head) item
-    const int row = cc.row, head = cc.head;
-    advance_unit(p, H, cc);
-    if (u + 1 == u1 || cc.page == 0) {
-      const int np = p.row_priv_npages[row];
-      const int first = (p.row_unit_off[row] + head * np) / p.priv_per;
-      const int slot = p.row_nslots[row] + (gw - first);
+    if (++s == kPrivStages) {
+      s = 0;
+      phase ^= 1u;
+    }
+    if (item_end) {
+      // piece end: partial of (row, head) in slot nslots(row) + piece index
+      const int row = cur.row, head = cur.head;
+      const int first = (head * NPT + p.row_unit_off[row]) / p.priv_per;
+      const int slot = p.row_head_base[(long long)row * H + head] + (gw - first);
       const long long pi = part_index(p, H, row, slot, head);
-      reinterpret_cast<float4*>(a.part_o + pi * kHeadDim)[lane] = o;
-      if (lane == 0) a.part_ml[pi] = make_float2(m, l);
-      if (arrive_last_warp(a, p, row, head, lane)) {
-        merge_row_head_warp(a, p, row, head, out, out_f32, lane);
-        if (lane == 0) a.counters[row * H + head] = 0;
+      float lsum = l;
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+      if (g == 0) {
+        float2* po = reinterpret_cast<float2*>(a.part_o + pi * kHeadDim);
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][0], o[nt][1]);
+        if (t4 == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
       m = -INFINITY;
       l = 0.f;
-      o = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (u + 1 < u1) load_q(cc.row, cc.head);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+#pragma unroll
+      for (int kt = 0; kt < 8; ++kt) {
+        qa[kt][0] = qn[kt][0];
+        qa[kt][1] = qn[kt][1];
+      }
+    }
+    cur = nxt;
+    if (u + 1 - wbase >= 32 && u + 1 < u1) {
+      wbase += 32;
+      lo = hi;
+      hi = load_meta(wbase + 32);
     }
   }
 }
@@ -226,20 +258,20 @@ __device__ __forceinline__ uint32_t sw128(int row, int c16) {
 }
 
 __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
-    ArenaDev a, PlanDev p, int layer, const __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ out,
-    float* __restrict__ out_f32, float scale_log2, const __grid_constant__ CUtensorMap tmap) {
+    ArenaDev a, PlanDev p, int layer, const __nv_bfloat16* __restrict__ q, float scale_log2,
+    const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kPmStages];
   __shared__ int s_rows[kMmaQBlock];
-  __shared__ int s_merge[kMmaQBlock];
-  __shared__ int s_nmerge;
 
-  const int item = blockIdx.x, head = blockIdx.y, tid = threadIdx.x;
+  const int item = blockIdx.x, tid = threadIdx.x;
+  const int head = p.it_head[item];
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int H = a.num_heads;
   const int npages = p.it_npages[item], ntok = p.it_ntok[item], poff = p.it_page_off[item];
-  const int nq = p.it_nq[item], qoff = p.it_q_off[item], slot = p.it_slot[item];
+  const int nq = p.it_nq[item], qoff = p.it_q_off[item];
+  const int* qslot = p.qslot + p.it_qslot_off[item];
   const int ntiles = (npages + kMmaTilePages - 1) / kMmaTilePages;
   const int planeK = (int)plane_index(layer, 0, head, H), planeV = (int)plane_index(layer, 1, head, H);
 
@@ -248,7 +280,6 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
     prefetch_tmap(&tmap);
     for (int s = 0; s < kPmStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
-    s_nmerge = 0;
   }
   // zero the ring once so rows of partial tiles never hold NaN bit patterns
   for (int i = tid; i < kPmStages * kPmStageBytes / 16; i += kPmThreads)
@@ -388,58 +419,53 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   if (active) {
     if (r0 < nq) {
-      const long long pi = part_index(p, H, s_rows[r0], slot, head);
+      const long long pi = part_index(p, H, s_rows[r0], qslot[r0], head);
       float2* po = reinterpret_cast<float2*>(a.part_o + pi * kHeadDim);
 #pragma unroll
       for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][0], o[nt][1]);
       if (t4 == 0) a.part_ml[pi] = make_float2(m0, l0);
     }
     if (r1 < nq) {
-      const long long pi = part_index(p, H, s_rows[r1], slot, head);
+      const long long pi = part_index(p, H, s_rows[r1], qslot[r1], head);
       float2* po = reinterpret_cast<float2*>(a.part_o + pi * kHeadDim);
 #pragma unroll
       for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][2], o[nt][3]);
       if (t4 == 0) a.part_ml[pi] = make_float2(m1, l1);
     }
   }
-  __threadfence();
-  __syncthreads();
-  if (tid < nq) {
-    const int row = s_rows[tid];
-    const int prev = atomicAdd(&a.counters[row * H + head], 1);
-    if (prev == expected_arrivals(p, row, head) - 1) s_merge[atomicAdd(&s_nmerge, 1)] = row;
-  }
-  __syncthreads();
-  const int nm = s_nmerge;
-  if (nm > 0) {
-    __threadfence();
-    for (int k = warp; k < nm; k += kPmThreads / 32) {
-      const int row = s_merge[k];
-      merge_row_head_warp(a, p, row, head, out, out_f32, lane);
-      if (lane == 0) a.counters[row * H + head] = 0;
-    }
-  }
+}
+
+// ================================================================== merge
+// K4: one warp per (row, head) combines every partial (shared-prefix splits
+// + private pieces) in log2 space and writes the bf16 row (fp32 optional).
+__global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __nv_bfloat16* __restrict__ out,
+                                                      float* __restrict__ out_f32) {
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int H = a.num_heads;
+  if (w >= p.num_rows * H) return;
+  merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane);
 }
 
 // ================================================================= append
-__global__ void fk_append_kernel(ArenaDev a, PlanDev p, int layer, const uint4* __restrict__ k,
-                                 const uint4* __restrict__ v) {
-  const int row = blockIdx.x;
+// K1: the step's new K/V rows -> (page, slot) of each row's leaf, for
+// layers [layer0, layer0 + gridDim.y); one warp per (row, head, layer).
+__global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, PlanDev p, int layer0,
+                                                       const uint4* __restrict__ k, const uint4* __restrict__ v) {
+  const int H = a.num_heads;
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= p.num_rows * H) return;
+  const int row = w / H, h = w % H;
   const int pg = p.app_page[row];
   if (pg < 0) return;
   const int slot = p.app_slot[row];
-  const int H = a.num_heads;
+  const int li = blockIdx.y, layer = layer0 + li;
   const long long plane_elems = a.num_pages * kPage * kHeadDim;
-  const int per_head = kHeadDim / 8;  // uint4 per head row
-  for (int i = threadIdx.x; i < 2 * H * per_head; i += blockDim.x) {
-    const int kv = i / (H * per_head);
-    const int rem = i % (H * per_head);
-    const int h = rem / per_head, c = rem % per_head;
-    const uint4* src = kv == 0 ? k : v;
-    uint4* dst = reinterpret_cast<uint4*>(a.kv + plane_index(layer, kv, h, H) * plane_elems +
-                                          ((long long)pg * kPage + slot) * kHeadDim);
-    dst[c] = src[((long long)row * H + h) * per_head + c];
-  }
+  const int kv = lane >> 4, c = lane & 15;  // 16 lanes x 16 B per row
+  const uint4* src = kv == 0 ? k : v;
+  const uint4 val = src[(((long long)li * p.num_rows + row) * H + h) * 16 + c];
+  uint4* dst = reinterpret_cast<uint4*>(a.kv + plane_index(layer, kv, h, H) * plane_elems +
+                                        ((long long)pg * kPage + slot) * kHeadDim);
+  dst[c] = val;
 }
 
 // ============================================================== synthetic
@@ -492,37 +518,43 @@ __global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long
 }
 
 // ============================================================== launchers
-cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, void* out,
-                           float* out_f32, float scale_log2, cudaStream_t s) {
+cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
+                           const CUtensorMap* tmap, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fk_private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPwSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  if (p.priv_units == 0) return cudaSuccess;
   const int grid = (p.priv_warps + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta;
-  fk_private_kernel<<<grid, kPwThreads, kPwSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, (__nv_bfloat16*)out,
-                                                      out_f32, scale_log2);
+  fk_private_kernel<<<grid, kPwThreads, kPwSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, scale_log2, *tmap);
   return cudaGetLastError();
 }
 
-cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q, void* out,
-                              float* out_f32, float scale_log2, const CUtensorMap* tmap, cudaStream_t s) {
+cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, cudaStream_t s) {
+  const int warps = p.num_rows * a.num_heads;
+  fk_merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(a, p, (__nv_bfloat16*)out, out_f32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
+                              const CUtensorMap* tmap, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(p.tc_begin, a.num_heads);
-  fk_prefix_mma_kernel<<<grid, kPmThreads, kPmSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q,
-                                                         (__nv_bfloat16*)out, out_f32, scale_log2, *tmap);
+  dim3 grid(p.tc_begin);
+  fk_prefix_mma_kernel<<<grid, kPmThreads, kPmSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, scale_log2, *tmap);
   return cudaGetLastError();
 }
 
-cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer, const void* k, const void* v,
-                          cudaStream_t s) {
-  fk_append_kernel<<<p.num_rows, 256, 0, s>>>(a, p, layer, (const uint4*)k, (const uint4*)v);
+cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers, const void* k,
+                          const void* v, cudaStream_t s) {
+  dim3 grid((p.num_rows * a.num_heads + 7) / 8, nlayers);
+  fk_append_kernel<<<grid, 256, 0, s>>>(a, p, layer0, (const uint4*)k, (const uint4*)v);
   return cudaGetLastError();
 }
 

@@ -104,9 +104,7 @@ struct fk_pool {
   // scratch
   float* part_o = nullptr;
   float2* part_ml = nullptr;
-  int* counters = nullptr;
   size_t part_cap = 0;     // entries (rows*slots*H)
-  size_t counter_cap = 0;  // entries (rows*H)
 
   ArenaDev arena() const {
     ArenaDev a;
@@ -116,8 +114,7 @@ struct fk_pool {
     a.num_heads = desc.num_heads;
     a.part_o = part_o;
     a.part_ml = part_ml;
-    a.counters = counters;
-    return a;
+      return a;
   }
 };
 
@@ -199,15 +196,6 @@ int ensure_scratch(fk_pool* p, int rows, int slots) {
     FK_CUDA(cudaMalloc(&p->part_o, cap * D * sizeof(float)));
     FK_CUDA(cudaMalloc(&p->part_ml, cap * sizeof(float2)));
     p->part_cap = cap;
-  }
-  const size_t cneed = (size_t)std::max(rows, 1) * H;
-  if (cneed > p->counter_cap) {
-    size_t cap = std::max(cneed, p->counter_cap * 2);
-    if (p->counters) FK_CUDA(cudaFree(p->counters));
-    p->counters = nullptr;
-    FK_CUDA(cudaMalloc(&p->counters, cap * sizeof(int)));
-    FK_CUDA(cudaMemset(p->counters, 0, cap * sizeof(int)));
-    p->counter_cap = cap;
   }
   return FK_OK;
 }
@@ -298,7 +286,6 @@ int fk_pool_destroy(fk_pool* p) {
     if (p->kv) cudaFree(p->kv);
     if (p->part_o) cudaFree(p->part_o);
     if (p->part_ml) cudaFree(p->part_ml);
-    if (p->counters) cudaFree(p->counters);
   }
   delete p;
   return FK_OK;
@@ -461,12 +448,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   std::vector<int64_t> order;  // unique contexts, first-seen (row order, leaf->root)
   for (int r = 0; r < B; ++r) {
     int64_t cur = leaves[r];
-    auto it = p->ctxs.find(cur);
-    if (it == p->ctxs.end())
-      return fail(FK_UNKNOWN_CONTEXT, "unknown leaf context %lld", (long long)cur);
+    if (!p->ctxs.count(cur)) return fail(FK_UNKNOWN_CONTEXT, "unknown leaf context %lld", (long long)cur);
     while (cur >= 0) {
       auto ci = p->ctxs.find(cur);
-      if (ci == p->ctxs.end()) break;  // parent already discarded (engine.py:482 get() -> None)
+      if (ci == p->ctxs.end()) break;  // engine.py:482 contexts.get() -> None
       chain[r].push_back(cur);
       auto f = fan.find(cur);
       if (f == fan.end()) {
@@ -485,17 +470,16 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     for (int r = 0; r < B; ++r)
       for (int64_t c : chain[r]) batch_tokens += p->ctxs[c].tokens;
   }
-  auto is_shared = [&](int64_t c) {
-    return dedup && fan[c] >= 2 && p->ctxs[c].tokens > 0;
-  };
+  auto is_shared = [&](int64_t c) { return dedup && fan[c] >= 2 && p->ctxs[c].tokens > 0; };
 
-  // shared contexts: descendant rows (row order) and kernel class
+  // ---- shared contexts (K2 work) --------------------------------------------
   struct Shared {
     int64_t ctx;
-    std::vector<int> rows;
+    std::vector<int> rows;  // descendant rows, row order
     bool tc;
-    int splits = 1;
-    int slot_base = 0;
+    int splits = 1;         // mma path: head-independent page splits
+    int page_off = 0;
+    int q_off = 0;
   };
   std::vector<Shared> shared;
   std::unordered_map<int64_t, int> shared_idx;
@@ -513,94 +497,121 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       auto si = shared_idx.find(c);
       if (si != shared_idx.end()) shared[si->second].rows.push_back(r);
     }
-  // split policy: ~one wave of CTAs over all prefix work
-  {
-    int64_t total = 0;
-    for (auto& s : shared) {
-      const int qb = s.tc ? kTcQBlock : kMmaQBlock;
-      const int64_t nqb = ((int64_t)s.rows.size() + qb - 1) / qb;
-      total += (int64_t)p->ctxs[s.ctx].phys.size() * nqb * H;
-    }
-    const int64_t target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
-    int64_t per = std::max<int64_t>(p->min_split_pages, (total + target - 1) / std::max<int64_t>(target, 1));
-    for (auto& s : shared) {
-      const int tile = s.tc ? kTcTilePages : kMmaTilePages;
-      const int64_t ps = (per + tile - 1) / tile * tile;
-      const int64_t np = (int64_t)p->ctxs[s.ctx].phys.size();
-      s.splits = (int)std::max<int64_t>(1, (np + ps - 1) / ps);
-    }
-  }
-  // slot bases: sum of splits of shared proper ancestors (same for every
-  // descendant because the contexts form a forest)
-  std::vector<int> nslots(B, 0);
-  for (auto& s : shared) {
-    int base = 0;
-    int64_t cur = p->ctxs[s.ctx].parent;
-    while (cur >= 0) {
-      auto si = shared_idx.find(cur);
-      if (si != shared_idx.end()) base += shared[si->second].splits;
-      auto ci = p->ctxs.find(cur);
-      if (ci == p->ctxs.end()) break;
-      cur = ci->second.parent;
-    }
-    s.slot_base = base;
-  }
-  for (int r = 0; r < B; ++r)
-    for (int64_t c : chain[r]) {
-      auto si = shared_idx.find(c);
-      if (si != shared_idx.end()) nslots[r] += shared[si->second].splits;
-    }
-  // private stream-K geometry (filled after the private page lists below)
-  int max_slots = 1;
-
-  // host arrays
   std::vector<int32_t> pages, page_ntok, qrows;
-  std::vector<int32_t> it_page_off, it_npages, it_ntok, it_q_off, it_nq, it_slot;
-  int num_tc = 0, num_mma = 0;
-  // shared page lists first
-  std::vector<int32_t> shared_page_off(shared.size());
-  for (size_t i = 0; i < shared.size(); ++i) {
-    const Ctx& c = p->ctxs[shared[i].ctx];
-    shared_page_off[i] = (int32_t)pages.size();
+  for (auto& s : shared) {
+    const Ctx& c = p->ctxs[s.ctx];
+    s.page_off = (int)pages.size();
     for (size_t k = 0; k < c.phys.size(); ++k) {
       pages.push_back(c.phys[k]);
       page_ntok.push_back((int32_t)std::min<int64_t>(kPage, c.tokens - (int64_t)k * kPage));
     }
+    s.q_off = (int)qrows.size();
+    for (int r : s.rows) qrows.push_back(r);
   }
-  std::vector<int32_t> q_off(shared.size());
-  for (size_t i = 0; i < shared.size(); ++i) {
-    q_off[i] = (int32_t)qrows.size();
-    for (int r : shared[i].rows) qrows.push_back(r);
-  }
-  for (int pass = 0; pass < 2; ++pass) {  // mma items first, then tcgen05 items
-    for (size_t i = 0; i < shared.size(); ++i) {
-      const Shared& s = shared[i];
-      if ((int)s.tc != pass) continue;
-      const Ctx& c = p->ctxs[s.ctx];
-      const int64_t np = (int64_t)c.phys.size();
-      const int64_t ps = (np + s.splits - 1) / s.splits;
-      const int tile = s.tc ? kTcTilePages : kMmaTilePages;
-      const int64_t psr = (ps + tile - 1) / tile * tile;
-      const int qb = s.tc ? kTcQBlock : kMmaQBlock;
-      const int nq = (int)s.rows.size();
-      for (int sp = 0; sp < s.splits; ++sp) {
-        const int64_t p0 = sp * psr;
-        const int64_t p1 = std::min<int64_t>(np, p0 + psr);
-        const int64_t t0 = p0 * kPage;
-        const int64_t t1 = std::min<int64_t>(c.tokens, p1 * kPage);
-        for (int q0 = 0; q0 < nq; q0 += qb) {
-          it_page_off.push_back(shared_page_off[i] + (int32_t)p0);
-          it_npages.push_back((int32_t)std::max<int64_t>(0, p1 - p0));
-          it_ntok.push_back((int32_t)std::max<int64_t>(0, t1 - t0));
-          it_q_off.push_back(q_off[i] + q0);
-          it_nq.push_back(std::min(qb, nq - q0));
-          it_slot.push_back(s.slot_base + sp);
-          (s.tc ? num_tc : num_mma) += 1;
-        }
-      }
+  // mma split policy: ~one wave of CTAs over the mma-class prefix work
+  {
+    int64_t total = 0;
+    for (auto& s : shared)
+      if (!s.tc)
+        total += (int64_t)p->ctxs[s.ctx].phys.size() * ((s.rows.size() + kMmaQBlock - 1) / kMmaQBlock) * H;
+    const int64_t target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
+    const int64_t per = std::max<int64_t>(p->min_split_pages, (total + target - 1) / std::max<int64_t>(target, 1));
+    const int64_t ps = (per + kMmaTilePages - 1) / kMmaTilePages * kMmaTilePages;
+    for (auto& s : shared) {
+      const int64_t np = (int64_t)p->ctxs[s.ctx].phys.size();
+      s.splits = s.tc ? 1 : (int)std::max<int64_t>(1, (np + ps - 1) / ps);
     }
   }
-  // private streams
+  // items: mma (ctx, split, qblock, head) then tcgen05 (ctx, qblock, head)
+  struct Item {
+    int sh, split, q0, nq, head, page0, npages, ntok, units;
+  };
+  std::vector<Item> items;
+  int num_mma = 0, num_tc = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int si = 0; si < (int)shared.size(); ++si) {
+      const Shared& s = shared[si];
+      if ((int)s.tc != pass) continue;
+      const Ctx& c = p->ctxs[s.ctx];
+      const int np = (int)c.phys.size();
+      const int qb = s.tc ? kTcQBlock : kMmaQBlock;
+      const int nq = (int)s.rows.size();
+      const int psr = s.tc ? np : ((np + s.splits - 1) / s.splits + kMmaTilePages - 1) / kMmaTilePages * kMmaTilePages;
+      for (int sp = 0; sp < s.splits; ++sp) {
+        const int p0 = sp * psr, p1 = std::min(np, p0 + psr);
+        const int64_t t1 = std::min<int64_t>(c.tokens, (int64_t)p1 * kPage);
+        for (int q0 = 0; q0 < nq; q0 += qb)
+          for (int h = 0; h < H; ++h) {
+            Item it;
+            it.sh = si;
+            it.split = sp;
+            it.q0 = q0;
+            it.nq = std::min(qb, nq - q0);
+            it.head = h;
+            it.page0 = p0;
+            it.npages = std::max(0, p1 - p0);
+            it.ntok = (int)std::max<int64_t>(0, t1 - (int64_t)p0 * kPage);
+            it.units = (it.npages + kTcTilePages - 1) / kTcTilePages;
+            items.push_back(it);
+            (s.tc ? num_tc : num_mma) += 1;
+          }
+      }
+    }
+  // tcgen05 stream-K: tile units of all tc items spread evenly over <= one wave
+  std::vector<int32_t> it_unit_off(items.size(), 0);
+  int64_t tc_units = 0;
+  for (size_t i = num_mma; i < items.size(); ++i) {
+    it_unit_off[i] = (int32_t)tc_units;
+    tc_units += items[i].units;
+  }
+  const int64_t tc_target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
+  const int64_t tc_ctas = tc_units > 0 ? std::min<int64_t>(tc_target, tc_units) : 0;
+  const int64_t tc_per = tc_ctas > 0 ? (tc_units + tc_ctas - 1) / tc_ctas : 1;
+  auto item_pieces = [&](size_t i) -> int {
+    if ((int)i < num_mma) return 1;
+    const int64_t a0 = it_unit_off[i], b0 = a0 + items[i].units;
+    return items[i].units == 0 ? 1 : (int)((b0 - 1) / tc_per - a0 / tc_per + 1);
+  };
+  // per (shared ctx, qblock, head): pieces contributed to each of its rows
+  std::unordered_map<int64_t, int> pieces_of;  // key (sh * 4096 + qb) * H + h
+  auto pkey = [&](int sh, int qb, int h) { return ((int64_t)sh * 4096 + qb) * H + h; };
+  for (size_t i = 0; i < items.size(); ++i) {
+    const Item& it = items[i];
+    const int qb = it.q0 / (shared[it.sh].tc ? kTcQBlock : kMmaQBlock);
+    pieces_of[pkey(it.sh, qb, it.head)] += item_pieces(i);
+  }
+  // slot bases: per (row, head) walk the shared chain root -> leaf
+  std::vector<int32_t> row_head_base(std::max<int64_t>(B * H, 1), 0);
+  std::unordered_map<int64_t, int> base_at;  // key (row * H + h) * nshared + sh
+  const int64_t nsh = std::max<int64_t>((int64_t)shared.size(), 1);
+  std::vector<int> pos_in_ctx(shared.size(), 0);
+  for (int r = 0; r < B; ++r) {
+    for (int h = 0; h < H; ++h) {
+      int acc = 0;
+      for (auto ci = chain[r].rbegin(); ci != chain[r].rend(); ++ci) {
+        auto si = shared_idx.find(*ci);
+        if (si == shared_idx.end()) continue;
+        const Shared& s = shared[si->second];
+        const int j = (int)(std::find(s.rows.begin(), s.rows.end(), r) - s.rows.begin());
+        const int qb = j / (s.tc ? kTcQBlock : kMmaQBlock);
+        base_at[((int64_t)r * H + h) * nsh + si->second] = acc;
+        acc += pieces_of[pkey(si->second, qb, h)];
+      }
+      row_head_base[(int64_t)r * H + h] = acc;
+    }
+  }
+  std::vector<int32_t> it_qslot_off(items.size()), qslot;
+  for (size_t i = 0; i < items.size(); ++i) {
+    const Item& it = items[i];
+    const Shared& s = shared[it.sh];
+    it_qslot_off[i] = (int32_t)qslot.size();
+    for (int j = 0; j < it.nq; ++j) {
+      const int r = s.rows[it.q0 + j];
+      qslot.push_back(base_at[((int64_t)r * H + it.head) * nsh + it.sh] + ((int)i < num_mma ? it.split : 0));
+    }
+  }
+
+  // ---- private streams (K3 work) ----------------------------------------------
   std::vector<int32_t> row_priv_off(B), row_priv_np(B);
   for (int r = 0; r < B; ++r) {
     row_priv_off[r] = (int32_t)pages.size();
@@ -618,28 +629,34 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     }
     row_priv_np[r] = (int32_t)pages.size() - row_priv_off[r];
   }
-  // private stream-K: units (row, head, page); warps own equal unit ranges
-  std::vector<int32_t> row_unit_off(B);
-  int64_t U = 0;
+  // warp stream-K over units (head, flat private entry)
+  const int64_t priv_base = B > 0 ? row_priv_off[0] : (int64_t)pages.size();
+  const int64_t NPT = (int64_t)pages.size() - priv_base;
+  std::vector<int32_t> row_unit_off(std::max(B, 1), 0), page_row(std::max<int64_t>(NPT, 1), 0);
   for (int r = 0; r < B; ++r) {
-    row_unit_off[r] = (int32_t)U;
-    U += (int64_t)row_priv_np[r] * H;
+    row_unit_off[r] = (int32_t)(row_priv_off[r] - priv_base);
+    for (int k = 0; k < row_priv_np[r]; ++k) page_row[row_unit_off[r] + k] = r;
   }
+  const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
-  int64_t G = std::min<int64_t>((int64_t)p->num_sms * kPrivWarpsPerCta,
-                                (U + kPrivMinUnits - 1) / kPrivMinUnits);
+  int64_t G = std::min<int64_t>((int64_t)p->num_sms * kPrivWarpsPerCta, (U + kPrivMinUnits - 1) / kPrivMinUnits);
   G = std::max<int64_t>(G, 1);
   G = (G + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta * kPrivWarpsPerCta;
   const int64_t per = std::max<int64_t>(1, (U + G - 1) / G);
+  std::vector<int32_t> row_head_count(std::max<int64_t>(B * H, 1), 0);
+  int max_slots = 1;
   for (int r = 0; r < B; ++r) {
-    int maxp = 0;
     const int64_t np = row_priv_np[r];
-    if (np > 0)
-      for (int64_t h = 0; h < H; ++h) {
-        const int64_t a0 = row_unit_off[r] + h * np, b0 = a0 + np;
-        maxp = std::max<int>(maxp, (int)((b0 - 1) / per - a0 / per + 1));
+    for (int64_t h = 0; h < H; ++h) {
+      int pieces = 0;
+      if (np > 0) {
+        const int64_t a0 = h * NPT + row_unit_off[r], b0 = a0 + np;
+        pieces = (int)((b0 - 1) / per - a0 / per + 1);
       }
-    max_slots = std::max(max_slots, nslots[r] + maxp);
+      const int cnt = row_head_base[r * H + h] + pieces;
+      row_head_count[r * H + h] = cnt;
+      max_slots = std::max(max_slots, cnt);
+    }
   }
   // synthetic keys: (leaf uid, leaf tokens at plan time + rank << 40)
   std::vector<int64_t> row_uid(B), row_pos(B);
@@ -656,13 +673,14 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     }
   }
 
+  const int n_items = (int)items.size();
   if (info) {
     info->batch_tokens = batch_tokens;
     info->shared_tokens = shared_tokens;
     info->private_tokens = private_tokens;
     info->num_rows = B;
     info->num_shared_ctx = (int32_t)shared.size();
-    info->num_prefix_ctas = (int32_t)(it_page_off.size() * H);
+    info->num_prefix_ctas = (int32_t)(num_mma + tc_ctas);
     info->max_slots = max_slots;
     info->num_tc_items = num_tc;
     info->num_mma_items = num_mma;
@@ -673,21 +691,26 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     return FK_OK;
   }
 
-  // ---- upload ----
+  // ---- upload ---------------------------------------------------------------
   FK_CUDA(cudaSetDevice(p->desc.device));
   int rc = ensure_scratch(p, B, max_slots);
   if (rc != FK_OK) return rc;
-  const int n_items = (int)it_page_off.size();
+  const size_t ni = (size_t)std::max(n_items, 1);
+  const size_t nb = (size_t)std::max(B, 1);
+  const size_t nbh = (size_t)std::max<int64_t>(B * H, 1);
   Layout L;
-  const size_t o_it = L.add(sizeof(int32_t) * 6 * std::max(n_items, 1));
+  const size_t o_it = L.add(sizeof(int32_t) * 9 * ni);
   const size_t o_q = L.add(sizeof(int32_t) * std::max<size_t>(qrows.size(), 1));
-  const size_t o_rows = L.add(sizeof(int32_t) * 4 * std::max(B, 1));
+  const size_t o_qs = L.add(sizeof(int32_t) * std::max<size_t>(qslot.size(), 1));
+  const size_t o_rows = L.add(sizeof(int32_t) * 3 * nb);
+  const size_t o_rh = L.add(sizeof(int32_t) * 2 * nbh);
   const size_t o_pages = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
   const size_t o_pnt = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
-  const size_t o_uid = L.add(sizeof(int64_t) * std::max(B, 1));
-  const size_t o_pos = L.add(sizeof(int64_t) * std::max(B, 1));
-  const size_t o_app = L.add(sizeof(int32_t) * 2 * std::max(B, 1));
-  const size_t o_apos = L.add(sizeof(int64_t) * std::max(B, 1));
+  const size_t o_uid = L.add(sizeof(int64_t) * nb);
+  const size_t o_pos = L.add(sizeof(int64_t) * nb);
+  const size_t o_app = L.add(sizeof(int32_t) * 2 * nb);
+  const size_t o_apos = L.add(sizeof(int64_t) * nb);
+  const size_t o_prow = L.add(sizeof(int32_t) * page_row.size());
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
     FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
@@ -702,25 +725,30 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   auto put = [&](size_t off, const void* src, size_t bytes) {
     if (bytes) memcpy(h + off, src, bytes);
   };
-  const size_t ni = (size_t)std::max(n_items, 1);
   int32_t* itb = (int32_t*)(h + o_it);
   for (int i = 0; i < n_items; ++i) {
-    itb[0 * ni + i] = it_page_off[i];
-    itb[1 * ni + i] = it_npages[i];
-    itb[2 * ni + i] = it_ntok[i];
-    itb[3 * ni + i] = it_q_off[i];
-    itb[4 * ni + i] = it_nq[i];
-    itb[5 * ni + i] = it_slot[i];
+    const Item& it = items[i];
+    const Shared& sh = shared[it.sh];
+    itb[0 * ni + i] = sh.page_off + it.page0;
+    itb[1 * ni + i] = it.npages;
+    itb[2 * ni + i] = it.ntok;
+    itb[3 * ni + i] = sh.q_off + it.q0;
+    itb[4 * ni + i] = it.nq;
+    itb[5 * ni + i] = it.head;
+    itb[6 * ni + i] = it_unit_off[i];
+    itb[7 * ni + i] = it_qslot_off[i];
+    itb[8 * ni + i] = it.units;
   }
   put(o_q, qrows.data(), qrows.size() * 4);
-  const size_t nb = (size_t)std::max(B, 1);
+  put(o_qs, qslot.data(), qslot.size() * 4);
   int32_t* rb = (int32_t*)(h + o_rows);
   for (int r = 0; r < B; ++r) {
     rb[0 * nb + r] = row_priv_off[r];
     rb[1 * nb + r] = row_priv_np[r];
-    rb[2 * nb + r] = nslots[r];
-    rb[3 * nb + r] = row_unit_off[r];
+    rb[2 * nb + r] = row_unit_off[r];
   }
+  put(o_rh, row_head_base.data(), row_head_base.size() * 4);
+  put(o_rh + nbh * 4, row_head_count.data(), row_head_count.size() * 4);
   put(o_pages, pages.data(), pages.size() * 4);
   put(o_pnt, page_ntok.data(), page_ntok.size() * 4);
   put(o_uid, row_uid.data(), (size_t)B * 8);
@@ -731,6 +759,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     ab[nb + r] = 0;
   }
   memset(h + o_apos, 0, nb * 8);
+  put(o_prow, page_row.data(), page_row.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -745,16 +774,21 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.it_ntok = ditb + 2 * ni;
   pd.it_q_off = ditb + 3 * ni;
   pd.it_nq = ditb + 4 * ni;
-  pd.it_slot = ditb + 5 * ni;
+  pd.it_head = ditb + 5 * ni;
+  pd.it_unit_off = ditb + 6 * ni;
+  pd.it_qslot_off = ditb + 7 * ni;
+  pd.it_units = ditb + 8 * ni;
   pd.qrows = (const int32_t*)(d + o_q);
+  pd.qslot = (const int32_t*)(d + o_qs);
+  pd.tc_units = (int)tc_units;
+  pd.tc_per = (int)tc_per;
+  pd.tc_ctas = (int)tc_ctas;
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
-  pd.row_nslots = drb + 2 * nb;
-  pd.row_unit_off = drb + 3 * nb;
-  pd.priv_units = (int)U;
-  pd.priv_per = (int)per;
-  pd.priv_warps = (int)G;
+  pd.row_unit_off = drb + 2 * nb;
+  pd.row_head_base = (const int32_t*)(d + o_rh);
+  pd.row_head_count = (const int32_t*)(d + o_rh) + nbh;
   pd.pages = (const int32_t*)(d + o_pages);
   pd.page_ntok = (const int32_t*)(d + o_pnt);
   pd.row_uid = (const long long*)(d + o_uid);
@@ -762,6 +796,12 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.app_page = (const int32_t*)(d + o_app);
   pd.app_slot = (const int32_t*)(d + o_app) + nb;
   pd.app_pos = (const long long*)(d + o_apos);
+  pd.page_row = (const int32_t*)(d + o_prow);
+  pd.priv_base = (int)priv_base;
+  pd.priv_np = (int)NPT;
+  pd.priv_units = (int)U;
+  pd.priv_per = (int)per;
+  pd.priv_warps = (int)G;
   p->off_app_page = o_app;
   p->off_app_slot = o_app + nb * 4;
   p->off_app_pos = o_apos;
@@ -783,21 +823,24 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   ArenaDev a = p->arena();
   const bool has_mma = p->plan.tc_begin > 0;
   const bool has_tc = p->plan.num_items > p->plan.tc_begin;
-  if ((has_mma || has_tc) && !p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
+  if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
+  // K2 (shared prefixes) and K3 (private streams) only write partials, so
+  // their order is free; K4 merges every (row, head) afterwards.
   auto run_prefix = [&]() -> int {
-    if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, out, out_f32, scale_log2, &p->tmap, st));
-    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, out, out_f32, scale_log2, &p->tmap, st));
+    if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
+    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, st));
     return FK_OK;
   };
   if (p->launch_order == 0) {
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
-    FK_CUDA(launch_private(a, p->plan, layer, q, out, out_f32, scale_log2, st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, st));
   } else {
-    FK_CUDA(launch_private(a, p->plan, layer, q, out, out_f32, scale_log2, st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, st));
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
   }
+  FK_CUDA(launch_merge(a, p->plan, out, out_f32, st));
   return FK_OK;
 }
 
@@ -841,14 +884,20 @@ int fk_step_commit(fk_pool* p, const int64_t* positions, void* stream) {
 }
 
 int fk_append_kv(fk_pool* p, int32_t layer, const void* k, const void* v, void* stream) {
+  return fk_append_kv_layers(p, layer, 1, k, v, stream);
+}
+
+int fk_append_kv_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void* k, const void* v,
+                        void* stream) {
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (!p->committed) return fail(FK_INVALID_ARGUMENT, "fk_step_commit not called for this plan");
-  if (layer < 0 || layer >= p->desc.num_layers) return fail(FK_INVALID_ARGUMENT, "bad layer %d", layer);
+  if (layer0 < 0 || nlayers < 1 || layer0 + nlayers > p->desc.num_layers)
+    return fail(FK_INVALID_ARGUMENT, "bad layer range [%d, %d)", layer0, layer0 + nlayers);
   if (p->plan.num_rows == 0) return FK_OK;
   if (!k || !v) return fail(FK_INVALID_ARGUMENT, "null k/v");
   FK_CUDA(cudaSetDevice(p->desc.device));
-  FK_CUDA(launch_append(p->arena(), p->plan, layer, k, v, (cudaStream_t)stream));
+  FK_CUDA(launch_append(p->arena(), p->plan, layer0, nlayers, k, v, (cudaStream_t)stream));
   return FK_OK;
 }
 

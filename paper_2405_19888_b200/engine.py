@@ -618,11 +618,9 @@ class GpuEngine:
                 if k.device.type != "cuda":
                     k = k.to(self._dev, non_blocking=True)
                     v = v.to(self._dev, non_blocking=True)
-                layer_bytes = len(running) * geo.num_heads * geo.head_dim * 2
-                for layer in range(geo.num_layers):
-                    _lib.check(_lib.lib.fk_append_kv(
-                        self._pool.handle, layer, ctypes.c_void_p(k.data_ptr() + layer * layer_bytes),
-                        ctypes.c_void_p(v.data_ptr() + layer * layer_bytes), self._sp()))
+                _lib.check(_lib.lib.fk_append_kv_layers(self._pool.handle, 0, geo.num_layers,
+                                                        ctypes.c_void_p(k.data_ptr()),
+                                                        ctypes.c_void_p(v.data_ptr()), self._sp()))
         else:
             _lib.check(_lib.lib.fk_synth_append(self._pool.handle, self.model_seed, self.model_k_scale,
                                                 self._sp()))

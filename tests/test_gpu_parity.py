@@ -22,10 +22,22 @@ from gpu_check import check_history
 pytestmark = pytest.mark.gpu
 
 
+PATH = {"path": "mma"}
+
+
+@pytest.fixture(params=["mma", "tc"], autouse=True)
+def prefix_path(request):
+    """Every case runs with the shared prefixes on the warp-level mma.sync
+    kernel and again on the tcgen05 kernel (fan-out threshold 2)."""
+    PATH["path"] = request.param
+    yield request.param
+
+
 def make_engine(cuda_device, H, L=1, shared=True, k_scale=1.0, seed=0x5EED, kv_tokens=1 << 20, **kw):
     eng = P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=kv_tokens, device=cuda_device,
                       geometry=P.ModelGeometry(L, H, 128), model=P.SyntheticDecodeModel(seed, k_scale),
                       capture_f32=True, keep_history=True, **kw)
+    eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, 2 if PATH["path"] == "tc" else 0)
     return eng
 
 
@@ -137,6 +149,25 @@ def test_many_splits(cuda_device):
     fork_group(eng, 1000, [20, 21], out_len=2)
     run_steps(eng, 2)
     assert eng.last_plan.max_slots > 5
+    check_history(eng)
+
+
+def test_stream_k_pieces_cross_items(cuda_device):
+    """Few CTAs over many prefix tiles: stream-K ranges cut items mid-way and
+    span head / context boundaries (tcgen05), many splits (mma)."""
+    eng = make_engine(cuda_device, H=5, L=2)
+    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 7)
+    fork_group(eng, 2100, [33] * 9, out_len=2, tag="a", seed=1)
+    fork_group(eng, 700, [3] * 140, out_len=2, tag="b", seed=2)  # 140 rows: 2 x 128-query blocks
+    run_steps(eng, 2)
+    check_history(eng)
+
+
+def test_headline_shape_one_layer(cuda_device):
+    """LLaMA-13B head count, 6k prefix x 64 forks x 256: the bench shape, 1 layer."""
+    eng = make_engine(cuda_device, H=40, L=1)
+    fork_group(eng, 6000, [256] * 64, out_len=1)
+    run_steps(eng, 1)
     check_history(eng)
 
 
