@@ -14,7 +14,7 @@ from ctypes import POINTER, c_char_p, c_float, c_int32, c_int64, c_size_t, c_uin
 
 from .errors import ContextBusy, KernelError, OutOfMemory, UnknownContext, UnknownParentContext
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libforkattn.so")
+LIB_PATH = os.environ.get("FK_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libforkattn.so")
 
 FK_OK = 0
 FK_OUT_OF_MEMORY = 1

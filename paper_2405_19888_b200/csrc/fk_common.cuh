@@ -3,6 +3,7 @@
 // the log-sum-exp merge of per-(row, head) partials.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_runtime.h>
 #include <cstdint>
 #include "fk_internal.h"
 
@@ -74,6 +75,28 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
+// Launch with optional programmatic dependent launch (PDL): the kernel may
+// start while its stream predecessor is still running; it must call
+// pdl_wait_primary() before touching the predecessor's results.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// programmatic dependent launch (PDL) controls
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_primary() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -155,25 +178,52 @@ __device__ __forceinline__ int partial_count(const PlanDev& p, int H, int row, i
 // all (no partial) produce zeros.
 __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
                                                     __nv_bfloat16* out, float* out_f32, int lane) {
+  // two dependent rounds: (m, l) of every slot lane-parallel, then every
+  // slot's o (4 dims per lane) with all loads in flight together
   const int H = a.num_heads;
   const int ns = partial_count(p, H, row, head);
-  float M = -INFINITY;
-  for (int k = lane; k < ns; k += 32) M = fmaxf(M, __ldcg(&a.part_ml[part_index(p, H, row, k, head)].x));
+  const long long base = part_index(p, H, row, 0, head);  // slot stride is H
+  float2 ml = make_float2(-INFINITY, 0.f);
+  if (lane < ns) ml = __ldcg(&a.part_ml[base + (long long)lane * H]);
+  float M = ml.x;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float L = 0.f;
+  const float w = (M == -INFINITY || lane >= ns) ? 0.f : ex2(ml.x - M);
+  float L = ml.y * w;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (M != -INFINITY) {
-    for (int k = 0; k < ns; ++k) {
-      const long long pi = part_index(p, H, row, k, head);
-      const float2 ml = __ldcg(&a.part_ml[pi]);
-      const float w = ex2(ml.x - M);
-      L += ml.y * w;
-      const float4 o = __ldcg(reinterpret_cast<const float4*>(a.part_o + pi * kHeadDim) + lane);
-      acc.x += o.x * w;
-      acc.y += o.y * w;
-      acc.z += o.z * w;
-      acc.w += o.w * w;
+  if (ns > 32) {  // rare (many splits): generic lane-strided path
+    M = -INFINITY;
+    for (int k = lane; k < ns; k += 32) M = fmaxf(M, __ldcg(&a.part_ml[base + (long long)k * H].x));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    L = 0.f;
+    if (M != -INFINITY)
+      for (int k = 0; k < ns; ++k) {
+        const float2 mk = __ldcg(&a.part_ml[base + (long long)k * H]);
+        const float wk = ex2(mk.x - M);
+        L += mk.y * wk;
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)k * H) * kHeadDim) + lane);
+        acc.x = fmaf(v.x, wk, acc.x);
+        acc.y = fmaf(v.y, wk, acc.y);
+        acc.z = fmaf(v.z, wk, acc.z);
+        acc.w = fmaf(v.w, wk, acc.w);
+      }
+  }
+  for (int k0 = 0; k0 < ns && ns <= 32; k0 += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      v[k] = k0 + k < ns ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)(k0 + k) * H) * kHeadDim) + lane)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float wk = __shfl_sync(0xffffffffu, w, (k0 + k) & 31);
+      acc.x = fmaf(v[k].x, wk, acc.x);
+      acc.y = fmaf(v[k].y, wk, acc.y);
+      acc.z = fmaf(v[k].z, wk, acc.z);
+      acc.w = fmaf(v[k].w, wk, acc.w);
     }
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;

@@ -39,6 +39,7 @@ struct PlanDev {
   const int* qrows;        // request rows
   const int* qslot;        // slot of piece 0 for each (item, query)
   int tc_units, tc_per, tc_ctas;  // tcgen05 stream-K geometry
+  const int* tc_start_item;       // [tc_ctas] item holding each CTA's first unit
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;
@@ -81,11 +82,12 @@ inline __host__ __device__ long long plane_index(int layer, int kv, int head, in
 
 // Launchers (fk_kernels.cu).  All return cudaError_t of the launch.
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
-                           float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
+                           float scale_log2, const CUtensorMap* tmap, bool pdl, cudaStream_t s);
 cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
                               float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
-                             float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
+                             float scale_log2, const CUtensorMap* tmap, const CUtensorMap* tmap_run,
+                             cudaStream_t s);
 cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32,
                          cudaStream_t s);
 cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers,

@@ -40,6 +40,14 @@ struct UnitMeta {
 };
 
 // Streaming warps only write partials; fk_merge_kernel combines them.
+// With PDL this grid can start while the prefix grid of the same layer is
+// still running (disjoint partial slots); thread 0 of each CTA waits for that
+// grid before exiting so "private grid complete" implies "prefix complete".
+struct PdlTail {
+  __device__ ~PdlTail() {
+    if (threadIdx.x == 0) pdl_wait_primary();
+  }
+};
 __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
                                                                    float scale_log2,
@@ -50,6 +58,8 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
+  pdl_launch_dependents();  // the merge kernel may launch now (it waits for us)
+  PdlTail tail;             // on exit: this grid completes only after the prefix grid
 
   // ---------------------------------------------------- streaming warps
   const int g = lane >> 2, t4 = lane & 3;
@@ -265,6 +275,7 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
   __shared__ uint64_t full[kPmStages];
   __shared__ int s_rows[kMmaQBlock];
 
+  pdl_launch_dependents();
   const int item = blockIdx.x, tid = threadIdx.x;
   const int head = p.it_head[item];
   const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
@@ -440,6 +451,7 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
 // + private pieces) in log2 space and writes the bf16 row (fp32 optional).
 __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __nv_bfloat16* __restrict__ out,
                                                       float* __restrict__ out_f32) {
+  pdl_wait_primary();  // partials of the prefix and private grids are complete
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int H = a.num_heads;
   if (w >= p.num_rows * H) return;
@@ -519,7 +531,7 @@ __global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long
 
 // ============================================================== launchers
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                           const CUtensorMap* tmap, cudaStream_t s) {
+                           const CUtensorMap* tmap, bool pdl, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fk_private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPwSmem);
@@ -528,14 +540,14 @@ cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const
   }
   if (p.priv_units == 0) return cudaSuccess;
   const int grid = (p.priv_warps + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta;
-  fk_private_kernel<<<grid, kPwThreads, kPwSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, scale_log2, *tmap);
-  return cudaGetLastError();
+  return launch_k(fk_private_kernel, dim3(grid), dim3(kPwThreads), kPwSmem, s, pdl, a, p, layer,
+                  (const __nv_bfloat16*)q, scale_log2, *tmap);
 }
 
 cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, cudaStream_t s) {
   const int warps = p.num_rows * a.num_heads;
-  fk_merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(a, p, (__nv_bfloat16*)out, out_f32);
-  return cudaGetLastError();
+  return launch_k(fk_merge_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, true, a, p, (__nv_bfloat16*)out,
+                  out_f32);
 }
 
 cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,

@@ -81,12 +81,13 @@ struct fk_pool {
   // device arena
   __nv_bfloat16* kv = nullptr;
   size_t arena_bytes = 0;
-  alignas(64) CUtensorMap tmap;
+  alignas(64) CUtensorMap tmap;      // box {64 dims, 16 rows}: one page
+  alignas(64) CUtensorMap tmap_run;  // box {64 dims, 128 rows}: 8 contiguous pages
   bool tmap_ok = false;
   int num_sms = 148;
 
   // options
-  int64_t tc_min_fanout = 0;
+  int64_t tc_min_fanout = 2;  // tcgen05 for every shared context until the sweep says otherwise
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
   int64_t min_split_pages = 8;
@@ -143,6 +144,11 @@ int encode_tmap(fk_pool* p) {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FK_CUDA_ERROR, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  cuuint32_t box_run[3] = {64, (cuuint32_t)(kPage * kTcTilePages), 1};
+  r = fn(&p->tmap_run, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p->kv, dims, strides, box_run, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FK_CUDA_ERROR, "cuTensorMapEncodeTiled (run) failed (%d)", (int)r);
   p->tmap_ok = true;
   return FK_OK;
 }
@@ -711,6 +717,13 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_app = L.add(sizeof(int32_t) * 2 * nb);
   const size_t o_apos = L.add(sizeof(int64_t) * nb);
   const size_t o_prow = L.add(sizeof(int32_t) * page_row.size());
+  std::vector<int32_t> tc_start(std::max<int64_t>(tc_ctas, 1), 0);
+  for (int64_t b = 0, i = num_mma; b < tc_ctas; ++b) {
+    const int64_t u = b * tc_per;
+    while (i + 1 < (int64_t)items.size() && it_unit_off[i + 1] <= u) ++i;
+    tc_start[b] = (int32_t)i;
+  }
+  const size_t o_tcs = L.add(sizeof(int32_t) * tc_start.size());
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
     FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
@@ -760,6 +773,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   memset(h + o_apos, 0, nb * 8);
   put(o_prow, page_row.data(), page_row.size() * 4);
+  put(o_tcs, tc_start.data(), tc_start.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -783,6 +797,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.tc_units = (int)tc_units;
   pd.tc_per = (int)tc_per;
   pd.tc_ctas = (int)tc_ctas;
+  pd.tc_start_item = (const int32_t*)(d + o_tcs);
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
@@ -828,15 +843,17 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   // their order is free; K4 merges every (row, head) afterwards.
   auto run_prefix = [&]() -> int {
     if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
-    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, st));
+    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, st));
     return FK_OK;
   };
+  // the private grid may overlap the prefix grid (PDL) only when that grid
+  // belongs to this layer; otherwise it must fully follow earlier work
   if (p->launch_order == 0) {
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, has_mma || has_tc, st));
   } else {
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, false, st));
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
   }
