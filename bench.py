@@ -70,12 +70,13 @@ class ClockSampler:
         self.gpu = gpu
         self.proc = None
         self.lines = []
+        self.t_mark = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -83,7 +84,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self):
+        """Start of the timed region: only samples after this count."""
+        self.t_mark = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
@@ -96,7 +101,10 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [ln for t, ln in self.lines if self.t_mark is None or t >= self.t_mark]
+        if not lines:  # timed region shorter than one sample period
+            lines = [ln for _, ln in self.lines[-2:]]
+        for ln in lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -227,13 +235,15 @@ def cpu_baseline(cfg, budget_s=12.0, impl_steps=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tc-min-fanout", type=int, default=None)
+    ap.add_argument("--corun", type=int, default=None, help="FK_OPT_CORUN (default: library default, 1)")
+    ap.add_argument("--prefix-rate-pct", type=int, default=None)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -276,9 +286,20 @@ def main():
     from paper_2405_19888_b200 import _lib
 
     eng, rows = build_engine(cfg, device, torch, out_len=2 * (args.steps + args.warmup) + 64)
-    if args.tc_min_fanout is not None:
-        eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, args.tc_min_fanout)
+    def apply_options(e):
+        if args.tc_min_fanout is not None:
+            e.set_option(_lib.FK_OPT_TC_MIN_FANOUT, args.tc_min_fanout)
+        if args.corun is not None:
+            e.set_option(_lib.FK_OPT_CORUN, args.corun)
+        if args.prefix_rate_pct is not None:
+            e.set_option(_lib.FK_OPT_PREFIX_RATE_PCT, args.prefix_rate_pct)
+
+    apply_options(eng)
     L, H = cfg["L"], cfg["H"]
+    # the clock sampler starts before the warm-up so nvidia-smi's own start-up
+    # (NVML init) is outside the timed region
+    clocks = ClockSampler(device)
+    clocks.start()
     for _ in range(max(args.warmup, 3)):
         eng.step()
     torch.cuda.synchronize(device)
@@ -295,9 +316,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    clocks = ClockSampler(device)
     barrier()
-    clocks.start()
+    clocks.mark()
     t_steps = time_steps(eng, args.steps, torch)
     barrier()
     # per-layer attention alone for the roofline (same plan as the last step)
@@ -322,6 +342,7 @@ def main():
         torch.cuda.empty_cache()
         eng2, rows2 = build_engine(cfg, device, torch, host_inputs=True,
                                    out_len=2 * (args.steps + args.warmup) + 64)
+        apply_options(eng2)
         for _ in range(max(args.warmup, 3)):
             eng2.step()
         barrier()

@@ -97,7 +97,13 @@ enum {
   FK_OPT_TC_MIN_FANOUT = 1,   /* fan-out at/above which prefix items use tcgen05 (0 = never) */
   FK_OPT_PREFIX_TARGET_CTAS = 2, /* prefix split target (default: 1 wave of SMs) */
   FK_OPT_LAUNCH_ORDER = 3,    /* 0 prefix->private (default), 1 private->prefix (tests merge paths) */
-  FK_OPT_MIN_SPLIT_PAGES = 4  /* minimum pages per prefix split */
+  FK_OPT_MIN_SPLIT_PAGES = 4, /* minimum pages per prefix split */
+  FK_OPT_CORUN = 5,           /* 1 (default): tcgen05 prefix CTAs and the private stream split the
+                                 SMs and run concurrently; 0: each kernel gets every SM in turn */
+  FK_OPT_PREFIX_RATE_PCT = 6, /* co-run SM split: prefix per-SM KV rate relative to the private
+                                 stream's, in percent (default 80) */
+  FK_OPT_PDL = 7              /* 1 (default): programmatic dependent launch between a layer's
+                                 kernels; 0: plain stream order */
 };
 
 /* ---- context forest ------------------------------------------------------ */

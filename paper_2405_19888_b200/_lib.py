@@ -29,6 +29,9 @@ FK_OPT_TC_MIN_FANOUT = 1
 FK_OPT_PREFIX_TARGET_CTAS = 2
 FK_OPT_LAUNCH_ORDER = 3
 FK_OPT_MIN_SPLIT_PAGES = 4
+FK_OPT_CORUN = 5
+FK_OPT_PREFIX_RATE_PCT = 6
+FK_OPT_PDL = 7
 
 
 class PoolDesc(ctypes.Structure):

@@ -544,9 +544,9 @@ cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const
                   (const __nv_bfloat16*)q, scale_log2, *tmap);
 }
 
-cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, cudaStream_t s) {
+cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, bool pdl, cudaStream_t s) {
   const int warps = p.num_rows * a.num_heads;
-  return launch_k(fk_merge_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, true, a, p, (__nv_bfloat16*)out,
+  return launch_k(fk_merge_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, pdl, a, p, (__nv_bfloat16*)out,
                   out_f32);
 }
 

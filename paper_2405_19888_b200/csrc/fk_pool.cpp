@@ -90,7 +90,10 @@ struct fk_pool {
   int64_t tc_min_fanout = 2;  // tcgen05 for every shared context until the sweep says otherwise
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
+  int64_t pdl = 1;  // programmatic dependent launch between the layer's kernels
   int64_t min_split_pages = 8;
+  int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
+  int64_t prefix_rate_pct = 80;  // prefix KV bytes/s per SM relative to the private stream's
 
   // plan (host mirror + device)
   PlanSlot slots[2];
@@ -327,7 +330,10 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_TC_MIN_FANOUT: p->tc_min_fanout = value; break;
     case FK_OPT_PREFIX_TARGET_CTAS: p->prefix_target_ctas = value; break;
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
+    case FK_OPT_PDL: p->pdl = value; break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
+    case FK_OPT_CORUN: p->corun = value; break;
+    case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
     default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
   }
   return FK_OK;
@@ -570,7 +576,23 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     it_unit_off[i] = (int32_t)tc_units;
     tc_units += items[i].units;
   }
-  const int64_t tc_target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
+  // Spatial co-run: when every shared context is on the tcgen05 path, its
+  // persistent CTAs take X SMs and the private stream-K grid the other
+  // S - X, launched back to back (PDL) so both stream HBM at once.  X splits
+  // the SMs in proportion to each side's bytes over its per-SM rate.
+  int64_t priv_tok_heads = 0;
+  for (int r = 0; r < B; ++r)
+    for (int64_t c : chain[r])
+      if (!is_shared(c)) priv_tok_heads += p->ctxs[c].tokens * H;
+  int64_t tc_tok_heads = 0;
+  for (size_t i = num_mma; i < items.size(); ++i) tc_tok_heads += items[i].ntok;
+  const bool corun = p->corun && num_mma == 0 && tc_units > 0 && priv_tok_heads > 0 && p->num_sms > 1;
+  int64_t tc_target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
+  if (corun && p->prefix_target_ctas <= 0) {
+    const double wp = (double)tc_tok_heads * 100.0 / (double)p->prefix_rate_pct;
+    const double wv = (double)priv_tok_heads;
+    tc_target = std::min<int64_t>(p->num_sms - 1, std::max<int64_t>(1, std::llround(p->num_sms * wp / (wp + wv))));
+  }
   const int64_t tc_ctas = tc_units > 0 ? std::min<int64_t>(tc_target, tc_units) : 0;
   const int64_t tc_per = tc_ctas > 0 ? (tc_units + tc_ctas - 1) / tc_ctas : 1;
   auto item_pieces = [&](size_t i) -> int {
@@ -645,7 +667,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
-  int64_t G = std::min<int64_t>((int64_t)p->num_sms * kPrivWarpsPerCta, (U + kPrivMinUnits - 1) / kPrivMinUnits);
+  const int64_t priv_sms = corun ? std::max<int64_t>(1, p->num_sms - tc_ctas) : p->num_sms;
+  int64_t G = std::min<int64_t>(priv_sms * kPrivWarpsPerCta, (U + kPrivMinUnits - 1) / kPrivMinUnits);
   G = std::max<int64_t>(G, 1);
   G = (G + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta * kPrivWarpsPerCta;
   const int64_t per = std::max<int64_t>(1, (U + G - 1) / G);
@@ -851,13 +874,13 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_order == 0) {
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, has_mma || has_tc, st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, p->pdl && (has_mma || has_tc), st));
   } else {
     FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, false, st));
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
   }
-  FK_CUDA(launch_merge(a, p->plan, out, out_f32, st));
+  FK_CUDA(launch_merge(a, p->plan, out, out_f32, p->pdl != 0, st));
   return FK_OK;
 }
 

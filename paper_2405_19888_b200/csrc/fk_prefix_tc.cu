@@ -1,24 +1,27 @@
 // K2 on the 5th-generation tensor cores: shared-prefix decode attention for
 // large fan-out (engine.py:473-483 dedup made real).
 //
-// One CTA per SM, stream-K over 128-token tile units of all tcgen05-class
-// items (shared context x 128-query block x head), so every SM streams the
-// same number of prefix bytes.  Warp roles:
-//   warp 0     TMA producer: K and V page boxes (SWIZZLE_128B) into a
-//              3-stage 64 KiB ring (mbarrier complete_tx); a partial last
-//              tile is padded with copies of a valid page (masked later)
+// Persistent CTAs (one per SM of the prefix share), stream-K over 128-token
+// tile units of all tcgen05-class items (shared context x 128-query block x
+// head), so every CTA streams the same number of prefix bytes.  Warp roles:
+//   warp 0     TMA producer: K and V page boxes (SWIZZLE_128B) into split
+//              rings -- K 3 x 32 KiB (freed as soon as S is computed), V
+//              4 x 32 KiB (held through softmax and P.V); a partial last tile
+//              is padded with copies of a valid page (masked later)
 //   warp 1     TMEM owner + single-thread MMA issuer:
-//                S[128 q x 128 tok]  = Q . K^T      (SS, K-major A and B)
+//                S[128 q x 128 tok]  = Q . K^T      (TS: Q from TMEM,
+//                                                    K K-major from smem)
 //                O[128 q x 128 dim] += P . V        (TS: P from TMEM,
 //                                                    V MN-major from smem)
 //              P is split hi + lo in bf16 (two MMAs) for ~16-bit accuracy;
 //              O accumulates in TMEM across the whole piece.
-//   warps 2-9  softmax, two threads per query row (TMEM lane), 64 score
-//              columns each: tile max (pair exchange through smem), P written
+//   warps 2-9  softmax: tile max (pair exchange through smem), P written
 //              back over S with tcgen05.st, lazy rescale: the running max only
 //              moves when a tile exceeds it by > 8 (log2), and only then is
 //              the row of O in TMEM rescaled -- P <= 2^8 keeps fp32 safe.
-// TMEM: S/P buffers at columns 0 and 128, O at 256.
+//              Fan-out <= 64 uses the 16-lane layout (4 threads per row).
+// TMEM columns: S/P buffers at 0 and 128, O at 256, Q at 384.
+// Keeping Q in TMEM frees its 32 KiB of shared memory for a 4th V stage.
 #include "fk_tcgen05.cuh"
 
 #include <cstdio>
@@ -27,20 +30,26 @@ namespace fk {
 
 constexpr int kTcSoftmaxWarps = 8;
 constexpr int kTcThreads = (2 + kTcSoftmaxWarps) * 32;
-constexpr int kTcStages = 3;
+constexpr int kTcKStages = 3;                      // K ring (released right after S = Q.K^T)
+constexpr int kTcVStages = 4;                      // V ring (held through softmax and P.V)
 constexpr int kTcHalf = 128 * 128;                 // 128 rows x 128 B
 constexpr int kTcTileBytes = 2 * kTcHalf;          // one K or V tile (32 KiB)
 constexpr int kTcStageBytes = 2 * kTcTileBytes;    // K + V
-constexpr int kTcQBytes = 2 * kTcHalf;
 struct TcMisc {
-  uint64_t k_full[kTcStages], k_empty[kTcStages], v_full[kTcStages], v_empty[kTcStages];
+  uint64_t k_full[kTcKStages], k_empty[kTcKStages], v_full[kTcVStages], v_empty[kTcVStages];
   uint64_t s_full[2], p_full[2], o_done, q_full;
   uint32_t tmem_base;
   float s_max[2][2][128];  // [tile parity][half][row]
   float s_l[128];
 };
-constexpr int kTcSmem = kTcQBytes + kTcStages * kTcStageBytes + (int)sizeof(TcMisc);
+constexpr int kTcSmem = (kTcKStages + kTcVStages) * kTcTileBytes + (int)sizeof(TcMisc);
+static_assert(kTcSmem <= 232448, "prefix kernel exceeds the 227 KB opt-in shared memory");
+constexpr uint32_t kTmemQ = 384;                   // TMEM columns of Q (A operand of S = Q.K^T)
 constexpr float kRescaleThreshold = 8.0f;          // log2 units
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
 
 #ifdef FK_TIMELINE
 __device__ unsigned long long fk_tl[256];
@@ -76,9 +85,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   // all shared state is dynamic (no static smem), so the buffer starts at
   // the 1 KiB-aligned base SWIZZLE_128B needs
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem;
-  uint8_t* sKV = smem + kTcQBytes;
-  TcMisc& ms = *reinterpret_cast<TcMisc*>(smem + kTcQBytes + kTcStages * kTcStageBytes);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + kTcKStages * kTcTileBytes;
+  TcMisc& ms = *reinterpret_cast<TcMisc*>(smem + (kTcKStages + kTcVStages) * kTcTileBytes);
   uint64_t* k_full = ms.k_full;
   uint64_t* k_empty = ms.k_empty;
   uint64_t* v_full = ms.v_full;
@@ -102,9 +111,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   TL(160);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < kTcKStages; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kTcVStages; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
@@ -161,9 +172,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 #pragma unroll
       for (int j = 0; j < kTcTilePages; ++j) pl[j] = __shfl_sync(0xffffffffu, win, pg0 - wbase + (j < np ? j : 0));
       if (lane == 0) {
-        const int s = t % kTcStages;
         const int planeK = (int)plane_index(layer, 0, head, H), planeV = (int)plane_index(layer, 1, head, H);
-        uint8_t* st = sKV + s * kTcStageBytes;
         // 8 physically consecutive pages -> one 128-row box per half (the
         // common case: a context's pages come from one allocation);
         // otherwise one 16-row box per page, a partial tile padded with a
@@ -171,31 +180,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         bool run = np == kTcTilePages;
 #pragma unroll
         for (int j = 1; j < kTcTilePages; ++j) run = run && pl[j] == pl[0] + j;
-        if (t >= kTcStages) mbar_wait(&k_empty[s], ((t / kTcStages) - 1) & 1);
+        auto load_tile = [&](uint8_t* st, int plane, uint64_t* bar) {
+          mbar_expect_tx(bar, kTcTilePages * 2 * 2048);
+          if (run) {
+            tma_load_3d(st, &tmap_run, 0, pl[0] * kPage, plane, bar);
+            tma_load_3d(st + kTcHalf, &tmap_run, 64, pl[0] * kPage, plane, bar);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kTcTilePages; ++j) {
+              tma_load_3d(st + j * 2048, &tmap, 0, pl[j] * kPage, plane, bar);
+              tma_load_3d(st + kTcHalf + j * 2048, &tmap, 64, pl[j] * kPage, plane, bar);
+            }
+          }
+        };
+        const int sk = t % kTcKStages, sv = t % kTcVStages;
+        if (t >= kTcKStages) mbar_wait(&k_empty[sk], ((t / kTcKStages) - 1) & 1);
         if (t < 16) TL(128 + t);
-        mbar_expect_tx(&k_full[s], kTcTilePages * 2 * 2048);
-        if (run) {
-          tma_load_3d(st, &tmap_run, 0, pl[0] * kPage, planeK, &k_full[s]);
-          tma_load_3d(st + kTcHalf, &tmap_run, 64, pl[0] * kPage, planeK, &k_full[s]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < kTcTilePages; ++j) {
-            tma_load_3d(st + j * 2048, &tmap, 0, pl[j] * kPage, planeK, &k_full[s]);
-            tma_load_3d(st + kTcHalf + j * 2048, &tmap, 64, pl[j] * kPage, planeK, &k_full[s]);
-          }
-        }
-        if (t >= kTcStages) mbar_wait(&v_empty[s], ((t / kTcStages) - 1) & 1);
-        mbar_expect_tx(&v_full[s], kTcTilePages * 2 * 2048);
-        if (run) {
-          tma_load_3d(st + kTcTileBytes, &tmap_run, 0, pl[0] * kPage, planeV, &v_full[s]);
-          tma_load_3d(st + kTcTileBytes + kTcHalf, &tmap_run, 64, pl[0] * kPage, planeV, &v_full[s]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < kTcTilePages; ++j) {
-            tma_load_3d(st + kTcTileBytes + j * 2048, &tmap, 0, pl[j] * kPage, planeV, &v_full[s]);
-            tma_load_3d(st + kTcTileBytes + kTcHalf + j * 2048, &tmap, 64, pl[j] * kPage, planeV, &v_full[s]);
-          }
-        }
+        load_tile(sK + sk * kTcTileBytes, planeK, &k_full[sk]);
+        if (t >= kTcVStages) mbar_wait(&v_empty[sv], ((t / kTcVStages) - 1) & 1);
+        load_tile(sV + sv * kTcTileBytes, planeV, &v_full[sv]);
       }
       __syncwarp();
       tc_advance(p, c);
@@ -209,21 +212,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     if (lane == 0) {
       TcCursor cs = c0, cp = c0;
       int nitem = 0, ts = 0, tp = 0, pv_seg = 0;
-      const uint32_t qaddr = smem_u32(sQ);
       while (tp < T) {
         if (ts < T && ts <= tp + 1) {
           const bool starts = ts == 0 || cs.tile == 0;
-          const int s = ts % kTcStages;
-          if ((!starts || mbar_try_wait(&q_full, nitem & 1)) && mbar_try_wait(&k_full[s], (ts / kTcStages) & 1)) {
+          const int s = ts % kTcKStages;
+          if ((!starts || mbar_try_wait(&q_full, nitem & 1)) && mbar_try_wait(&k_full[s], (ts / kTcKStages) & 1)) {
             if (starts) ++nitem;
             if (ts < 16) TL(ts);
             tc_fence_after();
-            const uint32_t kaddr = smem_u32(sKV + s * kTcStageBytes);
+            const uint32_t kaddr = smem_u32(sK + s * kTcTileBytes);
             const int sb = ts & 1;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint32_t off = (kk >> 2) * kTcHalf + (kk & 3) * 32;
-              mma_ss(tm + sb * 128, sdesc(qaddr + off, 16, 1024), sdesc(kaddr + off, 16, 1024), kIdescQK, kk > 0);
+              mma_ts(tm + sb * 128, tm + kTmemQ + kk * 8, sdesc(kaddr + off, 16, 1024), kIdescQK, kk > 0);
             }
             mma_commit(&s_full[sb]);
             mma_commit(&k_empty[s]);
@@ -234,12 +236,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
           }
         }
         {
-          const int sb = tp & 1, s = tp % kTcStages;
-          if (tp < ts && mbar_try_wait(&p_full[sb], (tp >> 1) & 1) && mbar_try_wait(&v_full[s], (tp / kTcStages) & 1)) {
+          const int sb = tp & 1, s = tp % kTcVStages;
+          if (tp < ts && mbar_try_wait(&p_full[sb], (tp >> 1) & 1) && mbar_try_wait(&v_full[s], (tp / kTcVStages) & 1)) {
             if (tp == 0 || cp.tile == 0) pv_seg = tp;
             if (tp < 16) TL(32 + tp);
             tc_fence_after();
-            const uint32_t vaddr = smem_u32(sKV + s * kTcStageBytes + kTcTileBytes);
+            const uint32_t vaddr = smem_u32(sV + s * kTcTileBytes);
             const uint32_t p_tm = tm + sb * 128;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
@@ -258,38 +260,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     }
   } else {
     // ------------------------------------------------- softmax / epilogue
+    // Two thread->score layouts, chosen per piece:
+    //  * 32-lane (fan-out > 64): thread = one TMEM lane (query row) of its
+    //    warp's quarter, 64 score columns (half = which 64);
+    //  * 16-lane (fan-out <= 64): only lanes 0-15 of each quarter hold real
+    //    rows, so the warp reads them with the 16x32bx2 shape and each thread
+    //    owns 32 columns (sub = lane / 16 picks which 32 of its half's 64):
+    //    half the TMEM reads, exp2s and conversions per thread.
     const int quarter = warp & 3;               // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;           // which 64 score columns / 64 O columns
-    const int row = quarter * 32 + lane;
+    const int row = quarter * 32 + lane;        // Q staging row (32-lane view)
     // query j sits in TMEM lane 32*(j%4) + j/4: a partial block spreads its
     // rows over all four lane quarters, i.e. over all four SM sub-partitions
     const int qj = 4 * lane + quarter;
+    const int sub = lane >> 4;
+    const int row16 = quarter * 32 + (lane & 15);
+    const int qj16 = 4 * (lane & 15) + quarter;
     const uint32_t lane_tm = tm + ((uint32_t)(quarter * 32) << 16);
     const int bar_id = 1 + quarter;             // named barrier of the two warps sharing these rows
     TcCursor c = c0;
     float m = -INFINITY, l = 0.f;
     int nq = 0, head = 0, ntok = 0, seg_start = 0;
-    bool active = false;
+    bool active = false, r16 = false;
     for (int t = 0; t < T; ++t) {
       const int item = c.item;
       if (t == 0 || c.tile == 0) {
-        // new piece: stage this thread's half of its Q row (SW128 K-major)
+        // new piece: this thread's half of its Q row -> TMEM (A operand of
+        // S = Q.K^T: row = lane, 2 bf16 per 32-bit column)
         seg_start = t;
         nq = p.it_nq[item];
         head = p.it_head[item];
         ntok = p.it_ntok[item];
         active = quarter < nq;
+        r16 = nq <= 64;
         const bool real = qj < nq;
-        const uint4* src = real ? reinterpret_cast<const uint4*>(
-                                      q + ((long long)p.qrows[p.it_q_off[item] + qj] * H + head) * kHeadDim)
-                                : nullptr;
+        uint32_t qr[32];
+        if (real) {
+          const uint4* src = reinterpret_cast<const uint4*>(
+              q + ((long long)p.qrows[p.it_q_off[item] + qj] * H + head) * kHeadDim) + half * 8;
 #pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-          const int cch = half * 8 + k8;
-          const uint4 v = real ? src[cch] : make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(sQ + half * kTcHalf + row * 128 + ((k8 ^ (row & 7)) << 4)) = v;
+          for (int k8 = 0; k8 < 8; ++k8) {
+            const uint4 v = src[k8];
+            qr[4 * k8] = v.x;
+            qr[4 * k8 + 1] = v.y;
+            qr[4 * k8 + 2] = v.z;
+            qr[4 * k8 + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) qr[i] = 0u;
         }
-        fence_proxy_async();
+        tmem_st32(lane_tm + kTmemQ + half * 32, qr);
+        tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&q_full);
         m = -INFINITY;
@@ -299,123 +322,158 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       mbar_wait(&s_full[sb], (t >> 1) & 1);
       if (warp == 4 && lane == 0 && t < 16) TL(64 + t);
       tc_fence_after();
+      // o_done completes once per PV.  s_full(t) implies PV(t-2) is done
+      // (issued before S(t), in-order pipe) and PV(t) needs P(t), so here
+      // the barrier has completed phase t-2 or t-1: a parity wait for t-1
+      // is unambiguous.  A piece end must retire PV(t-1) before P(t) is
+      // released, so its later wait for PV(t) is unambiguous too.
+      const bool piece_end = c.tile + 1 == p.it_units[item] || t == T - 1;
       if (active) {
-        const int valid = ntok - c.tile * 128 - half * 64;  // valid columns among this thread's 64
-        const uint32_t s_tm = lane_tm + sb * 128 + half * 64;
-        uint32_t r0[32], r1[32];
-        tmem_ld32(s_tm, r0);
-        tmem_ld32(s_tm + 32, r1);
-        tmem_wait_ld();
-        if (warp == 4 && lane == 0 && t < 16) TL(176 + t);
-        float mx;
-        if (valid >= 64) {  // full tile: tree max, no masking
-          float t8[8];
+        auto tile = [&](auto mode) {
+          constexpr bool R16 = decltype(mode)::value;
+          constexpr int NCH = R16 ? 1 : 2;  // 32-column chunks per thread
+          const int my_row = R16 ? row16 : row;
+          const int col0 = half * 64 + (R16 ? sub * 32 : 0);
+          const int valid = ntok - c.tile * 128 - col0;  // valid columns among this thread's
+          const uint32_t s_tm = lane_tm + sb * 128 + half * 64;
+          uint32_t r[NCH][32];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            t8[k] = fmaxf(fmaxf(__uint_as_float(r0[4 * k]), __uint_as_float(r0[4 * k + 1])),
-                          fmaxf(__uint_as_float(r0[4 * k + 2]), __uint_as_float(r0[4 * k + 3])));
-            t8[k] = fmaxf(t8[k], fmaxf(fmaxf(__uint_as_float(r1[4 * k]), __uint_as_float(r1[4 * k + 1])),
-                                       fmaxf(__uint_as_float(r1[4 * k + 2]), __uint_as_float(r1[4 * k + 3]))));
+          for (int cc = 0; cc < NCH; ++cc) {
+            if (R16) tmem_ld16x2(s_tm, r[cc]);
+            else tmem_ld32(s_tm + cc * 32, r[cc]);
           }
-          mx = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])), fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7])));
-        } else {
-          mx = -INFINITY;
+          tmem_wait_ld();
+          if (warp == 4 && lane == 0 && t < 16) TL(176 + t);
+          float mx = -INFINITY;
+          if (valid >= 32 * NCH) {  // full: tree max, no masking
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            if (e < valid) mx = fmaxf(mx, __uint_as_float(r0[e]));
-            if (e + 32 < valid) mx = fmaxf(mx, __uint_as_float(r1[e]));
-          }
-        }
-        s_max[sb][half][row] = mx;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        if (warp == 4 && lane == 0 && t < 16) TL(192 + t);
-        const float tile_max = fmaxf(mx, s_max[sb][half ^ 1][row]) * scale_log2;
-        // lazy rescale: keep the running max unless the tile exceeds it by > 8
-        if (tile_max > m + kRescaleThreshold) {
-          const float m_new = tile_max;
-          if (t > seg_start) {
-            const float alpha = ex2(m - m_new);
-            l *= alpha;
-            mbar_wait(&o_done, (t - 1) & 1);  // PV(t-1) has landed in O
-            tc_fence_after();
-            const uint32_t o_tm = lane_tm + 256 + half * 64;
+            for (int cc = 0; cc < NCH; ++cc) {
+              float t8[8];
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              uint32_t o[32];
-              tmem_ld32(o_tm + cc * 32, o);
-              tmem_wait_ld();
-#pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st32(o_tm + cc * 32, o);
+              for (int k = 0; k < 8; ++k)
+                t8[k] = fmaxf(fmaxf(__uint_as_float(r[cc][4 * k]), __uint_as_float(r[cc][4 * k + 1])),
+                              fmaxf(__uint_as_float(r[cc][4 * k + 2]), __uint_as_float(r[cc][4 * k + 3])));
+              mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
+                                   fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7]))));
             }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < NCH; ++cc)
+#pragma unroll
+              for (int e = 0; e < 32; ++e)
+                if (cc * 32 + e < valid) mx = fmaxf(mx, __uint_as_float(r[cc][e]));
           }
-          m = m_new;
-        }
-        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-        const bool full = valid >= 64;
+          if (R16) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+          s_max[sb][half][my_row] = mx;
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          if (warp == 4 && lane == 0 && t < 16) TL(192 + t);
+          const float tile_max = fmaxf(mx, s_max[sb][half ^ 1][my_row]) * scale_log2;
+          // lazy rescale: keep the running max unless the tile exceeds it by > 8
+          const bool rescale = tile_max > m + kRescaleThreshold;
+          if (t > 0 && ((rescale && t > seg_start) || piece_end)) mbar_wait(&o_done, (t - 1) & 1);
+          if (rescale) {
+            if (t > seg_start) {
+              const float alpha = ex2(m - tile_max);
+              l *= alpha;
+              tc_fence_after();
+              const uint32_t o_tm = lane_tm + 256 + half * 64;
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const uint32_t* r = cc == 0 ? r0 : r1;
-          // per 16-token k-step: 8 columns of bf16x2 P_hi then 8 of P_lo
-          uint32_t pk[32];
+              for (int cc = 0; cc < NCH; ++cc) {
+                uint32_t o[32];
+                if (R16) tmem_ld16x2(o_tm, o);
+                else tmem_ld32(o_tm + cc * 32, o);
+                tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int c2 = cc * 32 + 2 * e;
-            float p0 = ex2(fmaf(__uint_as_float(r[2 * e]), scale_log2, -m));
-            float p1 = ex2(fmaf(__uint_as_float(r[2 * e + 1]), scale_log2, -m));
-            if (!full) {
-              p0 = c2 < valid ? p0 : 0.f;
-              p1 = c2 + 1 < valid ? p1 : 0.f;
+                for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                if (R16) tmem_st16x2(o_tm, o);
+                else tmem_st32(o_tm + cc * 32, o);
+              }
             }
-            sum4[e & 3] += p0 + p1;
-            const uint32_t hpk = pack_bf16(p0, p1);
-            pk[(e >> 3) * 16 + (e & 7)] = hpk;
-            pk[(e >> 3) * 16 + 8 + (e & 7)] = pack_bf16(p0 - bf_lo(hpk), p1 - bf_hi(hpk));
+            m = tile_max;
           }
-          tmem_st32(s_tm + cc * 32, pk);
-        }
-        const float sum = (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
-        if (warp == 4 && lane == 0 && t < 16) TL(208 + t);
-        tmem_wait_st();
-        if (warp == 4 && lane == 0 && t < 16) TL(224 + t);
-        l += sum;
+          float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+          const bool full = valid >= 32 * NCH;
+#pragma unroll
+          for (int cc = 0; cc < NCH; ++cc) {
+            // per 16-token k-step: 8 columns of bf16x2 P_hi then 8 of P_lo.
+            // hi = p truncated to bf16, lo = (p - hi) truncated: ~16 mantissa
+            // bits from two byte-permutes and one subtract (no F2F converts)
+            uint32_t pk[32];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int c2 = cc * 32 + 2 * e;
+              float p0 = ex2(fmaf(__uint_as_float(r[cc][2 * e]), scale_log2, -m));
+              float p1 = ex2(fmaf(__uint_as_float(r[cc][2 * e + 1]), scale_log2, -m));
+              if (!full) {
+                p0 = c2 < valid ? p0 : 0.f;
+                p1 = c2 + 1 < valid ? p1 : 0.f;
+              }
+              sum4[e & 3] += p0 + p1;
+              const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
+              pk[(e >> 3) * 16 + (e & 7)] = __byte_perm(u0, u1, 0x7632);
+              const float l0 = p0 - __uint_as_float(u0 & 0xFFFF0000u);
+              const float l1 = p1 - __uint_as_float(u1 & 0xFFFF0000u);
+              pk[(e >> 3) * 16 + 8 + (e & 7)] = __byte_perm(__float_as_uint(l0), __float_as_uint(l1), 0x7632);
+            }
+            if (R16) tmem_st16x2(s_tm, pk);
+            else tmem_st32(s_tm + cc * 32, pk);
+          }
+          l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+          if (warp == 4 && lane == 0 && t < 16) TL(208 + t);
+          tmem_wait_st();
+          if (warp == 4 && lane == 0 && t < 16) TL(224 + t);
+        };
+        if (r16) tile(BoolC<true>{});
+        else tile(BoolC<false>{});
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[sb]);
       if (warp == 4 && lane == 0 && t < 16) TL(80 + t);
-      const bool last = c.tile + 1 == p.it_units[item];
-      if (last || t == T - 1) {
+      if (piece_end) {
         // piece end: O (unnormalised, running max m) -> partial slot
         mbar_wait(&o_done, t & 1);
         if (warp == 4 && lane == 0 && t < 16) TL(96 + t);
         tc_fence_after();
         if (active) {
-          const int piece = blockIdx.x - p.it_unit_off[item] / p.tc_per;
-          const bool real = qj < nq;
-          long long pi = 0;
-          if (real) {
-            const int r = p.qrows[p.it_q_off[item] + qj];
-            const int k = p.qslot[p.it_qslot_off[item] + qj] + piece;
-            pi = part_index(p, H, r, k, head);
-          }
-          const uint32_t o_tm = lane_tm + 256 + half * 64;
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(o_tm + cc * 32, o);
-            tmem_wait_ld();
+          auto epilogue = [&](auto mode) {
+            constexpr bool R16 = decltype(mode)::value;
+            constexpr int NCH = R16 ? 1 : 2;
+            const int my_row = R16 ? row16 : row;
+            const int my_q = R16 ? qj16 : qj;
+            const int col0 = half * 64 + (R16 ? sub * 32 : 0);
+            const int piece = blockIdx.x - p.it_unit_off[item] / p.tc_per;
+            const bool real = my_q < nq;
+            long long pi = 0;
             if (real) {
-              float4* po = reinterpret_cast<float4*>(a.part_o + pi * kHeadDim + half * 64 + cc * 32);
-#pragma unroll
-              for (int i4 = 0; i4 < 8; ++i4)
-                po[i4] = make_float4(__uint_as_float(o[4 * i4]), __uint_as_float(o[4 * i4 + 1]),
-                                     __uint_as_float(o[4 * i4 + 2]), __uint_as_float(o[4 * i4 + 3]));
+              const int r = p.qrows[p.it_q_off[item] + my_q];
+              const int k = p.qslot[p.it_qslot_off[item] + my_q] + piece;
+              pi = part_index(p, H, r, k, head);
             }
-          }
-          if (half == 1) s_l[row] = l;
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-          if (half == 0 && real) a.part_ml[pi] = make_float2(m, l + s_l[row]);
+            const uint32_t o_tm = lane_tm + 256 + half * 64;
+#pragma unroll
+            for (int cc = 0; cc < NCH; ++cc) {
+              uint32_t o[32];
+              if (R16) tmem_ld16x2(o_tm, o);
+              else tmem_ld32(o_tm + cc * 32, o);
+              tmem_wait_ld();
+              if (real) {
+                float4* po = reinterpret_cast<float4*>(a.part_o + pi * kHeadDim + col0 + cc * 32);
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4)
+                  po[i4] = make_float4(__uint_as_float(o[4 * i4]), __uint_as_float(o[4 * i4 + 1]),
+                                       __uint_as_float(o[4 * i4 + 2]), __uint_as_float(o[4 * i4 + 3]));
+              }
+            }
+            float lr = l;
+            if (R16) lr += __shfl_xor_sync(0xffffffffu, lr, 16);
+            const bool lead = !R16 || sub == 0;
+            if (half == 1 && lead) s_l[my_row] = lr;
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            if (half == 0 && lead && real) a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
+          };
+          if (r16) epilogue(BoolC<true>{});
+          else epilogue(BoolC<false>{});
         }
         tc_fence_before();
         if (warp == 4 && lane == 0 && t < 16) TL(112 + t);

@@ -203,3 +203,14 @@ def test_engine_pages_are_physical_and_logical_ids_monotonic(cuda_device):
     logical, physical = eng.context_pages("e0.c0")
     assert logical == list(range(4))
     assert len(set(physical)) == 4
+
+
+@pytest.mark.parametrize("corun", [0, 1])
+def test_corun_and_serial_sm_split(cuda_device, corun):
+    """FK_OPT_CORUN=1 splits the SMs between the tcgen05 prefix CTAs and the
+    private stream (launched back to back); 0 gives each kernel every SM."""
+    eng = make_engine(cuda_device, H=8, L=2)
+    eng.set_option(_lib.FK_OPT_CORUN, corun)
+    fork_group(eng, 1500, [300, 17, 64, 250, 129] * 4, out_len=3)
+    run_steps(eng, 3)
+    check_history(eng)
