@@ -141,6 +141,10 @@ def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=409
         fork_group(eng, cfg["P"], [cfg["S"]] * cfg["B"], out_len=out_len, seed=seed)
     drain_fills(eng)
     rows = len(eng.gens)
+    # back the whole run's decode growth now, so no arena growth (a device-wide
+    # copy) lands in the timed region
+    st = eng.pool_stats()
+    eng.reserve_pages(st.num_pages - st.free_pages + rows * (out_len // 16 + 2))
     shape = (L, rows, H, 128)
     gen = torch.Generator(device="cpu").manual_seed(seed)
     q = torch.randn(shape, generator=gen).to(torch.bfloat16)

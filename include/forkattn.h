@@ -101,7 +101,7 @@ enum {
   FK_OPT_CORUN = 5,           /* 1 (default): tcgen05 prefix CTAs and the private stream split the
                                  SMs and run concurrently; 0: each kernel gets every SM in turn */
   FK_OPT_PREFIX_RATE_PCT = 6, /* co-run SM split: prefix per-SM KV rate relative to the private
-                                 stream's, in percent (default 80) */
+                                 stream's, in percent (default 50) */
   FK_OPT_PDL = 7              /* 1 (default): programmatic dependent launch between a layer's
                                  kernels; 0: plain stream order */
 };

@@ -93,7 +93,7 @@ struct fk_pool {
   int64_t pdl = 1;  // programmatic dependent launch between the layer's kernels
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
-  int64_t prefix_rate_pct = 80;  // prefix KV bytes/s per SM relative to the private stream's
+  int64_t prefix_rate_pct = 50;  // prefix KV bytes/s per SM relative to the private stream's (measured optimum, headline)
 
   // plan (host mirror + device)
   PlanSlot slots[2];
@@ -197,7 +197,9 @@ int ensure_scratch(fk_pool* p, int rows, int slots) {
   const size_t H = p->desc.num_heads, D = p->desc.head_dim;
   const size_t need = (size_t)std::max(rows, 1) * std::max(slots, 1) * H;
   if (need > p->part_cap) {
-    size_t cap = std::max(need, p->part_cap * 2);
+    // headroom: max_slots moves by one as suffixes cross page boundaries, and
+    // every reallocation is a device-wide sync (cudaFree)
+    size_t cap = std::max(need + need / 2, p->part_cap * 2);
     if (p->part_o) FK_CUDA(cudaFree(p->part_o));
     if (p->part_ml) FK_CUDA(cudaFree(p->part_ml));
     p->part_o = nullptr;
@@ -211,7 +213,8 @@ int ensure_scratch(fk_pool* p, int rows, int slots) {
 
 int ensure_slot(fk_pool* p, PlanSlot& s, size_t bytes) {
   if (bytes <= s.cap) return FK_OK;
-  size_t cap = std::max(bytes, s.cap * 2);
+  // pinned allocations are slow: start at 256 KiB and double
+  size_t cap = std::max({bytes + bytes / 2, s.cap * 2, (size_t)256 << 10});
   if (s.armed) FK_CUDA(cudaEventSynchronize(s.done));
   if (s.host) FK_CUDA(cudaFreeHost(s.host));
   if (s.dev) FK_CUDA(cudaFree(s.dev));

@@ -354,6 +354,12 @@ class GpuEngine:
     def set_option(self, option: int, value: int) -> None:
         self._pool.set_option(option, value)
 
+    def reserve_pages(self, num_pages: int) -> None:
+        """Back at least `num_pages` physical pages now (fk_pool_reserve_pages).
+        The arena otherwise grows on demand, and a growth is a device-wide
+        copy of every live page -- do it before latency matters."""
+        _lib.check(_lib.lib.fk_pool_reserve_pages(self._pool.handle, int(num_pages)))
+
     def pool_stats(self) -> _lib.PoolStats:
         return self._pool.stats()
 
@@ -573,13 +579,84 @@ class GpuEngine:
                                          ctypes.byref(self.last_plan)))
         return int(self.last_plan.batch_tokens)
 
+    def _host_pipeline(self, shape):
+        """Device buffers, copy streams and per-layer events for host-resident
+        TensorDecodeModel rows (allocated once per shape)."""
+        torch = self._torch
+        hp = getattr(self, "_hp", None)
+        if hp is None or hp["shape"] != shape:
+            L = shape[0]
+            with torch.cuda.device(self._dev):
+                hp = {
+                    "shape": shape,
+                    "q": torch.empty(shape, dtype=torch.bfloat16, device=self._dev),
+                    "k": torch.empty(shape, dtype=torch.bfloat16, device=self._dev),
+                    "v": torch.empty(shape, dtype=torch.bfloat16, device=self._dev),
+                    "out": torch.empty(shape, dtype=torch.bfloat16, device=self._dev),
+                    "h2d": torch.cuda.Stream(self._dev),
+                    "d2h": torch.cuda.Stream(self._dev),
+                    "ev_q": [torch.cuda.Event() for _ in range(L)],
+                    "ev_o": [torch.cuda.Event() for _ in range(L)],
+                    "ev_kv": torch.cuda.Event(),
+                    "ev_d2h": torch.cuda.Event(),
+                    "ev_step": None,
+                }
+            self._hp = hp
+        return hp
+
+    def _decode_attention_host(self, running: List[GenerationTask]) -> None:
+        """Host (pinned) Q/K/V in, host output out, pipelined per layer: the
+        H2D copy of layer l+1's Q and the D2H copy of layer l-1's output run
+        on their own streams (copy engines) under layer l's attention."""
+        torch = self._torch
+        geo = self.geometry
+        model = self.model
+        B = len(running)
+        shape = (geo.num_layers, B, geo.num_heads, geo.head_dim)
+        hp = self._host_pipeline(shape)
+        st, h2d, d2h = self._stream, hp["h2d"], hp["d2h"]
+        if model.host_out is None or tuple(model.host_out.shape) != shape:
+            model.host_out = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
+        with torch.cuda.device(self._dev):
+            if hp["ev_step"] is not None:  # the previous step is done with the buffers
+                h2d.wait_event(hp["ev_step"])
+                d2h.wait_event(hp["ev_step"])
+            with torch.cuda.stream(h2d):
+                for layer in range(geo.num_layers):
+                    hp["q"][layer].copy_(model.q[layer], non_blocking=True)
+                    hp["ev_q"][layer].record(h2d)
+                if model.k is not None:
+                    hp["k"].copy_(model.k, non_blocking=True)
+                    hp["v"].copy_(model.v, non_blocking=True)
+                    hp["ev_kv"].record(h2d)
+            q, out = hp["q"], hp["out"]
+            layer_elems = B * geo.num_heads * geo.head_dim
+            for layer in range(geo.num_layers):
+                st.wait_event(hp["ev_q"][layer])
+                _lib.check(_lib.lib.fk_attn_decode(self._pool.handle, layer,
+                                                   ctypes.c_void_p(q.data_ptr() + layer * layer_elems * 2),
+                                                   ctypes.c_void_p(out.data_ptr() + layer * layer_elems * 2),
+                                                   None, self._sp()))
+                hp["ev_o"][layer].record(st)
+                d2h.wait_event(hp["ev_o"][layer])
+                with torch.cuda.stream(d2h):
+                    model.host_out[layer].copy_(out[layer], non_blocking=True)
+            hp["ev_d2h"].record(d2h)
+            st.wait_event(hp["ev_d2h"])  # the step completes with its output on the host
+        self.last_output = out
+        self.last_output_f32 = None
+        self.last_rows = [g.request_id for g in running]
+
     def _decode_attention(self, running: List[GenerationTask]) -> None:
         torch = self._torch
         geo = self.geometry
         B = len(running)
         shape = (geo.num_layers, B, geo.num_heads, geo.head_dim)
+        model = self.model
+        if isinstance(model, TensorDecodeModel) and model.q.device.type != "cuda" and not self.capture_f32:
+            self._decode_attention_host(running)
+            return
         with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
-            model = self.model
             if isinstance(model, TensorDecodeModel):
                 q = model.q
                 if q.device.type != "cuda":
@@ -615,7 +692,12 @@ class GpuEngine:
             geo = self.geometry
             with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
                 k, v = model.k, model.v
-                if k.device.type != "cuda":
+                hp = getattr(self, "_hp", None)
+                if k.device.type != "cuda" and hp is not None and hp["shape"] == tuple(k.shape):
+                    # copied in under this step's attention (_decode_attention_host)
+                    self._stream.wait_event(hp["ev_kv"])
+                    k, v = hp["k"], hp["v"]
+                elif k.device.type != "cuda":
                     k = k.to(self._dev, non_blocking=True)
                     v = v.to(self._dev, non_blocking=True)
                 _lib.check(_lib.lib.fk_append_kv_layers(self._pool.handle, 0, geo.num_layers,
@@ -624,6 +706,11 @@ class GpuEngine:
         else:
             _lib.check(_lib.lib.fk_synth_append(self._pool.handle, self.model_seed, self.model_k_scale,
                                                 self._sp()))
+        hp = getattr(self, "_hp", None)
+        if hp is not None:  # next step's copies may reuse the buffers after this point
+            if hp["ev_step"] is None:
+                hp["ev_step"] = torch.cuda.Event()
+            hp["ev_step"].record(self._stream)
 
     def _snapshot(self, running: List[GenerationTask]) -> List[List[Tuple[int, int]]]:
         """Per row: [(context uid, tokens)] root -> leaf at plan time."""

@@ -38,7 +38,7 @@ def main(path):
         b = m.get("dram__bytes_read.sum", [])
         mt = sum(t) / len(t) if t else 0
         mb = sum(b) / len(b) if b else 0
-        print(f"{k:32s} {len(t):5d} {mt:9.2f} {sum(t)/total:6.1%} {mb:9.1f} {mb/mt*1e-3 if mt else 0:8.0f}")
+        print(f"{k:32s} {len(t):5d} {mt:9.2f} {sum(t)/total:6.1%} {mb:9.1f} {mb/mt*1e3 if mt else 0:8.0f}")
 
 
 if __name__ == "__main__":
