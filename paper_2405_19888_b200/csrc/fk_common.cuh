@@ -75,6 +75,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
+
+// Debug builds (-DFK_TIMELINE): per-CTA start/end stamps of the attention
+// kernels, read back with fk_debug_cta_timeline (profiles/cta_timeline.py).
+#ifdef FK_TIMELINE
+#define CTA_TL_DECL(name) __device__ unsigned long long name[1024][2]
+#define CTA_TL_START(name) do { if (threadIdx.x == 0 && blockIdx.x < 1024) name[blockIdx.x][0] = global_ns(); } while (0)
+#define CTA_TL_END(name) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) name[blockIdx.x][1] = global_ns(); } while (0)  // last writer ~ last warp
+#else
+#define CTA_TL_DECL(name) static_assert(true, "")
+#define CTA_TL_START(name) do { } while (0)
+#define CTA_TL_END(name) do { } while (0)
+#endif
+
 // Launch with optional programmatic dependent launch (PDL): the kernel may
 // start while its stream predecessor is still running; it must call
 // pdl_wait_primary() before touching the predecessor's results.

@@ -39,6 +39,8 @@ struct UnitMeta {
   int pg, ntok, row, head;
 };
 
+CTA_TL_DECL(fk_tl_cta_priv);
+
 // Streaming warps only write partials; fk_merge_kernel combines them.
 // With PDL this grid can start while the prefix grid of the same layer is
 // still running (disjoint partial slots); thread 0 of each CTA waits for that
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
+  CTA_TL_START(fk_tl_cta_priv);
   pdl_launch_dependents();  // the merge kernel may launch now (it waits for us)
   PdlTail tail;             // on exit: this grid completes only after the prefix grid
 
@@ -250,6 +253,18 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
       hi = load_meta(wbase + 32);
     }
   }
+  CTA_TL_END(fk_tl_cta_priv);
+}
+
+extern "C" int fk_debug_cta_timeline_priv(unsigned long long* out, int n) {
+#ifdef FK_TIMELINE
+  if (cudaDeviceSynchronize() != cudaSuccess) return 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_priv, sizeof(unsigned long long) * 2 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+#else
+  (void)out;
+  (void)n;
+  return 5;
+#endif
 }
 
 // ======================================================= prefix (mma.sync)
@@ -451,7 +466,8 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
 // + private pieces) in log2 space and writes the bf16 row (fp32 optional).
 __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __nv_bfloat16* __restrict__ out,
                                                       float* __restrict__ out_f32) {
-  pdl_wait_primary();  // partials of the prefix and private grids are complete
+  pdl_wait_primary();       // partials of the prefix and private grids are complete
+  pdl_launch_dependents();  // the next layer's first kernel may start (other partial half)
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int H = a.num_heads;
   if (w >= p.num_rows * H) return;

@@ -90,7 +90,7 @@ struct fk_pool {
   int64_t tc_min_fanout = 2;  // tcgen05 for every shared context until the sweep says otherwise
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
-  int64_t pdl = 1;  // programmatic dependent launch between the layer's kernels
+  int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
   int64_t prefix_rate_pct = 50;  // prefix KV bytes/s per SM relative to the private stream's (measured optimum, headline)
@@ -108,7 +108,8 @@ struct fk_pool {
   // scratch
   float* part_o = nullptr;
   float2* part_ml = nullptr;
-  size_t part_cap = 0;     // entries (rows*slots*H)
+  size_t part_cap = 0;     // entries (rows*slots*H) per half
+  int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
 
   ArenaDev arena() const {
     ArenaDev a;
@@ -204,8 +205,10 @@ int ensure_scratch(fk_pool* p, int rows, int slots) {
     if (p->part_ml) FK_CUDA(cudaFree(p->part_ml));
     p->part_o = nullptr;
     p->part_ml = nullptr;
-    FK_CUDA(cudaMalloc(&p->part_o, cap * D * sizeof(float)));
-    FK_CUDA(cudaMalloc(&p->part_ml, cap * sizeof(float2)));
+    // two halves: consecutive fk_attn_decode launches alternate, so a layer's
+    // kernels may start (PDL) while the previous layer's merge still reads
+    FK_CUDA(cudaMalloc(&p->part_o, 2 * cap * D * sizeof(float)));
+    FK_CUDA(cudaMalloc(&p->part_ml, 2 * cap * sizeof(float2)));
     p->part_cap = cap;
   }
   return FK_OK;
@@ -862,14 +865,23 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   cudaStream_t st = (cudaStream_t)stream;
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p->desc.head_dim));
   ArenaDev a = p->arena();
+  if (p->launch_parity) {
+    a.part_o += p->part_cap * p->desc.head_dim;
+    a.part_ml += p->part_cap;
+  }
+  p->launch_parity ^= 1;
   const bool has_mma = p->plan.tc_begin > 0;
   const bool has_tc = p->plan.num_items > p->plan.tc_begin;
+  // cross-layer PDL: this layer's first kernel may start while the previous
+  // layer's merge runs (it writes the other half of the partials and reads
+  // q only after griddepcontrol.wait); never behind the mma prefix kernel
+  const bool xl = p->pdl >= 2 && !has_mma;
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
   // K2 (shared prefixes) and K3 (private streams) only write partials, so
   // their order is free; K4 merges every (row, head) afterwards.
   auto run_prefix = [&]() -> int {
     if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
-    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, st));
+    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, xl, st));
     return FK_OK;
   };
   // the private grid may overlap the prefix grid (PDL) only when that grid
@@ -877,7 +889,8 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_order == 0) {
     int rc = run_prefix();
     if (rc != FK_OK) return rc;
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, p->pdl && (has_mma || has_tc), st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap,
+                           (p->pdl && (has_mma || has_tc)) || (xl && !has_tc), st));
   } else {
     FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, false, st));
     int rc = run_prefix();

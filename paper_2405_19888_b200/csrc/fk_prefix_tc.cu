@@ -34,7 +34,6 @@ constexpr int kTcKStages = 3;                      // K ring (released right aft
 constexpr int kTcVStages = 4;                      // V ring (held through softmax and P.V)
 constexpr int kTcHalf = 128 * 128;                 // 128 rows x 128 B
 constexpr int kTcTileBytes = 2 * kTcHalf;          // one K or V tile (32 KiB)
-constexpr int kTcStageBytes = 2 * kTcTileBytes;    // K + V
 struct TcMisc {
   uint64_t k_full[kTcKStages], k_empty[kTcKStages], v_full[kTcVStages], v_empty[kTcVStages];
   uint64_t s_full[2], p_full[2], o_done, q_full;
@@ -44,7 +43,8 @@ struct TcMisc {
 };
 constexpr int kTcSmem = (kTcKStages + kTcVStages) * kTcTileBytes + (int)sizeof(TcMisc);
 static_assert(kTcSmem <= 232448, "prefix kernel exceeds the 227 KB opt-in shared memory");
-constexpr uint32_t kTmemQ = 384;                   // TMEM columns of Q (A operand of S = Q.K^T)
+constexpr uint32_t kTmemQ = 384;                   // TMEM columns of Q (A operand of S = Q.K^T):
+                                                   // two 64-column buffers, piece k uses k & 1
 constexpr float kRescaleThreshold = 8.0f;          // log2 units
 template <bool B>
 struct BoolC {
@@ -57,6 +57,8 @@ __device__ unsigned long long fk_tl[256];
 #else
 #define TL(i) do { } while (0)
 #endif
+
+CTA_TL_DECL(fk_tl_cta_prefix);
 
 // unit cursor over the tcgen05 items of the plan
 struct TcCursor {
@@ -105,10 +107,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   const int H = a.num_heads;
   const int u0 = blockIdx.x * p.tc_per;
   const int u1 = min(p.tc_units, u0 + p.tc_per);
-  pdl_launch_dependents();  // the private grid may start on SMs we release
+  pdl_launch_dependents();  // the private grid may start on the SMs we leave free
   if (u0 >= u1) return;
   const int T = u1 - u0;
   TL(160);
+  CTA_TL_START(fk_tl_cta_prefix);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcKStages; ++s) {
@@ -149,17 +152,44 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       prefetch_tmap(&tmap_run);
     }
     TcCursor c = c0;
-    int cur_item = -1, head = 0, npi = 0, poff = 0;
-    int wbase = 0, win = 0, nwin = 0;
+    // the next item's metadata is fetched one tile after switching to the
+    // current item and its first page window one tile later, so an item
+    // switch never waits on a dependent global load
+    int cur_item = c0.item, head = p.it_head[c0.item], npi = p.it_npages[c0.item], poff = p.it_page_off[c0.item];
+    int wbase = c0.tile * kTcTilePages;
+    int win = wbase + lane < npi ? p.pages[poff + wbase + lane] : 0;
+    int nwin = wbase + 32 + lane < npi ? p.pages[poff + wbase + 32 + lane] : 0;
+    int n_head = 0, n_npi = 0, n_poff = 0, n_win = 0, n_nwin = 0, n_stage = 0;  // 0 none, 1 meta, 2 + window
     for (int t = 0; t < T; ++t) {
       if (c.item != cur_item) {
+        if (n_stage < 1) {
+          n_head = p.it_head[c.item];
+          n_npi = p.it_npages[c.item];
+          n_poff = p.it_page_off[c.item];
+        }
+        if (n_stage < 2) {
+          n_win = lane < n_npi ? p.pages[n_poff + lane] : 0;
+          n_nwin = 32 + lane < n_npi ? p.pages[n_poff + 32 + lane] : 0;
+        }
         cur_item = c.item;
-        head = p.it_head[cur_item];
-        npi = p.it_npages[cur_item];
-        poff = p.it_page_off[cur_item];
-        wbase = c.tile * kTcTilePages;
-        win = wbase + lane < npi ? p.pages[poff + wbase + lane] : 0;
-        nwin = wbase + 32 + lane < npi ? p.pages[poff + wbase + 32 + lane] : 0;
+        head = n_head;
+        npi = n_npi;
+        poff = n_poff;
+        wbase = 0;  // a later item always starts at its tile 0
+        win = n_win;
+        nwin = n_nwin;
+        n_stage = 0;
+      } else if (cur_item + 1 < p.num_items) {
+        if (n_stage == 1) {
+          n_win = lane < n_npi ? p.pages[n_poff + lane] : 0;
+          n_nwin = 32 + lane < n_npi ? p.pages[n_poff + 32 + lane] : 0;
+          n_stage = 2;
+        } else if (n_stage == 0) {
+          n_head = p.it_head[cur_item + 1];
+          n_npi = p.it_npages[cur_item + 1];
+          n_poff = p.it_page_off[cur_item + 1];
+          n_stage = 1;
+        }
       }
       const int pg0 = c.tile * kTcTilePages;
       if (pg0 >= wbase + 32) {  // slide the window
@@ -218,6 +248,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
           const int s = ts % kTcKStages;
           if ((!starts || mbar_try_wait(&q_full, nitem & 1)) && mbar_try_wait(&k_full[s], (ts / kTcKStages) & 1)) {
             if (starts) ++nitem;
+            const uint32_t q_tm = tm + kTmemQ + (uint32_t)(((nitem - 1) & 1) * 64);
             if (ts < 16) TL(ts);
             tc_fence_after();
             const uint32_t kaddr = smem_u32(sK + s * kTcTileBytes);
@@ -225,7 +256,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint32_t off = (kk >> 2) * kTcHalf + (kk & 3) * 32;
-              mma_ts(tm + sb * 128, tm + kTmemQ + kk * 8, sdesc(kaddr + off, 16, 1024), kIdescQK, kk > 0);
+              mma_ts(tm + sb * 128, q_tm + kk * 8, sdesc(kaddr + off, 16, 1024), kIdescQK, kk > 0);
             }
             mma_commit(&s_full[sb]);
             mma_commit(&k_empty[s]);
@@ -282,39 +313,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     float m = -INFINITY, l = 0.f;
     int nq = 0, head = 0, ntok = 0, seg_start = 0;
     bool active = false, r16 = false;
+    // Q of piece k -> TMEM buffer k & 1 (this thread's half of its row; the
+    // A operand layout of S = Q.K^T: row = lane, 2 bf16 per 32-bit column).
+    // Piece k+1's Q is staged while piece k's last P.V runs, so S of the
+    // next piece does not wait for the epilogue.
+    auto stage_q = [&](int it, int k) {
+      const int nq_i = p.it_nq[it];
+      uint32_t qr[32];
+      if (qj < nq_i) {
+        const uint4* src = reinterpret_cast<const uint4*>(
+            q + ((long long)p.qrows[p.it_q_off[it] + qj] * H + p.it_head[it]) * kHeadDim) + half * 8;
+#pragma unroll
+        for (int k8 = 0; k8 < 8; ++k8) {
+          const uint4 v = src[k8];
+          qr[4 * k8] = v.x;
+          qr[4 * k8 + 1] = v.y;
+          qr[4 * k8 + 2] = v.z;
+          qr[4 * k8 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) qr[i] = 0u;
+      }
+      tmem_st32(lane_tm + kTmemQ + (uint32_t)((k & 1) * 64) + half * 32, qr);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_full);
+    };
+    int piece_k = 0;
+    // under cross-layer PDL the previous layer's merge may still be running:
+    // q and the partials are touched only after it has completed
+    pdl_wait_primary();
+    if (T > 0) stage_q(c0.item, 0);
     for (int t = 0; t < T; ++t) {
       const int item = c.item;
       if (t == 0 || c.tile == 0) {
-        // new piece: this thread's half of its Q row -> TMEM (A operand of
-        // S = Q.K^T: row = lane, 2 bf16 per 32-bit column)
         seg_start = t;
         nq = p.it_nq[item];
         head = p.it_head[item];
         ntok = p.it_ntok[item];
         active = quarter < nq;
         r16 = nq <= 64;
-        const bool real = qj < nq;
-        uint32_t qr[32];
-        if (real) {
-          const uint4* src = reinterpret_cast<const uint4*>(
-              q + ((long long)p.qrows[p.it_q_off[item] + qj] * H + head) * kHeadDim) + half * 8;
-#pragma unroll
-          for (int k8 = 0; k8 < 8; ++k8) {
-            const uint4 v = src[k8];
-            qr[4 * k8] = v.x;
-            qr[4 * k8 + 1] = v.y;
-            qr[4 * k8 + 2] = v.z;
-            qr[4 * k8 + 3] = v.w;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) qr[i] = 0u;
-        }
-        tmem_st32(lane_tm + kTmemQ + half * 32, qr);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&q_full);
         m = -INFINITY;
         l = 0.f;
       }
@@ -431,7 +471,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       if (lane == 0) mbar_arrive(&p_full[sb]);
       if (warp == 4 && lane == 0 && t < 16) TL(80 + t);
       if (piece_end) {
-        // piece end: O (unnormalised, running max m) -> partial slot
+        // next piece's Q first (S of its first tile can then run under this
+        // epilogue), then O (unnormalised, running max m) -> partial slot
+        if (t + 1 < T) stage_q(item + 1, piece_k + 1);
+        ++piece_k;
         mbar_wait(&o_done, t & 1);
         if (warp == 4 && lane == 0 && t < 16) TL(96 + t);
         tc_fence_after();
@@ -483,10 +526,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   }
   tc_fence_before();
   __syncthreads();
+  CTA_TL_END(fk_tl_cta_prefix);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
   }
+}
+
+extern "C" int fk_debug_cta_timeline_prefix(unsigned long long* out, int n) {
+#ifdef FK_TIMELINE
+  if (cudaDeviceSynchronize() != cudaSuccess) return 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_prefix, sizeof(unsigned long long) * 2 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+#else
+  (void)out;
+  (void)n;
+  return 5;
+#endif
 }
 
 extern "C" int fk_debug_timeline(unsigned long long* out, int n) {
@@ -501,7 +556,7 @@ extern "C" int fk_debug_timeline(unsigned long long* out, int n) {
 }
 
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                             const CUtensorMap* tmap, const CUtensorMap* tmap_run, cudaStream_t s) {
+                             const CUtensorMap* tmap, const CUtensorMap* tmap_run, bool pdl, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
@@ -518,9 +573,8 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, con
     attr = true;
   }
   if (p.tc_ctas == 0) return cudaSuccess;
-  fk_prefix_tc_kernel<<<p.tc_ctas, kTcThreads, kTcSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, scale_log2,
-                                                             *tmap, *tmap_run);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, p, layer,
+                           (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run);
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, fk_prefix_tc_kernel);

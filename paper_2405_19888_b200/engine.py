@@ -341,6 +341,10 @@ class GpuEngine:
             self._dev = torch.device("cuda", device)
             with torch.cuda.device(self._dev):
                 self._stream = torch.cuda.Stream(self._dev)
+            # The engine owns Q's producer side (its own buffers, ordered by
+            # stream events), so a layer's kernels may start under the previous
+            # layer's merge (cross-layer programmatic dependent launch).
+            self._pool.set_option(_lib.FK_OPT_PDL, 2)
 
     # -- device plumbing ------------------------------------------------------
 

@@ -1,0 +1,60 @@
+"""Per-CTA start/end of the prefix (tcgen05) and private kernels for the last
+layer of a bench-shaped step (debug build, FK_LIB_PATH=profiles/build/
+libforkattn_tl.so).  Diagnostic only.
+
+    python profiles/cta_timeline.py [--config ...] [--opt PREFIX_RATE_PCT=50]
+"""
+import argparse
+import ctypes
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("FK_LIB_PATH", os.path.join(ROOT, "profiles", "build", "libforkattn_tl.so"))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2405_19888_b200 import _lib  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
+    ap.add_argument("--opt", action="append", default=[])
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    eng, rows = bench.build_engine(cfg, 0, torch, out_len=32)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        eng.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
+    for _ in range(4):
+        eng.step()
+    torch.cuda.synchronize()
+    info = eng.last_plan
+    npre, npriv = info.num_prefix_ctas, (eng._pool and 1024)
+    out = {}
+    for name in ("prefix", "priv"):
+        fn = getattr(_lib.lib, "fk_debug_cta_timeline_" + name)
+        fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+        buf = (ctypes.c_ulonglong * 2048)()
+        assert fn(buf, 1024) == 0
+        out[name] = [(buf[2 * i], buf[2 * i + 1]) for i in range(1024)]
+    # the prefix grid of the last layer started first
+    pre = [x for x in out["prefix"][:info.num_prefix_ctas] if x[0]]
+    t0 = min(s for s, _ in pre)
+    priv = [x for x in out["priv"] if x[0] and x[0] >= t0 - 1000 and x[1] >= x[0]]
+    for name, xs in (("prefix", pre), ("private", priv)):
+        st = sorted((s - t0) / 1e3 for s, _ in xs)
+        en = sorted((e - t0) / 1e3 for _, e in xs)
+        print(f"{name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} {st[-1]:7.2f}"
+              f"   end min/med/max {en[0]:7.2f} {statistics.median(en):7.2f} {en[-1]:7.2f}")
+    print("prefix ends:", " ".join("%.1f" % ((e - t0) / 1e3) for _, e in pre))
+    print("private ends (sorted):", " ".join("%.1f" % x for x in sorted((e - t0) / 1e3 for _, e in priv)))
+    print("plan:", info.num_rows, "rows", info.num_prefix_ctas, "prefix CTAs", info.max_slots, "slots")
+
+
+if __name__ == "__main__":
+    main()
