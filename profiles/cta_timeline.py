@@ -44,8 +44,10 @@ def main():
         out[name] = [(buf[2 * i], buf[2 * i + 1]) for i in range(1024)]
     # the prefix grid of the last layer started first
     pre = [x for x in out["prefix"][:info.num_prefix_ctas] if x[0]]
+    t_last = max(s for s, _ in pre)  # CTAs of the last launch started within a few us
+    pre = [x for x in pre if x[0] >= t_last - 20000]
     t0 = min(s for s, _ in pre)
-    priv = [x for x in out["priv"] if x[0] and x[0] >= t0 - 1000 and x[1] >= x[0]]
+    priv = [x for x in out["priv"] if x[0] and abs(x[0] - t0) < 50000 and x[1] >= x[0]]
     for name, xs in (("prefix", pre), ("private", priv)):
         st = sorted((s - t0) / 1e3 for s, _ in xs)
         en = sorted((e - t0) / 1e3 for _, e in xs)
