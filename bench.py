@@ -335,7 +335,8 @@ def main():
     peak, peak_kind = load_peaks()
     achieved = bytes_layer / t_layer / 1e9
     value = world * rows * args.steps / t_steps
-    launches_per_step = L * (1 + int(info.num_mma_items > 0) + int(info.num_tc_items > 0)) + L
+    # per layer: prefix kernel(s) + private + merge; per step: one K/V append
+    launches_per_step = L * (1 + int(info.num_mma_items > 0) + int(info.num_tc_items > 0)) + L + 1
     batch_tokens = info.batch_tokens
 
     # ---- e2e: host (pinned) inputs through the engine API
@@ -363,6 +364,15 @@ def main():
     else:
         eng.close()
 
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per layer (prefix + private + merge) from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(args.config)
+        if tr:
+            traffic, traffic_src = tr["layer_bytes"], tr["source"]
+    except Exception:
+        pass
+
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
@@ -383,7 +393,8 @@ def main():
             "data": "synthetic",
             "config": workload,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_kind": peak_kind,
                          "kernel": "fk_attn_decode (prefix + private/merge kernels, one layer)",
                          "alg_bytes_per_layer": bytes_layer, "layer_us": t_layer * 1e6,
                          "batch_tokens": batch_tokens,

@@ -882,21 +882,26 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
   // K2 (shared prefixes) and K3 (private streams) only write partials, so
   // their order is free; K4 merges every (row, head) afterwards.
-  auto run_prefix = [&]() -> int {
+  auto run_prefix = [&](bool pdl_tc, bool after_private) -> int {
     if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
-    if (has_tc) FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, xl, st));
+    if (has_tc)
+      FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc, after_private, st));
     return FK_OK;
   };
-  // the private grid may overlap the prefix grid (PDL) only when that grid
-  // belongs to this layer; otherwise it must fully follow earlier work
+  // Launch order 0: prefix -> private (PDL: private fills the SMs the prefix
+  // grid leaves free; its CTAs wait for the prefix grid on exit).  Order 1:
+  // private -> prefix (PDL when the tcgen05 grid is the only prefix grid; its
+  // CTAs then wait for the private grid on exit).  Either way the second
+  // grid's completion implies the first's, which the merge waits for.
   if (p->launch_order == 0) {
-    int rc = run_prefix();
+    int rc = run_prefix(xl, false);
     if (rc != FK_OK) return rc;
     FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap,
                            (p->pdl && (has_mma || has_tc)) || (xl && !has_tc), st));
   } else {
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, false, st));
-    int rc = run_prefix();
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, xl, st));
+    const bool chained = p->pdl && has_tc && !has_mma && p->plan.priv_units > 0;
+    int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;
   }
   FK_CUDA(launch_merge(a, p->plan, out, out_f32, p->pdl != 0, st));

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
                                                                      const __nv_bfloat16* __restrict__ q,
                                                                      float scale_log2,
                                                                      const __grid_constant__ CUtensorMap tmap,
-                                                                     const __grid_constant__ CUtensorMap tmap_run) {
+                                                                     const __grid_constant__ CUtensorMap tmap_run,
+                                                                     int after_private) {
   // all shared state is dynamic (no static smem), so the buffer starts at
   // the 1 KiB-aligned base SWIZZLE_128B needs
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -108,7 +109,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   const int u0 = blockIdx.x * p.tc_per;
   const int u1 = min(p.tc_units, u0 + p.tc_per);
   pdl_launch_dependents();  // the private grid may start on the SMs we leave free
-  if (u0 >= u1) return;
+  // Launched behind the private grid (launch order 1), this grid's completion
+  // must imply that grid's: thread 0 waits for it on exit.
+  if (u0 >= u1) {
+    if (after_private && threadIdx.x == 0) pdl_wait_primary();
+    return;
+  }
   const int T = u1 - u0;
   TL(160);
   CTA_TL_START(fk_tl_cta_prefix);
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     int piece_k = 0;
     // under cross-layer PDL the previous layer's merge may still be running:
     // q and the partials are touched only after it has completed
-    pdl_wait_primary();
+    if (!after_private) pdl_wait_primary();
     if (T > 0) stage_q(c0.item, 0);
     for (int t = 0; t < T; ++t) {
       const int item = c.item;
@@ -531,6 +537,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
   }
+  if (after_private && threadIdx.x == 0) pdl_wait_primary();
 }
 
 extern "C" int fk_debug_cta_timeline_prefix(unsigned long long* out, int n) {
@@ -556,7 +563,8 @@ extern "C" int fk_debug_timeline(unsigned long long* out, int n) {
 }
 
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                             const CUtensorMap* tmap, const CUtensorMap* tmap_run, bool pdl, cudaStream_t s) {
+                             const CUtensorMap* tmap, const CUtensorMap* tmap_run, bool pdl, bool after_private,
+                             cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
@@ -574,7 +582,7 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, con
   }
   if (p.tc_ctas == 0) return cudaSuccess;
   cudaError_t e = launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, p, layer,
-                           (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run);
+                           (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run, after_private ? 1 : 0);
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, fk_prefix_tc_kernel);
