@@ -154,6 +154,26 @@ int fk_append_kv(fk_pool* pool, int32_t layer, const void* k, const void* v,
 int fk_append_kv_layers(fk_pool* pool, int32_t layer0, int32_t nlayers,
                         const void* k, const void* v, void* stream);
 
+/* ---- fill (prefill KV content) ------------------------------------------- */
+/* The KV half of Engine.fill (engine.py:225-255; the paper's Fill "calculates
+ * and fills the KV cache"): write caller K/V rows for tokens
+ * [pos0, pos1) of ctx (already grown by fk_ctx_grow) into its pages, for
+ * layers [layer0, layer0 + nlayers).  k, v: [nlayers][pos1 - pos0][H][D] bf16
+ * (device).  The copy is stream-ordered; the host pointers may be reused
+ * once `stream` has passed it. */
+int fk_fill_kv(fk_pool* pool, int64_t ctx, int64_t pos0, int64_t pos1, int32_t layer0, int32_t nlayers,
+               const void* k, const void* v, void* stream);
+
+/* ---- prefix migration -------------------------------------- */
+/* Copy the KV of tokens [0, ntok) of src_ctx (in pool `src`, possibly on
+ * another GPU) into dst_ctx of pool `dst` (already grown to >= ntok tokens),
+ * all layers.  Across devices the copy kernel runs on dst's GPU and reads
+ * src's arena over NVLink peer access (enabled on first use).  Lets a fork
+ * group land on a GPU that does not hold its shared prefix without
+ * re-running prefill (scheduler.py:217-221 `shared-ctx` restriction). */
+int fk_ctx_copy_kv(fk_pool* dst, int64_t dst_ctx, const fk_pool* src, int64_t src_ctx, int64_t ntok,
+                   void* stream);
+
 /* ---- synthetic model (deterministic KV / Q; the oracle restates it) ------ */
 /* Fill tokens [pos0, pos1) of ctx for every layer/head with the counter-hash
  * generator.  k_scale multiplies K (stress). */

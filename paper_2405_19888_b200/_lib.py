@@ -93,6 +93,8 @@ SIGNATURES = [
     ("fk_step_commit", c_int32, [c_void_p, POINTER(c_int64), c_void_p]),
     ("fk_append_kv", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("fk_append_kv_layers", c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    ("fk_fill_kv", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    ("fk_ctx_copy_kv", c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p]),
     ("fk_synth_fill", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_float, c_void_p]),
     ("fk_synth_queries", c_int32, [c_void_p, c_uint64, c_void_p, c_void_p]),
     ("fk_synth_append", c_int32, [c_void_p, c_uint64, c_float, c_void_p]),

@@ -95,6 +95,10 @@ cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int n
 cudaError_t launch_synth_fill(const ArenaDev& a, const int* pages_dev, int npages_first,
                               long long uid, long long pos0, long long pos1,
                               unsigned long long seed, float k_scale, cudaStream_t s);
+cudaError_t launch_fill_kv(const ArenaDev& a, const int* pages_dev, int first_page, long long pos0, int ntok,
+                           int layer0, int nlayers, const void* k, const void* v, cudaStream_t s);
+cudaError_t launch_copy_pages(const ArenaDev& dst, const void* src_kv, long long src_num_pages, const int* pages_dev,
+                              int npages, cudaStream_t s);
 cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p,
                                  unsigned long long seed, void* q_all, cudaStream_t s);
 cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p,

@@ -496,6 +496,58 @@ __global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, PlanDev p, i
   dst[c] = val;
 }
 
+// ================================================================== fill
+// Caller K/V rows for tokens [pos0, pos0 + ntok) of one context -> pages,
+// for layers [layer0, layer0 + gridDim.y).  One warp per (token, head):
+// lanes 0-15 move the 256 B K row, lanes 16-31 the V row, 16 B each.
+// src k/v: [nlayers][ntok][H][D] bf16.
+__global__ void __launch_bounds__(256) fk_fill_kv_kernel(ArenaDev a, const int* __restrict__ pages, int first_page,
+                                                        long long pos0, int ntok, int layer0,
+                                                        const uint4* __restrict__ k, const uint4* __restrict__ v) {
+  const int H = a.num_heads;
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= ntok * H) return;
+  const int t = w / H, h = w % H;
+  const int li = blockIdx.y, layer = layer0 + li;
+  const long long pos = pos0 + t;
+  const int pg = pages[pos / kPage - first_page];
+  const int slot = (int)(pos % kPage);
+  const long long plane_elems = a.num_pages * kPage * kHeadDim;
+  const int kv = lane >> 4, c = lane & 15;
+  const uint4* src = kv == 0 ? k : v;
+  const uint4 val = src[(((long long)li * ntok + t) * H + h) * 16 + c];
+  uint4* dst = reinterpret_cast<uint4*>(a.kv + plane_index(layer, kv, h, H) * plane_elems +
+                                        ((long long)pg * kPage + slot) * kHeadDim);
+  dst[c] = val;
+}
+
+// ============================================================ migration
+// Context KV pages from another pool (another GPU over NVLink peer access, or
+// the same GPU) into this pool: one CTA per (page pair, plane chunk), each
+// thread moves 16 B of a 4 KiB (layer, kv, head, page) block.  src_kv is a
+// peer-mapped pointer when the pools live on different devices.
+__global__ void __launch_bounds__(256) fk_copy_pages_kernel(ArenaDev dst, const __nv_bfloat16* __restrict__ src_kv,
+                                                           long long src_num_pages, const int* __restrict__ pages,
+                                                           int npages) {
+  const int j = blockIdx.x;  // page pair
+  const int planes = dst.num_layers * 2 * dst.num_heads;
+  const int sp = pages[j], dp = pages[npages + j];
+  const long long dplane = dst.num_pages * kPage * kHeadDim, splane = src_num_pages * kPage * kHeadDim;
+  for (int pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const uint4* s = reinterpret_cast<const uint4*>(src_kv + pl * splane + (long long)sp * kPage * kHeadDim);
+    uint4* d = reinterpret_cast<uint4*>(dst.kv + pl * dplane + (long long)dp * kPage * kHeadDim);
+    d[threadIdx.x] = __ldg(s + threadIdx.x);  // 256 x 16 B = one 4 KiB page block
+  }
+}
+
+cudaError_t launch_copy_pages(const ArenaDev& dst, const void* src_kv, long long src_num_pages, const int* pages_dev,
+                              int npages, cudaStream_t s) {
+  const int planes = dst.num_layers * 2 * dst.num_heads;
+  dim3 grid(npages, planes < 64 ? planes : 64);
+  fk_copy_pages_kernel<<<grid, 256, 0, s>>>(dst, (const __nv_bfloat16*)src_kv, src_num_pages, pages_dev, npages);
+  return cudaGetLastError();
+}
+
 // ============================================================== synthetic
 __global__ void fk_synth_fill_kernel(ArenaDev a, const int* __restrict__ pages, int first_page, long long uid,
                                      long long pos0, unsigned long long seed, float k_scale) {
@@ -591,6 +643,14 @@ cudaError_t launch_synth_fill(const ArenaDev& a, const int* pages_dev, int first
                               cudaStream_t s) {
   dim3 grid((unsigned)(pos1 - pos0), a.num_layers);
   fk_synth_fill_kernel<<<grid, 256, 0, s>>>(a, pages_dev, first_page, uid, pos0, seed, k_scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_kv(const ArenaDev& a, const int* pages_dev, int first_page, long long pos0, int ntok,
+                           int layer0, int nlayers, const void* k, const void* v, cudaStream_t s) {
+  dim3 grid((unsigned)((ntok * a.num_heads + 7) / 8), nlayers);
+  fk_fill_kv_kernel<<<grid, 256, 0, s>>>(a, pages_dev, first_page, pos0, ntok, layer0, (const uint4*)k,
+                                          (const uint4*)v);
   return cudaGetLastError();
 }
 

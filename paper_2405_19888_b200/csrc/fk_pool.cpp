@@ -988,6 +988,73 @@ int fk_synth_fill(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, uint64_t 
   return FK_OK;
 }
 
+int fk_fill_kv(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, int32_t layer0, int32_t nlayers,
+               const void* k, const void* v, void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  auto it = p->ctxs.find(ctx);
+  if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)ctx);
+  const Ctx& c = it->second;
+  if (pos0 < 0 || pos1 < pos0 || pos1 > c.tokens)
+    return fail(FK_INVALID_ARGUMENT, "bad range [%lld, %lld) of %lld", (long long)pos0, (long long)pos1,
+                (long long)c.tokens);
+  if (layer0 < 0 || nlayers < 1 || layer0 + nlayers > p->desc.num_layers)
+    return fail(FK_INVALID_ARGUMENT, "bad layer range [%d, %d)", layer0, layer0 + nlayers);
+  if (pos1 == pos0) return FK_OK;
+  if (!k || !v) return fail(FK_INVALID_ARGUMENT, "null k/v");
+  if (pos1 - pos0 > INT32_MAX / p->desc.num_heads) return fail(FK_INVALID_ARGUMENT, "fill too large");
+  FK_CUDA(cudaSetDevice(p->desc.device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t first = pos0 / kPage, last = (pos1 - 1) / kPage;
+  const int n = (int)(last - first + 1);
+  int* dpages = nullptr;
+  FK_CUDA(cudaMallocAsync(&dpages, sizeof(int) * n, st));
+  FK_CUDA(cudaMemcpyAsync(dpages, c.phys.data() + first, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  FK_CUDA(launch_fill_kv(p->arena(), dpages, (int)first, pos0, (int)(pos1 - pos0), layer0, nlayers, k, v, st));
+  FK_CUDA(cudaFreeAsync(dpages, st));
+  return FK_OK;
+}
+
+int fk_ctx_copy_kv(fk_pool* dst, int64_t dst_ctx, const fk_pool* src, int64_t src_ctx, int64_t ntok,
+                   void* stream) {
+  if (!dst || !src) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!dst->on_device || !src->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
+  if (dst->desc.num_layers != src->desc.num_layers || dst->desc.num_heads != src->desc.num_heads ||
+      dst->desc.head_dim != src->desc.head_dim)
+    return fail(FK_INVALID_ARGUMENT, "pools have different model geometry");
+  auto di = dst->ctxs.find(dst_ctx);
+  if (di == dst->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown context %lld", (long long)dst_ctx);
+  auto si = src->ctxs.find(src_ctx);
+  if (si == src->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown source context %lld", (long long)src_ctx);
+  if (ntok < 0 || ntok > si->second.tokens || ntok > di->second.tokens)
+    return fail(FK_INVALID_ARGUMENT, "copy of %lld tokens exceeds a context (%lld -> %lld)", (long long)ntok,
+                (long long)si->second.tokens, (long long)di->second.tokens);
+  if (ntok == 0) return FK_OK;
+  FK_CUDA(cudaSetDevice(dst->desc.device));
+  if (src->desc.device != dst->desc.device) {
+    int can = 0;
+    FK_CUDA(cudaDeviceCanAccessPeer(&can, dst->desc.device, src->desc.device));
+    if (!can) return fail(FK_CUDA_ERROR, "device %d cannot access device %d", dst->desc.device, src->desc.device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(src->desc.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) return fail(FK_CUDA_ERROR, "peer access: %s", cudaGetErrorString(e));
+  }
+  const int n = (int)((ntok + kPage - 1) / kPage);
+  std::vector<int32_t> pairs(2 * (size_t)n);
+  for (int j = 0; j < n; ++j) {
+    pairs[j] = si->second.phys[j];
+    pairs[n + j] = di->second.phys[j];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int* dpages = nullptr;
+  FK_CUDA(cudaMallocAsync(&dpages, sizeof(int) * 2 * n, st));
+  FK_CUDA(cudaMemcpyAsync(dpages, pairs.data(), sizeof(int) * 2 * n, cudaMemcpyHostToDevice, st));
+  FK_CUDA(launch_copy_pages(dst->arena(), src->kv, src->num_pages, dpages, n, st));
+  FK_CUDA(cudaFreeAsync(dpages, st));
+  // pairs (pageable) was staged by the H2D copy before this call returns
+  return FK_OK;
+}
+
 int fk_synth_queries(fk_pool* p, uint64_t seed, void* q_all, void* stream) {
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");

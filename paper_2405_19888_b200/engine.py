@@ -412,9 +412,26 @@ class GpuEngine:
         return ctx
 
     def fill(self, token_ids: Sequence[int], context_id: str, parent_context_id: Optional[str] = None,
-             request_id: Optional[str] = None, boundary_hash: Optional[int] = None) -> int:
-        """Allocate pages for the new tokens, write their KV (synthetic
-        prefill stand-in) and queue the fill work; atomic on OutOfMemory."""
+             request_id: Optional[str] = None, boundary_hash: Optional[int] = None, *, kv=None,
+             kv_from=None) -> int:
+        """Allocate pages for the new tokens, write their KV and queue the
+        fill work; atomic on OutOfMemory (engine.py:225-255).
+
+        `kv=(k, v)`: the model's K/V rows for these tokens, device tensors
+        [L][len(token_ids)][H][D] bf16, written into the pages (fk_fill_kv).
+        `kv_from=(engine, context_id)`: copy the first len(token_ids) tokens'
+        K/V of a context held by another GpuEngine (another GPU: NVLink peer
+        reads, fk_ctx_copy_kv) -- a shared prefix migrates instead of being
+        prefilled again.  The new context must be fresh.
+        Without either, the deterministic synthetic generator stands in for
+        the prefill (tests, bench)."""
+        if kv is not None:
+            self._check_rows(kv, len(token_ids))
+        if kv_from is not None:
+            src_eng, src_id = kv_from
+            src_ctx = src_eng.get_context(src_id)
+            if context_id in self.contexts or len(token_ids) > src_ctx.token_count or self.device is None:
+                raise ValueError("kv_from needs a fresh context on a device engine and <= source tokens")
         fresh = context_id not in self.contexts
         ctx = self.create_context(context_id, parent_context_id) if fresh else self.get_context(context_id)
         before = ctx.token_count
@@ -425,8 +442,29 @@ class GpuEngine:
                 self._discard_context(ctx)
             raise
         if self.device is not None and len(token_ids) > 0:
-            _lib.check(_lib.lib.fk_synth_fill(self._pool.handle, ctx.uid, before, ctx.token_count,
-                                              self.model_seed, self.model_k_scale, self._sp()))
+            if kv_from is not None:
+                torch = self._torch
+                ev = torch.cuda.Event()
+                ev.record(src_eng.stream)  # the source pages are written
+                self._stream.wait_event(ev)
+                _lib.check(_lib.lib.fk_ctx_copy_kv(self._pool.handle, ctx.uid, src_eng._pool.handle, src_ctx.uid,
+                                                   len(token_ids), self._sp()))
+                done = torch.cuda.Event()
+                done.record(self._stream)
+                src_eng.stream.wait_event(done)  # the source may not recycle them before the copy
+            elif kv is not None:
+                k, v = kv
+                with self._torch.cuda.device(self._dev):
+                    # the caller's tensors are consumed on the engine stream
+                    self._stream.wait_stream(self._torch.cuda.current_stream(self._dev))
+                _lib.check(_lib.lib.fk_fill_kv(self._pool.handle, ctx.uid, before, ctx.token_count, 0,
+                                               self.geometry.num_layers, ctypes.c_void_p(k.data_ptr()),
+                                               ctypes.c_void_p(v.data_ptr()), self._sp()))
+                k.record_stream(self._stream)
+                v.record_stream(self._stream)
+            else:
+                _lib.check(_lib.lib.fk_synth_fill(self._pool.handle, ctx.uid, before, ctx.token_count,
+                                                  self.model_seed, self.model_k_scale, self._sp()))
         if boundary_hash is not None:
             ctx.chain_hashes.append(boundary_hash)
             if boundary_hash not in self.registry:
@@ -437,6 +475,17 @@ class GpuEngine:
             self.pending_fills[request_id] = self.pending_fills.get(request_id, 0) + 1
             self.request_leaf[request_id] = context_id
         return len(token_ids)
+
+    def _check_rows(self, kv, n: int) -> None:
+        if self.device is None:
+            raise ValueError("kv rows need a device engine")
+        geo = self.geometry
+        want = (geo.num_layers, n, geo.num_heads, geo.head_dim)
+        for t in kv:
+            if (tuple(t.shape) != want or t.dtype != self._torch.bfloat16 or t.device != self._dev
+                    or not t.is_contiguous()):
+                raise ValueError(f"kv rows must be contiguous bf16 {want} on {self._dev}, got "
+                                 f"{tuple(t.shape)} {t.dtype} {t.device}")
 
     @property
     def model_seed(self) -> int:

@@ -247,3 +247,94 @@ def test_host_tensor_pipeline_matches_device_tensors(cuda_device):
         eng.close()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_fill_with_model_kv_rows(cuda_device):
+    """fill(kv=(k, v)) writes the caller's prefill rows (fk_fill_kv); decode
+    attention over them matches fp64 softmax over the same bf16 values, for
+    a shared prefix, ragged leaves (partial pages) and the step's appended
+    rows."""
+    import torch
+
+    from oracle import forkattn_oracle as O
+
+    H, L = 4, 2
+    dev = torch.device("cuda", cuda_device)
+    eng = make_engine(cuda_device, H=H, L=L)
+    g = torch.Generator().manual_seed(11)
+
+    def rows(n):
+        return [torch.randn((L, n, H, 128), generator=g).to(torch.bfloat16) for _ in range(2)]
+
+    ctx_kv = {}
+    pk, pv = rows(333)
+    eng.fill([1] * 333, "root", None, boundary_hash=1, kv=(pk.to(dev), pv.to(dev)))
+    ctx_kv["root"] = (pk, pv)
+    lens = [5, 16, 17, 40]
+    for i, n in enumerate(lens):
+        lk, lv = rows(n)
+        eng.fill([1] * n, f"leaf{i}", "root", boundary_hash=10 + i, kv=(lk.to(dev), lv.to(dev)))
+        ctx_kv[f"leaf{i}"] = (lk, lv)
+        eng.generate(f"r{i}", f"leaf{i}", [1] * 3, "")
+    from paper_2405_19888_b200.workloads import drain_fills
+    drain_fills(eng)
+    B = len(lens)
+    q = torch.randn((L, B, H, 128), generator=g).to(torch.bfloat16)
+    k_new, v_new = rows(B)
+    eng.model = P.TensorDecodeModel(q.to(dev), k_new.to(dev), v_new.to(dev))
+    eng.capture_f32 = False
+    outs = []
+    for _ in range(2):
+        eng.step()
+        eng.stream.synchronize()
+        outs.append(eng.last_output.float().cpu().numpy())
+    for step, out in enumerate(outs):
+        for b in range(B):
+            kk = torch.cat([ctx_kv["root"][0], ctx_kv[f"leaf{b}"][0]] + ([k_new[:, b:b + 1]] if step else []), 1)
+            vv = torch.cat([ctx_kv["root"][1], ctx_kv[f"leaf{b}"][1]] + ([v_new[:, b:b + 1]] if step else []), 1)
+            for layer in range(L):
+                want = O.attend(q[layer, b].float().numpy(), kk[layer].float().numpy(),
+                                vv[layer].float().numpy())
+                r = O.tolerance_report(out[layer, b], want)
+                assert r["max_abs"] <= 2e-2 and r["rel_l2"] <= 4e-3, (step, b, layer, r)
+
+
+def test_prefix_migration_between_pools(cuda_device):
+    """fill(kv_from=(engine, ctx)) copies a context's KV from another pool
+    (fk_ctx_copy_kv; NVLink peer reads when the pools are on different GPUs,
+    here both on cuda_device): decoding the migrated forest gives outputs
+    bit-identical to decoding it where it was prefilled."""
+    import torch
+
+    H, L = 4, 2
+    a = make_engine(cuda_device, H=H, L=L)
+    b = make_engine(cuda_device, H=H, L=L)
+    b.fill([7] * 16, "pad", None)  # different physical pages in b
+    lens = [3, 16, 40]
+    a.fill([1] * 700, "root", None, boundary_hash=1)
+    b.fill([1] * 700, "root", None, boundary_hash=1, kv_from=(a, "root"))
+    for i, n in enumerate(lens):
+        a.fill([1] * n, f"l{i}", "root", boundary_hash=10 + i)
+        b.fill([1] * n, f"l{i}", "root", boundary_hash=10 + i, kv_from=(a, f"l{i}"))
+        for e in (a, b):
+            e.generate(f"r{i}", f"l{i}", [1] * 2, "")
+    from paper_2405_19888_b200.workloads import drain_fills
+    g = torch.Generator().manual_seed(5)
+    dev = torch.device("cuda", cuda_device)
+    q, k, v = (torch.randn((L, len(lens), H, 128), generator=g).to(torch.bfloat16).to(dev) for _ in range(3))
+    outs = []
+    for e in (a, b):
+        drain_fills(e)
+        e.model = P.TensorDecodeModel(q, k, v)
+        e.capture_f32 = False
+        got = []
+        for _ in range(2):
+            e.step()
+            e.stream.synchronize()
+            got.append(e.last_output.cpu().clone())
+        outs.append(got)
+    assert a.context_pages("root")[1] != b.context_pages("root")[1]
+    for x, y in zip(*outs):
+        assert torch.equal(x, y)
+    a.close()
+    b.close()
