@@ -650,12 +650,26 @@ class GpuEngine:
                     "d2h": torch.cuda.Stream(self._dev),
                     "ev_q": [torch.cuda.Event() for _ in range(L)],
                     "ev_o": [torch.cuda.Event() for _ in range(L)],
+                    # copy granularity: layer chunks of 1, 1, 2, 4, 8, 8, ... so
+                    # layer 0 waits for one layer's rows and the host issues few
+                    # copies and events per step
+                    "chunks": self._layer_chunks(L),
                     "ev_kv": torch.cuda.Event(),
                     "ev_d2h": torch.cuda.Event(),
-                    "ev_step": None,
+                    "ev_start": torch.cuda.Event(),
                 }
             self._hp = hp
         return hp
+
+    @staticmethod
+    def _layer_chunks(L: int) -> List[Tuple[int, int]]:
+        out, a, n = [], 0, 1
+        while a < L:
+            b = min(L, a + n)
+            out.append((a, b))
+            a = b
+            n = min(8, 2 * n) if len(out) > 1 else 1
+        return out
 
     def _decode_attention_host(self, running: List[GenerationTask]) -> None:
         """Host (pinned) Q/K/V in, host output out, pipelined per layer: the
@@ -671,29 +685,35 @@ class GpuEngine:
         if model.host_out is None or tuple(model.host_out.shape) != shape:
             model.host_out = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
         with torch.cuda.device(self._dev):
-            if hp["ev_step"] is not None:  # the previous step is done with the buffers
-                h2d.wait_event(hp["ev_step"])
-                d2h.wait_event(hp["ev_step"])
+            # Copies start once this step's plan upload (on the engine stream,
+            # after the previous step's append) has gone: the buffers are free
+            # then, and the plan never queues behind this step's 50 MB of K/V
+            # rows on the copy engine.
+            hp["ev_start"].record(st)
+            h2d.wait_event(hp["ev_start"])
+            d2h.wait_event(hp["ev_start"])
+            chunks = hp["chunks"]
             with torch.cuda.stream(h2d):
-                for layer in range(geo.num_layers):
-                    hp["q"][layer].copy_(model.q[layer], non_blocking=True)
-                    hp["ev_q"][layer].record(h2d)
+                for ci, (a, b) in enumerate(chunks):
+                    hp["q"][a:b].copy_(model.q[a:b], non_blocking=True)
+                    hp["ev_q"][ci].record(h2d)
                 if model.k is not None:
                     hp["k"].copy_(model.k, non_blocking=True)
                     hp["v"].copy_(model.v, non_blocking=True)
                     hp["ev_kv"].record(h2d)
             q, out = hp["q"], hp["out"]
             layer_elems = B * geo.num_heads * geo.head_dim
-            for layer in range(geo.num_layers):
-                st.wait_event(hp["ev_q"][layer])
-                _lib.check(_lib.lib.fk_attn_decode(self._pool.handle, layer,
-                                                   ctypes.c_void_p(q.data_ptr() + layer * layer_elems * 2),
-                                                   ctypes.c_void_p(out.data_ptr() + layer * layer_elems * 2),
-                                                   None, self._sp()))
-                hp["ev_o"][layer].record(st)
-                d2h.wait_event(hp["ev_o"][layer])
+            qp, op, handle, sp = q.data_ptr(), out.data_ptr(), self._pool.handle, self._sp()
+            for ci, (a, b) in enumerate(chunks):
+                st.wait_event(hp["ev_q"][ci])
+                for layer in range(a, b):
+                    _lib.check(_lib.lib.fk_attn_decode(handle, layer,
+                                                       ctypes.c_void_p(qp + layer * layer_elems * 2),
+                                                       ctypes.c_void_p(op + layer * layer_elems * 2), None, sp))
+                hp["ev_o"][ci].record(st)
+                d2h.wait_event(hp["ev_o"][ci])
                 with torch.cuda.stream(d2h):
-                    model.host_out[layer].copy_(out[layer], non_blocking=True)
+                    model.host_out[a:b].copy_(out[a:b], non_blocking=True)
             hp["ev_d2h"].record(d2h)
             st.wait_event(hp["ev_d2h"])  # the step completes with its output on the host
         self.last_output = out
@@ -759,11 +779,6 @@ class GpuEngine:
         else:
             _lib.check(_lib.lib.fk_synth_append(self._pool.handle, self.model_seed, self.model_k_scale,
                                                 self._sp()))
-        hp = getattr(self, "_hp", None)
-        if hp is not None:  # next step's copies may reuse the buffers after this point
-            if hp["ev_step"] is None:
-                hp["ev_step"] = torch.cuda.Event()
-            hp["ev_step"].record(self._stream)
 
     def _snapshot(self, running: List[GenerationTask]) -> List[List[Tuple[int, int]]]:
         """Per row: [(context uid, tokens)] root -> leaf at plan time."""

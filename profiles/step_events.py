@@ -25,9 +25,10 @@ def main():
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[])
+    ap.add_argument("--host", action="store_true", help="pinned-host Q/K/V (the e2e path)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
-    eng, rows = bench.build_engine(cfg, 0, torch, out_len=4 * args.steps + 16)
+    eng, rows = bench.build_engine(cfg, 0, torch, host_inputs=args.host, out_len=4 * args.steps + 16)
     from paper_2405_19888_b200 import _lib
     for kv in args.opt:
         k, v = kv.split("=")
@@ -49,6 +50,8 @@ def main():
     print("device ms/step:", " ".join("%.3f" % d for d in dev))
     print("host   ms/step:", " ".join("%.3f" % (1e3 * h) for h in host))
     print("median device %.3f ms, host %.3f ms" % (statistics.median(dev), 1e3 * statistics.median(host)))
+    if args.host:
+        return
     t_layer = bench.time_layers(eng, 5, torch)
     print("back-to-back layer %.1f us -> x%d = %.3f ms" % (1e6 * t_layer, cfg["L"], 1e3 * t_layer * cfg["L"]))
     # step with the device drained before it: the host cost alone
