@@ -863,17 +863,28 @@ class GpuEngine:
                             finished, failed, fill_completed)
         self.reports.append(report)
         if snapshot is not None:
-            self.history.append({
-                "rows": [g.request_id for g in running],
-                "chains": snapshot,
-                "leaf_uid": [self.contexts[g.context_id].uid if g.context_id in self.contexts else -1
-                             for g in running],
-                "batch_tokens": batch_tokens,
-                "output": None if self.last_output is None else self.last_output.detach().to("cpu", copy=True),
-                "output_f32": None if self.last_output_f32 is None else self.last_output_f32.detach().to("cpu", copy=True),
-                "positions": positions,
-            })
+            self.history.append(self._history_record(running, snapshot, batch_tokens, positions))
         return report
+
+    def _history_record(self, running, snapshot, batch_tokens, positions) -> Dict[str, Any]:
+        """Snapshot for the parity tests: the outputs are copied to the host on
+        the engine stream, i.e. after this step's kernels."""
+        def host(t):
+            if t is None:
+                return None
+            with self._torch.cuda.stream(self._stream):
+                return t.detach().to("cpu", copy=True)
+
+        return {
+            "rows": [g.request_id for g in running],
+            "chains": snapshot,
+            "leaf_uid": [self.contexts[g.context_id].uid if g.context_id in self.contexts else -1
+                         for g in running],
+            "batch_tokens": batch_tokens,
+            "output": host(self.last_output),
+            "output_f32": host(self.last_output_f32),
+            "positions": positions,
+        }
 
     # -- request lifecycle (engine.py:488-538) -------------------------------------
 
