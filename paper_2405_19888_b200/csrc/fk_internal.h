@@ -16,7 +16,8 @@ constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
 constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
 constexpr int kPrivWarpsPerCta = 8;  // private stream-K kernel: independent warps per CTA
 constexpr int kPrivStages = 3;       // per-warp smem ring depth (8 KiB K+V page per stage)
-constexpr int kPrivMinUnits = 4;     // minimum pages per private warp
+constexpr int kPrivMinChunk = 4;     // private guided schedule: smallest chunk (pages)
+constexpr int kPrivMaxChunk = 32;    // largest chunk (one lane-parallel metadata load)
 
 // Device view of one step plan.  All arrays live in one device buffer.
 // Partials of (row, head) live at slots [0, row_head_count): shared-prefix
@@ -48,15 +49,18 @@ struct PlanDev {
   const int* row_head_count;   // [rows][H] partials the merge combines
   const int* pages;            // physical page ids
   const int* page_ntok;        // valid tokens per page entry
-  // private stream-K: units u in [0, H * priv_np) = (head, flat private page
-  // entry e): head = u / priv_np, entry = priv_base + u % priv_np.  Global
-  // warp w owns units [w * priv_per, (w + 1) * priv_per).
+  // private schedule: units u in [0, H * priv_np) = (head, flat private page
+  // entry e): head = u / priv_np, entry = priv_base + u % priv_np, cut into
+  // chunks [priv_chunk_start[c], priv_chunk_start[c + 1]) that warps grab
+  // from a ticket counter.
   const int* page_row;         // row of each flat private entry
   int priv_base;               // offset of the private entries in pages[]
   int priv_np;                 // number of private page entries (NPT)
   int priv_units;              // U = H * NPT
-  int priv_per;                // units per warp
-  int priv_warps;              // G
+  int priv_nchunks;
+  int priv_warps;              // grid warps (grid = priv_warps / kPrivWarpsPerCta)
+  const int* priv_chunk_start; // [priv_nchunks + 1]
+  const int* priv_rh_chunk0;   // [rows][H] first chunk of each (row, head) item
   // synthetic keys per row
   const long long* row_uid;    // leaf context uid
   const long long* row_pos;    // leaf tokens at plan time + (rank << 40)
@@ -74,6 +78,7 @@ struct ArenaDev {
   int num_heads;
   float* part_o;          // [rows][max_slots][H][D]
   float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
+  unsigned long long* ticket;  // private chunk ticket counter (never reset)
 };
 
 inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {
@@ -82,7 +87,8 @@ inline __host__ __device__ long long plane_index(int layer, int kv, int head, in
 
 // Launchers (fk_kernels.cu).  All return cudaError_t of the launch.
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
-                           float scale_log2, const CUtensorMap* tmap, bool pdl, cudaStream_t s);
+                           float scale_log2, const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl,
+                           cudaStream_t s);
 cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
                               float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q,

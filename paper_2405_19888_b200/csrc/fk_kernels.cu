@@ -17,14 +17,17 @@
 namespace fk {
 
 // =========================================================== private (n_c=1)
-// Warp-granular stream-K over units u = (head, flat private page entry):
-// global warp w streams units [w*per, (w+1)*per) through its own smem ring
-// (TMA, SWIZZLE_128B boxes {64 dims, 16 tokens}: K lo/hi, V lo/hi = 8 KiB per
-// page), so every warp moves the same bytes and no block barrier exists.
-// Per page: S = q.K^T and O += P.V on mma.sync m16n8k16 with the single query
-// in row 0 (the tensor pipe replaces ~400 CUDA-core instructions per page),
-// online softmax on the row-0 fragments, P split hi+lo in bf16.
-// An item (row, head) cut by a range boundary yields one partial per piece.
+// Units u = (head, flat private page entry e), head-major.  The plan cuts the
+// unit list into chunks of decreasing size (guided: big first, 4-unit ones
+// at the end) and every warp grabs chunk after chunk from a ticket counter,
+// streaming each chunk's pages through its own 3-stage smem ring (TMA,
+// SWIZZLE_128B boxes {64 dims, 16 tokens}: K lo/hi, V lo/hi = 8 KiB per
+// page).  Slow SMs simply take fewer chunks, and CTAs that only get an SM
+// when the tcgen05 prefix CTAs retire take the leftovers -- no static tail.
+// Per page: S = q.K^T and O += P.V on mma.sync m16n8k16 with the single
+// query in row 0, online softmax on the row-0 fragments, P split hi+lo.
+// A chunk always ends a piece: (row, head, chunk) -> one partial slot
+// row_head_base + (chunk - first chunk of the item), fixed by the plan.
 constexpr int kPwThreads = kPrivWarpsPerCta * 32;
 constexpr int kPwStageBytes = 8192;
 constexpr int kPwSmem = kPrivWarpsPerCta * kPrivStages * kPwStageBytes + 1024;
@@ -53,24 +56,29 @@ struct PdlTail {
 __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
                                                                    float scale_log2,
-                                                                   const __grid_constant__ CUtensorMap tmap) {
+                                                                   const __grid_constant__ CUtensorMap tmap,
+                                                                   unsigned long long ticket_base) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kPrivWarpsPerCta][kPrivStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
-  CTA_TL_START(fk_tl_cta_priv);
+  CTA_TL_START(fk_tl_cta_priv, layer);
   pdl_launch_dependents();  // the merge kernel may launch now (it waits for us)
   PdlTail tail;             // on exit: this grid completes only after the prefix grid
 
-  // ---------------------------------------------------- streaming warps
   const int g = lane >> 2, t4 = lane & 3;
-  const int gw = blockIdx.x * kPrivWarpsPerCta + warp;
-  const int NPT = p.priv_np;
-  const int u0 = gw * p.priv_per;
-  const int u1 = min(p.priv_units, u0 + p.priv_per);
-  if (u0 >= u1) return;
+  const int NPT = p.priv_np, nch = p.priv_nchunks;
+  // every warp stops after its first failing ticket: a launch consumes
+  // exactly nchunks + (grid warps) tickets (the host advances ticket_base)
+  auto grab = [&]() -> int {
+    int c = 0;
+    if (lane == 0) c = (int)(atomicAdd(a.ticket, 1ull) - ticket_base);
+    return __shfl_sync(0xffffffffu, c, 0);
+  };
+  int ca = grab();
+  if (ca >= nch) return;
 
   uint8_t* ring = smem + warp * kPrivStages * kPwStageBytes;
   if (lane == 0) {
@@ -80,34 +88,31 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
   }
   __syncwarp();
 
-  // unit metadata, 64-unit window held lane-parallel in registers
-  auto load_meta = [&](int ub) {
+  // unit metadata of a chunk (<= 32 units) held lane-parallel in registers
+  auto load_chunk = [&](int c, int& len) {
     UnitMeta m{0, 0, 0, 0};
-    const int u = ub + lane;
-    if (u < u1) {
-      const int e = u % NPT;
-      m.head = u / NPT;
-      m.pg = p.pages[p.priv_base + e];
-      m.ntok = p.page_ntok[p.priv_base + e];
-      m.row = p.page_row[e];
+    len = 0;
+    if (c < nch) {
+      const int u0 = p.priv_chunk_start[c];
+      len = p.priv_chunk_start[c + 1] - u0;
+      if (lane < len) {
+        const int u = u0 + lane;
+        const int e = u % NPT;
+        m.head = u / NPT;
+        m.pg = p.pages[p.priv_base + e];
+        m.ntok = p.page_ntok[p.priv_base + e];
+        m.row = p.page_row[e];
+      }
     }
     return m;
   };
-  int wbase = u0;
-  UnitMeta lo = load_meta(wbase), hi = load_meta(wbase + 32);
-  auto meta = [&](int u) {  // warp-uniform u in [wbase, wbase + 64)
-    const int idx = u - wbase;
-    const int src = idx & 31;
-    UnitMeta a0, b0;
-    a0.pg = __shfl_sync(0xffffffffu, lo.pg, src);
-    a0.ntok = __shfl_sync(0xffffffffu, lo.ntok, src);
-    a0.row = __shfl_sync(0xffffffffu, lo.row, src);
-    a0.head = __shfl_sync(0xffffffffu, lo.head, src);
-    b0.pg = __shfl_sync(0xffffffffu, hi.pg, src);
-    b0.ntok = __shfl_sync(0xffffffffu, hi.ntok, src);
-    b0.row = __shfl_sync(0xffffffffu, hi.row, src);
-    b0.head = __shfl_sync(0xffffffffu, hi.head, src);
-    return idx < 32 ? a0 : b0;
+  auto sh = [&](const UnitMeta& m, int i) {
+    UnitMeta r;
+    r.pg = __shfl_sync(0xffffffffu, m.pg, i);
+    r.ntok = __shfl_sync(0xffffffffu, m.ntok, i);
+    r.row = __shfl_sync(0xffffffffu, m.row, i);
+    r.head = __shfl_sync(0xffffffffu, m.head, i);
+    return r;
   };
   auto issue = [&](int s, const UnitMeta& m) {  // lane 0 only
     uint8_t* st = ring + s * kPwStageBytes;
@@ -118,14 +123,29 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
     tma_load_3d(st + 4096, &tmap, 0, m.pg * kPage, pv, &full[warp][s]);
     tma_load_3d(st + 6144, &tmap, 64, m.pg * kPage, pv, &full[warp][s]);
   };
-  int pu = u0;
-  for (int s = 0; s < kPrivStages && pu < u1; ++s, ++pu) {
-    const UnitMeta m = meta(pu);
-    if (lane == 0) issue(s, m);
-  }
+
+  int la = 0, lb = 0;
+  UnitMeta ma = load_chunk(ca, la);
+  int cb = grab();
+  UnitMeta mb = load_chunk(cb, lb);
+  // consumer index i in chunk A; issue index ia relative to A's start (may
+  // run into chunk B); seq = units consumed by this warp (ring position)
+  int i = 0, ia = 0;
+  unsigned seq = 0;
+  auto issue_ahead = [&]() {
+    while (ia - i < kPrivStages && ia < la + lb) {
+      const UnitMeta m = ia < la ? sh(ma, ia) : sh(mb, ia - la);
+      if (lane == 0) {
+        if (ia - i > 0 || seq > 0) fence_proxy_async();
+        issue((int)((seq + (unsigned)(ia - i)) % kPrivStages), m);
+      }
+      ++ia;
+    }
+  };
+  issue_ahead();
 
   // q as the A operand: row 0 of a 16 x 128 tile (lanes 0-3 hold it);
-  // the next item's q is prefetched one page ahead into qn
+  // the next piece's q is prefetched one page ahead into qn
   uint32_t qa[8][2], qn[8][2];
   auto fetch_q = [&](uint32_t (&dst)[8][2], int row, int head) {
     const uint32_t* Q = reinterpret_cast<const uint32_t*>(q + ((long long)row * H + head) * kHeadDim);
@@ -135,27 +155,28 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
       dst[kt][1] = g == 0 ? Q[kt * 8 + 4 + t4] : 0u;
     }
   };
-  UnitMeta cur = meta(u0);
+  UnitMeta cur = sh(ma, 0);
   fetch_q(qa, cur.row, cur.head);
   float o[16][4];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  for (int k = 0; k < 16; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
   float m = -INFINITY, l = 0.f;
   const int mi = lane >> 3, ri = lane & 7;
-  int s = 0;
-  uint32_t phase = 0;
 
-  for (int u = u0; u < u1; ++u) {
-    const bool last = u + 1 == u1;
-    const UnitMeta nxt = last ? cur : meta(u + 1);
-    const bool item_end = last || nxt.row != cur.row || nxt.head != cur.head;
-    if (item_end && !last) fetch_q(qn, nxt.row, nxt.head);
-    mbar_wait(&full[warp][s], phase);
+  while (true) {
+    // the unit after this one (next in A, else first of B) decides the piece end
+    const bool chunk_last = i + 1 == la;
+    const bool have_next = !chunk_last || lb > 0;
+    const UnitMeta nxt = !chunk_last ? sh(ma, i + 1) : (lb > 0 ? sh(mb, 0) : cur);
+    const bool piece_end = chunk_last || nxt.row != cur.row || nxt.head != cur.head;
+    if (piece_end && have_next) fetch_q(qn, nxt.row, nxt.head);
+    const int s = (int)(seq % kPrivStages);
+    mbar_wait(&full[warp][s], (seq / kPrivStages) & 1);
     const uint32_t Ks = smem_u32(ring + s * kPwStageBytes);
     const uint32_t Vs = Ks + 4096;
     float sc[2][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+    for (int k = 0; k < 2; ++k) sc[k][0] = sc[k][1] = sc[k][2] = sc[k][3] = 0.f;
 #pragma unroll
     for (int kt = 0; kt < 8; ++kt) {
       uint32_t b0, b1, b2, b3;
@@ -195,9 +216,9 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
     pl[2] = pack_bf16(pr[2] - bf_lo(ph[2]), pr[3] - bf_hi(ph[2]));
     ph[1] = ph[3] = pl[1] = pl[3] = 0u;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      o[i][0] *= alpha;
-      o[i][1] *= alpha;
+    for (int k = 0; k < 16; ++k) {
+      o[k][0] *= alpha;
+      o[k][1] *= alpha;
     }
 #pragma unroll
     for (int dp = 0; dp < 8; ++dp) {
@@ -209,23 +230,14 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
       mma_bf16(o[2 * dp + 1], pl, b2, b3);
     }
     __syncwarp();  // every lane is done reading stage s
-    if (pu < u1) {
-      const UnitMeta nm = meta(pu);
-      if (lane == 0) {
-        fence_proxy_async();
-        issue(s, nm);
-      }
-      ++pu;
-    }
-    if (++s == kPrivStages) {
-      s = 0;
-      phase ^= 1u;
-    }
-    if (item_end) {
-      // piece end: partial of (row, head) in slot nslots(row) + piece index
+    ++i;
+    ++seq;
+    issue_ahead();
+    if (piece_end) {
+      // partial of (row, head) from this chunk
       const int row = cur.row, head = cur.head;
-      const int first = (head * NPT + p.row_unit_off[row]) / p.priv_per;
-      const int slot = p.row_head_base[(long long)row * H + head] + (gw - first);
+      const long long rh = (long long)row * H + head;
+      const int slot = p.row_head_base[rh] + (ca - p.priv_rh_chunk0[rh]);
       const long long pi = part_index(p, H, row, slot, head);
       float lsum = l;
       lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
@@ -239,27 +251,34 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
       m = -INFINITY;
       l = 0.f;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      for (int k = 0; k < 16; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
 #pragma unroll
       for (int kt = 0; kt < 8; ++kt) {
         qa[kt][0] = qn[kt][0];
         qa[kt][1] = qn[kt][1];
       }
     }
-    cur = nxt;
-    if (u + 1 - wbase >= 32 && u + 1 < u1) {
-      wbase += 32;
-      lo = hi;
-      hi = load_meta(wbase + 32);
+    if (chunk_last) {
+      if (lb == 0) break;  // the ticket counter ran dry
+      // B becomes A; grab the chunk after it
+      ia -= la;
+      i = 0;
+      ca = cb;
+      ma = mb;
+      la = lb;
+      cb = grab();
+      mb = load_chunk(cb, lb);
+      issue_ahead();
     }
+    cur = nxt;
   }
-  CTA_TL_END(fk_tl_cta_priv);
+  CTA_TL_END(fk_tl_cta_priv, layer);
 }
 
 extern "C" int fk_debug_cta_timeline_priv(unsigned long long* out, int n) {
 #ifdef FK_TIMELINE
   if (cudaDeviceSynchronize() != cudaSuccess) return 6;
-  return cudaMemcpyFromSymbol(out, fk_tl_cta_priv, sizeof(unsigned long long) * 2 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_priv, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
 #else
   (void)out;
   (void)n;
@@ -599,7 +618,7 @@ __global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long
 
 // ============================================================== launchers
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                           const CUtensorMap* tmap, bool pdl, cudaStream_t s) {
+                           const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(fk_private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPwSmem);
@@ -607,9 +626,9 @@ cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const
     attr = true;
   }
   if (p.priv_units == 0) return cudaSuccess;
-  const int grid = (p.priv_warps + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta;
+  const int grid = p.priv_warps / kPrivWarpsPerCta;
   return launch_k(fk_private_kernel, dim3(grid), dim3(kPwThreads), kPwSmem, s, pdl, a, p, layer,
-                  (const __nv_bfloat16*)q, scale_log2, *tmap);
+                  (const __nv_bfloat16*)q, scale_log2, *tmap, ticket_base);
 }
 
 cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, bool pdl, cudaStream_t s) {

@@ -110,6 +110,8 @@ struct fk_pool {
   float2* part_ml = nullptr;
   size_t part_cap = 0;     // entries (rows*slots*H) per half
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
+  unsigned long long* ticket = nullptr;  // device: private chunk tickets (never reset)
+  unsigned long long ticket_base = 0;    // tickets consumed by earlier private launches
 
   ArenaDev arena() const {
     ArenaDev a;
@@ -119,6 +121,7 @@ struct fk_pool {
     a.num_heads = desc.num_heads;
     a.part_o = part_o;
     a.part_ml = part_ml;
+    a.ticket = ticket;
       return a;
   }
 };
@@ -278,6 +281,12 @@ int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
         return fail(FK_CUDA_ERROR, "cudaEventCreate failed");
       }
     }
+    if (cudaMalloc(&p->ticket, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(p->ticket, 0, sizeof(unsigned long long)) != cudaSuccess) {
+      cudaGetLastError();
+      fk_pool_destroy(p);
+      return fail(FK_CUDA_ERROR, "ticket counter allocation failed");
+    }
     int rc = reserve_pages(p, desc->num_pages);
     if (rc != FK_OK) {
       fk_pool_destroy(p);
@@ -301,6 +310,7 @@ int fk_pool_destroy(fk_pool* p) {
     if (p->kv) cudaFree(p->kv);
     if (p->part_o) cudaFree(p->part_o);
     if (p->part_ml) cudaFree(p->part_ml);
+    if (p->ticket) cudaFree(p->ticket);
   }
   delete p;
   return FK_OK;
@@ -676,12 +686,30 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
+  // Guided dynamic schedule: chunks shrink from ~U / (2 W) pages to 4 as the
+  // list drains (W = warps that start at once), warps grab them from a ticket
+  // counter.  The grid covers every SM: in co-run the CTAs beyond the free
+  // SMs start when tcgen05 prefix CTAs retire and take the leftovers.
   const int64_t priv_sms = corun ? std::max<int64_t>(1, p->num_sms - tc_ctas) : p->num_sms;
-  int64_t G = std::min<int64_t>(priv_sms * kPrivWarpsPerCta, (U + kPrivMinUnits - 1) / kPrivMinUnits);
-  G = std::max<int64_t>(G, 1);
-  G = (G + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta * kPrivWarpsPerCta;
-  const int64_t per = std::max<int64_t>(1, (U + G - 1) / G);
-  std::vector<int32_t> row_head_count(std::max<int64_t>(B * H, 1), 0);
+  const int64_t w_active = priv_sms * kPrivWarpsPerCta;
+  std::vector<int32_t> chunk_start;
+  for (int64_t pos = 0; pos < U;) {
+    int64_t sz = (U - pos + 2 * w_active - 1) / (2 * w_active);
+    sz = std::min<int64_t>(std::max<int64_t>(sz, kPrivMinChunk), kPrivMaxChunk);
+    sz = std::min<int64_t>(sz, U - pos);
+    chunk_start.push_back((int32_t)pos);
+    pos += sz;
+  }
+  const int64_t nchunks = (int64_t)chunk_start.size();
+  chunk_start.push_back((int32_t)U);
+  const int64_t grid_ctas = std::max<int64_t>(
+      1, std::min<int64_t>(p->num_sms, (nchunks + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta));
+  const int64_t G = grid_ctas * kPrivWarpsPerCta;
+  auto chunk_of = [&](int64_t u) {
+    return (int64_t)(std::upper_bound(chunk_start.begin(), chunk_start.end() - 1, (int32_t)u) -
+                     chunk_start.begin()) - 1;
+  };
+  std::vector<int32_t> row_head_count(std::max<int64_t>(B * H, 1), 0), rh_chunk0(std::max<int64_t>(B * H, 1), 0);
   int max_slots = 1;
   for (int r = 0; r < B; ++r) {
     const int64_t np = row_priv_np[r];
@@ -689,7 +717,9 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       int pieces = 0;
       if (np > 0) {
         const int64_t a0 = h * NPT + row_unit_off[r], b0 = a0 + np;
-        pieces = (int)((b0 - 1) / per - a0 / per + 1);
+        const int64_t c0 = chunk_of(a0);
+        rh_chunk0[r * H + h] = (int32_t)c0;
+        pieces = (int)(chunk_of(b0 - 1) - c0 + 1);
       }
       const int cnt = row_head_base[r * H + h] + pieces;
       row_head_count[r * H + h] = cnt;
@@ -749,6 +779,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_app = L.add(sizeof(int32_t) * 2 * nb);
   const size_t o_apos = L.add(sizeof(int64_t) * nb);
   const size_t o_prow = L.add(sizeof(int32_t) * page_row.size());
+  const size_t o_cs = L.add(sizeof(int32_t) * chunk_start.size());
+  const size_t o_rhc = L.add(sizeof(int32_t) * rh_chunk0.size());
   std::vector<int32_t> tc_start(std::max<int64_t>(tc_ctas, 1), 0);
   for (int64_t b = 0, i = num_mma; b < tc_ctas; ++b) {
     const int64_t u = b * tc_per;
@@ -805,6 +837,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   memset(h + o_apos, 0, nb * 8);
   put(o_prow, page_row.data(), page_row.size() * 4);
+  put(o_cs, chunk_start.data(), chunk_start.size() * 4);
+  put(o_rhc, rh_chunk0.data(), rh_chunk0.size() * 4);
   put(o_tcs, tc_start.data(), tc_start.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
@@ -847,8 +881,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.priv_base = (int)priv_base;
   pd.priv_np = (int)NPT;
   pd.priv_units = (int)U;
-  pd.priv_per = (int)per;
+  pd.priv_nchunks = (int)nchunks;
   pd.priv_warps = (int)G;
+  pd.priv_chunk_start = (const int32_t*)(d + o_cs);
+  pd.priv_rh_chunk0 = (const int32_t*)(d + o_rhc);
   p->off_app_page = o_app;
   p->off_app_slot = o_app + nb * 4;
   p->off_app_pos = o_apos;
@@ -888,6 +924,13 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
       FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc, after_private, st));
     return FK_OK;
   };
+  // every warp of a private launch stops after its first failing ticket, so
+  // a launch consumes exactly nchunks + grid warps tickets
+  auto take_tickets = [&]() -> unsigned long long {
+    const unsigned long long base = p->ticket_base;
+    if (p->plan.priv_units > 0) p->ticket_base += (unsigned long long)(p->plan.priv_nchunks + p->plan.priv_warps);
+    return base;
+  };
   // Launch order 0: prefix -> private (PDL: private fills the SMs the prefix
   // grid leaves free; its CTAs wait for the prefix grid on exit).  Order 1:
   // private -> prefix (PDL when the tcgen05 grid is the only prefix grid; its
@@ -896,10 +939,10 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_order == 0) {
     int rc = run_prefix(xl, false);
     if (rc != FK_OK) return rc;
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap,
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, take_tickets(),
                            (p->pdl && (has_mma || has_tc)) || (xl && !has_tc), st));
   } else {
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, xl, st));
+    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, take_tickets(), xl, st));
     const bool chained = p->pdl && has_tc && !has_mma && p->plan.priv_units > 0;
     int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;

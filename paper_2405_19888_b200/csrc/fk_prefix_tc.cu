@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   }
   const int T = u1 - u0;
   TL(160);
-  CTA_TL_START(fk_tl_cta_prefix);
+  CTA_TL_START(fk_tl_cta_prefix, layer);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcKStages; ++s) {
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   }
   tc_fence_before();
   __syncthreads();
-  CTA_TL_END(fk_tl_cta_prefix);
+  CTA_TL_END(fk_tl_cta_prefix, layer);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 extern "C" int fk_debug_cta_timeline_prefix(unsigned long long* out, int n) {
 #ifdef FK_TIMELINE
   if (cudaDeviceSynchronize() != cudaSuccess) return 6;
-  return cudaMemcpyFromSymbol(out, fk_tl_cta_prefix, sizeof(unsigned long long) * 2 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_prefix, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
 #else
   (void)out;
   (void)n;

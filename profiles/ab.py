@@ -1,0 +1,56 @@
+"""Interleaved A/B of pool options on one engine (diagnostic): for R rounds,
+each option set runs N engine steps timed with CUDA events; prints the median
+algorithmic GB/s per set (the suffixes grow every step).  Interleaving cancels the clock drift between separate runs.
+
+    python profiles/ab.py --set PREFIX_RATE_PCT=40 --set PREFIX_RATE_PCT=50 [--rounds 5 --steps 8]
+    (a set may hold several options: --set "CORUN=0,PDL=1")
+"""
+import argparse
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2405_19888_b200 import _lib  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
+    ap.add_argument("--set", action="append", required=True)
+    ap.add_argument("--rounds", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=8)
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    eng, rows = bench.build_engine(cfg, 0, torch, out_len=args.rounds * len(args.set) * (args.steps + 2) + 32)
+    sets = [[kv.split("=") for kv in s.split(",")] for s in args.set]
+    res = {s: [] for s in args.set}
+    st = eng.stream
+    for _ in range(3):
+        eng.step()
+    for r in range(args.rounds):
+        for name, opts in zip(args.set, sets):
+            for k, v in opts:
+                eng.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
+            eng.step()
+            eng.step()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nbytes = 0
+            a.record(st)
+            for _ in range(args.steps):
+                eng.step()
+                nbytes += cfg["L"] * bench.alg_bytes_per_layer(eng.last_plan, rows, cfg["H"])
+            b.record(st)
+            b.synchronize()
+            res[name].append(nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)  # algorithmic GB/s
+    for name in args.set:
+        v = res[name]
+        print(f"{name:40s} median {statistics.median(v):7.0f} GB/s (alg., whole step)  max {max(v):7.0f}  all {' '.join('%.0f' % x for x in v)}")
+
+
+if __name__ == "__main__":
+    main()

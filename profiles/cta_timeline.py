@@ -1,6 +1,6 @@
 """Per-CTA start/end of the prefix (tcgen05) and private kernels for the last
-layer of a bench-shaped step (debug build, FK_LIB_PATH=profiles/build/
-libforkattn_tl.so).  Diagnostic only.
+two layers of a bench-shaped step (debug build, FK_LIB_PATH=profiles/build/
+libforkattn_tl.so; stamps are kept per layer parity).  Diagnostic only.
 
     python profiles/cta_timeline.py [--config ...] [--opt PREFIX_RATE_PCT=50]
 """
@@ -34,27 +34,28 @@ def main():
         eng.step()
     torch.cuda.synchronize()
     info = eng.last_plan
-    npre, npriv = info.num_prefix_ctas, (eng._pool and 1024)
     out = {}
     for name in ("prefix", "priv"):
         fn = getattr(_lib.lib, "fk_debug_cta_timeline_" + name)
         fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-        buf = (ctypes.c_ulonglong * 2048)()
+        buf = (ctypes.c_ulonglong * 4096)()
         assert fn(buf, 1024) == 0
-        out[name] = [(buf[2 * i], buf[2 * i + 1]) for i in range(1024)]
-    # the prefix grid of the last layer started first
-    pre = [x for x in out["prefix"][:info.num_prefix_ctas] if x[0]]
-    t_last = max(s for s, _ in pre)  # CTAs of the last launch started within a few us
-    pre = [x for x in pre if x[0] >= t_last - 20000]
-    t0 = min(s for s, _ in pre)
-    priv = [x for x in out["priv"] if x[0] and abs(x[0] - t0) < 50000 and x[1] >= x[0]]
-    for name, xs in (("prefix", pre), ("private", priv)):
-        st = sorted((s - t0) / 1e3 for s, _ in xs)
-        en = sorted((e - t0) / 1e3 for _, e in xs)
-        print(f"{name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} {st[-1]:7.2f}"
-              f"   end min/med/max {en[0]:7.2f} {statistics.median(en):7.2f} {en[-1]:7.2f}")
-    print("prefix ends:", " ".join("%.1f" % ((e - t0) / 1e3) for _, e in pre))
-    print("private ends (sorted):", " ".join("%.1f" % x for x in sorted((e - t0) / 1e3 for _, e in priv)))
+        out[name] = [[(buf[par * 2048 + 2 * i], buf[par * 2048 + 2 * i + 1]) for i in range(1024)] for par in (0, 1)]
+    L = cfg["L"]
+    pars = [(L - 2) & 1, (L - 1) & 1]  # second-to-last layer, last layer
+    t0 = None
+    for par in pars:
+        pre = [x for x in out["prefix"][par][:info.num_prefix_ctas] if x[0]]
+        t_last = max(s for s, _ in pre)
+        pre = [x for x in pre if x[0] >= t_last - 20000]
+        priv = [x for x in out["priv"][par] if x[0] and abs(x[0] - t_last) < 60000 and x[1] >= x[0]]
+        if t0 is None:
+            t0 = min(s for s, _ in pre + priv)
+        for name, xs in (("prefix", pre), ("private", priv)):
+            st = sorted((s - t0) / 1e3 for s, _ in xs)
+            en = sorted((e - t0) / 1e3 for _, e in xs)
+            print(f"layer%2 {par} {name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} "
+                  f"{st[-1]:7.2f}   end min/med/max {en[0]:7.2f} {statistics.median(en):7.2f} {en[-1]:7.2f}")
     print("plan:", info.num_rows, "rows", info.num_prefix_ctas, "prefix CTAs", info.max_slots, "slots")
 
 
