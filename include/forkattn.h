@@ -141,6 +141,19 @@ int fk_step_plan(fk_pool* pool, const int64_t* leaves, int32_t num_rows,
  * growth, engine.py:416-434). */
 int fk_attn_decode(fk_pool* pool, int32_t layer, const void* q, void* out,
                    float* out_f32, void* stream);
+/* fk_attn_decode for layers [layer0, layer0 + nlayers) in one call, when the
+ * queries of several layers are ready at once (layer i reads
+ * q + i * q_layer_stride bytes, writes out + i * out_layer_stride); the
+ * kernels and their ordering are exactly those of the per-layer calls. */
+int fk_attn_decode_layers(fk_pool* pool, int32_t layer0, int32_t nlayers, const void* q,
+                          int64_t q_layer_stride, void* out, int64_t out_layer_stride, float* out_f32,
+                          int64_t f32_layer_stride, void* stream);
+/* The one-token growth of every planned row, in row (gens) order, with the
+ * sequential OOM rule of engine.py:431-438: positions[r] = token index of
+ * row r's new token, or -1 if its grow failed (OutOfMemory: that request
+ * fails, the others continue); new_ids[r] = the logical block id the grow
+ * allocated, or -1.  Host-only pools use it too (no device work). */
+int fk_step_grow(fk_pool* pool, int64_t* positions, int64_t* new_ids);
 /* After the Python mirror grew each leaf by one token (engine.py:431-438):
  * positions[r] = slot index (token count before the grow) of row r's new
  * token, or -1 when that grow failed (OOM).  Uploads append targets. */

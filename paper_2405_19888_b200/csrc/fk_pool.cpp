@@ -951,6 +951,43 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   return FK_OK;
 }
 
+int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void* q, int64_t q_layer_stride,
+                          void* out, int64_t out_layer_stride, float* out_f32, int64_t f32_layer_stride,
+                          void* stream) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (nlayers < 0 || layer0 < 0 || layer0 + nlayers > p->desc.num_layers)
+    return fail(FK_INVALID_ARGUMENT, "bad layer range [%d, %d)", layer0, layer0 + nlayers);
+  for (int32_t i = 0; i < nlayers; ++i) {
+    const int rc = fk_attn_decode(p, layer0 + i, (const char*)q + i * q_layer_stride, (char*)out + i * out_layer_stride,
+                                  out_f32 ? (float*)((char*)out_f32 + i * f32_layer_stride) : nullptr, stream);
+    if (rc != FK_OK) return rc;
+  }
+  return FK_OK;
+}
+
+int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids) {
+  if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
+  if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
+  const int B = (int)p->plan_leaves.size();
+  if (B > 0 && (!positions || !new_ids)) return fail(FK_INVALID_ARGUMENT, "null output");
+  for (int r = 0; r < B; ++r) {  // gens order, one token each (engine.py:431-443)
+    auto it = p->ctxs.find(p->plan_leaves[r]);
+    if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "leaf of row %d vanished", r);
+    const int64_t pos = it->second.tokens;
+    int64_t n = 0;
+    const int rc = fk_ctx_grow(p, p->plan_leaves[r], pos + 1, &new_ids[r], 1, &n);
+    if (rc == FK_OUT_OF_MEMORY) {
+      positions[r] = -1;
+      new_ids[r] = -1;
+      continue;
+    }
+    if (rc != FK_OK) return rc;
+    positions[r] = pos;
+    if (n == 0) new_ids[r] = -1;
+  }
+  return FK_OK;
+}
+
 int fk_step_commit(fk_pool* p, const int64_t* positions, void* stream) {
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");

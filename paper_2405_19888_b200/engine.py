@@ -334,6 +334,7 @@ class GpuEngine:
         self._stream = None
         self._leaf_buf = (ctypes.c_int64 * 64)()
         self._pos_buf = (ctypes.c_int64 * 64)()
+        self._id_buf = (ctypes.c_int64 * 64)()
         if device is not None:
             import torch
 
@@ -625,6 +626,7 @@ class GpuEngine:
         if B > len(self._leaf_buf):
             self._leaf_buf = (ctypes.c_int64 * (2 * B))()
             self._pos_buf = (ctypes.c_int64 * (2 * B))()
+            self._id_buf = (ctypes.c_int64 * (2 * B))()
         for i, g in enumerate(running):
             self._leaf_buf[i] = self.contexts[g.context_id].uid
         _lib.check(_lib.lib.fk_step_plan(self._pool.handle, self._leaf_buf, B,
@@ -706,10 +708,9 @@ class GpuEngine:
             qp, op, handle, sp = q.data_ptr(), out.data_ptr(), self._pool.handle, self._sp()
             for ci, (a, b) in enumerate(chunks):
                 st.wait_event(hp["ev_q"][ci])
-                for layer in range(a, b):
-                    _lib.check(_lib.lib.fk_attn_decode(handle, layer,
-                                                       ctypes.c_void_p(qp + layer * layer_elems * 2),
-                                                       ctypes.c_void_p(op + layer * layer_elems * 2), None, sp))
+                _lib.check(_lib.lib.fk_attn_decode_layers(handle, a, b - a, ctypes.c_void_p(qp + a * layer_elems * 2),
+                                                          layer_elems * 2, ctypes.c_void_p(op + a * layer_elems * 2),
+                                                          layer_elems * 2, None, 0, sp))
                 hp["ev_o"][ci].record(st)
                 d2h.wait_event(hp["ev_o"][ci])
                 with torch.cuda.stream(d2h):
@@ -740,13 +741,13 @@ class GpuEngine:
                                                      ctypes.c_void_p(q.data_ptr()), self._sp()))
             out = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
             f32 = torch.empty(shape, dtype=torch.float32, device=self._dev) if self.capture_f32 else None
+            # every layer's queries are already on the device: one C call
+            # launches the layers' kernels back to back (fk_attn_decode_layers)
             layer_elems = B * geo.num_heads * geo.head_dim
-            for layer in range(geo.num_layers):
-                qp = q.data_ptr() + layer * layer_elems * 2
-                op = out.data_ptr() + layer * layer_elems * 2
-                fp = ctypes.c_void_p(f32.data_ptr() + layer * layer_elems * 4) if f32 is not None else None
-                _lib.check(_lib.lib.fk_attn_decode(self._pool.handle, layer, ctypes.c_void_p(qp),
-                                                   ctypes.c_void_p(op), fp, self._sp()))
+            _lib.check(_lib.lib.fk_attn_decode_layers(
+                self._pool.handle, 0, geo.num_layers, ctypes.c_void_p(q.data_ptr()), layer_elems * 2,
+                ctypes.c_void_p(out.data_ptr()), layer_elems * 2,
+                ctypes.c_void_p(f32.data_ptr()) if f32 is not None else None, layer_elems * 4, self._sp()))
             self.last_output = out
             self.last_output_f32 = f32
             if isinstance(model, TensorDecodeModel) and model.copy_out:
@@ -832,16 +833,23 @@ class GpuEngine:
         self.busy_ns += elapsed
 
         positions: List[int] = []
-        for g in running:  # one token per running generation (engine.py:431-443)
+        if running:  # one token per running generation, gens order (engine.py:431-443), in one C call
+            _lib.check(_lib.lib.fk_step_grow(self._pool.handle, self._pos_buf, self._id_buf))
+        for i, g in enumerate(running):
             ctx = self.contexts[g.context_id]
-            pos = ctx.token_count
-            try:
-                self.store.grow(ctx, pos + 1)
-            except OutOfMemory as exc:
+            pos = int(self._pos_buf[i])
+            if pos < 0:  # OutOfMemory: only this request fails (PagedKvStore.grow message)
+                need = self.store.blocks_for(ctx.token_count + 1) - len(ctx.block_ids)
                 g.done = True
-                failed.append((g.request_id, str(exc)))
+                failed.append((g.request_id, f"engine {ctx.engine_id}: need {need} blocks, "
+                                             f"{self.store.free_blocks} free"))
                 positions.append(-1)
                 continue
+            bid = int(self._id_buf[i])
+            if bid >= 0:
+                self.store.owner[bid] = ctx.context_id
+                ctx.block_ids.append(bid)
+            ctx.token_count = pos + 1
             positions.append(pos)
             g.emitted += 1
             emitted[g.request_id] = 1

@@ -24,8 +24,12 @@ def main():
     ap.add_argument("--set", action="append", required=True)
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--shape", default=None, help="P,B,S[,L,H]: fork group shape instead of --config")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
+    if args.shape:
+        v = [int(x) for x in args.shape.split(",")]
+        cfg = dict(model="custom", P=v[0], B=v[1], S=v[2], L=v[3] if len(v) > 3 else 40, H=v[4] if len(v) > 4 else 40)
     eng, rows = bench.build_engine(cfg, 0, torch, out_len=args.rounds * len(args.set) * (args.steps + 2) + 32)
     sets = [[kv.split("=") for kv in s.split(",")] for s in args.set]
     res = {s: [] for s in args.set}
