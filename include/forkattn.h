@@ -102,10 +102,12 @@ enum {
                                  SMs and run concurrently; 0: each kernel gets every SM in turn */
   FK_OPT_PREFIX_RATE_PCT = 6, /* co-run SM split: prefix per-SM KV rate relative to the private
                                  stream's, in percent (default 50) */
-  FK_OPT_PDL = 7              /* programmatic dependent launch: 0 plain stream order; 1 (default)
+  FK_OPT_PDL = 7,             /* programmatic dependent launch: 0 plain stream order; 1 (default)
                                  between one layer's kernels; 2 also lets a layer's first kernel
                                  start under the previous layer's merge -- only when q is not
                                  written by the kernel launched right before fk_attn_decode */
+  FK_OPT_PRIV_MIN_CHUNK = 8   /* smallest chunk (pages) of the private kernel's guided dynamic
+                                 schedule, 1..32 (default 2): the granularity of its tail */
 };
 
 /* ---- context forest ------------------------------------------------------ */

@@ -32,6 +32,7 @@ FK_OPT_MIN_SPLIT_PAGES = 4
 FK_OPT_CORUN = 5
 FK_OPT_PREFIX_RATE_PCT = 6
 FK_OPT_PDL = 7
+FK_OPT_PRIV_MIN_CHUNK = 8
 
 
 class PoolDesc(ctypes.Structure):

@@ -90,6 +90,7 @@ struct fk_pool {
   int64_t tc_min_fanout = 2;  // tcgen05 for every shared context until the sweep says otherwise
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
+  int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
@@ -347,6 +348,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_PREFIX_TARGET_CTAS: p->prefix_target_ctas = value; break;
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
     case FK_OPT_PDL: p->pdl = value; break;
+    case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
     case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
@@ -695,7 +697,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   std::vector<int32_t> chunk_start;
   for (int64_t pos = 0; pos < U;) {
     int64_t sz = (U - pos + 2 * w_active - 1) / (2 * w_active);
-    sz = std::min<int64_t>(std::max<int64_t>(sz, kPrivMinChunk), kPrivMaxChunk);
+    sz = std::min<int64_t>(std::max<int64_t>(sz, p->priv_min_chunk), kPrivMaxChunk);
     sz = std::min<int64_t>(sz, U - pos);
     chunk_start.push_back((int32_t)pos);
     pos += sz;
