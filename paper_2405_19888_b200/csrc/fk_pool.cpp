@@ -704,8 +704,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   const int64_t nchunks = (int64_t)chunk_start.size();
   chunk_start.push_back((int32_t)U);
+  // launched first (order 1) the private grid must leave the prefix its SMs
+  const int64_t grid_sms = (corun && p->launch_order == 1) ? priv_sms : p->num_sms;
   const int64_t grid_ctas = std::max<int64_t>(
-      1, std::min<int64_t>(p->num_sms, (nchunks + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta));
+      1, std::min<int64_t>(grid_sms, (nchunks + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta));
   const int64_t G = grid_ctas * kPrivWarpsPerCta;
   auto chunk_of = [&](int64_t u) {
     return (int64_t)(std::upper_bound(chunk_start.begin(), chunk_start.end() - 1, (int32_t)u) -

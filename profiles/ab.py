@@ -51,6 +51,10 @@ def main():
             b.record(st)
             b.synchronize()
             res[name].append(nbytes / (a.elapsed_time(b) * 1e-3) / 1e9)  # algorithmic GB/s
+            if res[name][-1] < 0.7 * max(res[name]):
+                ps = eng.pool_stats()
+                print(f"outlier: round {r} set {name}: {a.elapsed_time(b) / args.steps:.3f} ms/step, pages "
+                      f"{ps.num_pages} free {ps.free_pages}, slots {eng.last_plan.max_slots}", flush=True)
     for name in args.set:
         v = res[name]
         print(f"{name:40s} median {statistics.median(v):7.0f} GB/s (alg., whole step)  max {max(v):7.0f}  all {' '.join('%.0f' % x for x in v)}")

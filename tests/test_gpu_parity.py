@@ -338,3 +338,36 @@ def test_prefix_migration_between_pools(cuda_device):
         assert torch.equal(x, y)
     a.close()
     b.close()
+
+
+def test_mapreduce_shape_one_layer(cuda_device):
+    """BASELINE config 4 per GPU: 2 groups of 32 forks over 2k-token chunk
+    prefixes, suffixes U[128, 1024] (random.Random(0)), 13B head count."""
+    rng = random.Random(0)
+    eng = make_engine(cuda_device, H=40, L=1)
+    for gi in range(2):
+        fork_group(eng, 2000, [rng.randint(128, 1024) for _ in range(32)], out_len=1, tag=f"g{gi}", seed=gi)
+    run_steps(eng, 1)
+    assert eng.last_plan.num_shared_ctx == 2 and eng.last_plan.num_rows == 64
+    check_history(eng)
+    assert_plan_matches_walk(eng)
+
+
+def test_nested_shape_one_layer(cuda_device):
+    """BASELINE config 5 per GPU: 4k system prompt -> 1k app prompt -> 64
+    users x 256, 13B head count (three-level chain, two shared levels)."""
+    eng = make_engine(cuda_device, H=40, L=1)
+    nested_forest(eng, root_len=4096, app_len=1024, n_apps=1, user_len=256, users_per_app=64, out_len=1)
+    run_steps(eng, 1)
+    assert eng.last_plan.num_shared_ctx == 2 and eng.last_plan.num_rows == 64
+    check_history(eng)
+    assert_plan_matches_walk(eng)
+
+
+def test_fanout_256_two_query_blocks(cuda_device):
+    """BASELINE config 3 at 256 forks: two 128-query tcgen05 blocks per head
+    (or four 64-query mma blocks) over one 6k prefix, 8 heads."""
+    eng = make_engine(cuda_device, H=8, L=1)
+    fork_group(eng, 6000, [64] * 256, out_len=1)
+    run_steps(eng, 1)
+    check_history(eng)
