@@ -94,7 +94,7 @@ cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, co
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
                              float scale_log2, const CUtensorMap* tmap, const CUtensorMap* tmap_run,
                              bool pdl, bool after_private, cudaStream_t s);
-cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, bool pdl,
+cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, int layer, bool pdl,
                          cudaStream_t s);
 cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers,
                           const void* k, const void* v, cudaStream_t s);

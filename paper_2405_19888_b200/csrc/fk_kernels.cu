@@ -483,14 +483,31 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
 // ================================================================== merge
 // K4: one warp per (row, head) combines every partial (shared-prefix splits
 // + private pieces) in log2 space and writes the bf16 row (fp32 optional).
+CTA_TL_DECL(fk_tl_cta_merge);
+
 __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __nv_bfloat16* __restrict__ out,
-                                                      float* __restrict__ out_f32) {
+                                                      float* __restrict__ out_f32, int layer) {
+  CTA_TL_START(fk_tl_cta_merge, layer);  // (timeline builds: [0] = after the wait)
   pdl_wait_primary();       // partials of the prefix and private grids are complete
   pdl_launch_dependents();  // the next layer's first kernel may start (other partial half)
+#ifdef FK_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) fk_tl_cta_merge[layer & 1][blockIdx.x][0] = global_ns();
+#endif
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int H = a.num_heads;
-  if (w >= p.num_rows * H) return;
-  merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane);
+  if (w < p.num_rows * H) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane);
+  CTA_TL_END(fk_tl_cta_merge, layer);
+}
+
+extern "C" int fk_debug_cta_timeline_merge(unsigned long long* out, int n) {
+#ifdef FK_TIMELINE
+  if (cudaDeviceSynchronize() != cudaSuccess) return 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_merge, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+#else
+  (void)out;
+  (void)n;
+  return 5;
+#endif
 }
 
 // ================================================================= append
@@ -631,10 +648,11 @@ cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const
                   (const __nv_bfloat16*)q, scale_log2, *tmap, ticket_base);
 }
 
-cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, bool pdl, cudaStream_t s) {
+cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, int layer, bool pdl,
+                         cudaStream_t s) {
   const int warps = p.num_rows * a.num_heads;
   return launch_k(fk_merge_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, pdl, a, p, (__nv_bfloat16*)out,
-                  out_f32);
+                  out_f32, layer);
 }
 
 cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,

@@ -951,7 +951,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
     int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;
   }
-  FK_CUDA(launch_merge(a, p->plan, out, out_f32, p->pdl != 0, st));
+  FK_CUDA(launch_merge(a, p->plan, out, out_f32, layer, p->pdl != 0, st));
   return FK_OK;
 }
 

@@ -35,7 +35,7 @@ def main():
     torch.cuda.synchronize()
     info = eng.last_plan
     out = {}
-    for name in ("prefix", "priv"):
+    for name in ("prefix", "priv", "merge"):
         fn = getattr(_lib.lib, "fk_debug_cta_timeline_" + name)
         fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
         buf = (ctypes.c_ulonglong * 4096)()
@@ -51,11 +51,13 @@ def main():
         priv = [x for x in out["priv"][par] if x[0] and abs(x[0] - t_last) < 60000 and x[1] >= x[0]]
         if t0 is None:
             t0 = min(s for s, _ in pre + priv)
-        for name, xs in (("prefix", pre), ("private", priv)):
+        mer = [x for x in out["merge"][par] if x[0] and abs(x[0] - t_last) < 200000 and x[1] >= x[0]]
+        for name, xs in (("prefix", pre), ("private", priv), ("merge*", mer)):
             st = sorted((s - t0) / 1e3 for s, _ in xs)
             en = sorted((e - t0) / 1e3 for _, e in xs)
             print(f"layer%2 {par} {name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} "
                   f"{st[-1]:7.2f}   end min/med/max {en[0]:7.2f} {statistics.median(en):7.2f} {en[-1]:7.2f}")
+    print("(merge* start = after its griddepcontrol.wait)")
     print("plan:", info.num_rows, "rows", info.num_prefix_ctas, "prefix CTAs", info.max_slots, "slots")
 
 
