@@ -342,6 +342,11 @@ class GpuEngine:
             self._dev = torch.device("cuda", device)
             with torch.cuda.device(self._dev):
                 self._stream = torch.cuda.Stream(self._dev)
+                # fills (prefill KV writes, prefix migrations) run on their own
+                # stream: decode waits only for the fills of contexts it reads
+                self._fill_stream = torch.cuda.Stream(self._dev)
+            self._fill_pending: Dict[str, Any] = {}  # context id -> event of its last fill
+            self._release_event = None  # engine-stream fence of the last page release
             # The engine owns Q's producer side (its own buffers, ordered by
             # stream events), so a layer's kernels may start under the previous
             # layer's merge (cross-layer programmatic dependent launch).
@@ -380,6 +385,7 @@ class GpuEngine:
 
     def close(self) -> None:
         if self._stream is not None:
+            self._fill_stream.synchronize()
             self._stream.synchronize()
         self._pool.close()
 
@@ -443,29 +449,40 @@ class GpuEngine:
                 self._discard_context(ctx)
             raise
         if self.device is not None and len(token_ids) > 0:
+            torch = self._torch
+            fs = self._fill_stream
+            fsp = ctypes.c_void_p(fs.cuda_stream)
+            if self._release_event is not None:  # recycled pages: earlier decode work is done with them
+                fs.wait_event(self._release_event)
+            prev = self._fill_pending.get(context_id)
+            if prev is not None:
+                fs.wait_event(prev)
             if kv_from is not None:
-                torch = self._torch
                 ev = torch.cuda.Event()
                 ev.record(src_eng.stream)  # the source pages are written
-                self._stream.wait_event(ev)
+                fs.wait_event(ev)
+                src_fill = src_eng._fill_pending.get(src_id)
+                if src_fill is not None:
+                    fs.wait_event(src_fill)
                 _lib.check(_lib.lib.fk_ctx_copy_kv(self._pool.handle, ctx.uid, src_eng._pool.handle, src_ctx.uid,
-                                                   len(token_ids), self._sp()))
-                done = torch.cuda.Event()
-                done.record(self._stream)
-                src_eng.stream.wait_event(done)  # the source may not recycle them before the copy
+                                                   len(token_ids), fsp))
             elif kv is not None:
                 k, v = kv
-                with self._torch.cuda.device(self._dev):
-                    # the caller's tensors are consumed on the engine stream
-                    self._stream.wait_stream(self._torch.cuda.current_stream(self._dev))
+                with torch.cuda.device(self._dev):
+                    fs.wait_stream(torch.cuda.current_stream(self._dev))  # the caller's tensors
                 _lib.check(_lib.lib.fk_fill_kv(self._pool.handle, ctx.uid, before, ctx.token_count, 0,
                                                self.geometry.num_layers, ctypes.c_void_p(k.data_ptr()),
-                                               ctypes.c_void_p(v.data_ptr()), self._sp()))
-                k.record_stream(self._stream)
-                v.record_stream(self._stream)
+                                               ctypes.c_void_p(v.data_ptr()), fsp))
+                k.record_stream(fs)
+                v.record_stream(fs)
             else:
                 _lib.check(_lib.lib.fk_synth_fill(self._pool.handle, ctx.uid, before, ctx.token_count,
-                                                  self.model_seed, self.model_k_scale, self._sp()))
+                                                  self.model_seed, self.model_k_scale, fsp))
+            done = torch.cuda.Event()
+            done.record(fs)
+            self._fill_pending[context_id] = done
+            if kv_from is not None:
+                src_eng.stream.wait_event(done)  # the source may not recycle its pages before the copy
         if boundary_hash is not None:
             ctx.chain_hashes.append(boundary_hash)
             if boundary_hash not in self.registry:
@@ -506,8 +523,13 @@ class GpuEngine:
         return task
 
     def _discard_context(self, ctx: Context) -> None:
+        if self.device is not None:  # fills into the recycled pages wait for this point
+            self._release_event = self._torch.cuda.Event()
+            self._release_event.record(self._stream)
         while ctx is not None:
             self.store.release(ctx)
+            if self.device is not None:
+                self._fill_pending.pop(ctx.context_id, None)
             for h in ctx.registered_hashes:
                 if self.registry.get(h) == ctx.context_id:
                     del self.registry[h]
@@ -781,6 +803,21 @@ class GpuEngine:
             _lib.check(_lib.lib.fk_synth_append(self._pool.handle, self.model_seed, self.model_k_scale,
                                                 self._sp()))
 
+    def _wait_fills(self, running: List[GenerationTask]) -> None:
+        """The decode stream waits for the pending fills of the contexts this
+        step reads (and only those: other fills keep overlapping decode)."""
+        seen: Set[str] = set()
+        for g in running:
+            for c in self._ancestors(self.contexts.get(g.context_id)):
+                if c.context_id in seen:
+                    break
+                seen.add(c.context_id)
+                ev = self._fill_pending.pop(c.context_id, None)
+                if ev is not None:
+                    self._stream.wait_event(ev)
+            if not self._fill_pending:
+                break
+
     def _snapshot(self, running: List[GenerationTask]) -> List[List[Tuple[int, int]]]:
         """Per row: [(context uid, tokens)] root -> leaf at plan time."""
         rows = []
@@ -815,6 +852,8 @@ class GpuEngine:
 
         running = [g for g in self.gens.values() if g.started and not g.done]
         batch_tokens = self._plan(running) if running else 0
+        if running and self.device is not None and self._fill_pending:
+            self._wait_fills(running)
         snapshot = self._snapshot(running) if (self.keep_history and running) else None
         if running and self.device is not None:
             self._decode_attention(running)

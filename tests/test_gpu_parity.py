@@ -371,3 +371,27 @@ def test_fanout_256_two_query_blocks(cuda_device):
     fork_group(eng, 6000, [64] * 256, out_len=1)
     run_steps(eng, 1)
     check_history(eng)
+
+
+def test_fill_while_decoding(cuda_device):
+    """Fills run on their own stream: a new fork group is prefilled between
+    decode steps of another, and finished contexts' pages are recycled into
+    it; decode waits only for the fills of contexts it reads."""
+    eng = make_engine(cuda_device, H=4, L=2)
+    fork_group(eng, 300, [20, 33], out_len=6, tag="a", seed=1)
+    run_steps(eng, 2)
+    fork_group(eng, 500, [7, 64, 90], out_len=3, tag="b", seed=2)  # joins mid-run
+    run_steps(eng, 3)
+    freed = 0
+    for rid, g in [(r, g) for r, g in eng.gens.items() if g.done]:
+        eng.finish_generation(rid)
+        if eng.contexts[g.context_id].refcount == 0:
+            eng.free_context(g.context_id)  # its pages go back to the free stack
+            freed += 1
+    assert freed > 0
+    free_before = eng.pool_stats().free_pages
+    fork_group(eng, 250, [16, 17], out_len=2, tag="c", seed=3)
+    assert eng.pool_stats().free_pages < free_before  # group c reuses recycled pages
+    run_steps(eng, 4)
+    check_history(eng)
+    assert_plan_matches_walk(eng)
