@@ -106,8 +106,10 @@ enum {
                                  between one layer's kernels; 2 also lets a layer's first kernel
                                  start under the previous layer's merge -- only when q is not
                                  written by the kernel launched right before fk_attn_decode */
-  FK_OPT_PRIV_MIN_CHUNK = 8   /* smallest chunk (pages) of the private kernel's guided dynamic
+  FK_OPT_PRIV_MIN_CHUNK = 8,  /* smallest chunk (pages) of the private kernel's guided dynamic
                                  schedule, 1..32 (default 2): the granularity of its tail */
+  FK_OPT_PRIV_STATIC_FIRST = 9 /* 1 (default): the private warps that start at once take their
+                                 first chunk by warp index instead of a ticket */
 };
 
 /* ---- context forest ------------------------------------------------------ */

@@ -33,6 +33,7 @@ FK_OPT_CORUN = 5
 FK_OPT_PREFIX_RATE_PCT = 6
 FK_OPT_PDL = 7
 FK_OPT_PRIV_MIN_CHUNK = 8
+FK_OPT_PRIV_STATIC_FIRST = 9
 
 
 class PoolDesc(ctypes.Structure):

@@ -59,6 +59,7 @@ struct PlanDev {
   int priv_units;              // U = H * NPT
   int priv_nchunks;
   int priv_warps;              // grid warps (grid = priv_warps / kPrivWarpsPerCta)
+  int priv_static;             // warps that start on chunk = warp index (the ones that start at once)
   const int* priv_chunk_start; // [priv_nchunks + 1]
   const int* priv_rh_chunk0;   // [rows][H] first chunk of each (row, head) item
   // synthetic keys per row

@@ -70,14 +70,19 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
 
   const int g = lane >> 2, t4 = lane & 3;
   const int NPT = p.priv_np, nch = p.priv_nchunks;
-  // every warp stops after its first failing ticket: a launch consumes
-  // exactly nchunks + (grid warps) tickets (the host advances ticket_base)
+  // The warps of the CTAs that start at once (the first priv_static of the
+  // grid) begin on chunk = their global warp index, with no ticket round trip
+  // before their first loads; every later chunk comes from a ticket:
+  // chunk = priv_static + ticket.  Each warp stops after its first failing
+  // ticket, so a launch consumes nchunks - priv_static + (grid warps) tickets
+  // (the host advances ticket_base by that).
+  const int gw = blockIdx.x * kPrivWarpsPerCta + warp;
   auto grab = [&]() -> int {
     int c = 0;
-    if (lane == 0) c = (int)(atomicAdd(a.ticket, 1ull) - ticket_base);
+    if (lane == 0) c = p.priv_static + (int)(atomicAdd(a.ticket, 1ull) - ticket_base);
     return __shfl_sync(0xffffffffu, c, 0);
   };
-  int ca = grab();
+  int ca = gw < p.priv_static ? gw : grab();
   if (ca >= nch) return;
 
   uint8_t* ring = smem + warp * kPrivStages * kPwStageBytes;

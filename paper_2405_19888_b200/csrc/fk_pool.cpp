@@ -91,6 +91,7 @@ struct fk_pool {
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
+  int64_t priv_static_first = 1;  // warps that start at once begin on a fixed chunk (no ticket)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
@@ -348,6 +349,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_PREFIX_TARGET_CTAS: p->prefix_target_ctas = value; break;
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
     case FK_OPT_PDL: p->pdl = value; break;
+    case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
@@ -887,6 +889,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.priv_units = (int)U;
   pd.priv_nchunks = (int)nchunks;
   pd.priv_warps = (int)G;
+  pd.priv_static = p->priv_static_first ? (int)std::min<int64_t>(std::min<int64_t>(w_active, G), nchunks) : 0;
   pd.priv_chunk_start = (const int32_t*)(d + o_cs);
   pd.priv_rh_chunk0 = (const int32_t*)(d + o_rhc);
   p->off_app_page = o_app;
@@ -928,11 +931,11 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
       FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc, after_private, st));
     return FK_OK;
   };
-  // every warp of a private launch stops after its first failing ticket, so
-  // a launch consumes exactly nchunks + grid warps tickets
+  // tickets a private launch consumes (fk_private_kernel): nchunks - static + grid warps
   auto take_tickets = [&]() -> unsigned long long {
     const unsigned long long base = p->ticket_base;
-    if (p->plan.priv_units > 0) p->ticket_base += (unsigned long long)(p->plan.priv_nchunks + p->plan.priv_warps);
+    if (p->plan.priv_units > 0)
+      p->ticket_base += (unsigned long long)(p->plan.priv_nchunks - p->plan.priv_static + p->plan.priv_warps);
     return base;
   };
   // Launch order 0: prefix -> private (PDL: private fills the SMs the prefix
