@@ -191,52 +191,67 @@ __device__ __forceinline__ int partial_count(const PlanDev& p, int H, int row, i
 // all (no partial) produce zeros.
 __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
                                                     __nv_bfloat16* out, float* out_f32, int lane) {
-  // two dependent rounds: (m, l) of every slot lane-parallel, then every
-  // slot's o (4 dims per lane) with all loads in flight together
+  // two dependent rounds: (m, l) of every slot lane-parallel (slot k in lane
+  // k % 32 of round k / 32, up to kMergeRounds rounds in registers), then
+  // every slot's o (4 dims per lane), 8 slots' loads in flight at a time
+  constexpr int kMergeRounds = 4;  // up to 128 partials per (row, head)
   const int H = a.num_heads;
   const int ns = partial_count(p, H, row, head);
   const long long base = part_index(p, H, row, 0, head);  // slot stride is H
-  float2 ml = make_float2(-INFINITY, 0.f);
-  if (lane < ns) ml = __ldcg(&a.part_ml[base + (long long)lane * H]);
-  float M = ml.x;
+  float2 ml[kMergeRounds];
+  float M = -INFINITY;
+#pragma unroll
+  for (int r = 0; r < kMergeRounds; ++r) {
+    const int k = r * 32 + lane;
+    ml[r] = k < ns ? __ldcg(&a.part_ml[base + (long long)k * H]) : make_float2(-INFINITY, 0.f);
+    M = fmaxf(M, ml[r].x);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  const float w = (M == -INFINITY || lane >= ns) ? 0.f : ex2(ml.x - M);
-  float L = ml.y * w;
+  float w[kMergeRounds];
+  float L = 0.f;
+#pragma unroll
+  for (int r = 0; r < kMergeRounds; ++r) {
+    w[r] = (M == -INFINITY || r * 32 + lane >= ns) ? 0.f : ex2(ml[r].x - M);
+    L = fmaf(ml[r].y, w[r], L);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (ns > 32) {  // rare (many splits): generic lane-strided path
-    M = -INFINITY;
-    for (int k = lane; k < ns; k += 32) M = fmaxf(M, __ldcg(&a.part_ml[base + (long long)k * H].x));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    L = 0.f;
-    if (M != -INFINITY)
-      for (int k = 0; k < ns; ++k) {
-        const float2 mk = __ldcg(&a.part_ml[base + (long long)k * H]);
-        const float wk = ex2(mk.x - M);
-        L += mk.y * wk;
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)k * H) * kHeadDim) + lane);
-        acc.x = fmaf(v.x, wk, acc.x);
-        acc.y = fmaf(v.y, wk, acc.y);
-        acc.z = fmaf(v.z, wk, acc.z);
-        acc.w = fmaf(v.w, wk, acc.w);
-      }
-  }
-  for (int k0 = 0; k0 < ns && ns <= 32; k0 += 8) {
+  const int nsm = min(ns, 32 * kMergeRounds);
+  for (int k0 = 0; k0 < nsm; k0 += 8) {
     float4 v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      v[k] = k0 + k < ns ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)(k0 + k) * H) * kHeadDim) + lane)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[k] = k0 + k < nsm ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)(k0 + k) * H) * kHeadDim) + lane)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int r = k0 >> 5;  // the 8 slots of this group share one round
+    float wr = w[0];
+#pragma unroll
+    for (int rr = 1; rr < kMergeRounds; ++rr) wr = r == rr ? w[rr] : wr;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const float wk = __shfl_sync(0xffffffffu, w, (k0 + k) & 31);
+      const float wk = __shfl_sync(0xffffffffu, wr, (k0 + k) & 31);
       acc.x = fmaf(v[k].x, wk, acc.x);
       acc.y = fmaf(v[k].y, wk, acc.y);
       acc.z = fmaf(v[k].z, wk, acc.z);
       acc.w = fmaf(v[k].w, wk, acc.w);
+    }
+  }
+  if (ns > 32 * kMergeRounds && M != -INFINITY) {  // beyond the register rounds: one slot at a time
+    // (the planner keeps far fewer partials; this only guards correctness)
+    for (int k = 32 * kMergeRounds; k < ns; ++k) M = fmaxf(M, __ldcg(&a.part_ml[base + (long long)k * H]).x);
+    acc = make_float4(0.f, 0.f, 0.f, 0.f);  // start over with the max of every slot
+    L = 0.f;
+    for (int k = 0; k < ns; ++k) {
+      const float2 mk = __ldcg(&a.part_ml[base + (long long)k * H]);
+      const float wk = ex2(mk.x - M);
+      L = fmaf(mk.y, wk, L);
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)k * H) * kHeadDim) + lane);
+      acc.x = fmaf(v.x, wk, acc.x);
+      acc.y = fmaf(v.y, wk, acc.y);
+      acc.z = fmaf(v.z, wk, acc.z);
+      acc.w = fmaf(v.w, wk, acc.w);
     }
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;

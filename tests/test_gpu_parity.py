@@ -395,3 +395,16 @@ def test_fill_while_decoding(cuda_device):
     run_steps(eng, 4)
     check_history(eng)
     assert_plan_matches_walk(eng)
+
+
+@pytest.mark.parametrize("suffix", [600, 2100])
+def test_merge_many_partials(cuda_device, suffix):
+    """One-page private chunks cut a long suffix into one partial per page:
+    > 32 partials (the merge's multi-round fast path) and > 128 (its
+    one-slot-at-a-time fallback) per (row, head)."""
+    eng = make_engine(cuda_device, H=2)
+    eng.set_option(_lib.FK_OPT_PRIV_MIN_CHUNK, 1)
+    fork_group(eng, 100, [suffix, 5], out_len=2)
+    run_steps(eng, 2)
+    assert eng.last_plan.max_slots > (128 if suffix > 2048 else 32)
+    check_history(eng)
