@@ -108,8 +108,10 @@ enum {
                                  written by the kernel launched right before fk_attn_decode */
   FK_OPT_PRIV_MIN_CHUNK = 8,  /* smallest chunk (pages) of the private kernel's guided dynamic
                                  schedule, 1..32 (default 2): the granularity of its tail */
-  FK_OPT_PRIV_STATIC_FIRST = 9 /* 1 (default): the private warps that start at once take their
+  FK_OPT_PRIV_STATIC_FIRST = 9, /* 1 (default): the private warps that start at once take their
                                  first chunk by warp index instead of a ticket */
+  FK_OPT_TC_BOUNDARY_COST = 10 /* tcgen05 stream-K balance: tiles a piece start mid-range costs a
+                                 CTA (default 4, measured) */
 };
 
 /* ---- context forest ------------------------------------------------------ */

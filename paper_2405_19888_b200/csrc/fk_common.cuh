@@ -79,13 +79,15 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // Debug builds (-DFK_TIMELINE): per-CTA start/end stamps of the attention
 // kernels, read back with fk_debug_cta_timeline (profiles/cta_timeline.py).
 #ifdef FK_TIMELINE
-#define CTA_TL_DECL(name) __device__ unsigned long long name[2][1024][2]
+#define CTA_TL_DECL(name) __device__ unsigned long long name[2][1024][4]
 #define CTA_TL_START(name, layer) do { if (threadIdx.x == 0 && blockIdx.x < 1024) name[(layer) & 1][blockIdx.x][0] = global_ns(); } while (0)
 #define CTA_TL_END(name, layer) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 1024) name[(layer) & 1][blockIdx.x][1] = global_ns(); } while (0)  // last writer ~ last warp
+#define CTA_TL_NOTE(name, layer, k, v) do { if (blockIdx.x < 1024) name[(layer) & 1][blockIdx.x][k] = (v); } while (0)
 #else
 #define CTA_TL_DECL(name) static_assert(true, "")
 #define CTA_TL_START(name, layer) do { } while (0)
 #define CTA_TL_END(name, layer) do { } while (0)
+#define CTA_TL_NOTE(name, layer, k, v) do { } while (0)
 #endif
 
 // Launch with optional programmatic dependent launch (PDL): the kernel may

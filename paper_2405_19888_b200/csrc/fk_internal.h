@@ -39,8 +39,10 @@ struct PlanDev {
   const int* it_units;     // 128-token tiles of the item
   const int* qrows;        // request rows
   const int* qslot;        // slot of piece 0 for each (item, query)
-  int tc_units, tc_per, tc_ctas;  // tcgen05 stream-K geometry
+  int tc_units, tc_ctas;          // tcgen05 stream-K geometry
   const int* tc_start_item;       // [tc_ctas] item holding each CTA's first unit
+  const int* tc_cta_start;        // [tc_ctas + 1] first unit of each CTA (cost-balanced)
+  const int* it_first_cta;        // per item: CTA holding its first unit (piece 0)
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;

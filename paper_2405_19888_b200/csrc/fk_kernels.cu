@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
 extern "C" int fk_debug_cta_timeline_priv(unsigned long long* out, int n) {
 #ifdef FK_TIMELINE
   if (cudaDeviceSynchronize() != cudaSuccess) return 6;
-  return cudaMemcpyFromSymbol(out, fk_tl_cta_priv, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_priv, sizeof(unsigned long long) * 8 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
 #else
   (void)out;
   (void)n;
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __
 extern "C" int fk_debug_cta_timeline_merge(unsigned long long* out, int n) {
 #ifdef FK_TIMELINE
   if (cudaDeviceSynchronize() != cudaSuccess) return 6;
-  return cudaMemcpyFromSymbol(out, fk_tl_cta_merge, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_merge, sizeof(unsigned long long) * 8 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
 #else
   (void)out;
   (void)n;

@@ -91,7 +91,8 @@ struct fk_pool {
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
-  int64_t priv_static_first = 1;  // warps that start at once begin on a fixed chunk (no ticket)
+  int64_t priv_static_first = 1;
+  int64_t tc_boundary_cost = 4;  // tiles a mid-range piece start costs a tcgen05 CTA (stream-K balance)  // warps that start at once begin on a fixed chunk (no ticket)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
@@ -350,6 +351,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
     case FK_OPT_PDL: p->pdl = value; break;
     case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
+    case FK_OPT_TC_BOUNDARY_COST: p->tc_boundary_cost = std::max<int64_t>(0, value); break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
@@ -607,21 +609,67 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   for (int r = 0; r < B; ++r)
     for (int64_t c : chain[r])
       if (!is_shared(c)) priv_tok_heads += p->ctxs[c].tokens * H;
-  int64_t tc_tok_heads = 0;
-  for (size_t i = num_mma; i < items.size(); ++i) tc_tok_heads += items[i].ntok;
+  // a 128-query block costs the softmax ~4/3 of a <= 64-query block per tile
+  // (the 16-lane layout only covers fan-outs <= 64; measured 2.5 vs 1.9 us)
+  double tc_tok_heads = 0.0;
+  for (size_t i = num_mma; i < items.size(); ++i) tc_tok_heads += items[i].ntok * (items[i].nq > 64 ? 4.0 / 3.0 : 1.0);
   const bool corun = p->corun && num_mma == 0 && tc_units > 0 && priv_tok_heads > 0 && p->num_sms > 1;
   int64_t tc_target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
   if (corun && p->prefix_target_ctas <= 0) {
-    const double wp = (double)tc_tok_heads * 100.0 / (double)p->prefix_rate_pct;
+    const double wp = tc_tok_heads * 100.0 / (double)p->prefix_rate_pct;
     const double wv = (double)priv_tok_heads;
     tc_target = std::min<int64_t>(p->num_sms - 1, std::max<int64_t>(1, std::llround(p->num_sms * wp / (wp + wv))));
   }
-  const int64_t tc_ctas = tc_units > 0 ? std::min<int64_t>(tc_target, tc_units) : 0;
-  const int64_t tc_per = tc_ctas > 0 ? (tc_units + tc_ctas - 1) / tc_ctas : 1;
+  // Cost-balanced stream-K: every tile costs 1 and every extra piece a CTA
+  // starts mid-range (epilogue + pipeline restart, ~2 tiles measured) costs
+  // tc_boundary_cost, so CTAs that cross item boundaries get fewer tiles and
+  // all of them finish together.  cta_start[b] = first unit of CTA b.
+  std::vector<int32_t> cta_start;
+  if (tc_units > 0) {
+    const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, tc_units));
+    const double bc = (double)p->tc_boundary_cost;
+    // the target is re-derived for every CTA from the work that is left, so
+    // rounding never piles up on the last one
+    double rest = (double)tc_units + bc * (double)(num_tc - 1);
+    auto target_for = [&](int64_t b) { return rest / (double)std::max<int64_t>(1, X - b); };
+    double cost = 0.0, target = target_for(0);
+    int64_t u = 0;
+    cta_start.push_back(0);
+    for (size_t i = num_mma; i < items.size(); ++i) {
+      if (cost > 0.0) {
+        cost += bc;
+      } else if (i > (size_t)num_mma) {
+        rest -= bc;  // this CTA starts at the item boundary: no extra piece
+        target = target_for((int64_t)cta_start.size() - 1);
+      }
+      int64_t left = items[i].units;
+      while (left > 0) {
+        const bool last_cta = (int64_t)cta_start.size() == X;
+        if (!last_cta && cost > 0.0 && target - cost < 0.5) {
+          rest -= cost;
+          cta_start.push_back((int32_t)u);
+          cost = 0.0;
+          target = target_for((int64_t)cta_start.size() - 1);
+          continue;
+        }
+        const int64_t take = last_cta ? left : std::min<int64_t>(left, std::max<int64_t>(1, std::llround(target - cost)));
+        u += take;
+        left -= take;
+        cost += (double)take;
+      }
+    }
+    cta_start.push_back((int32_t)tc_units);
+  }
+  const int64_t tc_ctas = cta_start.empty() ? 0 : (int64_t)cta_start.size() - 1;
+  auto cta_of = [&](int64_t u) {
+    return (int64_t)(std::upper_bound(cta_start.begin(), cta_start.end() - 1, (int32_t)u) - cta_start.begin()) - 1;
+  };
+  std::vector<int32_t> it_first_cta(items.size(), 0);
+  for (size_t i = num_mma; i < items.size(); ++i) it_first_cta[i] = (int32_t)cta_of(it_unit_off[i]);
   auto item_pieces = [&](size_t i) -> int {
     if ((int)i < num_mma) return 1;
     const int64_t a0 = it_unit_off[i], b0 = a0 + items[i].units;
-    return items[i].units == 0 ? 1 : (int)((b0 - 1) / tc_per - a0 / tc_per + 1);
+    return items[i].units == 0 ? 1 : (int)(cta_of(b0 - 1) - cta_of(a0) + 1);
   };
   // per (shared ctx, qblock, head): pieces contributed to each of its rows
   std::unordered_map<int64_t, int> pieces_of;  // key (sh * 4096 + qb) * H + h
@@ -789,11 +837,13 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_rhc = L.add(sizeof(int32_t) * rh_chunk0.size());
   std::vector<int32_t> tc_start(std::max<int64_t>(tc_ctas, 1), 0);
   for (int64_t b = 0, i = num_mma; b < tc_ctas; ++b) {
-    const int64_t u = b * tc_per;
+    const int64_t u = cta_start[b];
     while (i + 1 < (int64_t)items.size() && it_unit_off[i + 1] <= u) ++i;
     tc_start[b] = (int32_t)i;
   }
   const size_t o_tcs = L.add(sizeof(int32_t) * tc_start.size());
+  const size_t o_tccs = L.add(sizeof(int32_t) * std::max<size_t>(cta_start.size(), 1));
+  const size_t o_ifc = L.add(sizeof(int32_t) * ni);
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
     FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
@@ -846,6 +896,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   put(o_cs, chunk_start.data(), chunk_start.size() * 4);
   put(o_rhc, rh_chunk0.data(), rh_chunk0.size() * 4);
   put(o_tcs, tc_start.data(), tc_start.size() * 4);
+  put(o_tccs, cta_start.data(), cta_start.size() * 4);
+  put(o_ifc, it_first_cta.data(), it_first_cta.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -867,7 +919,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.qrows = (const int32_t*)(d + o_q);
   pd.qslot = (const int32_t*)(d + o_qs);
   pd.tc_units = (int)tc_units;
-  pd.tc_per = (int)tc_per;
+  pd.tc_cta_start = (const int32_t*)(d + o_tccs);
+  pd.it_first_cta = (const int32_t*)(d + o_ifc);
   pd.tc_ctas = (int)tc_ctas;
   pd.tc_start_item = (const int32_t*)(d + o_tcs);
   const int32_t* drb = (const int32_t*)(d + o_rows);

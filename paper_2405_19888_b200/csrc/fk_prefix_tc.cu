@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
-  const int u0 = blockIdx.x * p.tc_per;
-  const int u1 = min(p.tc_units, u0 + p.tc_per);
+  const int u0 = p.tc_cta_start[blockIdx.x];
+  const int u1 = p.tc_cta_start[blockIdx.x + 1];
   pdl_launch_dependents();  // the private grid may start on the SMs we leave free
   // Launched behind the private grid (launch order 1), this grid's completion
   // must imply that grid's: thread 0 waits for it on exit.
@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     // q and the partials are touched only after it has completed
     if (!after_private) pdl_wait_primary();
     if (T > 0) stage_q(c0.item, 0);
+    if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 2, T);
     for (int t = 0; t < T; ++t) {
       const int item = c.item;
       if (t == 0 || c.tile == 0) {
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         // epilogue), then O (unnormalised, running max m) -> partial slot
         if (t + 1 < T) stage_q(item + 1, piece_k + 1);
         ++piece_k;
+        if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 3, piece_k);
         mbar_wait(&o_done, t & 1);
         if (warp == 4 && lane == 0 && t < 16) TL(96 + t);
         tc_fence_after();
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             const int my_row = R16 ? row16 : row;
             const int my_q = R16 ? qj16 : qj;
             const int col0 = half * 64 + (R16 ? sub * 32 : 0);
-            const int piece = blockIdx.x - p.it_unit_off[item] / p.tc_per;
+            const int piece = blockIdx.x - p.it_first_cta[item];
             const bool real = my_q < nq;
             long long pi = 0;
             if (real) {
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 extern "C" int fk_debug_cta_timeline_prefix(unsigned long long* out, int n) {
 #ifdef FK_TIMELINE
   if (cudaDeviceSynchronize() != cudaSuccess) return 6;
-  return cudaMemcpyFromSymbol(out, fk_tl_cta_prefix, sizeof(unsigned long long) * 4 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
+  return cudaMemcpyFromSymbol(out, fk_tl_cta_prefix, sizeof(unsigned long long) * 8 * (n < 1024 ? n : 1024)) == cudaSuccess ? 0 : 6;
 #else
   (void)out;
   (void)n;

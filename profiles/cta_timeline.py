@@ -38,9 +38,11 @@ def main():
     for name in ("prefix", "priv", "merge"):
         fn = getattr(_lib.lib, "fk_debug_cta_timeline_" + name)
         fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-        buf = (ctypes.c_ulonglong * 4096)()
+        buf = (ctypes.c_ulonglong * 8192)()
         assert fn(buf, 1024) == 0
-        out[name] = [[(buf[par * 2048 + 2 * i], buf[par * 2048 + 2 * i + 1]) for i in range(1024)] for par in (0, 1)]
+        out[name] = [[(buf[par * 4096 + 4 * i], buf[par * 4096 + 4 * i + 1]) for i in range(1024)] for par in (0, 1)]
+        if name == "prefix":
+            notes = [[(buf[par * 4096 + 4 * i + 2], buf[par * 4096 + 4 * i + 3]) for i in range(1024)] for par in (0, 1)]
     L = cfg["L"]
     pars = [(L - 2) & 1, (L - 1) & 1]  # second-to-last layer, last layer
     t0 = None
@@ -58,6 +60,10 @@ def main():
             print(f"layer%2 {par} {name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} "
                   f"{st[-1]:7.2f}   end min/med/max {en[0]:7.2f} {statistics.median(en):7.2f} {en[-1]:7.2f}")
     print("(merge* start = after its griddepcontrol.wait)")
+    par = pars[-1]
+    print("last layer prefix CTAs (tiles, pieces, duration us):")
+    print(" ".join("%d/%d/%.0f" % (notes[par][i][0], notes[par][i][1], (out["prefix"][par][i][1] - out["prefix"][par][i][0]) / 1e3)
+                   for i in range(info.num_prefix_ctas)))
     print("plan:", info.num_rows, "rows", info.num_prefix_ctas, "prefix CTAs", info.max_slots, "slots")
 
 
