@@ -626,7 +626,9 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // all of them finish together.  cta_start[b] = first unit of CTA b.
   std::vector<int32_t> cta_start;
   if (tc_units > 0) {
-    const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, tc_units));
+    // at least ~4 tiles per CTA: a CTA's start-up (TMEM, barriers, first
+    // loads) costs about that much
+    const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, (tc_units + 3) / 4));
     const double bc = (double)p->tc_boundary_cost;
     // the target is re-derived for every CTA from the work that is left, so
     // rounding never piles up on the last one
@@ -661,6 +663,11 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     cta_start.push_back((int32_t)tc_units);
   }
   const int64_t tc_ctas = cta_start.empty() ? 0 : (int64_t)cta_start.size() - 1;
+  if (getenv("FK_DEBUG_PLAN")) {
+    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs:", (long long)tc_units, (long long)tc_ctas);
+    for (int32_t v : cta_start) fprintf(stderr, " %d", v);
+    fprintf(stderr, "\n");
+  }
   auto cta_of = [&](int64_t u) {
     return (int64_t)(std::upper_bound(cta_start.begin(), cta_start.end() - 1, (int32_t)u) - cta_start.begin()) - 1;
   };

@@ -415,29 +415,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
           asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
           if (warp == 4 && lane == 0 && t < 16) TL(192 + t);
           const float tile_max = fmaxf(mx, s_max[sb][half ^ 1][my_row]) * scale_log2;
-          // lazy rescale: keep the running max unless the tile exceeds it by > 8
+          // lazy rescale: a row keeps its running max unless the tile exceeds
+          // it by > 8.  tcgen05.ld/st are warp-collective (.sync.aligned), so
+          // the O rescale runs for the whole warp when any of its rows needs
+          // it (alpha = 1 for the others).
           const bool rescale = tile_max > m + kRescaleThreshold;
-          if (t > 0 && ((rescale && t > seg_start) || piece_end)) mbar_wait(&o_done, (t - 1) & 1);
-          if (rescale) {
-            if (t > seg_start) {
-              const float alpha = ex2(m - tile_max);
-              l *= alpha;
-              tc_fence_after();
-              const uint32_t o_tm = lane_tm + 256 + half * 64;
+          const bool warp_rescale = __any_sync(0xffffffffu, rescale) && t > seg_start;
+          if (t > 0 && (warp_rescale || piece_end)) mbar_wait(&o_done, (t - 1) & 1);
+          if (warp_rescale) {
+            const float alpha = rescale ? ex2(m - tile_max) : 1.f;
+            l *= alpha;
+            tc_fence_after();
+            const uint32_t o_tm = lane_tm + 256 + half * 64;
 #pragma unroll
-              for (int cc = 0; cc < NCH; ++cc) {
-                uint32_t o[32];
-                if (R16) tmem_ld16x2(o_tm, o);
-                else tmem_ld32(o_tm + cc * 32, o);
-                tmem_wait_ld();
+            for (int cc = 0; cc < NCH; ++cc) {
+              uint32_t o[32];
+              if (R16) tmem_ld16x2(o_tm, o);
+              else tmem_ld32(o_tm + cc * 32, o);
+              tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                if (R16) tmem_st16x2(o_tm, o);
-                else tmem_st32(o_tm + cc * 32, o);
-              }
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              if (R16) tmem_st16x2(o_tm, o);
+              else tmem_st32(o_tm + cc * 32, o);
             }
-            m = tile_max;
           }
+          if (rescale) m = tile_max;
           float sum4[4] = {0.f, 0.f, 0.f, 0.f};
           const bool full = valid >= 32 * NCH;
 #pragma unroll
