@@ -626,9 +626,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // all of them finish together.  cta_start[b] = first unit of CTA b.
   std::vector<int32_t> cta_start;
   if (tc_units > 0) {
-    // at least ~4 tiles per CTA: a CTA's start-up (TMEM, barriers, first
-    // loads) costs about that much
-    const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, (tc_units + 3) / 4));
+    // at least ~4 tiles per CTA unless FK_OPT_PREFIX_TARGET_CTAS says
+    // otherwise: a CTA's start-up (TMEM, barriers, first loads) costs about that
+    const int64_t cap = p->prefix_target_ctas > 0 ? tc_units : (tc_units + 3) / 4;
+    const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, cap));
     const double bc = (double)p->tc_boundary_cost;
     // the target is re-derived for every CTA from the work that is left, so
     // rounding never piles up on the last one
