@@ -106,3 +106,63 @@ def test_status_maps_to_reference_exception_classes():
         _lib.check(_lib.FK_CONTEXT_BUSY)
     with pytest.raises(errors.KernelError):
         _lib.check(_lib.FK_CUDA_ERROR)
+
+
+def test_step_grow_sequential_oom_rule():
+    """fk_step_grow: rows grow one token in row order; a row whose page does
+    not fit fails alone (engine.py:431-438), later rows that need no new page
+    still grow, ids come from the monotonic counter."""
+    h = _pool(total=4)
+    L = _lib.lib
+    for ctx, parent in ((1, -1), (2, 1), (3, 1), (4, 1)):
+        assert L.fk_ctx_create(h, ctx, parent) == _lib.FK_OK
+    ids = (ctypes.c_int64 * 8)()
+    n = ctypes.c_int64()
+    assert L.fk_ctx_grow(h, 1, 16, ids, 8, ctypes.byref(n)) == _lib.FK_OK  # block 0
+    assert L.fk_ctx_grow(h, 2, 16, ids, 8, ctypes.byref(n)) == _lib.FK_OK  # block 1 (full page)
+    assert L.fk_ctx_grow(h, 3, 5, ids, 8, ctypes.byref(n)) == _lib.FK_OK   # block 2 (room left)
+    assert L.fk_ctx_grow(h, 4, 16, ids, 8, ctypes.byref(n)) == _lib.FK_OK  # block 3: pool full
+    leaves = (ctypes.c_int64 * 3)(2, 3, 4)
+    info = _lib.PlanInfo()
+    assert L.fk_step_plan(h, leaves, 3, 1, None, ctypes.byref(info)) == _lib.FK_OK
+    assert info.batch_tokens == 16 + 16 + 5 + 16
+    pos = (ctypes.c_int64 * 3)()
+    new = (ctypes.c_int64 * 3)()
+    assert L.fk_step_grow(h, pos, new) == _lib.FK_OK
+    # row 0 (ctx 2) needs a new page -> OOM; row 1 (ctx 3) fits its page; row 2 needs one -> OOM
+    assert list(pos) == [-1, 5, -1]
+    assert list(new) == [-1, -1, -1]
+    tok = ctypes.c_int64()
+    nb = ctypes.c_int64()
+    par = ctypes.c_int64()
+    L.fk_ctx_info(h, 3, ctypes.byref(tok), ctypes.byref(nb), ctypes.byref(par))
+    assert (tok.value, nb.value, par.value) == (6, 1, 1)
+    L.fk_pool_destroy(h)
+
+
+def test_device_entry_points_refuse_host_only_pools():
+    h = _pool(total=10)
+    L = _lib.lib
+    assert L.fk_ctx_create(h, 1, -1) == _lib.FK_OK
+    ids = (ctypes.c_int64 * 4)()
+    n = ctypes.c_int64()
+    assert L.fk_ctx_grow(h, 1, 20, ids, 4, ctypes.byref(n)) == _lib.FK_OK
+    assert L.fk_fill_kv(h, 1, 0, 20, 0, 1, None, None, None) == _lib.FK_NO_DEVICE
+    assert L.fk_ctx_copy_kv(h, 1, h, 1, 20, None) == _lib.FK_NO_DEVICE
+    assert L.fk_synth_fill(h, 1, 0, 20, 1, 1.0, None) == _lib.FK_NO_DEVICE
+    leaves = (ctypes.c_int64 * 1)(1)
+    info = _lib.PlanInfo()
+    assert L.fk_step_plan(h, leaves, 1, 1, None, ctypes.byref(info)) == _lib.FK_OK
+    assert L.fk_attn_decode_layers(h, 0, 1, None, 0, None, 0, None, 0, None) == _lib.FK_NO_DEVICE
+    L.fk_pool_destroy(h)
+
+
+def test_options_validate():
+    h = _pool()
+    L = _lib.lib
+    for opt, val in ((_lib.FK_OPT_TC_MIN_FANOUT, 0), (_lib.FK_OPT_CORUN, 0), (_lib.FK_OPT_PREFIX_RATE_PCT, 60),
+                     (_lib.FK_OPT_PDL, 2), (_lib.FK_OPT_PRIV_MIN_CHUNK, 4), (_lib.FK_OPT_PRIV_STATIC_FIRST, 0),
+                     (_lib.FK_OPT_TC_BOUNDARY_COST, 3), (_lib.FK_OPT_LAUNCH_ORDER, 1)):
+        assert L.fk_pool_set_option(h, opt, val) == _lib.FK_OK
+    assert L.fk_pool_set_option(h, 999, 1) == _lib.FK_INVALID_ARGUMENT
+    L.fk_pool_destroy(h)
