@@ -22,6 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--set", action="append", required=True)
+    ap.add_argument("--base", default="", help="K=V,... applied before every set (options persist otherwise)")
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--shape", default=None, help="P,B,S[,L,H]: fork group shape instead of --config")
@@ -37,8 +38,9 @@ def main():
     for _ in range(3):
         eng.step()
     for r in range(args.rounds):
+        base = [kv.split("=") for kv in args.base.split(",") if kv]
         for name, opts in zip(args.set, sets):
-            for k, v in opts:
+            for k, v in base + opts:
                 eng.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
             eng.step()
             eng.step()
