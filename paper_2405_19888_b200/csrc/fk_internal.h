@@ -14,7 +14,7 @@ constexpr int kMmaQBlock = 64; // queries per mma.sync prefix CTA (4 warps x 16 
 constexpr int kTcQBlock = 128; // queries per tcgen05 prefix CTA (M = 128 rows)
 constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
 constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
-constexpr int kPrivWarpsPerCta = 8;  // private stream-K kernel: independent warps per CTA
+constexpr int kPrivWarpsPerCta = 8;  // private kernel: independent warps per CTA
 constexpr int kPrivStages = 3;       // per-warp smem ring depth (8 KiB K+V page per stage)
 constexpr int kPrivMinChunk = 2;     // private guided schedule: smallest chunk (pages), default
 constexpr int kPrivMaxChunk = 32;    // largest chunk (one lane-parallel metadata load)

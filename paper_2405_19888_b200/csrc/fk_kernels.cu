@@ -1,17 +1,20 @@
 // sm_100a decode-attention kernels for shared-prefix ("fork") batches.
 //
-//  K3+K4  fk_private_kernel   per (row, head): streams the row's private pages
-//                             (fan-out 1 contexts, engine.py:484 per-request
-//                             chain cost) with 1-D bulk copies into a 4-stage
-//                             smem ring, CUDA-core online softmax, then arrives
-//                             on the (row, head) counter and, if last, merges
-//                             every partial ("amalgamating").
-//  K2     fk_prefix_mma_kernel per (shared context split, 64-query block,
-//                             head): TMA (SWIZZLE_128B) page tiles, Q.K^T and
-//                             P.V on mma.sync m16n8k16 — the warp-level path
-//                             for small fan-out (engine.py:473-483 dedup).
-//  K1     fk_append_kernel     new K/V row -> (page, slot).
-//         fk_synth_*           deterministic synthetic KV / Q (oracle restates).
+//  K3  fk_private_kernel    fan-out-1 contexts (the per-request suffix,
+//                           engine.py:484 per-request chain cost): warps take
+//                           guided chunks of (head, page) units from a ticket
+//                           counter, TMA page boxes into per-warp 3-stage smem
+//                           rings, q.K^T and P.V on mma.sync, one partial per
+//                           (row, head, chunk) piece.
+//  K2  fk_prefix_mma_kernel shared contexts on the warp-level path (opt-in,
+//                           FK_OPT_TC_MIN_FANOUT): per (context split, 64-query
+//                           block, head), TMA (SWIZZLE_128B) page tiles, mma.sync.
+//                           The default K2 is fk_prefix_tc_kernel (tcgen05).
+//  K4  fk_merge_kernel      LSE merge of every (row, head)'s partials
+//                           ("amalgamating ... interim results").
+//  K1  fk_append_kernel     new K/V rows -> (page, slot); fk_fill_kv_kernel and
+//                           fk_copy_pages_kernel fill / migrate context KV.
+//      fk_synth_*           deterministic synthetic KV / Q (oracle restates).
 #include "fk_common.cuh"
 
 namespace fk {

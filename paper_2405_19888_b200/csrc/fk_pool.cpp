@@ -92,7 +92,7 @@ struct fk_pool {
   int64_t launch_order = 0;
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
   int64_t priv_static_first = 1;
-  int64_t tc_boundary_cost = 4;  // tiles a mid-range piece start costs a tcgen05 CTA (stream-K balance)  // warps that start at once begin on a fixed chunk (no ticket)
+  int64_t tc_boundary_cost = 4;  // tiles a mid-range piece start costs a tcgen05 CTA (stream-K balance)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
@@ -252,8 +252,8 @@ extern "C" {
 const char* fk_last_error(void) { return g_last_error.c_str(); }
 
 const char* fk_build_info(void) {
-  return "forkattn sm_100a (" __DATE__ " " __TIME__ "): private paged decode + mma.sync/tcgen05 "
-         "shared-prefix attention + last-arriver LSE merge";
+  return "forkattn sm_100a (" __DATE__ " " __TIME__ "): tcgen05/TMEM/TMA shared-prefix attention "
+         "co-run with a dynamic paged private stream, PDL-chained LSE merge";
 }
 
 int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
@@ -594,7 +594,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
           }
       }
     }
-  // tcgen05 stream-K: tile units of all tc items spread evenly over <= one wave
+  // tcgen05 stream-K: tile units of all tc items over <= one wave of CTAs
   std::vector<int32_t> it_unit_off(items.size(), 0);
   int64_t tc_units = 0;
   for (size_t i = num_mma; i < items.size(); ++i) {
@@ -736,7 +736,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     }
     row_priv_np[r] = (int32_t)pages.size() - row_priv_off[r];
   }
-  // warp stream-K over units (head, flat private entry)
+  // private units (head, flat private entry), head-major
   const int64_t priv_base = B > 0 ? row_priv_off[0] : (int64_t)pages.size();
   const int64_t NPT = (int64_t)pages.size() - priv_base;
   std::vector<int32_t> row_unit_off(std::max(B, 1), 0), page_row(std::max<int64_t>(NPT, 1), 0);

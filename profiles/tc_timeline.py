@@ -13,7 +13,7 @@ from paper_2405_19888_b200.workloads import fork_group  # noqa: E402
 
 eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 22, device=0, geometry=P.ModelGeometry(2, 40, 128))
 eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, 2)
-fork_group(eng, 6000, [256] * 64, out_len=8)
+fork_group(eng, 6000, [256] * int(os.environ.get("FK_TL_FORKS", "64")), out_len=8)
 for _ in range(3):
     eng.step()
 torch.cuda.synchronize()
