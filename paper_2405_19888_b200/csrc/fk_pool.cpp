@@ -87,11 +87,11 @@ struct fk_pool {
   int num_sms = 148;
 
   // options
-  int64_t tc_min_fanout = 2;  // tcgen05 for every shared context until the sweep says otherwise
+  int64_t tc_min_fanout = 2;  // tcgen05 for every shared context (measured faster than mma.sync at fan-out 2..32)
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
-  int64_t priv_static_first = 1;
+  int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
   int64_t tc_boundary_cost = 4;  // tiles a mid-range piece start costs a tcgen05 CTA (stream-K balance)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
