@@ -34,7 +34,7 @@ FK_OPT_PREFIX_RATE_PCT = 6
 FK_OPT_PDL = 7
 FK_OPT_PRIV_MIN_CHUNK = 8
 FK_OPT_PRIV_STATIC_FIRST = 9
-FK_OPT_TC_BOUNDARY_COST = 10
+FK_OPT_TC_MIN_CHUNK = 10
 
 
 class PoolDesc(ctypes.Structure):

@@ -14,6 +14,7 @@ constexpr int kMmaQBlock = 64; // queries per mma.sync prefix CTA (4 warps x 16 
 constexpr int kTcQBlock = 128; // queries per tcgen05 prefix CTA (M = 128 rows)
 constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
 constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
+constexpr int kTcMaxChunk = 24;   // largest tcgen05 chunk (tiles)
 constexpr int kPrivWarpsPerCta = 8;  // private kernel: independent warps per CTA
 constexpr int kPrivStages = 3;       // per-warp smem ring depth (8 KiB K+V page per stage)
 constexpr int kPrivMinChunk = 2;     // private guided schedule: smallest chunk (pages), default
@@ -39,10 +40,15 @@ struct PlanDev {
   const int* it_units;     // 128-token tiles of the item
   const int* qrows;        // request rows
   const int* qslot;        // slot of piece 0 for each (item, query)
-  int tc_units, tc_ctas;          // tcgen05 stream-K geometry
-  const int* tc_start_item;       // [tc_ctas] item holding each CTA's first unit
-  const int* tc_cta_start;        // [tc_ctas + 1] first unit of each CTA (cost-balanced)
-  const int* it_first_cta;        // per item: CTA holding its first unit (piece 0)
+  // tcgen05 dynamic schedule: chunks of consecutive tiles of one item, in
+  // unit order with guided (shrinking) sizes; CTA b starts on chunk b, then
+  // takes chunk = tc_ctas + ticket (ArenaDev::ticket_tc - tc_ticket_base).
+  int tc_units, tc_ctas, tc_nchunks;
+  unsigned long long tc_ticket_base;
+  const int* tc_chunk_item;       // [tc_nchunks]
+  const int* tc_chunk_tile0;      // [tc_nchunks] first tile within the item
+  const int* tc_chunk_tile1;      // [tc_nchunks] end tile (exclusive)
+  const int* it_first_chunk;      // per item: its first chunk (piece 0)
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;
@@ -81,7 +87,8 @@ struct ArenaDev {
   int num_heads;
   float* part_o;          // [rows][max_slots][H][D]
   float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
-  unsigned long long* ticket;  // private chunk ticket counter (never reset)
+  unsigned long long* ticket;     // private chunk ticket counter (never reset)
+  unsigned long long* ticket_tc;  // tcgen05 prefix chunk ticket counter (never reset)
 };
 
 inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {

@@ -92,7 +92,7 @@ struct fk_pool {
   int64_t launch_order = 0;
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
-  int64_t tc_boundary_cost = 4;  // tiles a mid-range piece start costs a tcgen05 CTA (stream-K balance)
+  int64_t tc_min_chunk = 24;  // smallest tcgen05 chunk (tiles); measured: every chunk end costs ~3 us of epilogue, so coarse wins
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
@@ -115,6 +115,7 @@ struct fk_pool {
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
   unsigned long long* ticket = nullptr;  // device: private chunk tickets (never reset)
   unsigned long long ticket_base = 0;    // tickets consumed by earlier private launches
+  unsigned long long ticket_tc_base = 0; // ... and by earlier tcgen05 prefix launches
 
   ArenaDev arena() const {
     ArenaDev a;
@@ -125,6 +126,7 @@ struct fk_pool {
     a.part_o = part_o;
     a.part_ml = part_ml;
     a.ticket = ticket;
+    a.ticket_tc = ticket ? ticket + 1 : nullptr;
       return a;
   }
 };
@@ -284,8 +286,8 @@ int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
         return fail(FK_CUDA_ERROR, "cudaEventCreate failed");
       }
     }
-    if (cudaMalloc(&p->ticket, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMemset(p->ticket, 0, sizeof(unsigned long long)) != cudaSuccess) {
+    if (cudaMalloc(&p->ticket, 2 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(p->ticket, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
       cudaGetLastError();
       fk_pool_destroy(p);
       return fail(FK_CUDA_ERROR, "ticket counter allocation failed");
@@ -351,7 +353,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
     case FK_OPT_PDL: p->pdl = value; break;
     case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
-    case FK_OPT_TC_BOUNDARY_COST: p->tc_boundary_cost = std::max<int64_t>(0, value); break;
+    case FK_OPT_TC_MIN_CHUNK: p->tc_min_chunk = std::min<int64_t>(kTcMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
@@ -620,64 +622,47 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     const double wv = (double)priv_tok_heads;
     tc_target = std::min<int64_t>(p->num_sms - 1, std::max<int64_t>(1, std::llround(p->num_sms * wp / (wp + wv))));
   }
-  // Cost-balanced stream-K: every tile costs 1 and every extra piece a CTA
-  // starts mid-range (epilogue + pipeline restart, ~2 tiles measured) costs
-  // tc_boundary_cost, so CTAs that cross item boundaries get fewer tiles and
-  // all of them finish together.  cta_start[b] = first unit of CTA b.
-  std::vector<int32_t> cta_start;
+  // Dynamic tcgen05 schedule: the tile units are cut into chunks that never
+  // cross an item, guided sizes (about remaining / (2 X) tiles, shrinking to
+  // tc_min_chunk), so the X persistent CTAs -- CTA b starts on chunk b, then
+  // takes tickets -- finish together whatever their per-SM bandwidth.  Each
+  // chunk is one piece (one partial slot per query row).
+  std::vector<int32_t> ch_item, ch_t0, ch_t1;
+  std::vector<int32_t> it_first_chunk(items.size(), 0);
+  int64_t tc_ctas = 0;
   if (tc_units > 0) {
     // at least ~4 tiles per CTA unless FK_OPT_PREFIX_TARGET_CTAS says
     // otherwise: a CTA's start-up (TMEM, barriers, first loads) costs about that
     const int64_t cap = p->prefix_target_ctas > 0 ? tc_units : (tc_units + 3) / 4;
     const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, cap));
-    const double bc = (double)p->tc_boundary_cost;
-    // the target is re-derived for every CTA from the work that is left, so
-    // rounding never piles up on the last one
-    double rest = (double)tc_units + bc * (double)(num_tc - 1);
-    auto target_for = [&](int64_t b) { return rest / (double)std::max<int64_t>(1, X - b); };
-    double cost = 0.0, target = target_for(0);
-    int64_t u = 0;
-    cta_start.push_back(0);
+    int64_t rest = tc_units;
     for (size_t i = num_mma; i < items.size(); ++i) {
-      if (cost > 0.0) {
-        cost += bc;
-      } else if (i > (size_t)num_mma) {
-        rest -= bc;  // this CTA starts at the item boundary: no extra piece
-        target = target_for((int64_t)cta_start.size() - 1);
-      }
-      int64_t left = items[i].units;
-      while (left > 0) {
-        const bool last_cta = (int64_t)cta_start.size() == X;
-        if (!last_cta && cost > 0.0 && target - cost < 0.5) {
-          rest -= cost;
-          cta_start.push_back((int32_t)u);
-          cost = 0.0;
-          target = target_for((int64_t)cta_start.size() - 1);
-          continue;
-        }
-        const int64_t take = last_cta ? left : std::min<int64_t>(left, std::max<int64_t>(1, std::llround(target - cost)));
-        u += take;
-        left -= take;
-        cost += (double)take;
+      it_first_chunk[i] = (int32_t)ch_item.size();
+      int tile = 0;
+      while (tile < items[i].units) {
+        int64_t sz = (rest + 2 * X - 1) / (2 * X);
+        sz = std::min<int64_t>(std::max<int64_t>(sz, p->tc_min_chunk), kTcMaxChunk);
+        sz = std::min<int64_t>(sz, items[i].units - tile);
+        ch_item.push_back((int32_t)i);
+        ch_t0.push_back(tile);
+        ch_t1.push_back((int32_t)(tile + sz));
+        tile += (int)sz;
+        rest -= sz;
       }
     }
-    cta_start.push_back((int32_t)tc_units);
+    tc_ctas = std::min<int64_t>(X, (int64_t)ch_item.size());
   }
-  const int64_t tc_ctas = cta_start.empty() ? 0 : (int64_t)cta_start.size() - 1;
+  const int64_t tc_nchunks = (int64_t)ch_item.size();
   if (getenv("FK_DEBUG_PLAN")) {
-    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs:", (long long)tc_units, (long long)tc_ctas);
-    for (int32_t v : cta_start) fprintf(stderr, " %d", v);
+    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs, %lld chunks:", (long long)tc_units, (long long)tc_ctas,
+            (long long)tc_nchunks);
+    for (size_t k = 0; k < ch_item.size(); ++k) fprintf(stderr, " %d:%d-%d", ch_item[k], ch_t0[k], ch_t1[k]);
     fprintf(stderr, "\n");
   }
-  auto cta_of = [&](int64_t u) {
-    return (int64_t)(std::upper_bound(cta_start.begin(), cta_start.end() - 1, (int32_t)u) - cta_start.begin()) - 1;
-  };
-  std::vector<int32_t> it_first_cta(items.size(), 0);
-  for (size_t i = num_mma; i < items.size(); ++i) it_first_cta[i] = (int32_t)cta_of(it_unit_off[i]);
   auto item_pieces = [&](size_t i) -> int {
     if ((int)i < num_mma) return 1;
-    const int64_t a0 = it_unit_off[i], b0 = a0 + items[i].units;
-    return items[i].units == 0 ? 1 : (int)(cta_of(b0 - 1) - cta_of(a0) + 1);
+    const int64_t next = (i + 1 < items.size()) ? it_first_chunk[i + 1] : tc_nchunks;
+    return items[i].units == 0 ? 1 : (int)(next - it_first_chunk[i]);
   };
   // per (shared ctx, qblock, head): pieces contributed to each of its rows
   std::unordered_map<int64_t, int> pieces_of;  // key (sh * 4096 + qb) * H + h
@@ -843,14 +828,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_prow = L.add(sizeof(int32_t) * page_row.size());
   const size_t o_cs = L.add(sizeof(int32_t) * chunk_start.size());
   const size_t o_rhc = L.add(sizeof(int32_t) * rh_chunk0.size());
-  std::vector<int32_t> tc_start(std::max<int64_t>(tc_ctas, 1), 0);
-  for (int64_t b = 0, i = num_mma; b < tc_ctas; ++b) {
-    const int64_t u = cta_start[b];
-    while (i + 1 < (int64_t)items.size() && it_unit_off[i + 1] <= u) ++i;
-    tc_start[b] = (int32_t)i;
-  }
-  const size_t o_tcs = L.add(sizeof(int32_t) * tc_start.size());
-  const size_t o_tccs = L.add(sizeof(int32_t) * std::max<size_t>(cta_start.size(), 1));
+  const size_t nchb = sizeof(int32_t) * std::max<size_t>(ch_item.size(), 1);
+  const size_t o_chi = L.add(nchb);
+  const size_t o_ch0 = L.add(nchb);
+  const size_t o_ch1 = L.add(nchb);
   const size_t o_ifc = L.add(sizeof(int32_t) * ni);
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
@@ -903,9 +884,10 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   put(o_prow, page_row.data(), page_row.size() * 4);
   put(o_cs, chunk_start.data(), chunk_start.size() * 4);
   put(o_rhc, rh_chunk0.data(), rh_chunk0.size() * 4);
-  put(o_tcs, tc_start.data(), tc_start.size() * 4);
-  put(o_tccs, cta_start.data(), cta_start.size() * 4);
-  put(o_ifc, it_first_cta.data(), it_first_cta.size() * 4);
+  put(o_chi, ch_item.data(), ch_item.size() * 4);
+  put(o_ch0, ch_t0.data(), ch_t0.size() * 4);
+  put(o_ch1, ch_t1.data(), ch_t1.size() * 4);
+  put(o_ifc, it_first_chunk.data(), it_first_chunk.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -927,10 +909,13 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.qrows = (const int32_t*)(d + o_q);
   pd.qslot = (const int32_t*)(d + o_qs);
   pd.tc_units = (int)tc_units;
-  pd.tc_cta_start = (const int32_t*)(d + o_tccs);
-  pd.it_first_cta = (const int32_t*)(d + o_ifc);
   pd.tc_ctas = (int)tc_ctas;
-  pd.tc_start_item = (const int32_t*)(d + o_tcs);
+  pd.tc_nchunks = (int)tc_nchunks;
+  pd.tc_ticket_base = 0;  // set per launch
+  pd.tc_chunk_item = (const int32_t*)(d + o_chi);
+  pd.tc_chunk_tile0 = (const int32_t*)(d + o_ch0);
+  pd.tc_chunk_tile1 = (const int32_t*)(d + o_ch1);
+  pd.it_first_chunk = (const int32_t*)(d + o_ifc);
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
@@ -986,6 +971,11 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
   // K2 (shared prefixes) and K3 (private streams) only write partials, so
   // their order is free; K4 merges every (row, head) afterwards.
+  // a tcgen05 launch consumes exactly tc_nchunks tickets (fk_prefix_tc_kernel)
+  if (has_tc) {
+    p->plan.tc_ticket_base = p->ticket_tc_base;
+    p->ticket_tc_base += (unsigned long long)p->plan.tc_nchunks;
+  }
   auto run_prefix = [&](bool pdl_tc, bool after_private) -> int {
     if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
     if (has_tc)

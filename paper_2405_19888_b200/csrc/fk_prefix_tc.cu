@@ -34,9 +34,12 @@ constexpr int kTcKStages = 3;                      // K ring (released right aft
 constexpr int kTcVStages = 4;                      // V ring (held through softmax and P.V)
 constexpr int kTcHalf = 128 * 128;                 // 128 rows x 128 B
 constexpr int kTcTileBytes = 2 * kTcHalf;          // one K or V tile (32 KiB)
+constexpr int kTcChunkQ = 16;                      // chunk queue entries (producer lead <= ~6 chunks)
 struct TcMisc {
   uint64_t k_full[kTcKStages], k_empty[kTcKStages], v_full[kTcVStages], v_empty[kTcVStages];
   uint64_t s_full[2], p_full[2], o_done, q_full;
+  uint64_t cq_full[kTcChunkQ];  // chunk queue: the producer posts each chunk id it streams
+  int cq[kTcChunkQ];
   uint32_t tmem_base;
   float s_max[2][2][128];  // [tile parity][half][row]
   float s_l[128];
@@ -60,23 +63,26 @@ __device__ unsigned long long fk_tl[256];
 
 CTA_TL_DECL(fk_tl_cta_prefix);
 
-// unit cursor over the tcgen05 items of the plan
+// Tile cursor over a CTA's dynamic chunk sequence.  Chunk c covers tiles
+// [tc_chunk_tile0[c], tc_chunk_tile1[c]) of item tc_chunk_item[c]; the i-th
+// chunk a CTA streams is posted by its producer in queue entry i.
 struct TcCursor {
-  int item, tile;
+  int qi;     // queue index of the current chunk
+  int chunk;  // chunk id, or -1 once the counter ran dry
+  int item, tile, tile1;
 };
-__device__ __forceinline__ TcCursor tc_locate(const PlanDev& p, int u) {
-  int lo = p.tc_begin, hi = p.num_items - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (p.it_unit_off[mid] <= u) lo = mid; else hi = mid - 1;
+__device__ __forceinline__ void tc_load_chunk(const PlanDev& p, TcCursor& c, int chunk) {
+  c.chunk = chunk;
+  if (chunk >= 0) {
+    c.item = p.tc_chunk_item[chunk];
+    c.tile = p.tc_chunk_tile0[chunk];
+    c.tile1 = p.tc_chunk_tile1[chunk];
   }
-  return TcCursor{lo, u - p.it_unit_off[lo]};
 }
-__device__ __forceinline__ void tc_advance(const PlanDev& p, TcCursor& c) {
-  if (++c.tile == p.it_units[c.item]) {
-    ++c.item;
-    c.tile = 0;
-  }
+// consumers: read queue entry i (posted by this CTA's producer)
+__device__ __forceinline__ int tc_read_queue(uint64_t* cq_full, const int* cq, int i) {
+  mbar_wait(&cq_full[i % kTcChunkQ], (i / kTcChunkQ) & 1);
+  return ((volatile const int*)cq)[i % kTcChunkQ];
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a, PlanDev p, int layer,
@@ -106,16 +112,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
-  const int u0 = p.tc_cta_start[blockIdx.x];
-  const int u1 = p.tc_cta_start[blockIdx.x + 1];
+  const int nch = p.tc_nchunks;
   pdl_launch_dependents();  // the private grid may start on the SMs we leave free
   // Launched behind the private grid (launch order 1), this grid's completion
   // must imply that grid's: thread 0 waits for it on exit.
-  if (u0 >= u1) {
+  if ((int)blockIdx.x >= nch) {
     if (after_private && threadIdx.x == 0) pdl_wait_primary();
     return;
   }
-  const int T = u1 - u0;
   TL(160);
   CTA_TL_START(fk_tl_cta_prefix, layer);
 
@@ -134,6 +138,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     }
     mbar_init(&o_done, 1);
     mbar_init(&q_full, kTcSoftmaxWarps);
+    for (int i = 0; i < kTcChunkQ; ++i) mbar_init(&ms.cq_full[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -145,55 +150,90 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = tmem_base_sh;
-  const int start_item = p.tc_start_item[blockIdx.x];
-  const TcCursor c0{start_item, u0 - p.it_unit_off[start_item]};
+  uint64_t* cq_full = ms.cq_full;
+  int* cq = ms.cq;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    // The whole warp walks the tiles; page ids are prefetched lane-parallel
-    // into a 2 x 32-entry register window (4 tiles ahead), so no dependent
-    // global load sits between two tiles' TMA issues.  Lane 0 issues.
+    // Dynamic chunks: the CTA's first chunk is its index, every later one a
+    // ticket (chunk = grid + ticket); lane 0 posts each chunk id in the queue
+    // one chunk ahead of streaming it.  Page ids are prefetched lane-parallel
+    // into a 2 x 32-entry register window; the next chunk's item metadata and
+    // first window are fetched over the following two tiles, so a chunk
+    // switch never waits on a dependent global load.  Lane 0 issues the TMA.
     if (lane == 0) {
       prefetch_tmap(&tmap);
       prefetch_tmap(&tmap_run);
     }
-    TcCursor c = c0;
-    // the next item's metadata is fetched one tile after switching to the
-    // current item and its first page window one tile later, so an item
-    // switch never waits on a dependent global load
-    int cur_item = c0.item, head = p.it_head[c0.item], npi = p.it_npages[c0.item], poff = p.it_page_off[c0.item];
-    int wbase = c0.tile * kTcTilePages;
+    auto grab = [&]() -> int {
+      int c = 0;
+      if (lane == 0) {
+        c = (int)gridDim.x + (int)(atomicAdd(a.ticket_tc, 1ull) - p.tc_ticket_base);
+        if (c >= nch) c = -1;
+      }
+      return __shfl_sync(0xffffffffu, c, 0);
+    };
+    auto post = [&](int i, int chunk) {
+      if (lane == 0) {
+        ((volatile int*)cq)[i % kTcChunkQ] = chunk;
+        mbar_arrive(&cq_full[i % kTcChunkQ]);
+      }
+    };
+    TcCursor c;
+    c.qi = 0;
+    tc_load_chunk(p, c, (int)blockIdx.x);
+    post(0, c.chunk);
+    int nxt = grab();  // the chunk after the current one, posted right away
+    post(1, nxt);
+    int head = p.it_head[c.item], npi = p.it_npages[c.item], poff = p.it_page_off[c.item];
+    int wbase = c.tile * kTcTilePages;
     int win = wbase + lane < npi ? p.pages[poff + wbase + lane] : 0;
     int nwin = wbase + 32 + lane < npi ? p.pages[poff + wbase + 32 + lane] : 0;
-    int n_head = 0, n_npi = 0, n_poff = 0, n_win = 0, n_nwin = 0, n_stage = 0;  // 0 none, 1 meta, 2 + window
-    for (int t = 0; t < T; ++t) {
-      if (c.item != cur_item) {
+    int n_item = 0, n_tile0 = 0, n_tile1 = 0, n_head = 0, n_npi = 0, n_poff = 0, n_win = 0, n_nwin = 0;
+    int n_stage = 0;  // 0 nothing, 1 metadata, 2 metadata + first window of chunk `nxt`
+    for (int t = 0;; ++t) {
+      if (c.tile == c.tile1) {  // current chunk done: switch to `nxt`
+        if (nxt < 0) break;
         if (n_stage < 1) {
-          n_head = p.it_head[c.item];
-          n_npi = p.it_npages[c.item];
-          n_poff = p.it_page_off[c.item];
+          n_item = p.tc_chunk_item[nxt];
+          n_tile0 = p.tc_chunk_tile0[nxt];
+          n_tile1 = p.tc_chunk_tile1[nxt];
+          n_head = p.it_head[n_item];
+          n_npi = p.it_npages[n_item];
+          n_poff = p.it_page_off[n_item];
         }
         if (n_stage < 2) {
-          n_win = lane < n_npi ? p.pages[n_poff + lane] : 0;
-          n_nwin = 32 + lane < n_npi ? p.pages[n_poff + 32 + lane] : 0;
+          const int wb = n_tile0 * kTcTilePages;
+          n_win = wb + lane < n_npi ? p.pages[n_poff + wb + lane] : 0;
+          n_nwin = wb + 32 + lane < n_npi ? p.pages[n_poff + wb + 32 + lane] : 0;
         }
-        cur_item = c.item;
+        ++c.qi;
+        c.chunk = nxt;
+        c.item = n_item;
+        c.tile = n_tile0;
+        c.tile1 = n_tile1;
         head = n_head;
         npi = n_npi;
         poff = n_poff;
-        wbase = 0;  // a later item always starts at its tile 0
+        wbase = n_tile0 * kTcTilePages;
         win = n_win;
         nwin = n_nwin;
         n_stage = 0;
-      } else if (cur_item + 1 < p.num_items) {
+        nxt = grab();
+        post(c.qi + 1, nxt);
+      } else if (nxt >= 0) {
         if (n_stage == 1) {
-          n_win = lane < n_npi ? p.pages[n_poff + lane] : 0;
-          n_nwin = 32 + lane < n_npi ? p.pages[n_poff + 32 + lane] : 0;
+          const int wb = n_tile0 * kTcTilePages;
+          n_win = wb + lane < n_npi ? p.pages[n_poff + wb + lane] : 0;
+          n_nwin = wb + 32 + lane < n_npi ? p.pages[n_poff + wb + 32 + lane] : 0;
           n_stage = 2;
         } else if (n_stage == 0) {
-          n_head = p.it_head[cur_item + 1];
-          n_npi = p.it_npages[cur_item + 1];
-          n_poff = p.it_page_off[cur_item + 1];
+          n_item = p.tc_chunk_item[nxt];
+          n_tile0 = p.tc_chunk_tile0[nxt];
+          n_tile1 = p.tc_chunk_tile1[nxt];
+          n_head = p.it_head[n_item];
+          n_npi = p.it_npages[n_item];
+          n_poff = p.it_page_off[n_item];
           n_stage = 1;
         }
       }
@@ -237,24 +277,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         load_tile(sV + sv * kTcTileBytes, planeV, &v_full[sv]);
       }
       __syncwarp();
-      tc_advance(p, c);
+      ++c.tile;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // Two in-order streams polled by one thread: S(t) = Q.K^T as soon as K(t)
-    // lands (and, at a piece start, its Q is staged), PV(t) as soon as P(t)
+    // lands (and, at a chunk start, its Q is staged), PV(t) as soon as P(t)
     // and V(t) are ready.  S(t) reuses the TMEM buffer of P(t-2), so it is
     // only issued after PV(t-2) (the tensor pipe executes in issue order).
+    // Every chunk is a piece: P.V restarts its accumulator at a chunk start.
     if (lane == 0) {
-      TcCursor cs = c0, cp = c0;
-      int nitem = 0, ts = 0, tp = 0, pv_seg = 0;
-      while (tp < T) {
-        if (ts < T && ts <= tp + 1) {
-          const bool starts = ts == 0 || cs.tile == 0;
+      TcCursor cs, cp;
+      cs.qi = cp.qi = 0;
+      tc_load_chunk(p, cs, tc_read_queue(cq_full, cq, 0));
+      cp = cs;
+      bool s_new = true, p_new = true;  // the next S / PV is a chunk's first tile
+      int ts = 0, tp = 0;
+      while (cp.chunk >= 0) {
+        if (cs.chunk >= 0 && ts <= tp + 1) {
           const int s = ts % kTcKStages;
-          if ((!starts || mbar_try_wait(&q_full, nitem & 1)) && mbar_try_wait(&k_full[s], (ts / kTcKStages) & 1)) {
-            if (starts) ++nitem;
-            const uint32_t q_tm = tm + kTmemQ + (uint32_t)(((nitem - 1) & 1) * 64);
+          if ((!s_new || mbar_try_wait(&q_full, cs.qi & 1)) && mbar_try_wait(&k_full[s], (ts / kTcKStages) & 1)) {
+            const uint32_t q_tm = tm + kTmemQ + (uint32_t)((cs.qi & 1) * 64);
             if (ts < 16) TL(ts);
             tc_fence_after();
             const uint32_t kaddr = smem_u32(sK + s * kTcTileBytes);
@@ -267,15 +310,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             mma_commit(&s_full[sb]);
             mma_commit(&k_empty[s]);
             if (ts < 16) TL(16 + ts);
-            tc_advance(p, cs);
             ++ts;
+            s_new = false;
+            if (++cs.tile == cs.tile1) {
+              ++cs.qi;
+              tc_load_chunk(p, cs, tc_read_queue(cq_full, cq, cs.qi));
+              s_new = true;
+            }
             continue;
           }
         }
         {
           const int sb = tp & 1, s = tp % kTcVStages;
           if (tp < ts && mbar_try_wait(&p_full[sb], (tp >> 1) & 1) && mbar_try_wait(&v_full[s], (tp / kTcVStages) & 1)) {
-            if (tp == 0 || cp.tile == 0) pv_seg = tp;
             if (tp < 16) TL(32 + tp);
             tc_fence_after();
             const uint32_t vaddr = smem_u32(sV + s * kTcTileBytes);
@@ -283,14 +330,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
               const uint64_t bdesc = sdesc(vaddr + kk * 2048, kTcHalf, 1024);
-              mma_ts(tm + 256, p_tm + kk * 16, bdesc, kIdescPV, (tp > pv_seg || kk > 0) ? 1u : 0u);
+              mma_ts(tm + 256, p_tm + kk * 16, bdesc, kIdescPV, (!p_new || kk > 0) ? 1u : 0u);
               mma_ts(tm + 256, p_tm + kk * 16 + 8, bdesc, kIdescPV, 1u);
             }
             mma_commit(&o_done);
             mma_commit(&v_empty[s]);
             if (tp < 16) TL(48 + tp);
-            tc_advance(p, cp);
             ++tp;
+            p_new = false;
+            if (++cp.tile == cp.tile1) {
+              ++cp.qi;
+              tc_load_chunk(p, cp, tc_read_queue(cq_full, cq, cp.qi));
+              p_new = true;
+            }
           }
         }
       }
@@ -315,14 +367,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     const int qj16 = 4 * (lane & 15) + quarter;
     const uint32_t lane_tm = tm + ((uint32_t)(quarter * 32) << 16);
     const int bar_id = 1 + quarter;             // named barrier of the two warps sharing these rows
-    TcCursor c = c0;
     float m = -INFINITY, l = 0.f;
-    int nq = 0, head = 0, ntok = 0, seg_start = 0;
+    int nq = 0, head = 0, ntok = 0;
     bool active = false, r16 = false;
-    // Q of piece k -> TMEM buffer k & 1 (this thread's half of its row; the
-    // A operand layout of S = Q.K^T: row = lane, 2 bf16 per 32-bit column).
-    // Piece k+1's Q is staged while piece k's last P.V runs, so S of the
-    // next piece does not wait for the epilogue.
+    // Q of the chunk at queue index k -> TMEM buffer k & 1 (this thread's half
+    // of its row; the A operand layout of S = Q.K^T: row = lane, 2 bf16 per
+    // 32-bit column).  The next chunk's Q is staged while this chunk's last
+    // P.V runs, so S of the next chunk does not wait for the epilogue.
     auto stage_q = [&](int it, int k) {
       const int nq_i = p.it_nq[it];
       uint32_t qr[32];
@@ -347,16 +398,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_full);
     };
-    int piece_k = 0;
     // under cross-layer PDL the previous layer's merge may still be running:
     // q and the partials are touched only after it has completed
     if (!after_private) pdl_wait_primary();
-    if (T > 0) stage_q(c0.item, 0);
-    if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 2, T);
-    for (int t = 0; t < T; ++t) {
+    TcCursor c;
+    c.qi = 0;
+    tc_load_chunk(p, c, tc_read_queue(cq_full, cq, 0));
+    stage_q(c.item, 0);
+    bool chunk_start = true;
+    int t = 0;
+    for (; c.chunk >= 0; ++t) {
       const int item = c.item;
-      if (t == 0 || c.tile == 0) {
-        seg_start = t;
+      if (chunk_start) {
         nq = p.it_nq[item];
         head = p.it_head[item];
         ntok = p.it_ntok[item];
@@ -374,7 +427,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       // the barrier has completed phase t-2 or t-1: a parity wait for t-1
       // is unambiguous.  A piece end must retire PV(t-1) before P(t) is
       // released, so its later wait for PV(t) is unambiguous too.
-      const bool piece_end = c.tile + 1 == p.it_units[item] || t == T - 1;
+      const bool piece_end = c.tile + 1 == c.tile1;  // every chunk is one piece
       if (active) {
         auto tile = [&](auto mode) {
           constexpr bool R16 = decltype(mode)::value;
@@ -420,7 +473,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
           // the O rescale runs for the whole warp when any of its rows needs
           // it (alpha = 1 for the others).
           const bool rescale = tile_max > m + kRescaleThreshold;
-          const bool warp_rescale = __any_sync(0xffffffffu, rescale) && t > seg_start;
+          const bool warp_rescale = __any_sync(0xffffffffu, rescale) && !chunk_start;
           if (t > 0 && (warp_rescale || piece_end)) mbar_wait(&o_done, (t - 1) & 1);
           if (warp_rescale) {
             const float alpha = rescale ? ex2(m - tile_max) : 1.f;
@@ -479,12 +532,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[sb]);
       if (warp == 4 && lane == 0 && t < 16) TL(80 + t);
+      const int chunk = c.chunk;
+      chunk_start = false;
       if (piece_end) {
-        // next piece's Q first (S of its first tile can then run under this
+        // next chunk's Q first (S of its first tile can then run under this
         // epilogue), then O (unnormalised, running max m) -> partial slot
-        if (t + 1 < T) stage_q(item + 1, piece_k + 1);
-        ++piece_k;
-        if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 3, piece_k);
+        const int next = tc_read_queue(cq_full, cq, c.qi + 1);
+        if (next >= 0) stage_q(p.tc_chunk_item[next], c.qi + 1);
+        if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 3, c.qi + 1);
         mbar_wait(&o_done, t & 1);
         if (warp == 4 && lane == 0 && t < 16) TL(96 + t);
         tc_fence_after();
@@ -495,7 +550,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             const int my_row = R16 ? row16 : row;
             const int my_q = R16 ? qj16 : qj;
             const int col0 = half * 64 + (R16 ? sub * 32 : 0);
-            const int piece = blockIdx.x - p.it_first_cta[item];
+            const int piece = chunk - p.it_first_chunk[item];
             const bool real = my_q < nq;
             long long pi = 0;
             if (real) {
@@ -530,9 +585,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         }
         tc_fence_before();
         if (warp == 4 && lane == 0 && t < 16) TL(112 + t);
+        ++c.qi;
+        tc_load_chunk(p, c, next);
+        chunk_start = true;
+      } else {
+        ++c.tile;
       }
-      tc_advance(p, c);
     }
+    if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 2, t);
   }
   tc_fence_before();
   __syncthreads();

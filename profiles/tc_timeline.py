@@ -13,6 +13,9 @@ from paper_2405_19888_b200.workloads import fork_group  # noqa: E402
 
 eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 22, device=0, geometry=P.ModelGeometry(2, 40, 128))
 eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, 2)
+for kv in filter(None, os.environ.get("FK_TL_OPT", "").split(",")):  # e.g. FK_TL_OPT=TC_MIN_CHUNK=4
+    k, v = kv.split("=")
+    eng.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
 fork_group(eng, 6000, [256] * int(os.environ.get("FK_TL_FORKS", "64")), out_len=8)
 for _ in range(3):
     eng.step()

@@ -144,7 +144,8 @@ def test_large_fanout_multiple_query_blocks(cuda_device):
 
 def test_many_splits(cuda_device):
     eng = make_engine(cuda_device, H=2)
-    eng.set_option(_lib.FK_OPT_MIN_SPLIT_PAGES, 1)
+    eng.set_option(_lib.FK_OPT_MIN_SPLIT_PAGES, 1)  # mma path: one split per page
+    eng.set_option(_lib.FK_OPT_TC_MIN_CHUNK, 1)     # tcgen05 path: one-tile chunks
     eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4096)
     fork_group(eng, 1000, [20, 21], out_len=2)
     run_steps(eng, 2)
