@@ -374,23 +374,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     // of its row; the A operand layout of S = Q.K^T: row = lane, 2 bf16 per
     // 32-bit column).  The next chunk's Q is staged while this chunk's last
     // P.V runs, so S of the next chunk does not wait for the epilogue.
+    // (a chunk's last tile prefetches the next chunk's Q lines into L1 --
+    // prefetch_q, no registers held -- and its piece end loads and stages them)
+    auto q_line = [&](int it) -> const uint4* {
+      return qj < p.it_nq[it] ? reinterpret_cast<const uint4*>(
+                                    q + ((long long)p.qrows[p.it_q_off[it] + qj] * H + p.it_head[it]) * kHeadDim) +
+                                    half * 8
+                              : nullptr;
+    };
+    auto prefetch_q = [&](int it) {
+      const uint4* src = q_line(it);
+      if (src) asm volatile("prefetch.global.L1 [%0];" ::"l"(src));
+    };
     auto stage_q = [&](int it, int k) {
-      const int nq_i = p.it_nq[it];
+      const uint4* src = q_line(it);
       uint32_t qr[32];
-      if (qj < nq_i) {
-        const uint4* src = reinterpret_cast<const uint4*>(
-            q + ((long long)p.qrows[p.it_q_off[it] + qj] * H + p.it_head[it]) * kHeadDim) + half * 8;
 #pragma unroll
-        for (int k8 = 0; k8 < 8; ++k8) {
-          const uint4 v = src[k8];
-          qr[4 * k8] = v.x;
-          qr[4 * k8 + 1] = v.y;
-          qr[4 * k8 + 2] = v.z;
-          qr[4 * k8 + 3] = v.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) qr[i] = 0u;
+      for (int k8 = 0; k8 < 8; ++k8) {
+        const uint4 v = src ? src[k8] : make_uint4(0u, 0u, 0u, 0u);
+        qr[4 * k8] = v.x;
+        qr[4 * k8 + 1] = v.y;
+        qr[4 * k8 + 2] = v.z;
+        qr[4 * k8 + 3] = v.w;
       }
       tmem_st32(lane_tm + kTmemQ + (uint32_t)((k & 1) * 64) + half * 32, qr);
       tmem_wait_st();
@@ -418,6 +423,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         m = -INFINITY;
         l = 0.f;
       }
+      // the last tile of a chunk: the next chunk's Q loads go out now and
+      // land while this tile's scores are processed
+      const bool piece_end = c.tile + 1 == c.tile1;  // every chunk is one piece
+      const int next = piece_end ? tc_read_queue(cq_full, cq, c.qi + 1) : -1;
+      if (next >= 0) prefetch_q(p.tc_chunk_item[next]);
       const int sb = t & 1;
       mbar_wait(&s_full[sb], (t >> 1) & 1);
       if (warp == 4 && lane == 0 && t < 16) TL(64 + t);
@@ -427,7 +437,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       // the barrier has completed phase t-2 or t-1: a parity wait for t-1
       // is unambiguous.  A piece end must retire PV(t-1) before P(t) is
       // released, so its later wait for PV(t) is unambiguous too.
-      const bool piece_end = c.tile + 1 == c.tile1;  // every chunk is one piece
       if (active) {
         auto tile = [&](auto mode) {
           constexpr bool R16 = decltype(mode)::value;
@@ -537,7 +546,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       if (piece_end) {
         // next chunk's Q first (S of its first tile can then run under this
         // epilogue), then O (unnormalised, running max m) -> partial slot
-        const int next = tc_read_queue(cq_full, cq, c.qi + 1);
+        if (warp == 4 && lane == 0) TL(243 + min(c.qi, 3) * 4);
         if (next >= 0) stage_q(p.tc_chunk_item[next], c.qi + 1);
         if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 3, c.qi + 1);
         mbar_wait(&o_done, t & 1);
@@ -565,6 +574,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
               if (R16) tmem_ld16x2(o_tm, o);
               else tmem_ld32(o_tm + cc * 32, o);
               tmem_wait_ld();
+              if (warp == 4 && lane == 0 && cc == 0) TL(240 + min(c.qi, 3) * 4);
               if (real) {
                 float4* po = reinterpret_cast<float4*>(a.part_o + pi * kHeadDim + col0 + cc * 32);
 #pragma unroll
@@ -573,11 +583,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
                                        __uint_as_float(o[4 * i4 + 2]), __uint_as_float(o[4 * i4 + 3]));
               }
             }
+            if (warp == 4 && lane == 0) TL(241 + min(c.qi, 3) * 4);
             float lr = l;
             if (R16) lr += __shfl_xor_sync(0xffffffffu, lr, 16);
             const bool lead = !R16 || sub == 0;
             if (half == 1 && lead) s_l[my_row] = lr;
             asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            if (warp == 4 && lane == 0) TL(242 + min(c.qi, 3) * 4);
             if (half == 0 && lead && real) a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
           };
           if (r16) epilogue(BoolC<true>{});

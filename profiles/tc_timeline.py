@@ -28,5 +28,8 @@ t0 = buf[160]
 names = {0: "kv_full", 16: "S_issued", 32: "p_full+o_free", 48: "PV_issued", 64: "s_full(sm)",
          80: "P_written", 96: "o_full(sm)", 112: "acc_done", 128: "kv_empty(prod)",
          176: "sm:S loaded", 192: "sm:max xchg", 208: "sm:P stored", 224: "sm:wait_st"}
+print("epilogue of the first 4 pieces (read queue, O loaded, stores issued, pair barrier):")
+for k in range(4):
+    print("  piece", k, " ".join(f"{(buf[240 + 4 * k + j] - t0) / 1e3:7.2f}" if buf[240 + 4 * k + j] > t0 else "   -   " for j in (3, 0, 1, 2)))
 for base, nm in names.items():
     print(f"{nm:16s}", " ".join(f"{(buf[base + t] - t0) / 1e3:7.2f}" if buf[base + t] > t0 else "   -   " for t in range(14)))
