@@ -520,8 +520,11 @@ extern "C" int fk_debug_cta_timeline_merge(unsigned long long* out, int n) {
 
 // ================================================================= append
 // K1: the step's new K/V rows -> (page, slot) of each row's leaf, for
-// layers [layer0, layer0 + gridDim.y); one warp per (row, head, layer).
-__global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, PlanDev p, int layer0,
+// layers [layer0, layer0 + nlayers).  One warp per (row, head) and group of
+// kAppendLayers layers: lanes 0-15 move K, 16-31 V, 16 B each; all of a
+// warp's loads are issued before its stores.
+constexpr int kAppendLayers = 8;
+__global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, PlanDev p, int layer0, int nlayers,
                                                        const uint4* __restrict__ k, const uint4* __restrict__ v) {
   const int H = a.num_heads;
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -530,14 +533,21 @@ __global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, PlanDev p, i
   const int pg = p.app_page[row];
   if (pg < 0) return;
   const int slot = p.app_slot[row];
-  const int li = blockIdx.y, layer = layer0 + li;
+  const int l0 = blockIdx.y * kAppendLayers;
   const long long plane_elems = a.num_pages * kPage * kHeadDim;
-  const int kv = lane >> 4, c = lane & 15;  // 16 lanes x 16 B per row
+  const int kv = lane >> 4, c = lane & 15;
   const uint4* src = kv == 0 ? k : v;
-  const uint4 val = src[(((long long)li * p.num_rows + row) * H + h) * 16 + c];
-  uint4* dst = reinterpret_cast<uint4*>(a.kv + plane_index(layer, kv, h, H) * plane_elems +
-                                        ((long long)pg * kPage + slot) * kHeadDim);
-  dst[c] = val;
+  uint4 val[kAppendLayers];
+#pragma unroll
+  for (int i = 0; i < kAppendLayers; ++i)
+    if (l0 + i < nlayers) val[i] = __ldcs(&src[(((long long)(l0 + i) * p.num_rows + row) * H + h) * 16 + c]);
+#pragma unroll
+  for (int i = 0; i < kAppendLayers; ++i)
+    if (l0 + i < nlayers) {
+      uint4* dst = reinterpret_cast<uint4*>(a.kv + plane_index(layer0 + l0 + i, kv, h, H) * plane_elems +
+                                            ((long long)pg * kPage + slot) * kHeadDim);
+      dst[c] = val[i];
+    }
 }
 
 // ================================================================== fill
@@ -678,8 +688,8 @@ cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, co
 
 cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers, const void* k,
                           const void* v, cudaStream_t s) {
-  dim3 grid((p.num_rows * a.num_heads + 7) / 8, nlayers);
-  fk_append_kernel<<<grid, 256, 0, s>>>(a, p, layer0, (const uint4*)k, (const uint4*)v);
+  dim3 grid((p.num_rows * a.num_heads + 7) / 8, (nlayers + kAppendLayers - 1) / kAppendLayers);
+  fk_append_kernel<<<grid, 256, 0, s>>>(a, p, layer0, nlayers, (const uint4*)k, (const uint4*)v);
   return cudaGetLastError();
 }
 
