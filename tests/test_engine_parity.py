@@ -60,7 +60,8 @@ def test_live_random_streams_match_reference():
 def test_reference_suites_with_engine_rebound(tmp_path):
     """The reference's own hot-path tests (engine, tokenizer, prefix,
     manager, experiments, acceptance) run with semflow's Engine replaced by
-    GpuEngine (the substitution point manager.py:130-139)."""
+    GpuEngine (the substitution point manager.py:130-139) and its FNV hash by
+    the C one."""
     names = ["test_engine.py", "test_acceptance.py", "test_manager.py", "test_experiments.py",
              "test_prefix.py", "test_tokenizer.py"]
     (tmp_path / "fk_rebind.py").write_text(textwrap.dedent(f"""
@@ -74,6 +75,11 @@ def test_reference_suites_with_engine_rebound(tmp_path):
         assert P.errors.REFERENCE_ERRORS
         se.Engine = P.GpuEngine
         sm.Engine = P.GpuEngine
+        # the chain hashes of render_prefix and the end hashes come from the
+        # C FNV-1a-64 (fk_fnv1a64_u32) too
+        import semflow.prefix as sp
+        import semflow.tokenizer as st
+        st.hash_token_ids = sp.hash_token_ids = se.hash_token_ids = P.hash_token_ids
 
         def pytest_sessionfinish(session, exitstatus):
             assert sm.Engine is P.GpuEngine
