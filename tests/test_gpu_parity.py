@@ -409,3 +409,17 @@ def test_merge_many_partials(cuda_device, suffix):
     run_steps(eng, 2)
     assert eng.last_plan.max_slots > (128 if suffix > 2048 else 32)
     check_history(eng)
+
+
+@pytest.mark.parametrize("min_chunk", [1, 3])
+def test_prefix_chunk_queue_wraps(cuda_device, min_chunk):
+    """Few tcgen05 CTAs, small chunks: each CTA streams 20+ chunks, so the
+    producer's chunk queue (16 entries) wraps several times, chunks of
+    several heads and both query-block layouts interleave per CTA."""
+    eng = make_engine(cuda_device, H=6, L=1)
+    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4)
+    eng.set_option(_lib.FK_OPT_TC_MIN_CHUNK, min_chunk)
+    fork_group(eng, 2300, [9] * 70, out_len=2, tag="a", seed=1)   # 70 rows: 32-lane layout
+    fork_group(eng, 1100, [4] * 20, out_len=2, tag="b", seed=2)   # 20 rows: 16-lane layout
+    run_steps(eng, 2)
+    check_history(eng)
