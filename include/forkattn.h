@@ -110,8 +110,9 @@ enum {
                                  schedule, 1..32 (default 2): the granularity of its tail */
   FK_OPT_PRIV_STATIC_FIRST = 9, /* 1 (default): the private warps that start at once take their
                                  first chunk by warp index instead of a ticket */
-  FK_OPT_TC_MIN_CHUNK = 10    /* smallest chunk (128-token tiles) of the tcgen05 prefix kernel's
+  FK_OPT_TC_MIN_CHUNK = 10,   /* smallest chunk (128-token tiles) of the tcgen05 prefix kernel's
                                  guided dynamic schedule, 1..24 (default 24: a chunk end costs ~3 us) */
+  FK_OPT_PRIV_WARPS = 11      /* private CTA shape: 8 warps x 3 stages (default), 6 x 4, 7 x 4 or 12 x 2 */
 };
 
 /* ---- context forest ------------------------------------------------------ */

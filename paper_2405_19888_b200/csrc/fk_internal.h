@@ -15,8 +15,7 @@ constexpr int kTcQBlock = 128; // queries per tcgen05 prefix CTA (M = 128 rows)
 constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
 constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
 constexpr int kTcMaxChunk = 24;   // largest tcgen05 chunk (tiles)
-constexpr int kPrivWarpsPerCta = 8;  // private kernel: independent warps per CTA
-constexpr int kPrivStages = 3;       // per-warp smem ring depth (8 KiB K+V page per stage)
+constexpr int kPrivWarpsPerCta = 8;  // private kernel default shape: 8 warps per CTA x 3 stages
 constexpr int kPrivMinChunk = 2;     // private guided schedule: smallest chunk (pages), default
 constexpr int kPrivMaxChunk = 32;    // largest chunk (one lane-parallel metadata load)
 
@@ -66,7 +65,8 @@ struct PlanDev {
   int priv_np;                 // number of private page entries (NPT)
   int priv_units;              // U = H * NPT
   int priv_nchunks;
-  int priv_warps;              // grid warps (grid = priv_warps / kPrivWarpsPerCta)
+  int priv_wpc;                // warps per private CTA (ring shape: 8 -> 3 stages, 6 -> 4, 12 -> 2)
+  int priv_warps;              // grid warps (grid = priv_warps / priv_wpc)
   int priv_static;             // warps that start on chunk = warp index (the ones that start at once)
   const int* priv_chunk_start; // [priv_nchunks + 1]
   const int* priv_rh_chunk0;   // [rows][H] first chunk of each (row, head) item

@@ -31,9 +31,9 @@ namespace fk {
 // query in row 0, online softmax on the row-0 fragments, P split hi+lo.
 // A chunk always ends a piece: (row, head, chunk) -> one partial slot
 // row_head_base + (chunk - first chunk of the item), fixed by the plan.
-constexpr int kPwThreads = kPrivWarpsPerCta * 32;
 constexpr int kPwStageBytes = 8192;
-constexpr int kPwSmem = kPrivWarpsPerCta * kPrivStages * kPwStageBytes + 1024;
+template <int STAGES, int WARPS>
+constexpr int priv_smem() { return WARPS * STAGES * kPwStageBytes + 1024; }
 
 // byte offset of (token row 0..15, 16-byte chunk 0..15) in one K or V page
 // held as two SWIZZLE_128B boxes of 16 rows x 128 B
@@ -56,14 +56,15 @@ struct PdlTail {
     if (threadIdx.x == 0) pdl_wait_primary();
   }
 };
-__global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
+template <int STAGES, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
                                                                    float scale_log2,
                                                                    const __grid_constant__ CUtensorMap tmap,
                                                                    unsigned long long ticket_base) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t full[kPrivWarpsPerCta][kPrivStages];
+  __shared__ uint64_t full[WARPS][STAGES];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
   // chunk = priv_static + ticket.  Each warp stops after its first failing
   // ticket, so a launch consumes nchunks - priv_static + (grid warps) tickets
   // (the host advances ticket_base by that).
-  const int gw = blockIdx.x * kPrivWarpsPerCta + warp;
+  const int gw = blockIdx.x * WARPS + warp;
   auto grab = [&]() -> int {
     int c = 0;
     if (lane == 0) c = p.priv_static + (int)(atomicAdd(a.ticket, 1ull) - ticket_base);
@@ -88,10 +89,10 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
   int ca = gw < p.priv_static ? gw : grab();
   if (ca >= nch) return;
 
-  uint8_t* ring = smem + warp * kPrivStages * kPwStageBytes;
+  uint8_t* ring = smem + warp * STAGES * kPwStageBytes;
   if (lane == 0) {
     prefetch_tmap(&tmap);
-    for (int s = 0; s < kPrivStages; ++s) mbar_init(&full[warp][s], 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[warp][s], 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -141,11 +142,11 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
   int i = 0, ia = 0;
   unsigned seq = 0;
   auto issue_ahead = [&]() {
-    while (ia - i < kPrivStages && ia < la + lb) {
+    while (ia - i < STAGES && ia < la + lb) {
       const UnitMeta m = ia < la ? sh(ma, ia) : sh(mb, ia - la);
       if (lane == 0) {
         if (ia - i > 0 || seq > 0) fence_proxy_async();
-        issue((int)((seq + (unsigned)(ia - i)) % kPrivStages), m);
+        issue((int)((seq + (unsigned)(ia - i)) % STAGES), m);
       }
       ++ia;
     }
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(kPwThreads, 1) fk_private_kernel(ArenaDev a, P
     const UnitMeta nxt = !chunk_last ? sh(ma, i + 1) : (lb > 0 ? sh(mb, 0) : cur);
     const bool piece_end = chunk_last || nxt.row != cur.row || nxt.head != cur.head;
     if (piece_end && have_next) fetch_q(qn, nxt.row, nxt.head);
-    const int s = (int)(seq % kPrivStages);
-    mbar_wait(&full[warp][s], (seq / kPrivStages) & 1);
+    const int s = (int)(seq % STAGES);
+    mbar_wait(&full[warp][s], (seq / STAGES) & 1);
     const uint32_t Ks = smem_u32(ring + s * kPwStageBytes);
     const uint32_t Vs = Ks + 4096;
     float sc[2][4];
@@ -652,18 +653,33 @@ __global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long
 }
 
 // ============================================================== launchers
-cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                           const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl, cudaStream_t s) {
+template <int STAGES, int WARPS>
+static cudaError_t launch_private_shape(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
+                                       float scale_log2, const CUtensorMap* tmap, unsigned long long ticket_base,
+                                       bool pdl, cudaStream_t s) {
   static bool attr = false;
+  constexpr int smem = priv_smem<STAGES, WARPS>();
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fk_private_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPwSmem);
+    cudaError_t e = cudaFuncSetAttribute(fk_private_kernel<STAGES, WARPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (p.priv_units == 0) return cudaSuccess;
-  const int grid = p.priv_warps / kPrivWarpsPerCta;
-  return launch_k(fk_private_kernel, dim3(grid), dim3(kPwThreads), kPwSmem, s, pdl, a, p, layer,
+  const int grid = p.priv_warps / WARPS;
+  return launch_k(fk_private_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, pdl, a, p, layer,
                   (const __nv_bfloat16*)q, scale_log2, *tmap, ticket_base);
+}
+
+cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
+                           const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl, cudaStream_t s) {
+  if (p.priv_units == 0) return cudaSuccess;
+  // ring shapes: per-warp stages x warps per CTA (192 KiB of stages; 7 x 4 = 224 KiB)
+  switch (p.priv_wpc) {
+    case 6: return launch_private_shape<4, 6>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 7: return launch_private_shape<4, 7>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 12: return launch_private_shape<2, 12>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    default: return launch_private_shape<3, 8>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+  }
 }
 
 cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, int layer, bool pdl,

@@ -91,6 +91,7 @@ struct fk_pool {
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
+  int64_t priv_wpc = kPrivWarpsPerCta;  // private CTA shape (warps; stages follow)
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
   int64_t tc_min_chunk = 24;  // smallest tcgen05 chunk (tiles); measured: every chunk end costs ~3 us of epilogue, so coarse wins
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
@@ -353,6 +354,11 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
     case FK_OPT_PDL: p->pdl = value; break;
     case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
+    case FK_OPT_PRIV_WARPS:
+      if (value != 6 && value != 7 && value != 8 && value != 12)
+        return fail(FK_INVALID_ARGUMENT, "private warps must be 6, 7, 8 or 12");
+      p->priv_wpc = value;
+      break;
     case FK_OPT_TC_MIN_CHUNK: p->tc_min_chunk = std::min<int64_t>(kTcMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
@@ -736,7 +742,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // counter.  The grid covers every SM: in co-run the CTAs beyond the free
   // SMs start when tcgen05 prefix CTAs retire and take the leftovers.
   const int64_t priv_sms = corun ? std::max<int64_t>(1, p->num_sms - tc_ctas) : p->num_sms;
-  const int64_t w_active = priv_sms * kPrivWarpsPerCta;
+  const int64_t wpc = p->priv_wpc;
+  const int64_t w_active = priv_sms * wpc;
   std::vector<int32_t> chunk_start;
   for (int64_t pos = 0; pos < U;) {
     int64_t sz = (U - pos + 2 * w_active - 1) / (2 * w_active);
@@ -750,8 +757,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // launched first (order 1) the private grid must leave the prefix its SMs
   const int64_t grid_sms = (corun && p->launch_order == 1) ? priv_sms : p->num_sms;
   const int64_t grid_ctas = std::max<int64_t>(
-      1, std::min<int64_t>(grid_sms, (nchunks + kPrivWarpsPerCta - 1) / kPrivWarpsPerCta));
-  const int64_t G = grid_ctas * kPrivWarpsPerCta;
+      1, std::min<int64_t>(grid_sms, (nchunks + wpc - 1) / wpc));
+  const int64_t G = grid_ctas * wpc;
   auto chunk_of = [&](int64_t u) {
     return (int64_t)(std::upper_bound(chunk_start.begin(), chunk_start.end() - 1, (int32_t)u) -
                      chunk_start.begin()) - 1;
@@ -934,6 +941,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.priv_np = (int)NPT;
   pd.priv_units = (int)U;
   pd.priv_nchunks = (int)nchunks;
+  pd.priv_wpc = (int)wpc;
   pd.priv_warps = (int)G;
   pd.priv_static = p->priv_static_first ? (int)std::min<int64_t>(std::min<int64_t>(w_active, G), nchunks) : 0;
   pd.priv_chunk_start = (const int32_t*)(d + o_cs);

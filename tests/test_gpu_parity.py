@@ -423,3 +423,14 @@ def test_prefix_chunk_queue_wraps(cuda_device, min_chunk):
     fork_group(eng, 1100, [4] * 20, out_len=2, tag="b", seed=2)   # 20 rows: 16-lane layout
     run_steps(eng, 2)
     check_history(eng)
+
+
+@pytest.mark.parametrize("warps", [6, 12])
+def test_private_ring_shapes(cuda_device, warps):
+    """FK_OPT_PRIV_WARPS: 6 warps x 4 stages and 12 warps x 2 stages per
+    private CTA give the same attention."""
+    eng = make_engine(cuda_device, H=4, L=2)
+    eng.set_option(_lib.FK_OPT_PRIV_WARPS, warps)
+    fork_group(eng, 400, [33, 100, 7, 260], out_len=3)
+    run_steps(eng, 3)
+    check_history(eng)
