@@ -36,6 +36,7 @@ FK_OPT_PRIV_MIN_CHUNK = 8
 FK_OPT_PRIV_STATIC_FIRST = 9
 FK_OPT_TC_MIN_CHUNK = 10
 FK_OPT_PRIV_WARPS = 11
+FK_OPT_GRAPH = 12
 
 
 class PoolDesc(ctypes.Structure):

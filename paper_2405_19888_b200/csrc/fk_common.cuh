@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstring>
+#include <vector>
 #include "fk_internal.h"
 
 namespace fk {
@@ -93,9 +95,29 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // Launch with optional programmatic dependent launch (PDL): the kernel may
 // start while its stream predecessor is still running; it must call
 // pdl_wait_primary() before touching the predecessor's results.
+template <typename T>
+inline void rec_push_arg(LaunchRec& r, const T& v) {
+  const size_t al = alignof(T) < 16 ? alignof(T) : 16;
+  size_t off = (r.bytes.size() + al - 1) / al * al;
+  r.bytes.resize(off + sizeof(T));
+  memcpy(r.bytes.data() + off, &v, sizeof(T));
+  r.offs.push_back(off);
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
                             Args&&... args) {
+  if (g_launch_rec) {
+    LaunchRec r;
+    r.func = (const void*)kernel;
+    r.grid = grid;
+    r.block = block;
+    r.smem = smem;
+    r.pdl = pdl;
+    (rec_push_arg<KArgs>(r, static_cast<KArgs>(args)), ...);
+    g_launch_rec->push_back(std::move(r));
+    return cudaSuccess;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

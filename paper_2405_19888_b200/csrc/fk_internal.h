@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <vector>
 
 namespace fk {
 
@@ -94,6 +95,27 @@ struct ArenaDev {
 inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {
   return ((long long)layer * 2 + kv) * H + head;
 }
+
+// A launch captured as data (function, geometry, PDL flag, argument bytes):
+// fk_attn_decode_layers records a step's launches and replays them as a CUDA
+// graph (first time: stream capture; afterwards: kernel-node parameter
+// updates), instead of issuing ~120 launches from the host every step.
+struct LaunchRec {
+  const void* func = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+  bool pdl = false;
+  std::vector<unsigned char> bytes;  // argument values, each at offs[i]
+  std::vector<size_t> offs;
+  std::vector<void*> args;           // pointers into bytes (rebuilt by finalize())
+  void finalize() {
+    args.resize(offs.size());
+    for (size_t i = 0; i < offs.size(); ++i) args[i] = bytes.data() + offs[i];
+  }
+};
+// Non-null while fk_attn_decode_layers records: launch_k appends instead of launching.
+extern thread_local std::vector<LaunchRec>* g_launch_rec;
+
 
 // Launchers (fk_kernels.cu).  All return cudaError_t of the launch.
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q,

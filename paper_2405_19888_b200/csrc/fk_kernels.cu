@@ -19,6 +19,8 @@
 
 namespace fk {
 
+thread_local std::vector<LaunchRec>* g_launch_rec = nullptr;
+
 // =========================================================== private (n_c=1)
 // Units u = (head, flat private page entry e), head-major.  The plan cuts the
 // unit list into chunks of decreasing size (guided: big first, 4-unit ones
@@ -697,9 +699,8 @@ cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, co
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(p.tc_begin);
-  fk_prefix_mma_kernel<<<grid, kPmThreads, kPmSmem, s>>>(a, p, layer, (const __nv_bfloat16*)q, scale_log2, *tmap);
-  return cudaGetLastError();
+  return launch_k(fk_prefix_mma_kernel, dim3(p.tc_begin), dim3(kPmThreads), kPmSmem, s, false, a, p, layer,
+                  (const __nv_bfloat16*)q, scale_log2, *tmap);
 }
 
 cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers, const void* k,

@@ -8,6 +8,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
+#include <map>
+#include <tuple>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -67,6 +70,25 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
+// A step's attention launches as one CUDA graph: captured the first time a
+// launch structure is seen, afterwards only its kernel-node parameters are
+// updated (the structure -- functions, grids, PDL edges -- stays).
+struct GraphCache {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> nodes;   // kernel nodes in launch order
+  std::vector<fk::LaunchRec> shape;     // structure of the captured launches (no argument bytes)
+  cudaStream_t stream = nullptr;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    nodes.clear();
+    shape.clear();
+  }
+};
+
 struct fk_pool {
   fk_pool_desc desc{};
   bool on_device = false;
@@ -95,6 +117,8 @@ struct fk_pool {
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
   int64_t tc_min_chunk = 24;  // smallest tcgen05 chunk (tiles); measured: every chunk end costs ~3 us of epilogue, so coarse wins
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
+  int64_t use_graph = 1;  // fk_attn_decode_layers replays a CUDA graph
+  std::map<std::tuple<int32_t, int32_t, cudaStream_t>, GraphCache> graphs;  // per (layer0, nlayers, stream)
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
   int64_t prefix_rate_pct = 50;  // prefix KV bytes/s per SM relative to the private stream's (measured optimum, headline)
@@ -317,6 +341,7 @@ int fk_pool_destroy(fk_pool* p) {
     if (p->part_o) cudaFree(p->part_o);
     if (p->part_ml) cudaFree(p->part_ml);
     if (p->ticket) cudaFree(p->ticket);
+    for (auto& kv : p->graphs) kv.second.reset();
   }
   delete p;
   return FK_OK;
@@ -353,6 +378,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_PREFIX_TARGET_CTAS: p->prefix_target_ctas = value; break;
     case FK_OPT_LAUNCH_ORDER: p->launch_order = value; break;
     case FK_OPT_PDL: p->pdl = value; break;
+    case FK_OPT_GRAPH: p->use_graph = value != 0; break;
     case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
     case FK_OPT_PRIV_WARPS:
       if (value != 6 && value != 7 && value != 8 && value != 12)
@@ -480,10 +506,14 @@ int fk_ctx_blocks(const fk_pool* p, int64_t ctx, int64_t* logical, int32_t* phys
 
 int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, void* stream,
                  fk_plan_info* info) {
+  static const bool plan_timing = getenv("FK_DEBUG_TIMING") != nullptr;
+  double pt[8] = {0};
+#define PT(n) do { if (plan_timing) pt[#n[1] - '0'] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); } while (0)
   if (!p || (B > 0 && !leaves) || B < 0) return fail(FK_INVALID_ARGUMENT, "bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t H = p->desc.num_heads;
 
+  PT(T0);
   // chains leaf -> root, fan-out per context (engine.py:476-482 walk)
   std::vector<std::vector<int64_t>> chain(B);
   std::unordered_map<int64_t, int> fan;
@@ -514,6 +544,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   auto is_shared = [&](int64_t c) { return dedup && fan[c] >= 2 && p->ctxs[c].tokens > 0; };
 
+  PT(T1);
   // ---- shared contexts (K2 work) --------------------------------------------
   struct Shared {
     int64_t ctx;
@@ -602,6 +633,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
           }
       }
     }
+  PT(T2);
   // tcgen05 stream-K: tile units of all tc items over <= one wave of CTAs
   std::vector<int32_t> it_unit_off(items.size(), 0);
   int64_t tc_units = 0;
@@ -670,30 +702,44 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     const int64_t next = (i + 1 < items.size()) ? it_first_chunk[i + 1] : tc_nchunks;
     return items[i].units == 0 ? 1 : (int)(next - it_first_chunk[i]);
   };
+  PT(T3);
   // per (shared ctx, qblock, head): pieces contributed to each of its rows
-  std::unordered_map<int64_t, int> pieces_of;  // key (sh * 4096 + qb) * H + h
-  auto pkey = [&](int sh, int qb, int h) { return ((int64_t)sh * 4096 + qb) * H + h; };
+  // (dense tables: this runs every step on the host)
+  const int64_t nsh = std::max<int64_t>((int64_t)shared.size(), 1);
+  std::vector<int64_t> qb_off(shared.size() + 1, 0);  // first (qblock, head) slot of each shared ctx
+  for (size_t si = 0; si < shared.size(); ++si) {
+    const int qbs = shared[si].tc ? kTcQBlock : kMmaQBlock;
+    qb_off[si + 1] = qb_off[si] + (int64_t)((shared[si].rows.size() + qbs - 1) / qbs) * H;
+  }
+  std::vector<int32_t> pieces_of(std::max<int64_t>(qb_off.back(), 1), 0);
   for (size_t i = 0; i < items.size(); ++i) {
     const Item& it = items[i];
     const int qb = it.q0 / (shared[it.sh].tc ? kTcQBlock : kMmaQBlock);
-    pieces_of[pkey(it.sh, qb, it.head)] += item_pieces(i);
+    pieces_of[qb_off[it.sh] + (int64_t)qb * H + it.head] += item_pieces(i);
   }
-  // slot bases: per (row, head) walk the shared chain root -> leaf
-  std::vector<int32_t> row_head_base(std::max<int64_t>(B * H, 1), 0);
-  std::unordered_map<int64_t, int> base_at;  // key (row * H + h) * nshared + sh
-  const int64_t nsh = std::max<int64_t>((int64_t)shared.size(), 1);
-  std::vector<int> pos_in_ctx(shared.size(), 0);
-  for (int r = 0; r < B; ++r) {
-    for (int h = 0; h < H; ++h) {
-      int acc = 0;
+  // each row's shared contexts root -> leaf, with its query block in each
+  std::vector<std::vector<std::pair<int, int>>> row_shared(B);
+  {
+    std::vector<int32_t> pos(shared.size() * (size_t)B, -1);  // [shared][row] -> position in s.rows
+    for (size_t si = 0; si < shared.size(); ++si)
+      for (size_t j = 0; j < shared[si].rows.size(); ++j) pos[si * B + shared[si].rows[j]] = (int32_t)j;
+    for (int r = 0; r < B; ++r)
       for (auto ci = chain[r].rbegin(); ci != chain[r].rend(); ++ci) {
         auto si = shared_idx.find(*ci);
         if (si == shared_idx.end()) continue;
-        const Shared& s = shared[si->second];
-        const int j = (int)(std::find(s.rows.begin(), s.rows.end(), r) - s.rows.begin());
-        const int qb = j / (s.tc ? kTcQBlock : kMmaQBlock);
-        base_at[((int64_t)r * H + h) * nsh + si->second] = acc;
-        acc += pieces_of[pkey(si->second, qb, h)];
+        const Shared& sc = shared[si->second];
+        row_shared[r].emplace_back(si->second, pos[(size_t)si->second * B + r] / (sc.tc ? kTcQBlock : kMmaQBlock));
+      }
+  }
+  // slot bases: per (row, head) walk the shared chain root -> leaf
+  std::vector<int32_t> row_head_base(std::max<int64_t>(B * H, 1), 0);
+  std::vector<int32_t> base_at((size_t)std::max<int64_t>(B * H * nsh, 1), 0);  // [(row * H + h) * nsh + sh]
+  for (int r = 0; r < B; ++r) {
+    for (int h = 0; h < H; ++h) {
+      int acc = 0;
+      for (const auto& sq : row_shared[r]) {
+        base_at[((int64_t)r * H + h) * nsh + sq.first] = acc;
+        acc += pieces_of[qb_off[sq.first] + (int64_t)sq.second * H + h];
       }
       row_head_base[(int64_t)r * H + h] = acc;
     }
@@ -701,14 +747,15 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   std::vector<int32_t> it_qslot_off(items.size()), qslot;
   for (size_t i = 0; i < items.size(); ++i) {
     const Item& it = items[i];
-    const Shared& s = shared[it.sh];
+    const Shared& sc = shared[it.sh];
     it_qslot_off[i] = (int32_t)qslot.size();
     for (int j = 0; j < it.nq; ++j) {
-      const int r = s.rows[it.q0 + j];
+      const int r = sc.rows[it.q0 + j];
       qslot.push_back(base_at[((int64_t)r * H + it.head) * nsh + it.sh] + ((int)i < num_mma ? it.split : 0));
     }
   }
 
+  PT(T4);
   // ---- private streams (K3 work) ----------------------------------------------
   std::vector<int32_t> row_priv_off(B), row_priv_np(B);
   for (int r = 0; r < B; ++r) {
@@ -737,6 +784,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
+  PT(T5);
   // Guided dynamic schedule: chunks shrink from ~U / (2 W) pages to 4 as the
   // list drains (W = warps that start at once), warps grab them from a ticket
   // counter.  The grid covers every SM: in co-run the CTAs beyond the free
@@ -759,27 +807,34 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int64_t grid_ctas = std::max<int64_t>(
       1, std::min<int64_t>(grid_sms, (nchunks + wpc - 1) / wpc));
   const int64_t G = grid_ctas * wpc;
-  auto chunk_of = [&](int64_t u) {
-    return (int64_t)(std::upper_bound(chunk_start.begin(), chunk_start.end() - 1, (int32_t)u) -
-                     chunk_start.begin()) - 1;
-  };
+  // items (row, head) are contiguous unit ranges in unit order (head-major,
+  // rows by their offset), so one forward sweep finds every item's chunks
   std::vector<int32_t> row_head_count(std::max<int64_t>(B * H, 1), 0), rh_chunk0(std::max<int64_t>(B * H, 1), 0);
   int max_slots = 1;
-  for (int r = 0; r < B; ++r) {
-    const int64_t np = row_priv_np[r];
-    for (int64_t h = 0; h < H; ++h) {
-      int pieces = 0;
-      if (np > 0) {
-        const int64_t a0 = h * NPT + row_unit_off[r], b0 = a0 + np;
-        const int64_t c0 = chunk_of(a0);
-        rh_chunk0[r * H + h] = (int32_t)c0;
-        pieces = (int)(chunk_of(b0 - 1) - c0 + 1);
+  {
+    std::vector<int> rows_by_off(B);
+    for (int r = 0; r < B; ++r) rows_by_off[r] = r;
+    std::sort(rows_by_off.begin(), rows_by_off.end(),
+              [&](int x, int y) { return row_unit_off[x] < row_unit_off[y]; });
+    int64_t c = 0;  // chunk holding the current unit
+    for (int64_t h = 0; h < H; ++h)
+      for (int r : rows_by_off) {
+        const int64_t np = row_priv_np[r];
+        int pieces = 0;
+        if (np > 0) {
+          const int64_t a0 = h * NPT + row_unit_off[r], b0 = a0 + np;
+          while (chunk_start[c + 1] <= a0) ++c;
+          const int64_t c0 = c;
+          while (chunk_start[c + 1] <= b0 - 1) ++c;
+          rh_chunk0[r * H + h] = (int32_t)c0;
+          pieces = (int)(c - c0 + 1);
+        }
+        const int cnt = row_head_base[r * H + h] + pieces;
+        row_head_count[r * H + h] = cnt;
+        max_slots = std::max(max_slots, cnt);
       }
-      const int cnt = row_head_base[r * H + h] + pieces;
-      row_head_count[r * H + h] = cnt;
-      max_slots = std::max(max_slots, cnt);
-    }
   }
+  PT(T6);
   // synthetic keys: (leaf uid, leaf tokens at plan time + rank << 40)
   std::vector<int64_t> row_uid(B), row_pos(B);
   p->plan_leaves.assign(leaves, leaves + B);
@@ -808,11 +863,17 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     info->num_mma_items = num_mma;
   }
   p->committed = false;
+  if (plan_timing) {
+    PT(T7);
+    fprintf(stderr, "fk plan us: walk %.0f shared %.0f tc %.0f slots %.0f priv %.0f sched %.0f keys %.0f\n",
+            pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4], pt[6] - pt[5], pt[7] - pt[6]);
+  }
   if (!p->on_device) {
     p->have_plan = true;
     return FK_OK;
   }
 
+  PT(T7);
   // ---- upload ---------------------------------------------------------------
   FK_CUDA(cudaSetDevice(p->desc.device));
   int rc = ensure_scratch(p, B, max_slots);
@@ -1023,11 +1084,97 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (nlayers < 0 || layer0 < 0 || layer0 + nlayers > p->desc.num_layers)
     return fail(FK_INVALID_ARGUMENT, "bad layer range [%d, %d)", layer0, layer0 + nlayers);
-  for (int32_t i = 0; i < nlayers; ++i) {
-    const int rc = fk_attn_decode(p, layer0 + i, (const char*)q + i * q_layer_stride, (char*)out + i * out_layer_stride,
-                                  out_f32 ? (float*)((char*)out_f32 + i * f32_layer_stride) : nullptr, stream);
-    if (rc != FK_OK) return rc;
+  auto run = [&]() -> int {
+    for (int32_t i = 0; i < nlayers; ++i) {
+      const int rc = fk_attn_decode(p, layer0 + i, (const char*)q + i * q_layer_stride,
+                                    (char*)out + i * out_layer_stride,
+                                    out_f32 ? (float*)((char*)out_f32 + i * f32_layer_stride) : nullptr, stream);
+      if (rc != FK_OK) return rc;
+    }
+    return FK_OK;
+  };
+  if (!p->use_graph || !p->on_device) return run();
+  static const bool timing = getenv("FK_DEBUG_TIMING") != nullptr;
+  auto now_us = []() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = timing ? now_us() : 0.0;
+  // 1. record the launches (same code path: tickets and partial halves advance)
+  std::vector<fk::LaunchRec> recs;
+  fk::g_launch_rec = &recs;
+  const int rc = run();
+  fk::g_launch_rec = nullptr;
+  if (rc != FK_OK) return rc;
+  if (recs.empty()) return FK_OK;
+  for (auto& r : recs) r.finalize();
+  cudaStream_t st = (cudaStream_t)stream;
+  GraphCache& G = p->graphs[std::make_tuple(layer0, nlayers, st)];
+  bool same = G.exec && G.stream == st && G.shape.size() == recs.size();
+  for (size_t i = 0; same && i < recs.size(); ++i) {
+    const fk::LaunchRec &a = G.shape[i], &b = recs[i];
+    same = a.func == b.func && a.grid.x == b.grid.x && a.grid.y == b.grid.y && a.block.x == b.block.x &&
+           a.smem == b.smem && a.pdl == b.pdl && a.offs == b.offs;
   }
+  const double t1 = timing ? now_us() : 0.0;
+  if (same) {
+    // 2a. known structure: new arguments into the instantiated graph
+    for (size_t i = 0; i < recs.size(); ++i) {
+      cudaKernelNodeParams kp = {};
+      kp.func = const_cast<void*>(recs[i].func);
+      kp.gridDim = recs[i].grid;
+      kp.blockDim = recs[i].block;
+      kp.sharedMemBytes = (unsigned)recs[i].smem;
+      kp.kernelParams = recs[i].args.data();
+      FK_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nodes[i], &kp));
+    }
+  } else {
+    // 2b. new structure: capture the launches (PDL attributes become
+    // programmatic edges) and instantiate
+    G.reset();
+    FK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    for (auto& r : recs) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = r.grid;
+      cfg.blockDim = r.block;
+      cfg.dynamicSmemBytes = r.smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = r.pdl ? 1 : 0;
+      cudaError_t e = cudaLaunchKernelExC(&cfg, r.func, r.args.data());
+      cudaStreamCaptureStatus cs;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd);
+      if (e != cudaSuccess || nd != 1) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return fail(FK_CUDA_ERROR, "graph capture: %s (%zu dependencies)", cudaGetErrorString(e), nd);
+      }
+      G.nodes.push_back(deps[0]);
+    }
+    FK_CUDA(cudaStreamEndCapture(st, &G.graph));
+    FK_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));
+    G.stream = st;
+    G.shape.resize(recs.size());
+    for (size_t i = 0; i < recs.size(); ++i) {
+      G.shape[i].func = recs[i].func;
+      G.shape[i].grid = recs[i].grid;
+      G.shape[i].block = recs[i].block;
+      G.shape[i].smem = recs[i].smem;
+      G.shape[i].pdl = recs[i].pdl;
+      G.shape[i].offs = recs[i].offs;
+    }
+  }
+  const double t2 = timing ? now_us() : 0.0;
+  FK_CUDA(cudaGraphLaunch(G.exec, st));
+  if (timing)
+    fprintf(stderr, "fk graph: %zu launches, record %.1f us, %s %.1f us, launch %.1f us\n", recs.size(), t1 - t0,
+            same ? "update" : "capture", t2 - t1, now_us() - t2);
   return FK_OK;
 }
 
