@@ -1093,7 +1093,8 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
     }
     return FK_OK;
   };
-  if (!p->use_graph || !p->on_device) return run();
+  // (the legacy default stream cannot be captured: direct launches there)
+  if (!p->use_graph || !p->on_device || stream == nullptr) return run();
   static const bool timing = getenv("FK_DEBUG_TIMING") != nullptr;
   auto now_us = []() {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
