@@ -110,12 +110,15 @@ enum {
                                  schedule, 1..32 (default 2): the granularity of its tail */
   FK_OPT_PRIV_STATIC_FIRST = 9, /* 1 (default): the private warps that start at once take their
                                  first chunk by warp index instead of a ticket */
-  FK_OPT_TC_MIN_CHUNK = 10,   /* smallest chunk (128-token tiles) of the tcgen05 prefix kernel's
-                                 guided dynamic schedule, 1..24 (default 24: a chunk end costs ~3 us) */
+  FK_OPT_TC_MIN_CHUNK = 10,   /* chunk size (128-token tiles) of the tcgen05 prefix kernel's dynamic
+                                 tail, 1..24 (default 4) */
   FK_OPT_PRIV_WARPS = 11,     /* private CTA shape: 8 warps x 3 stages (default), 6 x 4, 7 x 4 or 12 x 2 */
-  FK_OPT_GRAPH = 12           /* 1 (default): fk_attn_decode_layers replays its launches as a CUDA
+  FK_OPT_GRAPH = 12,          /* 1 (default): fk_attn_decode_layers replays its launches as a CUDA
                                  graph (captured once per launch structure, parameters updated in
                                  place afterwards); 0: direct launches */
+  FK_OPT_TC_DYN_PCT = 13,     /* share (%) of the prefix tiles the tcgen05 CTAs take dynamically after
+                                 their cost-balanced static ranges (default 0: measured, an epilogue per chunk costs more than the balance gains) */
+  FK_OPT_TC_BOUNDARY_COST = 14 /* static split: tiles a piece start mid-range costs a CTA (default 4) */
 };
 
 /* ---- context forest ------------------------------------------------------ */

@@ -37,6 +37,8 @@ FK_OPT_PRIV_STATIC_FIRST = 9
 FK_OPT_TC_MIN_CHUNK = 10
 FK_OPT_PRIV_WARPS = 11
 FK_OPT_GRAPH = 12
+FK_OPT_TC_DYN_PCT = 13
+FK_OPT_TC_BOUNDARY_COST = 14
 
 
 class PoolDesc(ctypes.Structure):

@@ -40,15 +40,17 @@ struct PlanDev {
   const int* it_units;     // 128-token tiles of the item
   const int* qrows;        // request rows
   const int* qslot;        // slot of piece 0 for each (item, query)
-  // tcgen05 dynamic schedule: chunks of consecutive tiles of one item, in
-  // unit order with guided (shrinking) sizes; CTA b starts on chunk b, then
-  // takes chunk = tc_ctas + ticket (ArenaDev::ticket_tc - tc_ticket_base).
+  // tcgen05 schedule: chunks of consecutive tiles of one item, in unit
+  // order; CTA b streams its static chunks, then takes dynamic ones by ticket
+  // (ArenaDev::ticket_tc - tc_ticket_base).
   int tc_units, tc_ctas, tc_nchunks;
   unsigned long long tc_ticket_base;
   const int* tc_chunk_item;       // [tc_nchunks]
   const int* tc_chunk_tile0;      // [tc_nchunks] first tile within the item
   const int* tc_chunk_tile1;      // [tc_nchunks] end tile (exclusive)
   const int* it_first_chunk;      // per item: its first chunk (piece 0)
+  const int* tc_cta_chunk0;       // [tc_ctas + 1]: CTA b's static chunks are [chunk0[b], chunk0[b + 1])
+  int tc_static_chunks;           // dynamic chunk = tc_static_chunks + ticket
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;

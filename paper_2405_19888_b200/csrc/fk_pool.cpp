@@ -115,7 +115,9 @@ struct fk_pool {
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
   int64_t priv_wpc = kPrivWarpsPerCta;  // private CTA shape (warps; stages follow)
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
-  int64_t tc_min_chunk = 24;  // smallest tcgen05 chunk (tiles); measured: every chunk end costs ~3 us of epilogue, so coarse wins
+  int64_t tc_min_chunk = 4;      // tcgen05 dynamic-tail chunk (tiles)
+  int64_t tc_dyn_pct = 0;        // share of the prefix tiles left to the dynamic tail (measured: 0 best)
+  int64_t tc_boundary_cost = 4;  // tiles a piece start mid-range costs a tcgen05 CTA (static split)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t use_graph = 1;  // fk_attn_decode_layers replays a CUDA graph
   std::map<std::tuple<int32_t, int32_t, cudaStream_t>, GraphCache> graphs;  // per (layer0, nlayers, stream)
@@ -386,6 +388,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
       p->priv_wpc = value;
       break;
     case FK_OPT_TC_MIN_CHUNK: p->tc_min_chunk = std::min<int64_t>(kTcMaxChunk, std::max<int64_t>(1, value)); break;
+    case FK_OPT_TC_DYN_PCT: p->tc_dyn_pct = std::min<int64_t>(100, std::max<int64_t>(0, value)); break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
@@ -660,40 +663,93 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     const double wv = (double)priv_tok_heads;
     tc_target = std::min<int64_t>(p->num_sms - 1, std::max<int64_t>(1, std::llround(p->num_sms * wp / (wp + wv))));
   }
-  // Dynamic tcgen05 schedule: the tile units are cut into chunks that never
-  // cross an item, guided sizes (about remaining / (2 X) tiles, shrinking to
-  // tc_min_chunk), so the X persistent CTAs -- CTA b starts on chunk b, then
-  // takes tickets -- finish together whatever their per-SM bandwidth.  Each
-  // chunk is one piece (one partial slot per query row).
-  std::vector<int32_t> ch_item, ch_t0, ch_t1;
+  // tcgen05 schedule, static + dynamic: the first (100 - tc_dyn_pct)% of the
+  // tile units are split into one cost-balanced range per CTA (a piece start
+  // mid-range costs tc_boundary_cost tiles), the rest into small chunks the
+  // CTAs that finish first take from a ticket counter, so per-SM speed
+  // differences even out without paying an epilogue per small chunk
+  // everywhere.  Chunks never cross an item and are listed in unit order (an
+  // item's chunks are contiguous: chunk - it_first_chunk = piece index).
+  std::vector<int32_t> ch_item, ch_t0, ch_t1, cta_chunk0;
   std::vector<int32_t> it_first_chunk(items.size(), 0);
-  int64_t tc_ctas = 0;
+  int64_t tc_ctas = 0, n_static = 0;
   if (tc_units > 0) {
     // at least ~4 tiles per CTA unless FK_OPT_PREFIX_TARGET_CTAS says
     // otherwise: a CTA's start-up (TMEM, barriers, first loads) costs about that
     const int64_t cap = p->prefix_target_ctas > 0 ? tc_units : (tc_units + 3) / 4;
     const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, cap));
-    int64_t rest = tc_units;
-    for (size_t i = num_mma; i < items.size(); ++i) {
-      it_first_chunk[i] = (int32_t)ch_item.size();
-      int tile = 0;
-      while (tile < items[i].units) {
-        int64_t sz = (rest + 2 * X - 1) / (2 * X);
-        sz = std::min<int64_t>(std::max<int64_t>(sz, p->tc_min_chunk), kTcMaxChunk);
-        sz = std::min<int64_t>(sz, items[i].units - tile);
+    const int64_t u_dyn = std::min<int64_t>(tc_units - X, tc_units * p->tc_dyn_pct / 100);
+    const int64_t u_s = tc_units - std::max<int64_t>(0, u_dyn);
+    // item of each unit boundary
+    auto emit = [&](int64_t a, int64_t b) {  // chunks for units [a, b), split at items
+      size_t i = num_mma;
+      while (i + 1 < items.size() && it_unit_off[i + 1] <= a) ++i;
+      while (a < b) {
+        const int64_t end = std::min<int64_t>(b, it_unit_off[i] + items[i].units);
         ch_item.push_back((int32_t)i);
-        ch_t0.push_back(tile);
-        ch_t1.push_back((int32_t)(tile + sz));
-        tile += (int)sz;
-        rest -= sz;
+        ch_t0.push_back((int32_t)(a - it_unit_off[i]));
+        ch_t1.push_back((int32_t)(end - it_unit_off[i]));
+        a = end;
+        ++i;
+      }
+    };
+    // cost-balanced static ranges over [0, u_s)
+    const double bc = (double)p->tc_boundary_cost;
+    int64_t n_bound = 0;  // item starts strictly inside (0, u_s)
+    for (size_t i = num_mma + 1; i < items.size(); ++i) n_bound += it_unit_off[i] < u_s;
+    double rest = (double)u_s + bc * (double)n_bound;
+    std::vector<int64_t> cut{0};
+    double cost = 0.0;
+    size_t nxt_item = num_mma + 1;
+    for (int64_t u = 0; u < u_s;) {
+      const int64_t b = (int64_t)cut.size() - 1;  // current CTA
+      const double target = rest / (double)std::max<int64_t>(1, X - b);
+      const int64_t item_end = nxt_item < items.size() ? std::min<int64_t>(u_s, it_unit_off[nxt_item]) : u_s;
+      const bool last = (int64_t)cut.size() == X;
+      int64_t take = last ? item_end - u
+                          : std::min<int64_t>(item_end - u, std::max<int64_t>(1, std::llround(target - cost)));
+      u += take;
+      cost += (double)take;
+      if (u == item_end && nxt_item < items.size() && it_unit_off[nxt_item] == u && u < u_s) {
+        ++nxt_item;
+        if (!last && target - cost < 0.5) {  // close the CTA at the item boundary
+          rest -= cost + bc;
+          cut.push_back(u);
+          cost = 0.0;
+        } else {
+          cost += bc;  // this CTA starts another piece
+        }
+      } else if (!last && u < u_s && target - cost < 0.5) {
+        rest -= cost;
+        cut.push_back(u);
+        cost = 0.0;
       }
     }
-    tc_ctas = std::min<int64_t>(X, (int64_t)ch_item.size());
+    cut.push_back(u_s);
+    tc_ctas = (int64_t)cut.size() - 1;
+    for (int64_t b = 0; b < tc_ctas; ++b) {
+      cta_chunk0.push_back((int32_t)ch_item.size());
+      emit(cut[b], cut[b + 1]);
+    }
+    n_static = (int64_t)ch_item.size();
+    cta_chunk0.push_back((int32_t)n_static);
+    // dynamic tail: small chunks within items
+    for (int64_t u = u_s; u < tc_units;) {
+      size_t i = num_mma;
+      while (i + 1 < items.size() && it_unit_off[i + 1] <= u) ++i;
+      const int64_t end = std::min<int64_t>(u + p->tc_min_chunk, it_unit_off[i] + items[i].units);
+      emit(u, end);
+      u = end;
+    }
+    for (size_t i = num_mma, k = 0; i < items.size(); ++i) {
+      while (k < ch_item.size() && ch_item[k] != (int32_t)i) ++k;
+      it_first_chunk[i] = (int32_t)k;
+    }
   }
   const int64_t tc_nchunks = (int64_t)ch_item.size();
   if (getenv("FK_DEBUG_PLAN")) {
-    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs, %lld chunks:", (long long)tc_units, (long long)tc_ctas,
-            (long long)tc_nchunks);
+    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs, %lld chunks (%lld static):", (long long)tc_units,
+            (long long)tc_ctas, (long long)tc_nchunks, (long long)n_static);
     for (size_t k = 0; k < ch_item.size(); ++k) fprintf(stderr, " %d:%d-%d", ch_item[k], ch_t0[k], ch_t1[k]);
     fprintf(stderr, "\n");
   }
@@ -901,6 +957,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_ch0 = L.add(nchb);
   const size_t o_ch1 = L.add(nchb);
   const size_t o_ifc = L.add(sizeof(int32_t) * ni);
+  const size_t o_cc0 = L.add(sizeof(int32_t) * std::max<size_t>(cta_chunk0.size(), 1));
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
     FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
@@ -956,6 +1013,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   put(o_ch0, ch_t0.data(), ch_t0.size() * 4);
   put(o_ch1, ch_t1.data(), ch_t1.size() * 4);
   put(o_ifc, it_first_chunk.data(), it_first_chunk.size() * 4);
+  put(o_cc0, cta_chunk0.data(), cta_chunk0.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -984,6 +1042,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.tc_chunk_tile0 = (const int32_t*)(d + o_ch0);
   pd.tc_chunk_tile1 = (const int32_t*)(d + o_ch1);
   pd.it_first_chunk = (const int32_t*)(d + o_ifc);
+  pd.tc_cta_chunk0 = (const int32_t*)(d + o_cc0);
+  pd.tc_static_chunks = (int)n_static;
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
@@ -1040,10 +1100,11 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
   // K2 (shared prefixes) and K3 (private streams) only write partials, so
   // their order is free; K4 merges every (row, head) afterwards.
-  // a tcgen05 launch consumes exactly tc_nchunks tickets (fk_prefix_tc_kernel)
+  // tickets a tcgen05 launch consumes (fk_prefix_tc_kernel): every dynamic
+  // chunk once, plus one failing ticket per CTA
   if (has_tc) {
     p->plan.tc_ticket_base = p->ticket_tc_base;
-    p->ticket_tc_base += (unsigned long long)p->plan.tc_nchunks;
+    p->ticket_tc_base += (unsigned long long)(p->plan.tc_nchunks - p->plan.tc_static_chunks + p->plan.tc_ctas);
   }
   auto run_prefix = [&](bool pdl_tc, bool after_private) -> int {
     if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));

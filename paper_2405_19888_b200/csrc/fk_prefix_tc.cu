@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   pdl_launch_dependents();  // the private grid may start on the SMs we leave free
   // Launched behind the private grid (launch order 1), this grid's completion
   // must imply that grid's: thread 0 waits for it on exit.
-  if ((int)blockIdx.x >= nch) {
+  if ((int)blockIdx.x >= p.tc_ctas || p.tc_cta_chunk0[blockIdx.x] == p.tc_cta_chunk0[blockIdx.x + 1]) {
     if (after_private && threadIdx.x == 0) pdl_wait_primary();
     return;
   }
@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    // Dynamic chunks: the CTA's first chunk is its index, every later one a
-    // ticket (chunk = grid + ticket); lane 0 posts each chunk id in the queue
+    // Chunks: the CTA's static range first, then tickets (chunk =
+    // tc_static_chunks + ticket); lane 0 posts each chunk id in the queue
     // one chunk ahead of streaming it.  Page ids are prefetched lane-parallel
     // into a 2 x 32-entry register window; the next chunk's item metadata and
     // first window are fetched over the following two tiles, so a chunk
@@ -165,10 +165,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       prefetch_tmap(&tmap);
       prefetch_tmap(&tmap_run);
     }
+    // static chunks first, then tickets (a CTA stops after its first failing one)
+    int sidx = p.tc_cta_chunk0[blockIdx.x];
+    const int send = p.tc_cta_chunk0[blockIdx.x + 1];
     auto grab = [&]() -> int {
+      if (sidx < send) return sidx++;
       int c = 0;
       if (lane == 0) {
-        c = (int)gridDim.x + (int)(atomicAdd(a.ticket_tc, 1ull) - p.tc_ticket_base);
+        c = p.tc_static_chunks + (int)(atomicAdd(a.ticket_tc, 1ull) - p.tc_ticket_base);
         if (c >= nch) c = -1;
       }
       return __shfl_sync(0xffffffffu, c, 0);
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     };
     TcCursor c;
     c.qi = 0;
-    tc_load_chunk(p, c, (int)blockIdx.x);
+    tc_load_chunk(p, c, grab());  // every CTA has at least one static chunk
     post(0, c.chunk);
     int nxt = grab();  // the chunk after the current one, posted right away
     post(1, nxt);
