@@ -418,6 +418,7 @@ def test_prefix_chunk_queue_wraps(cuda_device, min_chunk):
     several heads and both query-block layouts interleave per CTA."""
     eng = make_engine(cuda_device, H=6, L=1)
     eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4)
+    eng.set_option(_lib.FK_OPT_TC_DYN_PCT, 60)  # most tiles through the dynamic tail
     eng.set_option(_lib.FK_OPT_TC_MIN_CHUNK, min_chunk)
     fork_group(eng, 2300, [9] * 70, out_len=2, tag="a", seed=1)   # 70 rows: 32-lane layout
     fork_group(eng, 1100, [4] * 20, out_len=2, tag="b", seed=2)   # 20 rows: 16-lane layout
@@ -433,4 +434,17 @@ def test_private_ring_shapes(cuda_device, warps):
     eng.set_option(_lib.FK_OPT_PRIV_WARPS, warps)
     fork_group(eng, 400, [33, 100, 7, 260], out_len=3)
     run_steps(eng, 3)
+    check_history(eng)
+
+
+@pytest.mark.parametrize("dyn", [0, 100])
+def test_prefix_static_and_dynamic_schedules(cuda_device, dyn):
+    """FK_OPT_TC_DYN_PCT 0: only cost-balanced static ranges; 100: every
+    tcgen05 tile through ticketed 4-tile chunks (no static range beyond the
+    first chunk per CTA)."""
+    eng = make_engine(cuda_device, H=8, L=2)
+    eng.set_option(_lib.FK_OPT_TC_DYN_PCT, dyn)
+    fork_group(eng, 3000, [40] * 50, out_len=2, tag="a", seed=4)
+    fork_group(eng, 900, [5, 77, 130], out_len=2, tag="b", seed=5)
+    run_steps(eng, 2)
     check_history(eng)
