@@ -222,6 +222,12 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
   const int H = a.num_heads;
   const int ns = partial_count(p, H, row, head);
   const long long base = part_index(p, H, row, 0, head);  // slot stride is H
+  constexpr int kMergeEarly = 8;
+  float4 v0[kMergeEarly];
+#pragma unroll
+  for (int k = 0; k < kMergeEarly; ++k)
+    v0[k] = k < ns ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)k * H) * kHeadDim) + lane)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
   float2 ml[kMergeRounds];
   float M = -INFINITY;
 #pragma unroll
@@ -243,7 +249,17 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
   for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const int nsm = min(ns, 32 * kMergeRounds);
-  for (int k0 = 0; k0 < nsm; k0 += 8) {
+  // (the first kMergeEarly partials' o were loaded together with the (m, l)
+  // round above: one memory round trip for the common case)
+#pragma unroll
+  for (int k = 0; k < kMergeEarly; ++k) {
+    const float wk = __shfl_sync(0xffffffffu, w[0], k);
+    acc.x = fmaf(v0[k].x, wk, acc.x);
+    acc.y = fmaf(v0[k].y, wk, acc.y);
+    acc.z = fmaf(v0[k].z, wk, acc.z);
+    acc.w = fmaf(v0[k].w, wk, acc.w);
+  }
+  for (int k0 = kMergeEarly; k0 < nsm; k0 += 8) {
     float4 v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k)
