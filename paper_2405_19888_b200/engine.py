@@ -674,9 +674,7 @@ class GpuEngine:
                     "d2h": torch.cuda.Stream(self._dev),
                     "ev_q": [torch.cuda.Event() for _ in range(L)],
                     "ev_o": [torch.cuda.Event() for _ in range(L)],
-                    # copy granularity: layer chunks of 1, 1, 2, 4, 8, 8, ... so
-                    # layer 0 waits for one layer's rows and the host issues few
-                    # copies and events per step
+                    # copy granularity: layer chunks (see _layer_chunks)
                     "chunks": self._layer_chunks(L),
                     "ev_kv": torch.cuda.Event(),
                     "ev_d2h": torch.cuda.Event(),
@@ -687,12 +685,26 @@ class GpuEngine:
 
     @staticmethod
     def _layer_chunks(L: int) -> List[Tuple[int, int]]:
-        out, a, n = [], 0, 1
-        while a < L:
-            b = min(L, a + n)
-            out.append((a, b))
-            a = b
-            n = min(8, 2 * n) if len(out) > 1 else 1
+        """Copy chunks of the e2e path: 1 and 3 layers first (layer 0 waits
+        for one layer's rows), 8 in the middle, 4-layer chunks at the end (the
+        step ends with the last chunk's output copy).  Each chunk boundary is
+        an event wait in the stream, which breaks the PDL chain between layers,
+        so the middle chunks stay large."""
+        sizes, rest = [], L
+        for n in (1, 3):
+            if rest > 0:
+                sizes.append(min(n, rest))
+                rest -= sizes[-1]
+        while rest > 8:
+            sizes.append(8)
+            rest -= 8
+        while rest > 0:
+            sizes.append(min(4, rest))
+            rest -= sizes[-1]
+        out, a = [], 0
+        for n in sizes:
+            out.append((a, a + n))
+            a += n
         return out
 
     def _decode_attention_host(self, running: List[GenerationTask]) -> None:
