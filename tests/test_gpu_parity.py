@@ -448,3 +448,43 @@ def test_prefix_static_and_dynamic_schedules(cuda_device, dyn):
     fork_group(eng, 900, [5, 77, 130], out_len=2, tag="b", seed=5)
     run_steps(eng, 2)
     check_history(eng)
+
+
+def test_model_style_layer_chain_with_pdl(cuda_device):
+    """A model-style chain: layer l+1's queries are computed by a torch kernel
+    from layer l's attention output, right before fk_attn_decode(l + 1).
+    With the engine's cross-layer PDL (level 2) the outputs are bit-identical
+    to plain stream order (level 0): the prefix kernel reads q only after
+    griddepcontrol.wait."""
+    import ctypes
+
+    import torch
+
+    L, H = 4, 8
+    outs = {}
+    for pdl in (0, 2):
+        eng = make_engine(cuda_device, H=H, L=L)
+        eng.set_option(_lib.FK_OPT_PDL, pdl)
+        fork_group(eng, 900, [30, 64, 5, 100], out_len=2)
+        from paper_2405_19888_b200.workloads import drain_fills
+        drain_fills(eng)
+        running = [g for g in eng.gens.values() if g.started and not g.done]
+        eng._plan(running)
+        rows = len(running)
+        dev = torch.device("cuda", cuda_device)
+        g = torch.Generator().manual_seed(3)
+        q0 = torch.randn((rows, H, 128), generator=g).to(torch.bfloat16).to(dev)
+        res = []
+        with torch.cuda.stream(eng.stream):
+            q = q0
+            for layer in range(L):
+                out = torch.empty_like(q)
+                _lib.check(_lib.lib.fk_attn_decode(eng._pool.handle, layer, ctypes.c_void_p(q.data_ptr()),
+                                                   ctypes.c_void_p(out.data_ptr()), None, eng._sp()))
+                res.append(out)
+                q = (out.float() * 8.0 + q.float()).to(torch.bfloat16)  # the "rest of the layer"
+        eng.stream.synchronize()
+        outs[pdl] = [r.cpu() for r in res]
+        eng.close()
+    for a, b in zip(outs[0], outs[2]):
+        assert torch.equal(a, b)
