@@ -95,6 +95,17 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // Launch with optional programmatic dependent launch (PDL): the kernel may
 // start while its stream predecessor is still running; it must call
 // pdl_wait_primary() before touching the predecessor's results.
+// cudaFuncSetAttribute is per device: remember which devices a kernel's
+// dynamic shared-memory opt-in was set on (engines may share a process).
+inline bool attr_set_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return true;
+  mask |= bit;
+  return false;
+}
+
 template <typename T>
 inline void rec_push_arg(LaunchRec& r, const T& v) {
   const size_t al = alignof(T) < 16 ? alignof(T) : 16;

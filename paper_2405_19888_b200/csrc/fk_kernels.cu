@@ -659,13 +659,12 @@ template <int STAGES, int WARPS>
 static cudaError_t launch_private_shape(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
                                        float scale_log2, const CUtensorMap* tmap, unsigned long long ticket_base,
                                        bool pdl, cudaStream_t s) {
-  static bool attr = false;
+  static unsigned long long attr_devices = 0;
   constexpr int smem = priv_smem<STAGES, WARPS>();
-  if (!attr) {
+  if (!attr_set_on_device(attr_devices)) {
     cudaError_t e = cudaFuncSetAttribute(fk_private_kernel<STAGES, WARPS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int grid = p.priv_warps / WARPS;
   return launch_k(fk_private_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, pdl, a, p, layer,
@@ -693,11 +692,10 @@ cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* 
 
 cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
                               const CUtensorMap* tmap, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devices = 0;
+  if (!attr_set_on_device(attr_devices)) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   return launch_k(fk_prefix_mma_kernel, dim3(p.tc_begin), dim3(kPmThreads), kPmSmem, s, false, a, p, layer,
                   (const __nv_bfloat16*)q, scale_log2, *tmap);

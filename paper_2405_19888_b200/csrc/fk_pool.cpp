@@ -906,6 +906,12 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     }
   }
 
+  // the work-list invariant: the KV tokens the kernels stream
+  // per layer -- shared contexts once, private contexts per row -- are exactly
+  // Engine._batch_tokens(running) (engine.py:470-484)
+  if (shared_tokens + private_tokens != batch_tokens)
+    return fail(FK_INVALID_ARGUMENT, "work-list invariant violated: %lld shared + %lld private != %lld batch tokens",
+                (long long)shared_tokens, (long long)private_tokens, (long long)batch_tokens);
   const int n_items = (int)items.size();
   if (info) {
     info->batch_tokens = batch_tokens;

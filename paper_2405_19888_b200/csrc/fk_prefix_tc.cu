@@ -645,8 +645,8 @@ extern "C" int fk_debug_timeline(unsigned long long* out, int n) {
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
                              const CUtensorMap* tmap, const CUtensorMap* tmap_run, bool pdl, bool after_private,
                              cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devices = 0;
+  if (!attr_set_on_device(attr_devices)) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
     if (e != cudaSuccess) {
       cudaFuncAttributes fa;
@@ -658,7 +658,6 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, con
               cudaGetErrorString(e), fa.sharedSizeBytes, kTcSmem, optin, fa.numRegs, fa.localSizeBytes);
       return e;
     }
-    attr = true;
   }
   if (p.tc_ctas == 0) return cudaSuccess;
   cudaError_t e = launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, p, layer,
