@@ -1,10 +1,12 @@
-"""bench.py's JSON contract, checked on the CPU through the reference arm
-(the numpy oracle port; no GPU needed)."""
+"""bench.py's JSON contract: the reference arm on the CPU (the numpy oracle
+port), our arm on a GPU (roofline, launches, e2e and clock keys)."""
 
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -24,3 +26,21 @@ def test_reference_arm_line():
     assert d["config"]["workload"] == "llama7b_p6000_b64"
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+@pytest.mark.gpu
+def test_ours_arm_line():
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--config", "llama7b_p6000_b64", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0.3 < r["frac"] < 1.2
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["gpu_launches"] == 3 * (32 * 3 + 1)
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in d["clocks"] and d["n_gpus"] == 1 and d["scaling"] == "weak"
+    assert d["value"] > 1000
