@@ -68,6 +68,26 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Switches the calling thread to a pool's device and restores the caller's
+// device on scope exit, so engines on several GPUs can share a process
+// without moving each other's (or torch's) current device.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+#define FK_ON_DEVICE(dev)                                                                   \
+  DeviceGuard device_guard_(dev);                                                           \
+  if (device_guard_.err != cudaSuccess)                                                     \
+    return fail(FK_CUDA_ERROR, "cudaSetDevice(%d): %s", (int)(dev), cudaGetErrorString(device_guard_.err))
+
 }  // namespace
 
 // A step's attention launches as one CUDA graph: captured the first time a
@@ -196,7 +216,7 @@ int encode_tmap(fk_pool* p) {
 int reserve_pages(fk_pool* p, int64_t pages) {
   if (pages <= p->num_pages) return FK_OK;
   if (!p->on_device) return FK_OK;
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   const size_t D = p->desc.head_dim;
   const size_t planes = (size_t)p->desc.num_layers * 2 * p->desc.num_heads;
   const size_t new_bytes = planes * (size_t)pages * kPage * D * 2;
@@ -299,10 +319,10 @@ int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
   p->total_blocks = desc->total_blocks;
   p->on_device = desc->device >= 0;
   if (p->on_device) {
-    cudaError_t e = cudaSetDevice(desc->device);
-    if (e != cudaSuccess) {
+    DeviceGuard dg(desc->device);
+    if (dg.err != cudaSuccess) {
       delete p;
-      return fail(FK_CUDA_ERROR, "cudaSetDevice(%d): %s", desc->device, cudaGetErrorString(e));
+      return fail(FK_CUDA_ERROR, "cudaSetDevice(%d): %s", desc->device, cudaGetErrorString(dg.err));
     }
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc->device) == cudaSuccess)
@@ -332,7 +352,7 @@ int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
 int fk_pool_destroy(fk_pool* p) {
   if (!p) return FK_OK;
   if (p->on_device) {
-    cudaSetDevice(p->desc.device);
+    DeviceGuard dg(p->desc.device);
     cudaDeviceSynchronize();
     for (auto& s : p->slots) {
       if (s.host) cudaFreeHost(s.host);
@@ -937,7 +957,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
 
   PT(T7);
   // ---- upload ---------------------------------------------------------------
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   int rc = ensure_scratch(p, B, max_slots);
   if (rc != FK_OK) return rc;
   const size_t ni = (size_t)std::max(n_items, 1);
@@ -1088,7 +1108,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (layer < 0 || layer >= p->desc.num_layers) return fail(FK_INVALID_ARGUMENT, "bad layer %d", layer);
   if (p->plan.num_rows == 0) return FK_OK;
   if (!q || !out) return fail(FK_INVALID_ARGUMENT, "null q/out");
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   cudaStream_t st = (cudaStream_t)stream;
   const float scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p->desc.head_dim));
   ArenaDev a = p->arena();
@@ -1292,7 +1312,7 @@ int fk_step_commit(fk_pool* p, const int64_t* positions, void* stream) {
   }
   p->committed = true;
   if (!p->on_device || B == 0) return FK_OK;
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   PlanSlot& slot = p->slots[p->cur];
   char* h = (char*)slot.host;
   const size_t nb = (size_t)std::max(B, 1);
@@ -1321,7 +1341,7 @@ int fk_append_kv_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void*
     return fail(FK_INVALID_ARGUMENT, "bad layer range [%d, %d)", layer0, layer0 + nlayers);
   if (p->plan.num_rows == 0) return FK_OK;
   if (!k || !v) return fail(FK_INVALID_ARGUMENT, "null k/v");
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   FK_CUDA(launch_append(p->arena(), p->plan, layer0, nlayers, k, v, (cudaStream_t)stream));
   return FK_OK;
 }
@@ -1337,7 +1357,7 @@ int fk_synth_fill(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, uint64_t 
     return fail(FK_INVALID_ARGUMENT, "bad range [%lld, %lld) of %lld", (long long)pos0,
                 (long long)pos1, (long long)c.tokens);
   if (pos1 == pos0) return FK_OK;
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t first = pos0 / kPage, last = (pos1 - 1) / kPage;
   const int n = (int)(last - first + 1);
@@ -1364,7 +1384,7 @@ int fk_fill_kv(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, int32_t laye
   if (pos1 == pos0) return FK_OK;
   if (!k || !v) return fail(FK_INVALID_ARGUMENT, "null k/v");
   if (pos1 - pos0 > INT32_MAX / p->desc.num_heads) return fail(FK_INVALID_ARGUMENT, "fill too large");
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t first = pos0 / kPage, last = (pos1 - 1) / kPage;
   const int n = (int)(last - first + 1);
@@ -1391,7 +1411,7 @@ int fk_ctx_copy_kv(fk_pool* dst, int64_t dst_ctx, const fk_pool* src, int64_t sr
     return fail(FK_INVALID_ARGUMENT, "copy of %lld tokens exceeds a context (%lld -> %lld)", (long long)ntok,
                 (long long)si->second.tokens, (long long)di->second.tokens);
   if (ntok == 0) return FK_OK;
-  FK_CUDA(cudaSetDevice(dst->desc.device));
+  FK_ON_DEVICE(dst->desc.device);
   if (src->desc.device != dst->desc.device) {
     int can = 0;
     FK_CUDA(cudaDeviceCanAccessPeer(&can, dst->desc.device, src->desc.device));
@@ -1421,7 +1441,7 @@ int fk_synth_queries(fk_pool* p, uint64_t seed, void* q_all, void* stream) {
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   if (p->plan.num_rows == 0) return FK_OK;
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   FK_CUDA(launch_synth_queries(p->arena(), p->plan, seed, q_all, (cudaStream_t)stream));
   return FK_OK;
 }
@@ -1431,7 +1451,7 @@ int fk_synth_append(fk_pool* p, uint64_t seed, float k_scale, void* stream) {
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (!p->committed) return fail(FK_INVALID_ARGUMENT, "fk_step_commit not called for this plan");
   if (p->plan.num_rows == 0) return FK_OK;
-  FK_CUDA(cudaSetDevice(p->desc.device));
+  FK_ON_DEVICE(p->desc.device);
   FK_CUDA(launch_synth_append(p->arena(), p->plan, seed, k_scale, (cudaStream_t)stream));
   return FK_OK;
 }
