@@ -78,6 +78,8 @@ typedef struct {
   int32_t max_slots;       /* partial slots per (row, head) incl. the private one */
   int32_t num_tc_items;    /* prefix items routed to the tcgen05 kernel */
   int32_t num_mma_items;   /* prefix items routed to the warp-level mma.sync kernel */
+  int32_t fused_merge;     /* 1: each (row, head) is merged by its last partial's writer
+                              (no merge kernel); see FK_OPT_FUSED_MERGE */
 } fk_plan_info;
 
 /* ---- pool ---------------------------------------------------------------- */
@@ -118,7 +120,12 @@ enum {
                                  place afterwards); 0: direct launches */
   FK_OPT_TC_DYN_PCT = 13,     /* share (%) of the prefix tiles the tcgen05 CTAs take dynamically after
                                  their cost-balanced static ranges (default 0: measured, an epilogue per chunk costs more than the balance gains) */
-  FK_OPT_TC_BOUNDARY_COST = 14 /* static split: tiles a piece start mid-range costs a CTA (default 4) */
+  FK_OPT_TC_BOUNDARY_COST = 14, /* static split: tiles a piece start mid-range costs a CTA (default 4) */
+  FK_OPT_FUSED_MERGE = 15     /* 1 (default): the writer of the last partial of a (row, head) merges
+                                 it -- private warps directly, tcgen05 pieces through a queue the
+                                 private warps drain -- and no merge kernel runs (when the plan has
+                                 tcgen05 and private work, no mma.sync items, launch order 0);
+                                 0: a merge kernel after every layer */
 };
 
 /* ---- context forest ------------------------------------------------------ */

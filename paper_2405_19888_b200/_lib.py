@@ -39,6 +39,7 @@ FK_OPT_PRIV_WARPS = 11
 FK_OPT_GRAPH = 12
 FK_OPT_TC_DYN_PCT = 13
 FK_OPT_TC_BOUNDARY_COST = 14
+FK_OPT_FUSED_MERGE = 15
 
 
 class PoolDesc(ctypes.Structure):
@@ -78,6 +79,7 @@ class PlanInfo(ctypes.Structure):
         ("max_slots", c_int32),
         ("num_tc_items", c_int32),
         ("num_mma_items", c_int32),
+        ("fused_merge", c_int32),
     ]
 
 

@@ -74,6 +74,20 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// same with an L2 cache policy (createpolicy: evict_first for streams read once)
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -310,6 +324,93 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
   const float4 r = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   *reinterpret_cast<uint2*>(out + oi) = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
   if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = r;
+}
+
+// ------------------------------------------------------------ fused merge
+// Every partial writer counts its arrival on (row, head); the writer of the
+// last partial merges.  A private warp merges at once (merge_row_head_warp);
+// a tcgen05 piece row that arrives last is queued instead (its softmax warps
+// are the prefix pipeline's critical path) and the private warps drain the
+// queue -- one entry per chunk switch while streaming, then all of it once
+// their tickets run dry.  The ArenaDev::mctl words return to zero by the end
+// of the launch: counters by their merger, entries by their claimer, the
+// queue words by the last private warp out.
+__device__ __forceinline__ unsigned* mctl_cnt(const ArenaDev& a) { return a.mctl + 4; }
+__device__ __forceinline__ unsigned* mctl_queue(const ArenaDev& a) { return a.mctl + 4 + a.mctl_rh; }
+
+__device__ __forceinline__ void fused_merge_rh(const ArenaDev& a, const PlanDev& p, int rh, int lane) {
+  __threadfence();  // acquire: every other partial of rh is visible (ld.cg reads)
+  merge_row_head_warp(a, p, rh / a.num_heads, rh % a.num_heads, a.out, a.out_f32, lane);
+  if (lane == 0) mctl_cnt(a)[rh] = 0u;
+}
+
+// a private warp wrote the partial of (row, head): count it, merge if last
+__device__ __forceinline__ void fused_arrive_warp(const ArenaDev& a, const PlanDev& p, int row, int head, int lane) {
+  __threadfence();  // release this warp's partial stores before the count
+  __syncwarp();
+  const int rh = row * a.num_heads + head;
+  int last = 0;
+  if (lane == 0) last = atomicAdd(mctl_cnt(a) + rh, 1u) + 1u == (unsigned)p.row_head_count[rh];
+  if (__shfl_sync(0xffffffffu, last, 0)) fused_merge_rh(a, p, rh, lane);
+}
+
+// claim one queued (row, head) -- never past the tail -- and merge it
+__device__ __forceinline__ bool fused_drain_one(const ArenaDev& a, const PlanDev& p, int lane) {
+  int rh = -1;
+  if (lane == 0) {
+    volatile unsigned* c = a.mctl;
+    unsigned h = c[0];
+    while (h < c[1]) {
+      const unsigned old = atomicCAS(a.mctl, h, h + 1u);
+      if (old == h) {
+        volatile unsigned* e = mctl_queue(a) + h;
+        unsigned v;
+        while ((v = *e) == 0u) {  // reserved, being written
+        }
+        *e = 0u;
+        rh = (int)v - 1;
+        break;
+      }
+      h = old;
+    }
+  }
+  rh = __shfl_sync(0xffffffffu, rh, 0);
+  if (rh < 0) return false;
+  fused_merge_rh(a, p, rh, lane);
+  return true;
+}
+
+// a private warp with no chunk left: merge queued rows until every tcgen05
+// piece row has reported and the queue is empty; the last warp out of the
+// grid zeroes the queue words for the launch after next
+__device__ __forceinline__ void fused_drain_all(const ArenaDev& a, const PlanDev& p, int lane, unsigned grid_warps) {
+  while (true) {
+    if (fused_drain_one(a, p, lane)) continue;
+    int fin = 0;
+    if (lane == 0) {
+      volatile unsigned* c = a.mctl;
+      if (c[2] == (unsigned)p.tc_rows_total) {
+        __threadfence();
+        fin = c[0] >= c[1];
+      }
+    }
+    if (__shfl_sync(0xffffffffu, fin, 0)) break;
+    __nanosleep(200);
+  }
+  if (lane == 0 && atomicAdd(a.mctl + 3, 1u) + 1u == grid_warps) {
+    volatile unsigned* c = a.mctl;
+    c[0] = c[1] = c[2] = c[3] = 0u;
+  }
+}
+
+// a tcgen05 piece row wrote its partial (o stores fenced before the CTA
+// barrier that precedes this): count it; queue the row if it was last
+__device__ __forceinline__ void fused_arrive_tc_row(const ArenaDev& a, const PlanDev& p, int rh) {
+  __threadfence();
+  if (atomicAdd(mctl_cnt(a) + rh, 1u) + 1u == (unsigned)p.row_head_count[rh]) {
+    const unsigned idx = atomicAdd(a.mctl + 1, 1u);
+    *(volatile unsigned*)(mctl_queue(a) + idx) = (unsigned)rh + 1u;
+  }
 }
 
 }  // namespace fk

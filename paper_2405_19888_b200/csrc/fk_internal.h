@@ -51,6 +51,8 @@ struct PlanDev {
   const int* it_first_chunk;      // per item: its first chunk (piece 0)
   const int* tc_cta_chunk0;       // [tc_ctas + 1]: CTA b's static chunks are [chunk0[b], chunk0[b + 1])
   int tc_static_chunks;           // dynamic chunk = tc_static_chunks + ticket
+  int tc_rows_total;              // sum over chunks of the item's query rows (fused merge: reports)
+  int fused;                      // fused merge on this launch (set per launch)
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;
@@ -92,6 +94,14 @@ struct ArenaDev {
   float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
   unsigned long long* ticket;     // private chunk ticket counter (never reset)
   unsigned long long* ticket_tc;  // tcgen05 prefix chunk ticket counter (never reset)
+  // fused merge (this launch's half): [0] orphan queue head, [1] tail, [2]
+  // tcgen05 piece rows reported, [3] private warps done; then mctl_rh arrival
+  // counters per (row, head), then mctl_rh queue entries (row * H + head + 1).
+  // Every word returns to 0 by the end of the launch.
+  unsigned* mctl;
+  int mctl_rh;
+  __nv_bfloat16* out;     // this launch's outputs (fused merge)
+  float* out_f32;
 };
 
 inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {
@@ -127,7 +137,7 @@ cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, co
                               float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
                              float scale_log2, const CUtensorMap* tmap, const CUtensorMap* tmap_run,
-                             bool pdl, bool after_private, cudaStream_t s);
+                             bool pdl, bool after_private, bool trig_late, cudaStream_t s);
 cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, int layer, bool pdl,
                          cudaStream_t s);
 cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers,

@@ -89,7 +89,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     return __shfl_sync(0xffffffffu, c, 0);
   };
   int ca = gw < p.priv_static ? gw : grab();
-  if (ca >= nch) return;
+  if (ca >= nch) {
+    if (p.fused) fused_drain_all(a, p, lane, gridDim.x * WARPS);
+    return;
+  }
 
   uint8_t* ring = smem + warp * STAGES * kPwStageBytes;
   if (lane == 0) {
@@ -129,10 +132,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     uint8_t* st = ring + s * kPwStageBytes;
     const int pk = (int)plane_index(layer, 0, m.head, H), pv = (int)plane_index(layer, 1, m.head, H);
     mbar_expect_tx(&full[warp][s], kPwStageBytes);
-    tma_load_3d(st, &tmap, 0, m.pg * kPage, pk, &full[warp][s]);
-    tma_load_3d(st + 2048, &tmap, 64, m.pg * kPage, pk, &full[warp][s]);
-    tma_load_3d(st + 4096, &tmap, 0, m.pg * kPage, pv, &full[warp][s]);
-    tma_load_3d(st + 6144, &tmap, 64, m.pg * kPage, pv, &full[warp][s]);
+    // every private page is read once per layer: evict-first keeps L2 for the
+    // partials and the prefix tiles
+    const uint64_t pol = l2_policy_evict_first();
+    tma_load_3d_hint(st, &tmap, 0, m.pg * kPage, pk, &full[warp][s], pol);
+    tma_load_3d_hint(st + 2048, &tmap, 64, m.pg * kPage, pk, &full[warp][s], pol);
+    tma_load_3d_hint(st + 4096, &tmap, 0, m.pg * kPage, pv, &full[warp][s], pol);
+    tma_load_3d_hint(st + 6144, &tmap, 64, m.pg * kPage, pv, &full[warp][s], pol);
   };
 
   int la = 0, lb = 0;
@@ -259,6 +265,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
         for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][0], o[nt][1]);
         if (t4 == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
+      if (p.fused) fused_arrive_warp(a, p, row, head, lane);
       m = -INFINITY;
       l = 0.f;
 #pragma unroll
@@ -280,9 +287,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
       cb = grab();
       mb = load_chunk(cb, lb);
       issue_ahead();
+      if (p.fused) fused_drain_one(a, p, lane);  // a queued prefix row, if any, under the loads in flight
     }
     cur = nxt;
   }
+  if (p.fused) fused_drain_all(a, p, lane, gridDim.x * WARPS);
   CTA_TL_END(fk_tl_cta_priv, layer);
 }
 

@@ -160,6 +160,10 @@ struct fk_pool {
   float2* part_ml = nullptr;
   size_t part_cap = 0;     // entries (rows*slots*H) per half
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
+  unsigned* mctl = nullptr;  // fused merge words, two halves of 4 + 2 * mctl_rh (ArenaDev::mctl)
+  size_t mctl_rh = 0;
+  int64_t fused_merge = 1;   // FK_OPT_FUSED_MERGE
+  bool plan_fused_ok = false;  // the current plan admits the fused merge
   unsigned long long* ticket = nullptr;  // device: private chunk tickets (never reset)
   unsigned long long ticket_base = 0;    // tickets consumed by earlier private launches
   unsigned long long ticket_tc_base = 0; // ... and by earlier tcgen05 prefix launches
@@ -174,6 +178,10 @@ struct fk_pool {
     a.part_ml = part_ml;
     a.ticket = ticket;
     a.ticket_tc = ticket ? ticket + 1 : nullptr;
+    a.mctl = mctl;
+    a.mctl_rh = (int)mctl_rh;
+    a.out = nullptr;
+    a.out_f32 = nullptr;
       return a;
   }
 };
@@ -265,6 +273,15 @@ int ensure_scratch(fk_pool* p, int rows, int slots) {
     FK_CUDA(cudaMalloc(&p->part_o, 2 * cap * D * sizeof(float)));
     FK_CUDA(cudaMalloc(&p->part_ml, 2 * cap * sizeof(float2)));
     p->part_cap = cap;
+  }
+  const size_t rh = (size_t)std::max(rows, 1) * H;
+  if (rh > p->mctl_rh) {
+    const size_t cap = std::max(rh + rh / 2, p->mctl_rh * 2);
+    if (p->mctl) FK_CUDA(cudaFree(p->mctl));
+    p->mctl = nullptr;
+    FK_CUDA(cudaMalloc(&p->mctl, 2 * (4 + 2 * cap) * sizeof(unsigned)));
+    FK_CUDA(cudaMemset(p->mctl, 0, 2 * (4 + 2 * cap) * sizeof(unsigned)));
+    p->mctl_rh = cap;
   }
   return FK_OK;
 }
@@ -362,6 +379,7 @@ int fk_pool_destroy(fk_pool* p) {
     if (p->kv) cudaFree(p->kv);
     if (p->part_o) cudaFree(p->part_o);
     if (p->part_ml) cudaFree(p->part_ml);
+    if (p->mctl) cudaFree(p->mctl);
     if (p->ticket) cudaFree(p->ticket);
     for (auto& kv : p->graphs) kv.second.reset();
   }
@@ -409,10 +427,12 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
       break;
     case FK_OPT_TC_MIN_CHUNK: p->tc_min_chunk = std::min<int64_t>(kTcMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_TC_DYN_PCT: p->tc_dyn_pct = std::min<int64_t>(100, std::max<int64_t>(0, value)); break;
+    case FK_OPT_TC_BOUNDARY_COST: p->tc_boundary_cost = std::max<int64_t>(0, value); break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
     case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
+    case FK_OPT_FUSED_MERGE: p->fused_merge = value != 0; break;
     default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
   }
   return FK_OK;
@@ -933,6 +953,14 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     return fail(FK_INVALID_ARGUMENT, "work-list invariant violated: %lld shared + %lld private != %lld batch tokens",
                 (long long)shared_tokens, (long long)private_tokens, (long long)batch_tokens);
   const int n_items = (int)items.size();
+  // fused merge: every (row, head) must receive a partial, every tcgen05
+  // item a chunk, and the private warps (the queue's drainers) must exist
+  int64_t tc_rows_total = 0;
+  for (size_t k = 0; k < ch_item.size(); ++k) tc_rows_total += items[ch_item[k]].nq;
+  bool fused_ok = num_mma == 0 && tc_nchunks > 0 && U > 0 && B > 0;
+  for (size_t i = num_mma; i < items.size() && fused_ok; ++i) fused_ok = items[i].units > 0;
+  for (int64_t i = 0; i < B * H && fused_ok; ++i) fused_ok = row_head_count[i] > 0;
+  p->plan_fused_ok = fused_ok;
   if (info) {
     info->batch_tokens = batch_tokens;
     info->shared_tokens = shared_tokens;
@@ -943,6 +971,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     info->max_slots = max_slots;
     info->num_tc_items = num_tc;
     info->num_mma_items = num_mma;
+    info->fused_merge = (fused_ok && p->fused_merge && p->launch_order == 0) ? 1 : 0;
   }
   p->committed = false;
   if (plan_timing) {
@@ -1070,6 +1099,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.it_first_chunk = (const int32_t*)(d + o_ifc);
   pd.tc_cta_chunk0 = (const int32_t*)(d + o_cc0);
   pd.tc_static_chunks = (int)n_static;
+  pd.tc_rows_total = (int)tc_rows_total;
+  pd.fused = 0;
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
@@ -1115,6 +1146,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_parity) {
     a.part_o += p->part_cap * p->desc.head_dim;
     a.part_ml += p->part_cap;
+    a.mctl += 4 + 2 * p->mctl_rh;
   }
   p->launch_parity ^= 1;
   const bool has_mma = p->plan.tc_begin > 0;
@@ -1123,6 +1155,12 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   // layer's merge runs (it writes the other half of the partials and reads
   // q only after griddepcontrol.wait); never behind the mma prefix kernel
   const bool xl = p->pdl >= 2 && !has_mma;
+  // fused merge: the partial writers merge (fk_common.cuh); no K4
+  const bool fused = p->plan_fused_ok && p->fused_merge && p->launch_order == 0 && has_tc && !has_mma &&
+                     p->plan.priv_units > 0;
+  p->plan.fused = fused ? 1 : 0;
+  a.out = (__nv_bfloat16*)out;
+  a.out_f32 = out_f32;
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
   // K2 (shared prefixes) and K3 (private streams) only write partials, so
   // their order is free; K4 merges every (row, head) afterwards.
@@ -1135,7 +1173,8 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   auto run_prefix = [&](bool pdl_tc, bool after_private) -> int {
     if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
     if (has_tc)
-      FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc, after_private, st));
+      FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc, after_private,
+                               fused, st));
     return FK_OK;
   };
   // tickets a private launch consumes (fk_private_kernel): nchunks - static + grid warps
@@ -1161,7 +1200,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
     int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;
   }
-  FK_CUDA(launch_merge(a, p->plan, out, out_f32, layer, p->pdl != 0, st));
+  if (!fused) FK_CUDA(launch_merge(a, p->plan, out, out_f32, layer, p->pdl != 0, st));
   return FK_OK;
 }
 

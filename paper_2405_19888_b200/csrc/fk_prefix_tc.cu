@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
                                                                      float scale_log2,
                                                                      const __grid_constant__ CUtensorMap tmap,
                                                                      const __grid_constant__ CUtensorMap tmap_run,
-                                                                     int after_private) {
+                                                                     int after_private, int trig_late) {
   // all shared state is dynamic (no static smem), so the buffer starts at
   // the 1 KiB-aligned base SWIZZLE_128B needs
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -113,10 +113,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
   const int nch = p.tc_nchunks;
-  pdl_launch_dependents();  // the private grid may start on the SMs we leave free
+  // The private grid may start on the SMs we leave free: at once, or (fused
+  // merge, trig_late) once every thread has waited for the previous launch --
+  // the private grid then starts only after the previous layer completed, and
+  // every CTA of this grid is resident before any private warp can wait on
+  // its reports.
+  if (!trig_late) pdl_launch_dependents();
+  bool dep_done = !trig_late;
+  auto dep = [&]() {
+    if (!dep_done) {
+      pdl_wait_primary();
+      pdl_launch_dependents();
+      dep_done = true;
+    }
+  };
   // Launched behind the private grid (launch order 1), this grid's completion
   // must imply that grid's: thread 0 waits for it on exit.
   if ((int)blockIdx.x >= p.tc_ctas || p.tc_cta_chunk0[blockIdx.x] == p.tc_cta_chunk0[blockIdx.x + 1]) {
+    // (exit triggers the dependents)
     if (after_private && threadIdx.x == 0) pdl_wait_primary();
     return;
   }
@@ -170,6 +184,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     const int send = p.tc_cta_chunk0[blockIdx.x + 1];
     auto grab = [&]() -> int {
       if (sidx < send) return sidx++;
+      dep();  // tickets of the previous launch are all taken once it completed
       int c = 0;
       if (lane == 0) {
         c = p.tc_static_chunks + (int)(atomicAdd(a.ticket_tc, 1ull) - p.tc_ticket_base);
@@ -196,6 +211,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     int n_item = 0, n_tile0 = 0, n_tile1 = 0, n_head = 0, n_npi = 0, n_poff = 0, n_win = 0, n_nwin = 0;
     int n_stage = 0;  // 0 nothing, 1 metadata, 2 metadata + first window of chunk `nxt`
     for (int t = 0;; ++t) {
+      // a full ring: loads past it need the MMA, which needs the previous launch
+      if (t == (kTcKStages < kTcVStages ? kTcKStages : kTcVStages)) dep();
       if (c.tile == c.tile1) {  // current chunk done: switch to `nxt`
         if (nxt < 0) break;
         if (n_stage < 1) {
@@ -262,14 +279,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         for (int j = 1; j < kTcTilePages; ++j) run = run && pl[j] == pl[0] + j;
         auto load_tile = [&](uint8_t* st, int plane, uint64_t* bar) {
           mbar_expect_tx(bar, kTcTilePages * 2 * 2048);
+          // evict-first: a tile is read by one CTA (or, with two query
+          // blocks, two CTAs far apart in time); measured +3-4 % per step
+          const uint64_t pol = l2_policy_evict_first();
           if (run) {
-            tma_load_3d(st, &tmap_run, 0, pl[0] * kPage, plane, bar);
-            tma_load_3d(st + kTcHalf, &tmap_run, 64, pl[0] * kPage, plane, bar);
+            tma_load_3d_hint(st, &tmap_run, 0, pl[0] * kPage, plane, bar, pol);
+            tma_load_3d_hint(st + kTcHalf, &tmap_run, 64, pl[0] * kPage, plane, bar, pol);
           } else {
 #pragma unroll
             for (int j = 0; j < kTcTilePages; ++j) {
-              tma_load_3d(st + j * 2048, &tmap, 0, pl[j] * kPage, plane, bar);
-              tma_load_3d(st + kTcHalf + j * 2048, &tmap, 64, pl[j] * kPage, plane, bar);
+              tma_load_3d_hint(st + j * 2048, &tmap, 0, pl[j] * kPage, plane, bar, pol);
+              tma_load_3d_hint(st + kTcHalf + j * 2048, &tmap, 64, pl[j] * kPage, plane, bar, pol);
             }
           }
         };
@@ -283,7 +303,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       __syncwarp();
       ++c.tile;
     }
+    dep();
   } else if (warp == 1) {
+    dep();
     // ------------------------------------------------------------ MMA issuer
     // Two in-order streams polled by one thread: S(t) = Q.K^T as soon as K(t)
     // lands (and, at a chunk start, its Q is staged), PV(t) as soon as P(t)
@@ -410,6 +432,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     // under cross-layer PDL the previous layer's merge may still be running:
     // q and the partials are touched only after it has completed
     if (!after_private) pdl_wait_primary();
+    dep();
     TcCursor c;
     c.qi = 0;
     tc_load_chunk(p, c, tc_read_queue(cq_full, cq, 0));
@@ -566,8 +589,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             const int piece = chunk - p.it_first_chunk[item];
             const bool real = my_q < nq;
             long long pi = 0;
+            int r = 0;
             if (real) {
-              const int r = p.qrows[p.it_q_off[item] + my_q];
+              r = p.qrows[p.it_q_off[item] + my_q];
               const int k = p.qslot[p.it_qslot_off[item] + my_q] + piece;
               pi = part_index(p, H, r, k, head);
             }
@@ -592,9 +616,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             if (R16) lr += __shfl_xor_sync(0xffffffffu, lr, 16);
             const bool lead = !R16 || sub == 0;
             if (half == 1 && lead) s_l[my_row] = lr;
+            if (p.fused) __threadfence();  // both halves' o stores before the row's report
             asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
             if (warp == 4 && lane == 0) TL(242 + min(c.qi, 3) * 4);
             if (half == 0 && lead && real) a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
+            if (p.fused && half == 0) {
+              if (lead && real) fused_arrive_tc_row(a, p, r * H + head);
+              // then the rows' report: a queued row is visible before the count
+              const unsigned n = __popc(__ballot_sync(0xffffffffu, lead && real));
+              __threadfence();
+              if (lane == 0 && n) atomicAdd(a.mctl + 2, n);
+            }
           };
           if (r16) epilogue(BoolC<true>{});
           else epilogue(BoolC<false>{});
@@ -644,7 +676,7 @@ extern "C" int fk_debug_timeline(unsigned long long* out, int n) {
 
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
                              const CUtensorMap* tmap, const CUtensorMap* tmap_run, bool pdl, bool after_private,
-                             cudaStream_t s) {
+                             bool trig_late, cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   if (!attr_set_on_device(attr_devices)) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
@@ -661,7 +693,8 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, con
   }
   if (p.tc_ctas == 0) return cudaSuccess;
   cudaError_t e = launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, p, layer,
-                           (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run, after_private ? 1 : 0);
+                           (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run, after_private ? 1 : 0,
+                           trig_late ? 1 : 0);
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, fk_prefix_tc_kernel);

@@ -551,3 +551,43 @@ def test_full_size_fork_permutation(cuda_device):
     b = run(list(reversed(range(n))))
     d = (a - b).abs()
     assert d.max().item() <= 1e-2 and (d.norm() / a.norm()).item() <= 4e-3, (d.max().item(),)
+
+
+FUSED_SHAPES = {
+    # prefix rows finish last (long prefix, short private streams)
+    "prefix_last": dict(P=3000, lens=[5, 17, 33, 1] * 4, H=8, L=3),
+    # private rows finish last (short prefix, long private streams)
+    "private_last": dict(P=160, lens=[700, 300, 64, 900, 20], H=8, L=3),
+    # 129 forks: two query blocks per head, 32-lane epilogue
+    "two_qblocks": dict(P=520, lens=[3, 40, 130] * 43, H=4, L=2),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(FUSED_SHAPES))
+@pytest.mark.parametrize("pdl,graph", [(2, 1), (1, 0), (0, 1)])
+def test_fused_merge_matches_merge_kernel(cuda_device, shape, pdl, graph):
+    """FK_OPT_FUSED_MERGE: the last partial's writer merges (private warps at
+    once, prefix rows through the queue the private warps drain) -- the same
+    LSE merge over the same partials as the merge kernel, so the outputs are
+    bit-identical; both agree with the oracle."""
+    if PATH["path"] != "tc":
+        pytest.skip("the fused merge runs with tcgen05 prefix items")
+    s = FUSED_SHAPES[shape]
+    outs = []
+    for fused in (1, 0):
+        eng = make_engine(cuda_device, H=s["H"], L=s["L"])
+        eng.set_option(_lib.FK_OPT_FUSED_MERGE, fused)
+        eng.set_option(_lib.FK_OPT_PDL, pdl)
+        eng.set_option(_lib.FK_OPT_GRAPH, graph)
+        fork_group(eng, s["P"], s["lens"], out_len=4, seed=11)
+        run_steps(eng, 4)
+        assert eng.last_plan.fused_merge == fused
+        if fused:
+            check_history(eng)
+        outs.append([(r["output"], r["output_f32"]) for r in eng.history])
+    import torch
+
+    assert len(outs[0]) == len(outs[1]) == 4
+    for (a16, a32), (b16, b32) in zip(*outs):
+        assert torch.equal(a16.view(torch.int16), b16.view(torch.int16))
+        assert torch.equal(a32, b32)
