@@ -121,11 +121,12 @@ enum {
   FK_OPT_TC_DYN_PCT = 13,     /* share (%) of the prefix tiles the tcgen05 CTAs take dynamically after
                                  their cost-balanced static ranges (default 0: measured, an epilogue per chunk costs more than the balance gains) */
   FK_OPT_TC_BOUNDARY_COST = 14, /* static split: tiles a piece start mid-range costs a CTA (default 4) */
-  FK_OPT_FUSED_MERGE = 15     /* 1 (default): the writer of the last partial of a (row, head) merges
-                                 it -- private warps directly, tcgen05 pieces through a queue the
-                                 private warps drain -- and no merge kernel runs (when the plan has
-                                 tcgen05 and private work, no mma.sync items, launch order 0);
-                                 0: a merge kernel after every layer */
+  FK_OPT_FUSED_MERGE = 15     /* 1: no merge kernel -- the writer of the last partial of a (row, head)
+                                 merges it (private warps at once; rows a tcgen05 piece completes by
+                                 the row's owning private warp as it leaves, or by the tcgen05 CTA
+                                 if the owner has left); needs tcgen05 and private work, no mma.sync
+                                 items, launch order 0.  0 (default): a merge kernel after every
+                                 layer -- measured faster */
 };
 
 /* ---- context forest ------------------------------------------------------ */

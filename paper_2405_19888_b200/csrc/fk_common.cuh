@@ -327,90 +327,117 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
 }
 
 // ------------------------------------------------------------ fused merge
-// Every partial writer counts its arrival on (row, head); the writer of the
-// last partial merges.  A private warp merges at once (merge_row_head_warp);
-// a tcgen05 piece row that arrives last is queued instead (its softmax warps
-// are the prefix pipeline's critical path) and the private warps drain the
-// queue -- one entry per chunk switch while streaming, then all of it once
-// their tickets run dry.  The ArenaDev::mctl words return to zero by the end
-// of the launch: counters by their merger, entries by their claimer, the
-// queue words by the last private warp out.
+// Every partial writer counts its arrival on (row, head) with an acq_rel
+// atomic (release: its partial stores -- and, through the warp / CTA barrier
+// before it, its partners' -- precede the count; acquire: the last one sees
+// every other partial).  Who merges:
+//  * a private warp whose arrival was the last merges the row (the atomic's
+//    result is consumed one piece later, so its latency hides under the next
+//    piece's loads);
+//  * a row completed by a tcgen05 piece is merged by its owner, private warp
+//    rh % grid_warps, when that warp leaves -- unless the owner has already
+//    left, in which case the tcgen05 CTA marks the row's orphan slot and
+//    merges it when the CTA finishes.  Leaving = store "left" (this launch's
+//    epoch), SC fence, then read the owned rows' counters; the tcgen05 side
+//    does its arrival, SC fence, then reads the owner's "left": at least one
+//    side sees the other (store-buffering with fences), so every row is
+//    merged at least once.  A second merge of a row rewrites identical bytes.
+// ArenaDev::mctl (per launch half): from [4] the mctl_rh arrival counters,
+// then one orphan slot per (tcgen05 chunk, query row)
+// (PlanDev::tc_chunk_rowbase), then the private warps' "left" epochs.
+// Counters and slots return to 0 within the launch (their mergers); epochs
+// only grow.
 __device__ __forceinline__ unsigned* mctl_cnt(const ArenaDev& a) { return a.mctl + 4; }
-__device__ __forceinline__ unsigned* mctl_queue(const ArenaDev& a) { return a.mctl + 4 + a.mctl_rh; }
+__device__ __forceinline__ unsigned* mctl_orphans(const ArenaDev& a) { return a.mctl + 4 + a.mctl_rh; }
+__device__ __forceinline__ unsigned* mctl_left(const ArenaDev& a) { return a.mctl + 4 + a.mctl_rh + a.mctl_q; }
 
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
+
+// merge rh and zero its counter for the launch after next (a concurrent
+// second merger writes the same bytes and zeroes it again)
 __device__ __forceinline__ void fused_merge_rh(const ArenaDev& a, const PlanDev& p, int rh, int lane) {
-  __threadfence();  // acquire: every other partial of rh is visible (ld.cg reads)
   merge_row_head_warp(a, p, rh / a.num_heads, rh % a.num_heads, a.out, a.out_f32, lane);
   if (lane == 0) mctl_cnt(a)[rh] = 0u;
 }
 
-// a private warp wrote the partial of (row, head): count it, merge if last
-__device__ __forceinline__ void fused_arrive_warp(const ArenaDev& a, const PlanDev& p, int row, int head, int lane) {
-  __threadfence();  // release this warp's partial stores before the count
-  __syncwarp();
-  const int rh = row * a.num_heads + head;
-  int last = 0;
-  if (lane == 0) last = atomicAdd(mctl_cnt(a) + rh, 1u) + 1u == (unsigned)p.row_head_count[rh];
-  if (__shfl_sync(0xffffffffu, last, 0)) fused_merge_rh(a, p, rh, lane);
+// a private warp wrote the partial of rh: count it (lane 0); the caller
+// keeps the returned old count and the rh, and resolves them later
+__device__ __forceinline__ unsigned fused_arrive_issue(const ArenaDev& a, int rh, int lane) {
+  __syncwarp();  // every lane's partial stores precede lane 0's release
+  return lane == 0 ? atom_add_acq_rel(mctl_cnt(a) + rh, 1u) : 0u;
+}
+// ... and merges the row if that arrival was the last
+__device__ __forceinline__ void fused_arrive_resolve(const ArenaDev& a, const PlanDev& p, int rh, unsigned old,
+                                                     int lane) {
+  int last = lane == 0 && old + 1u == (unsigned)p.row_head_count[rh];
+  last = __shfl_sync(0xffffffffu, last, 0);
+  __syncwarp();  // lane 0's acquire precedes every lane's partial loads
+  if (last) fused_merge_rh(a, p, rh, lane);
 }
 
-// claim one queued (row, head) -- never past the tail -- and merge it
-__device__ __forceinline__ bool fused_drain_one(const ArenaDev& a, const PlanDev& p, int lane) {
-  int rh = -1;
+// a private warp leaves: announce it, then merge the owned rows that are
+// complete (rh = gw + k * grid_warps)
+__device__ __forceinline__ void fused_leave(const ArenaDev& a, const PlanDev& p, int gw, int grid_warps, int lane) {
   if (lane == 0) {
-    volatile unsigned* c = a.mctl;
-    unsigned h = c[0];
-    while (h < c[1]) {
-      const unsigned old = atomicCAS(a.mctl, h, h + 1u);
-      if (old == h) {
-        volatile unsigned* e = mctl_queue(a) + h;
-        unsigned v;
-        while ((v = *e) == 0u) {  // reserved, being written
-        }
-        *e = 0u;
-        rh = (int)v - 1;
-        break;
-      }
-      h = old;
+    *(volatile unsigned*)(mctl_left(a) + gw) = p.fused_epoch;
+    fence_sc();
+  }
+  __syncwarp();
+  const int nrh = p.num_rows * a.num_heads;
+  for (int base = gw; base < nrh; base += 32 * grid_warps) {
+    const int rh = base + lane * grid_warps;
+    bool done = false;
+    if (rh < nrh) done = ld_acquire(mctl_cnt(a) + rh) == (unsigned)p.row_head_count[rh];
+    unsigned m = __ballot_sync(0xffffffffu, done);
+    __syncwarp();
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1;
+      fused_merge_rh(a, p, base + l * grid_warps, lane);
     }
   }
-  rh = __shfl_sync(0xffffffffu, rh, 0);
-  if (rh < 0) return false;
-  fused_merge_rh(a, p, rh, lane);
-  return true;
 }
 
-// a private warp with no chunk left: merge queued rows until every tcgen05
-// piece row has reported and the queue is empty; the last warp out of the
-// grid zeroes the queue words for the launch after next
-__device__ __forceinline__ void fused_drain_all(const ArenaDev& a, const PlanDev& p, int lane, unsigned grid_warps) {
-  while (true) {
-    if (fused_drain_one(a, p, lane)) continue;
-    int fin = 0;
-    if (lane == 0) {
-      volatile unsigned* c = a.mctl;
-      if (c[2] == (unsigned)p.tc_rows_total) {
-        __threadfence();
-        fin = c[0] >= c[1];
-      }
+// a tcgen05 piece row's partial is written (both halves' stores precede
+// this, bar.sync): count it; if it completed the row and the row's owner
+// has left, mark the orphan slot for this CTA's end
+__device__ __forceinline__ void fused_arrive_tc_row(const ArenaDev& a, const PlanDev& p, int rh, int slot) {
+  if (atom_add_acq_rel(mctl_cnt(a) + rh, 1u) + 1u != (unsigned)p.row_head_count[rh]) return;
+  fence_sc();
+  if (*(volatile unsigned*)(mctl_left(a) + rh % p.priv_warps) == p.fused_epoch)
+    mctl_orphans(a)[slot] = (unsigned)rh + 1u;
+}
+
+// end of a tcgen05 CTA: merge the marked slots [s0, s1); orphan k (in slot
+// order) goes to warp k % nw.  Marks were written before a CTA barrier; the
+// caller zeroes the slots after another one.
+__device__ __forceinline__ void fused_merge_orphans(const ArenaDev& a, const PlanDev& p, int s0, int s1, int warp,
+                                                    int nw, int lane) {
+  unsigned* slots = mctl_orphans(a);
+  int k0 = 0;  // orphans before this group
+  for (int g = s0; g < s1; g += 32) {
+    const unsigned v = g + lane < s1 ? __ldcg(slots + g + lane) : 0u;
+    const unsigned m = __ballot_sync(0xffffffffu, v != 0u);
+    unsigned mine = 0u;  // lanes whose orphan ordinal falls on this warp
+    for (unsigned mm = m; mm; mm &= mm - 1) {
+      const int l = __ffs(mm) - 1;
+      if ((k0 + __popc(m & ((1u << l) - 1u))) % nw == warp) mine |= 1u << l;
     }
-    if (__shfl_sync(0xffffffffu, fin, 0)) break;
-    __nanosleep(200);
-  }
-  if (lane == 0 && atomicAdd(a.mctl + 3, 1u) + 1u == grid_warps) {
-    volatile unsigned* c = a.mctl;
-    c[0] = c[1] = c[2] = c[3] = 0u;
-  }
-}
-
-// a tcgen05 piece row wrote its partial (o stores fenced before the CTA
-// barrier that precedes this): count it; queue the row if it was last
-__device__ __forceinline__ void fused_arrive_tc_row(const ArenaDev& a, const PlanDev& p, int rh) {
-  __threadfence();
-  if (atomicAdd(mctl_cnt(a) + rh, 1u) + 1u == (unsigned)p.row_head_count[rh]) {
-    const unsigned idx = atomicAdd(a.mctl + 1, 1u);
-    *(volatile unsigned*)(mctl_queue(a) + idx) = (unsigned)rh + 1u;
+    for (; mine; mine &= mine - 1) {
+      const int l = __ffs(mine) - 1;
+      fused_merge_rh(a, p, (int)__shfl_sync(0xffffffffu, v, l) - 1, lane);
+    }
+    k0 += __popc(m);
   }
 }
-
 }  // namespace fk

@@ -51,8 +51,10 @@ struct PlanDev {
   const int* it_first_chunk;      // per item: its first chunk (piece 0)
   const int* tc_cta_chunk0;       // [tc_ctas + 1]: CTA b's static chunks are [chunk0[b], chunk0[b + 1])
   int tc_static_chunks;           // dynamic chunk = tc_static_chunks + ticket
-  int tc_rows_total;              // sum over chunks of the item's query rows (fused merge: reports)
   int fused;                      // fused merge on this launch (set per launch)
+  const int* tc_chunk_rowbase;    // [tc_nchunks + 1]: first orphan slot of each chunk (prefix sums of nq)
+  int tc_active_ctas;             // tcgen05 CTAs with at least one static chunk
+  unsigned fused_epoch;           // this launch's "left" value (fk_common.cuh; set per launch)
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;
@@ -94,12 +96,10 @@ struct ArenaDev {
   float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
   unsigned long long* ticket;     // private chunk ticket counter (never reset)
   unsigned long long* ticket_tc;  // tcgen05 prefix chunk ticket counter (never reset)
-  // fused merge (this launch's half): [0] orphan queue head, [1] tail, [2]
-  // tcgen05 piece rows reported, [3] private warps done; then mctl_rh arrival
-  // counters per (row, head), then mctl_rh queue entries (row * H + head + 1).
-  // Every word returns to 0 by the end of the launch.
+  // fused merge (this launch's half; layout in fk_common.cuh): control
+  // words, arrival counters per (row, head), orphan slots per tcgen05 row piece
   unsigned* mctl;
-  int mctl_rh;
+  int mctl_rh, mctl_q;
   __nv_bfloat16* out;     // this launch's outputs (fused merge)
   float* out_f32;
 };

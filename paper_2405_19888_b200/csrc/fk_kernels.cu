@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
   CTA_TL_START(fk_tl_cta_priv, layer);
+#ifdef FK_TIMELINE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) fk_tl_cta_priv[layer & 1][blockIdx.x][3] = 0;
+#endif
   pdl_launch_dependents();  // the merge kernel may launch now (it waits for us)
   PdlTail tail;             // on exit: this grid completes only after the prefix grid
 
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   };
   int ca = gw < p.priv_static ? gw : grab();
   if (ca >= nch) {
-    if (p.fused) fused_drain_all(a, p, lane, gridDim.x * WARPS);
+    if (p.fused) fused_leave(a, p, gw, gridDim.x * WARPS, lane);
     return;
   }
 
@@ -179,6 +182,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   for (int k = 0; k < 16; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
   float m = -INFINITY, l = 0.f;
   const int mi = lane >> 3, ri = lane & 7;
+  int pend_rh = -1;  // fused merge: the last piece's (row, head) and its arrival count
+  unsigned pend_old = 0u;
 
   while (true) {
     // the unit after this one (next in A, else first of B) decides the piece end
@@ -265,7 +270,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
         for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][0], o[nt][1]);
         if (t4 == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
-      if (p.fused) fused_arrive_warp(a, p, row, head, lane);
+      if (p.fused) {  // settle the previous piece's arrival, then count this one
+#ifdef FK_TIMELINE
+        const unsigned long long tf0 = global_ns();
+#endif
+        if (pend_rh >= 0) fused_arrive_resolve(a, p, pend_rh, pend_old, lane);
+        pend_rh = (int)rh;
+        pend_old = fused_arrive_issue(a, (int)rh, lane);
+#ifdef FK_TIMELINE
+        if (lane == 0 && blockIdx.x < 1024) atomicAdd(&fk_tl_cta_priv[layer & 1][blockIdx.x][3], global_ns() - tf0);
+#endif
+      }
       m = -INFINITY;
       l = 0.f;
 #pragma unroll
@@ -287,11 +302,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
       cb = grab();
       mb = load_chunk(cb, lb);
       issue_ahead();
-      if (p.fused) fused_drain_one(a, p, lane);  // a queued prefix row, if any, under the loads in flight
     }
     cur = nxt;
   }
-  if (p.fused) fused_drain_all(a, p, lane, gridDim.x * WARPS);
+#ifdef FK_TIMELINE
+  if (lane == 0) CTA_TL_NOTE(fk_tl_cta_priv, layer, 2, global_ns());
+#endif
+  if (p.fused) {
+    if (pend_rh >= 0) fused_arrive_resolve(a, p, pend_rh, pend_old, lane);
+    fused_leave(a, p, gw, gridDim.x * WARPS, lane);
+  }
   CTA_TL_END(fk_tl_cta_priv, layer);
 }
 

@@ -160,9 +160,11 @@ struct fk_pool {
   float2* part_ml = nullptr;
   size_t part_cap = 0;     // entries (rows*slots*H) per half
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
-  unsigned* mctl = nullptr;  // fused merge words, two halves of 4 + 2 * mctl_rh (ArenaDev::mctl)
-  size_t mctl_rh = 0;
-  int64_t fused_merge = 1;   // FK_OPT_FUSED_MERGE
+  unsigned* mctl = nullptr;  // fused merge words, two halves of 4 + mctl_rh + mctl_q (ArenaDev::mctl)
+  size_t mctl_rh = 0, mctl_q = 0;
+  unsigned fused_epoch = 0;  // "left" value of the latest fused launch
+  size_t mctl_left_cap() const { return (size_t)std::max(num_sms, 1) * 12; }  // private grid warps
+  int64_t fused_merge = 0;   // FK_OPT_FUSED_MERGE (measured slower than the merge kernel: off)
   bool plan_fused_ok = false;  // the current plan admits the fused merge
   unsigned long long* ticket = nullptr;  // device: private chunk tickets (never reset)
   unsigned long long ticket_base = 0;    // tickets consumed by earlier private launches
@@ -180,6 +182,7 @@ struct fk_pool {
     a.ticket_tc = ticket ? ticket + 1 : nullptr;
     a.mctl = mctl;
     a.mctl_rh = (int)mctl_rh;
+    a.mctl_q = (int)mctl_q;
     a.out = nullptr;
     a.out_f32 = nullptr;
       return a;
@@ -257,7 +260,7 @@ int reserve_pages(fk_pool* p, int64_t pages) {
   return encode_tmap(p);
 }
 
-int ensure_scratch(fk_pool* p, int rows, int slots) {
+int ensure_scratch(fk_pool* p, int rows, int slots, int64_t orphan_slots) {
   const size_t H = p->desc.num_heads, D = p->desc.head_dim;
   const size_t need = (size_t)std::max(rows, 1) * std::max(slots, 1) * H;
   if (need > p->part_cap) {
@@ -274,14 +277,16 @@ int ensure_scratch(fk_pool* p, int rows, int slots) {
     FK_CUDA(cudaMalloc(&p->part_ml, 2 * cap * sizeof(float2)));
     p->part_cap = cap;
   }
-  const size_t rh = (size_t)std::max(rows, 1) * H;
-  if (rh > p->mctl_rh) {
-    const size_t cap = std::max(rh + rh / 2, p->mctl_rh * 2);
+  const size_t rh = (size_t)std::max(rows, 1) * H, oq = (size_t)std::max<int64_t>(orphan_slots, 1);
+  if (rh > p->mctl_rh || oq > p->mctl_q) {
+    const size_t cap_rh = std::max(rh + rh / 2, p->mctl_rh), cap_q = std::max(oq + oq / 2, p->mctl_q);
+    const size_t bytes = 2 * (4 + cap_rh + cap_q + p->mctl_left_cap()) * sizeof(unsigned);
     if (p->mctl) FK_CUDA(cudaFree(p->mctl));
     p->mctl = nullptr;
-    FK_CUDA(cudaMalloc(&p->mctl, 2 * (4 + 2 * cap) * sizeof(unsigned)));
-    FK_CUDA(cudaMemset(p->mctl, 0, 2 * (4 + 2 * cap) * sizeof(unsigned)));
-    p->mctl_rh = cap;
+    FK_CUDA(cudaMalloc(&p->mctl, bytes));
+    FK_CUDA(cudaMemset(p->mctl, 0, bytes));
+    p->mctl_rh = cap_rh;
+    p->mctl_q = cap_q;
   }
   return FK_OK;
 }
@@ -955,8 +960,11 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int n_items = (int)items.size();
   // fused merge: every (row, head) must receive a partial, every tcgen05
   // item a chunk, and the private warps (the queue's drainers) must exist
-  int64_t tc_rows_total = 0;
-  for (size_t k = 0; k < ch_item.size(); ++k) tc_rows_total += items[ch_item[k]].nq;
+  // orphan slot of (tcgen05 chunk, query row): prefix sums of the chunks' rows
+  std::vector<int32_t> ch_rowbase(ch_item.size() + 1, 0);
+  for (size_t k = 0; k < ch_item.size(); ++k) ch_rowbase[k + 1] = ch_rowbase[k] + items[ch_item[k]].nq;
+  int tc_active = 0;
+  for (int64_t b = 0; b + 1 < (int64_t)cta_chunk0.size(); ++b) tc_active += cta_chunk0[b] < cta_chunk0[b + 1];
   bool fused_ok = num_mma == 0 && tc_nchunks > 0 && U > 0 && B > 0;
   for (size_t i = num_mma; i < items.size() && fused_ok; ++i) fused_ok = items[i].units > 0;
   for (int64_t i = 0; i < B * H && fused_ok; ++i) fused_ok = row_head_count[i] > 0;
@@ -987,7 +995,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   PT(T7);
   // ---- upload ---------------------------------------------------------------
   FK_ON_DEVICE(p->desc.device);
-  int rc = ensure_scratch(p, B, max_slots);
+  int rc = ensure_scratch(p, B, max_slots, ch_rowbase.back());
   if (rc != FK_OK) return rc;
   const size_t ni = (size_t)std::max(n_items, 1);
   const size_t nb = (size_t)std::max(B, 1);
@@ -1013,6 +1021,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_ch1 = L.add(nchb);
   const size_t o_ifc = L.add(sizeof(int32_t) * ni);
   const size_t o_cc0 = L.add(sizeof(int32_t) * std::max<size_t>(cta_chunk0.size(), 1));
+  const size_t o_crb = L.add(sizeof(int32_t) * ch_rowbase.size());
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
     FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
@@ -1069,6 +1078,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   put(o_ch1, ch_t1.data(), ch_t1.size() * 4);
   put(o_ifc, it_first_chunk.data(), it_first_chunk.size() * 4);
   put(o_cc0, cta_chunk0.data(), cta_chunk0.size() * 4);
+  put(o_crb, ch_rowbase.data(), ch_rowbase.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -1099,8 +1109,9 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.it_first_chunk = (const int32_t*)(d + o_ifc);
   pd.tc_cta_chunk0 = (const int32_t*)(d + o_cc0);
   pd.tc_static_chunks = (int)n_static;
-  pd.tc_rows_total = (int)tc_rows_total;
   pd.fused = 0;
+  pd.tc_chunk_rowbase = (const int32_t*)(d + o_crb);
+  pd.tc_active_ctas = tc_active;
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;
@@ -1146,7 +1157,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_parity) {
     a.part_o += p->part_cap * p->desc.head_dim;
     a.part_ml += p->part_cap;
-    a.mctl += 4 + 2 * p->mctl_rh;
+    a.mctl += 4 + p->mctl_rh + p->mctl_q + p->mctl_left_cap();
   }
   p->launch_parity ^= 1;
   const bool has_mma = p->plan.tc_begin > 0;
@@ -1159,6 +1170,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   const bool fused = p->plan_fused_ok && p->fused_merge && p->launch_order == 0 && has_tc && !has_mma &&
                      p->plan.priv_units > 0;
   p->plan.fused = fused ? 1 : 0;
+  if (fused) p->plan.fused_epoch = ++p->fused_epoch;
   a.out = (__nv_bfloat16*)out;
   a.out_f32 = out_f32;
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
@@ -1201,6 +1213,17 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
     if (rc != FK_OK) return rc;
   }
   if (!fused) FK_CUDA(launch_merge(a, p->plan, out, out_f32, layer, p->pdl != 0, st));
+  return FK_OK;
+}
+
+// debug (not in the C ABI): both halves of the fused-merge control block
+extern "C" int fk_debug_mctl(fk_pool* p, unsigned* out, int64_t n, int64_t* rh_cap) {
+  if (!p || !p->mctl) return FK_INVALID_ARGUMENT;
+  *rh_cap = (int64_t)p->mctl_rh;
+  const int64_t total = 2 * (4 + (int64_t)p->mctl_rh + (int64_t)p->mctl_q + (int64_t)p->mctl_left_cap());
+  FK_ON_DEVICE(p->desc.device);
+  FK_CUDA(cudaDeviceSynchronize());
+  FK_CUDA(cudaMemcpy(out, p->mctl, sizeof(unsigned) * std::min(n, total), cudaMemcpyDeviceToHost));
   return FK_OK;
 }
 

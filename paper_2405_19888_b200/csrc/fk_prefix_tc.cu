@@ -616,16 +616,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             if (R16) lr += __shfl_xor_sync(0xffffffffu, lr, 16);
             const bool lead = !R16 || sub == 0;
             if (half == 1 && lead) s_l[my_row] = lr;
-            if (p.fused) __threadfence();  // both halves' o stores before the row's report
             asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
             if (warp == 4 && lane == 0) TL(242 + min(c.qi, 3) * 4);
-            if (half == 0 && lead && real) a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
-            if (p.fused && half == 0) {
-              if (lead && real) fused_arrive_tc_row(a, p, r * H + head);
-              // then the rows' report: a queued row is visible before the count
-              const unsigned n = __popc(__ballot_sync(0xffffffffu, lead && real));
-              __threadfence();
-              if (lane == 0 && n) atomicAdd(a.mctl + 2, n);
+            if (half == 0 && lead && real) {
+              a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
+              // fused merge: both halves' stores precede this release (bar.sync)
+              if (p.fused) fused_arrive_tc_row(a, p, r * H + head, p.tc_chunk_rowbase[chunk] + my_q);
             }
           };
           if (r16) epilogue(BoolC<true>{});
@@ -648,6 +644,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
+  }
+  if (p.fused) {
+    // rows this CTA completed after their owners had left (fk_common.cuh):
+    // its static chunks' slots, and (last CTA out) the dynamic chunks'
+    const int b = blockIdx.x;
+    const int s0 = p.tc_chunk_rowbase[p.tc_cta_chunk0[b]], s1 = p.tc_chunk_rowbase[p.tc_cta_chunk0[b + 1]];
+    fused_merge_orphans(a, p, s0, s1, warp, kTcThreads / 32, lane);
+    __syncthreads();  // every warp has read the slots; this CTA's marks precede thread 0's release
+    for (int i = s0 + (int)threadIdx.x; i < s1; i += kTcThreads) mctl_orphans(a)[i] = 0u;
+    if (p.tc_nchunks > p.tc_static_chunks) {
+      if (threadIdx.x == 0)
+        ms.cq[0] = atom_add_acq_rel(a.mctl + 2, 1u) + 1u == (unsigned)p.tc_active_ctas;
+      __syncthreads();
+      if (ms.cq[0]) {
+        const int d0 = p.tc_chunk_rowbase[p.tc_static_chunks], d1 = p.tc_chunk_rowbase[p.tc_nchunks];
+        fused_merge_orphans(a, p, d0, d1, warp, kTcThreads / 32, lane);
+        __syncthreads();
+        for (int i = d0 + (int)threadIdx.x; i < d1; i += kTcThreads) mctl_orphans(a)[i] = 0u;
+        if (threadIdx.x == 0) a.mctl[2] = 0u;
+      }
+    }
   }
   if (after_private && threadIdx.x == 0) pdl_wait_primary();
 }

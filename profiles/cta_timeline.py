@@ -55,6 +55,9 @@ def main():
             t0 = min(s for s, _ in pre + priv)
         mer = [x for x in out["merge"][par] if x[0] and abs(x[0] - t_last) < 200000 and x[1] >= x[0]]
         for name, xs in (("prefix", pre), ("private", priv), ("merge*", mer)):
+            if not xs:
+                print(f"layer%2 {par} {name:8s} none")
+                continue
             st = sorted((s - t0) / 1e3 for s, _ in xs)
             en = sorted((e - t0) / 1e3 for _, e in xs)
             print(f"layer%2 {par} {name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} "

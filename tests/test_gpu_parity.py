@@ -560,16 +560,20 @@ FUSED_SHAPES = {
     "private_last": dict(P=160, lens=[700, 300, 64, 900, 20], H=8, L=3),
     # 129 forks: two query blocks per head, 32-lane epilogue
     "two_qblocks": dict(P=520, lens=[3, 40, 130] * 43, H=4, L=2),
+    # most prefix tiles in one-tile dynamic chunks: the last tcgen05 CTA out
+    # merges the orphans of the dynamic chunks
+    "dynamic_chunks": dict(P=2600, lens=[9, 2, 30, 1] * 3, H=4, L=2,
+                           opts=dict(TC_DYN_PCT=60, TC_MIN_CHUNK=1, PREFIX_TARGET_CTAS=6)),
 }
 
 
 @pytest.mark.parametrize("shape", sorted(FUSED_SHAPES))
 @pytest.mark.parametrize("pdl,graph", [(2, 1), (1, 0), (0, 1)])
 def test_fused_merge_matches_merge_kernel(cuda_device, shape, pdl, graph):
-    """FK_OPT_FUSED_MERGE: the last partial's writer merges (private warps at
-    once, prefix rows through the queue the private warps drain) -- the same
-    LSE merge over the same partials as the merge kernel, so the outputs are
-    bit-identical; both agree with the oracle."""
+    """FK_OPT_FUSED_MERGE=1: the last partial's writer merges (private warps at
+    once, prefix-completed rows by their owning private warp or the tcgen05
+    CTA) -- the same LSE merge over the same partials as the merge kernel,
+    so the outputs are bit-identical; both agree with the oracle."""
     if PATH["path"] != "tc":
         pytest.skip("the fused merge runs with tcgen05 prefix items")
     s = FUSED_SHAPES[shape]
@@ -579,6 +583,8 @@ def test_fused_merge_matches_merge_kernel(cuda_device, shape, pdl, graph):
         eng.set_option(_lib.FK_OPT_FUSED_MERGE, fused)
         eng.set_option(_lib.FK_OPT_PDL, pdl)
         eng.set_option(_lib.FK_OPT_GRAPH, graph)
+        for k, v in s.get("opts", {}).items():
+            eng.set_option(getattr(_lib, "FK_OPT_" + k), v)
         fork_group(eng, s["P"], s["lens"], out_len=4, seed=11)
         run_steps(eng, 4)
         assert eng.last_plan.fused_merge == fused

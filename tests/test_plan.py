@@ -81,9 +81,9 @@ def test_nested_plan_counts_every_level_once():
 
 
 def test_fused_merge_admission():
-    """FK_OPT_FUSED_MERGE: the plan reports the fused merge for a fork group
-    (tcgen05 prefix + private streams); the option, launch order 1, the
-    mma.sync prefix path and a plan without private streams turn it off."""
+    """FK_OPT_FUSED_MERGE=1: the plan reports the fused merge for a fork group
+    (tcgen05 prefix + private streams); launch order 1, the mma.sync prefix
+    path and a plan without private streams keep the merge kernel."""
     from paper_2405_19888_b200 import _lib
     from paper_2405_19888_b200.workloads import fork_group
 
@@ -95,8 +95,8 @@ def test_fused_merge_admission():
         eng._plan(list(eng.gens.values()))
         return eng.last_plan
 
-    assert plan(100).fused_merge == 1
-    assert plan(100, FUSED_MERGE=0).fused_merge == 0
-    assert plan(100, LAUNCH_ORDER=1).fused_merge == 0
-    assert plan(100, TC_MIN_FANOUT=0).fused_merge == 0  # mma.sync prefix items
-    assert plan(0).fused_merge == 0  # no private stream to drain the queue
+    assert plan(100).fused_merge == 0  # default: the merge kernel
+    assert plan(100, FUSED_MERGE=1).fused_merge == 1
+    assert plan(100, FUSED_MERGE=1, LAUNCH_ORDER=1).fused_merge == 0
+    assert plan(100, FUSED_MERGE=1, TC_MIN_FANOUT=0).fused_merge == 0  # mma.sync prefix items
+    assert plan(0, FUSED_MERGE=1).fused_merge == 0  # no private warps to own the rows
