@@ -370,19 +370,26 @@ __device__ __forceinline__ void fused_merge_rh(const ArenaDev& a, const PlanDev&
   if (lane == 0) mctl_cnt(a)[rh] = 0u;
 }
 
-// a private warp wrote the partial of rh: count it (lane 0); the caller
-// keeps the returned old count and the rh, and resolves them later
-__device__ __forceinline__ unsigned fused_arrive_issue(const ArenaDev& a, int rh, int lane) {
-  __syncwarp();  // every lane's partial stores precede lane 0's release
-  return lane == 0 ? atom_add_acq_rel(mctl_cnt(a) + rh, 1u) : 0u;
-}
-// ... and merges the row if that arrival was the last
-__device__ __forceinline__ void fused_arrive_resolve(const ArenaDev& a, const PlanDev& p, int rh, unsigned old,
-                                                     int lane) {
-  int last = lane == 0 && old + 1u == (unsigned)p.row_head_count[rh];
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Private warps count their pieces one piece late, so neither the release
+// (its stores long complete) nor the atomic's result (returned a piece ago)
+// stalls the stream.  At a piece end, before that piece's loads and stores:
+// read the result of the previous count (`pend`), fence (release for the
+// stored-but-uncounted piece `unrel`, acquire for `pend`), count `unrel`,
+// and merge `pend`'s row if its count was the last.
+__device__ __forceinline__ void fused_private_step(const ArenaDev& a, const PlanDev& p, int& unrel_rh, int& pend_rh,
+                                                   unsigned& pend_old, int lane) {
+  int last = lane == 0 && pend_rh >= 0 && pend_old + 1u == (unsigned)p.row_head_count[pend_rh];
+  const int merge_rh = pend_rh;
+  __syncwarp();
+  fence_acq_rel();
+  pend_rh = unrel_rh;
+  unrel_rh = -1;
+  if (pend_rh >= 0 && lane == 0) pend_old = atomicAdd(mctl_cnt(a) + pend_rh, 1u);
   last = __shfl_sync(0xffffffffu, last, 0);
-  __syncwarp();  // lane 0's acquire precedes every lane's partial loads
-  if (last) fused_merge_rh(a, p, rh, lane);
+  __syncwarp();
+  if (last) fused_merge_rh(a, p, merge_rh, lane);
 }
 
 // a private warp leaves: announce it, then merge the owned rows that are

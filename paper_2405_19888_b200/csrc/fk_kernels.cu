@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   for (int k = 0; k < 16; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
   float m = -INFINITY, l = 0.f;
   const int mi = lane >> 3, ri = lane & 7;
-  int pend_rh = -1;  // fused merge: the last piece's (row, head) and its arrival count
+  // fused merge (fk_common.cuh): the stored-but-uncounted piece's (row, head),
+  // and the counted one's with its count
+  int unrel_rh = -1, pend_rh = -1;
   unsigned pend_old = 0u;
 
   while (true) {
@@ -191,6 +193,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     const bool have_next = !chunk_last || lb > 0;
     const UnitMeta nxt = !chunk_last ? sh(ma, i + 1) : (lb > 0 ? sh(mb, 0) : cur);
     const bool piece_end = chunk_last || nxt.row != cur.row || nxt.head != cur.head;
+    if (p.fused && piece_end && (unrel_rh >= 0 || pend_rh >= 0)) {
+#ifdef FK_TIMELINE
+      const unsigned long long tf0 = global_ns();
+#endif
+      fused_private_step(a, p, unrel_rh, pend_rh, pend_old, lane);
+#ifdef FK_TIMELINE
+      if (lane == 0 && blockIdx.x < 1024) atomicAdd(&fk_tl_cta_priv[layer & 1][blockIdx.x][3], global_ns() - tf0);
+#endif
+    }
     if (piece_end && have_next) fetch_q(qn, nxt.row, nxt.head);
     const int s = (int)(seq % STAGES);
     mbar_wait(&full[warp][s], (seq / STAGES) & 1);
@@ -270,17 +281,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
         for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][0], o[nt][1]);
         if (t4 == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
-      if (p.fused) {  // settle the previous piece's arrival, then count this one
-#ifdef FK_TIMELINE
-        const unsigned long long tf0 = global_ns();
-#endif
-        if (pend_rh >= 0) fused_arrive_resolve(a, p, pend_rh, pend_old, lane);
-        pend_rh = (int)rh;
-        pend_old = fused_arrive_issue(a, (int)rh, lane);
-#ifdef FK_TIMELINE
-        if (lane == 0 && blockIdx.x < 1024) atomicAdd(&fk_tl_cta_priv[layer & 1][blockIdx.x][3], global_ns() - tf0);
-#endif
-      }
+      unrel_rh = (int)rh;
       m = -INFINITY;
       l = 0.f;
 #pragma unroll
@@ -308,10 +309,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
 #ifdef FK_TIMELINE
   if (lane == 0) CTA_TL_NOTE(fk_tl_cta_priv, layer, 2, global_ns());
 #endif
+#ifdef FK_TIMELINE
+  const unsigned long long tl0 = global_ns();
+#endif
   if (p.fused) {
-    if (pend_rh >= 0) fused_arrive_resolve(a, p, pend_rh, pend_old, lane);
+    fused_private_step(a, p, unrel_rh, pend_rh, pend_old, lane);  // count the last piece
+    fused_private_step(a, p, unrel_rh, pend_rh, pend_old, lane);  // settle it
     fused_leave(a, p, gw, gridDim.x * WARPS, lane);
   }
+#ifdef FK_TIMELINE
+  if (lane == 0 && blockIdx.x < 1024) atomicAdd(&fk_tl_cta_priv[layer & 1][blockIdx.x][3], (global_ns() - tl0) << 32);
+#endif
   CTA_TL_END(fk_tl_cta_priv, layer);
 }
 

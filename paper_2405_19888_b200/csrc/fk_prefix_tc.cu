@@ -620,8 +620,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             if (warp == 4 && lane == 0) TL(242 + min(c.qi, 3) * 4);
             if (half == 0 && lead && real) {
               a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
-              // fused merge: both halves' stores precede this release (bar.sync)
-              if (p.fused) fused_arrive_tc_row(a, p, r * H + head, p.tc_chunk_rowbase[chunk] + my_q);
+              // fused merge: a dynamic chunk's rows are counted here (both
+              // halves' stores precede this release: bar.sync); the static
+              // chunks' rows at the end of the CTA, in one batch
+              if (p.fused && chunk >= p.tc_static_chunks)
+                fused_arrive_tc_row(a, p, r * H + head, p.tc_chunk_rowbase[chunk] + my_q);
             }
           };
           if (r16) epilogue(BoolC<true>{});
@@ -649,7 +652,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     // rows this CTA completed after their owners had left (fk_common.cuh):
     // its static chunks' slots, and (last CTA out) the dynamic chunks'
     const int b = blockIdx.x;
-    const int s0 = p.tc_chunk_rowbase[p.tc_cta_chunk0[b]], s1 = p.tc_chunk_rowbase[p.tc_cta_chunk0[b + 1]];
+    const int c0 = p.tc_cta_chunk0[b], c1 = p.tc_cta_chunk0[b + 1];
+    const int s0 = p.tc_chunk_rowbase[c0], s1 = p.tc_chunk_rowbase[c1];
+    // count the static chunks' rows (their partials were stored before the
+    // __syncthreads above; the fence releases them), one row per thread
+    fence_acq_rel();
+    for (int sl = s0 + (int)threadIdx.x; sl < s1; sl += kTcThreads) {
+      int ck = c0;
+      while (p.tc_chunk_rowbase[ck + 1] <= sl) ++ck;
+      const int it = p.tc_chunk_item[ck];
+      const int rh = p.qrows[p.it_q_off[it] + (sl - p.tc_chunk_rowbase[ck])] * H + p.it_head[it];
+      if (atomicAdd(mctl_cnt(a) + rh, 1u) + 1u == (unsigned)p.row_head_count[rh]) {
+        fence_sc();
+        if (*(volatile unsigned*)(mctl_left(a) + rh % p.priv_warps) == p.fused_epoch)
+          mctl_orphans(a)[sl] = (unsigned)rh + 1u;
+      }
+    }
+    __syncthreads();
     fused_merge_orphans(a, p, s0, s1, warp, kTcThreads / 32, lane);
     __syncthreads();  // every warp has read the slots; this CTA's marks precede thread 0's release
     for (int i = s0 + (int)threadIdx.x; i < s1; i += kTcThreads) mctl_orphans(a)[i] = 0u;
