@@ -132,3 +132,23 @@ def test_block_twin_matches_reference_store():
             assert twin.grow(cid, n) == ok
             assert twin.blocks[cid] == ctxs[cid].block_ids
             assert (twin.used, twin.peak) == (ref.used_blocks, ref.peak_used)
+
+
+def test_attend_matches_torch_sdpa_fp64():
+    """The attention oracle is plain softmax(q k^T / sqrt(D)) v: an
+    independent implementation (torch.nn.functional.scaled_dot_product_attention
+    on the CPU, fp64) gives the same rows, including a peaky (K x 8) case and
+    one-token / page-boundary lengths."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    for T, kscale in ((1, 1.0), (16, 1.0), (17, 8.0), (300, 1.0), (300, 8.0)):
+        q = O.bf16_round(rng.standard_normal((4, 128), dtype=np.float32))
+        k = O.bf16_round(rng.standard_normal((T, 4, 128), dtype=np.float32) * kscale)
+        v = O.bf16_round(rng.standard_normal((T, 4, 128), dtype=np.float32))
+        got = O.attend(q, k, v)
+        tq = torch.from_numpy(q.astype(np.float64))[:, None, :]           # [H, 1, D]
+        tk = torch.from_numpy(k.astype(np.float64)).permute(1, 0, 2)      # [H, T, D]
+        tv = torch.from_numpy(v.astype(np.float64)).permute(1, 0, 2)
+        want = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv)[:, 0, :].numpy()
+        assert np.abs(got - want).max() < 1e-12, (T, kscale)
