@@ -29,8 +29,11 @@ thread_local std::vector<LaunchRec>* g_launch_rec = nullptr;
 // SWIZZLE_128B boxes {64 dims, 16 tokens}: K lo/hi, V lo/hi = 8 KiB per
 // page).  Slow SMs simply take fewer chunks, and CTAs that only get an SM
 // when the tcgen05 prefix CTAs retire take the leftovers -- no static tail.
-// Per page: S = q.K^T and O += P.V on mma.sync m16n8k16 with the single
-// query in row 0, online softmax on the row-0 fragments, P split hi+lo.
+// Per page, transposed so that M = 16 is the page's tokens / a 16-dim slice:
+// S^T = K.q^T (8 mma.sync m16n8k16, the K tile as stored is the A operand)
+// and o^T += V^T.p^T (8 x 2, V^T through ldmatrix.trans, P split hi+lo);
+// the single query is column 0.  Half the MMAs of the q-in-row-0 form
+// (measured +2 to +3 % per step).
 // A chunk always ends a piece: (row, head, chunk) -> one partial slot
 // row_head_base + (chunk - first chunk of the item), fixed by the plan.
 constexpr int kPwStageBytes = 8192;
@@ -164,8 +167,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   };
   issue_ahead();
 
-  // q as the A operand: row 0 of a 16 x 128 tile (lanes 0-3 hold it);
-  // the next piece's q is prefetched one page ahead into qn
+  // q^T as the B operand of S^T = K . q^T: column 0 of a 128 x 8 tile
+  // (lanes 0-3 hold it); the next piece's q is prefetched one page ahead into qn
   uint32_t qa[8][2], qn[8][2];
   auto fetch_q = [&](uint32_t (&dst)[8][2], int row, int head) {
     const uint32_t* Q = reinterpret_cast<const uint32_t*>(q + ((long long)row * H + head) * kHeadDim);
@@ -177,9 +180,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   };
   UnitMeta cur = sh(ma, 0);
   fetch_q(qa, cur.row, cur.head);
-  float o[16][4];
+  float o[8][4];  // o^T tiles: dims 16 mt + g (c0) and 16 mt + g + 8 (c2), column 0 (lanes t4 == 0)
 #pragma unroll
-  for (int k = 0; k < 16; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
+  for (int k = 0; k < 8; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
   float m = -INFINITY, l = 0.f;
   const int mi = lane >> 3, ri = lane & 7;
   // fused merge (fk_common.cuh): the stored-but-uncounted piece's (row, head),
@@ -207,60 +210,50 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     mbar_wait(&full[warp][s], (seq / STAGES) & 1);
     const uint32_t Ks = smem_u32(ring + s * kPwStageBytes);
     const uint32_t Vs = Ks + 4096;
-    float sc[2][4];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) sc[k][0] = sc[k][1] = sc[k][2] = sc[k][3] = 0.f;
+    // transposed products, M = the page's 16 tokens / 16 head dims:
+    // S^T = K . q^T (8 MMAs; the K tile is the A operand as stored) and
+    // o^T += V^T . p^T (8 x 2 MMAs; V^T by ldmatrix.trans).  Column 0 of
+    // each C tile is real: lanes t4 == 0 hold token / dim g and g + 8.
+    float st[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int kt = 0; kt < 8; ++kt) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(Ks + sw_page((mi >> 1) * 8 + ri, 2 * kt + (mi & 1)), b0, b1, b2, b3);
-      const uint32_t af[4] = {qa[kt][0], 0u, qa[kt][1], 0u};
-      mma_bf16(sc[0], af, b0, b1);
-      mma_bf16(sc[1], af, b2, b3);
+      uint32_t r0, r1, r2, r3;
+      ldsm_x4(Ks + sw_page((mi >> 1) * 8 + ri, 2 * kt + (mi & 1)), r0, r1, r2, r3);
+      const uint32_t af[4] = {r0, r2, r1, r3};
+      mma_bf16(st, af, qa[kt][0], qa[kt][1]);
     }
-    // row-0 online softmax (lanes 0-3 carry the 16 scores)
-    float v[4];
-    float mx = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int tok = nt * 8 + 2 * t4 + e;
-        v[nt * 2 + e] = tok < cur.ntok ? sc[nt][e] * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, v[nt * 2 + e]);
-      }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const bool real = t4 == 0;
+    const float v0 = real && g < cur.ntok ? st[0] * scale_log2 : -INFINITY;
+    const float v1 = real && g + 8 < cur.ntok ? st[2] * scale_log2 : -INFINITY;
+    float mx = fmaxf(v0, v1);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    mx = __shfl_sync(0xffffffffu, mx, 0);
     const float m_new = fmaxf(m, mx);
     const float alpha = ex2(m - m_new);
     m = m_new;
-    float pr[4];
-    float ps = 0.f;
+    const float p0 = real ? ex2(v0 - m_new) : 0.f, p1 = real ? ex2(v1 - m_new) : 0.f;
+    l = l * alpha + (p0 + p1);
+    // p^T as the B operand: lane (g, t4) takes tokens 2 t4, 2 t4 + 1 (b0) and
+    // 2 t4 + 8, 2 t4 + 9 (b1); token t sits in lane 4 (t & 7)
+    const float x0 = __shfl_sync(0xffffffffu, p0, 8 * t4), x1 = __shfl_sync(0xffffffffu, p0, 8 * t4 + 4);
+    const float y0 = __shfl_sync(0xffffffffu, p1, 8 * t4), y1 = __shfl_sync(0xffffffffu, p1, 8 * t4 + 4);
+    const uint32_t ph0 = pack_bf16(x0, x1), ph1 = pack_bf16(y0, y1);
+    const uint32_t pl0 = pack_bf16(x0 - bf_lo(ph0), x1 - bf_hi(ph0));
+    const uint32_t pl1 = pack_bf16(y0 - bf_lo(ph1), y1 - bf_hi(ph1));
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      pr[e] = g == 0 ? ex2(v[e] - m_new) : 0.f;
-      ps += pr[e];
-    }
-    l = l * alpha + ps;
-    uint32_t ph[4], pl[4];
-    ph[0] = pack_bf16(pr[0], pr[1]);
-    ph[2] = pack_bf16(pr[2], pr[3]);
-    pl[0] = pack_bf16(pr[0] - bf_lo(ph[0]), pr[1] - bf_hi(ph[0]));
-    pl[2] = pack_bf16(pr[2] - bf_lo(ph[2]), pr[3] - bf_hi(ph[2]));
-    ph[1] = ph[3] = pl[1] = pl[3] = 0u;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
+    for (int k = 0; k < 8; ++k) {
       o[k][0] *= alpha;
-      o[k][1] *= alpha;
+      o[k][2] *= alpha;
     }
 #pragma unroll
-    for (int dp = 0; dp < 8; ++dp) {
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(Vs + sw_page((mi & 1) * 8 + ri, 2 * dp + (mi >> 1)), b0, b1, b2, b3);
-      mma_bf16(o[2 * dp], ph, b0, b1);
-      mma_bf16(o[2 * dp + 1], ph, b2, b3);
-      mma_bf16(o[2 * dp], pl, b0, b1);
-      mma_bf16(o[2 * dp + 1], pl, b2, b3);
+    for (int mt = 0; mt < 8; ++mt) {
+      uint32_t r0, r1, r2, r3;
+      ldsm_x4_t(Vs + sw_page((mi >> 1) * 8 + ri, 2 * mt + (mi & 1)), r0, r1, r2, r3);
+      const uint32_t af[4] = {r0, r1, r2, r3};
+      mma_bf16(o[mt], af, ph0, ph1);
+      mma_bf16(o[mt], af, pl0, pl1);
     }
     __syncwarp();  // every lane is done reading stage s
     ++i;
@@ -273,19 +266,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
       const int slot = p.row_head_base[rh] + (ca - p.priv_rh_chunk0[rh]);
       const long long pi = part_index(p, H, row, slot, head);
       float lsum = l;
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
-      lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-      if (g == 0) {
-        float2* po = reinterpret_cast<float2*>(a.part_o + pi * kHeadDim);
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 4);
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 8);
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
+      if (t4 == 0) {
+        float* po = a.part_o + pi * kHeadDim;
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt) po[nt * 4 + t4] = make_float2(o[nt][0], o[nt][1]);
-        if (t4 == 0) a.part_ml[pi] = make_float2(m, lsum);
+        for (int mt = 0; mt < 8; ++mt) {
+          po[mt * 16 + g] = o[mt][0];
+          po[mt * 16 + g + 8] = o[mt][2];
+        }
+        if (g == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
       unrel_rh = (int)rh;
       m = -INFINITY;
       l = 0.f;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
+      for (int k = 0; k < 8; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
 #pragma unroll
       for (int kt = 0; kt < 8; ++kt) {
         qa[kt][0] = qn[kt][0];
