@@ -16,7 +16,7 @@ constexpr int kTcQBlock = 128; // queries per tcgen05 prefix CTA (M = 128 rows)
 constexpr int kMmaTilePages = 4;  // 64-token KV tile for the mma.sync path
 constexpr int kTcTilePages = 8;   // 128-token KV tile for the tcgen05 path
 constexpr int kTcMaxChunk = 24;   // largest tcgen05 chunk (tiles)
-constexpr int kPrivWarpsPerCta = 8;  // private kernel default shape: 8 warps per CTA x 3 stages
+constexpr int kPrivWarpsPerCta = 10;  // private kernel default shape: 10 warps per CTA x 2 stages (measured best)
 constexpr int kPrivMinChunk = 2;     // private guided schedule: smallest chunk (pages), default
 constexpr int kPrivMaxChunk = 32;    // largest chunk (one lane-parallel metadata load)
 
@@ -72,7 +72,7 @@ struct PlanDev {
   int priv_np;                 // number of private page entries (NPT)
   int priv_units;              // U = H * NPT
   int priv_nchunks;
-  int priv_wpc;                // warps per private CTA (ring shape: 8 -> 3 stages, 6 -> 4, 12 -> 2)
+  int priv_wpc;                // warps per private CTA (ring shape: 10 -> 2 stages, 8/9 -> 3, 6/7 -> 4, 12/14 -> 2)
   int priv_warps;              // grid warps (grid = priv_warps / priv_wpc)
   int priv_static;             // warps that start on chunk = warp index (the ones that start at once)
   const int* priv_chunk_start; // [priv_nchunks + 1]

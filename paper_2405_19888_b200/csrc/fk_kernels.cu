@@ -708,12 +708,16 @@ static cudaError_t launch_private_shape(const ArenaDev& a, const PlanDev& p, int
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
                            const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl, cudaStream_t s) {
   if (p.priv_units == 0) return cudaSuccess;
-  // ring shapes: per-warp stages x warps per CTA (192 KiB of stages; 7 x 4 = 224 KiB)
+  // ring shapes: per-warp stages x warps per CTA (8 KiB stages: 10 x 2 = 160 KiB, the
+  // default; 8 x 3 and 12 x 2 = 192 KiB; 7 x 4 = 224 KiB)
   switch (p.priv_wpc) {
     case 6: return launch_private_shape<4, 6>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 7: return launch_private_shape<4, 7>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 9: return launch_private_shape<3, 9>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 12: return launch_private_shape<2, 12>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    default: return launch_private_shape<3, 8>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 14: return launch_private_shape<2, 14>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 8: return launch_private_shape<3, 8>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    default: return launch_private_shape<2, 10>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
   }
 }
 
