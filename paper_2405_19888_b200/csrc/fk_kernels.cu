@@ -31,9 +31,10 @@ thread_local std::vector<LaunchRec>* g_launch_rec = nullptr;
 // when the tcgen05 prefix CTAs retire take the leftovers -- no static tail.
 // Per page, transposed so that M = 16 is the page's tokens / a 16-dim slice:
 // S^T = K.q^T (8 mma.sync m16n8k16, the K tile as stored is the A operand)
-// and o^T += V^T.p^T (8 x 2, V^T through ldmatrix.trans, P split hi+lo);
-// the single query is column 0.  Half the MMAs of the q-in-row-0 form
-// (measured +2 to +3 % per step).
+// and o^T += V^T.[p_hi p_lo]^T (8, V^T through ldmatrix.trans; P split hi +
+// lo into B columns 0 and 1, summed at the end): 16 MMAs per page against
+// 48 in the q-in-row-0 form (measured +2 to +3 %, and +0.6 % for the column
+// trick).
 // A chunk always ends a piece: (row, head, chunk) -> one partial slot
 // row_head_base + (chunk - first chunk of the item), fixed by the plan.
 constexpr int kPwStageBytes = 8192;
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   };
   UnitMeta cur = sh(ma, 0);
   fetch_q(qa, cur.row, cur.head);
-  float o[8][4];  // o^T tiles: dims 16 mt + g (c0) and 16 mt + g + 8 (c2), column 0 (lanes t4 == 0)
+  float o[8][4];  // o^T tiles, lanes t4 == 0: dims 16 mt + g (c0 hi, c1 lo) and 16 mt + g + 8 (c2, c3)
 #pragma unroll
   for (int k = 0; k < 8; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
   float m = -INFINITY, l = 0.f;
@@ -212,8 +213,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     const uint32_t Vs = Ks + 4096;
     // transposed products, M = the page's 16 tokens / 16 head dims:
     // S^T = K . q^T (8 MMAs; the K tile is the A operand as stored) and
-    // o^T += V^T . p^T (8 x 2 MMAs; V^T by ldmatrix.trans).  Column 0 of
-    // each C tile is real: lanes t4 == 0 hold token / dim g and g + 8.
+    // o^T += V^T . [p_hi p_lo]^T (8 MMAs; V^T by ldmatrix.trans).  Lanes
+    // t4 == 0 hold the real columns: token / dim g and g + 8.
     float st[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int kt = 0; kt < 8; ++kt) {
@@ -242,18 +243,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     const uint32_t ph0 = pack_bf16(x0, x1), ph1 = pack_bf16(y0, y1);
     const uint32_t pl0 = pack_bf16(x0 - bf_lo(ph0), x1 - bf_hi(ph0));
     const uint32_t pl1 = pack_bf16(y0 - bf_lo(ph1), y1 - bf_hi(ph1));
+    // P hi in column 0 and P lo in column 1 of one B operand (lanes g = 0 and
+    // g = 1): one MMA per 16-dim slice; o = column 0 + column 1 at the end
+    const uint32_t pb0 = g == 1 ? pl0 : ph0, pb1 = g == 1 ? pl1 : ph1;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       o[k][0] *= alpha;
+      o[k][1] *= alpha;
       o[k][2] *= alpha;
+      o[k][3] *= alpha;
     }
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) {
       uint32_t r0, r1, r2, r3;
       ldsm_x4_t(Vs + sw_page((mi >> 1) * 8 + ri, 2 * mt + (mi & 1)), r0, r1, r2, r3);
       const uint32_t af[4] = {r0, r1, r2, r3};
-      mma_bf16(o[mt], af, ph0, ph1);
-      mma_bf16(o[mt], af, pl0, pl1);
+      mma_bf16(o[mt], af, pb0, pb1);
     }
     __syncwarp();  // every lane is done reading stage s
     ++i;
@@ -273,8 +278,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
         float* po = a.part_o + pi * kHeadDim;
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
-          po[mt * 16 + g] = o[mt][0];
-          po[mt * 16 + g + 8] = o[mt][2];
+          po[mt * 16 + g] = o[mt][0] + o[mt][1];
+          po[mt * 16 + g + 8] = o[mt][2] + o[mt][3];
         }
         if (g == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
