@@ -244,13 +244,12 @@ __device__ __forceinline__ int partial_count(const PlanDev& p, int H, int row, i
 // output; one warp, 4 head-dim elements per lane.  Rows with no token at
 // all (no partial) produce zeros.
 __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
-                                                    __nv_bfloat16* out, float* out_f32, int lane) {
+                                                    __nv_bfloat16* out, float* out_f32, int lane, int ns) {
   // two dependent rounds: (m, l) of every slot lane-parallel (slot k in lane
   // k % 32 of round k / 32, up to kMergeRounds rounds in registers), then
   // every slot's o (4 dims per lane), 8 slots' loads in flight at a time
   constexpr int kMergeRounds = 4;  // up to 128 partials per (row, head)
   const int H = a.num_heads;
-  const int ns = partial_count(p, H, row, head);
   const long long base = part_index(p, H, row, 0, head);  // slot stride is H
   constexpr int kMergeEarly = 8;
   float4 v0[kMergeEarly];
@@ -329,6 +328,10 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
   const float4 r = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   *reinterpret_cast<uint2*>(out + oi) = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
   if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = r;
+}
+__device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
+                                                    __nv_bfloat16* out, float* out_f32, int lane) {
+  merge_row_head_warp(a, p, row, head, out, out_f32, lane, partial_count(p, a.num_heads, row, head));
 }
 
 // ------------------------------------------------------------ fused merge

@@ -538,14 +538,16 @@ CTA_TL_DECL(fk_tl_cta_merge);
 __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __nv_bfloat16* __restrict__ out,
                                                       float* __restrict__ out_f32, int layer) {
   CTA_TL_START(fk_tl_cta_merge, layer);  // (timeline builds: [0] = after the wait)
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int H = a.num_heads;
+  const bool mine = w < p.num_rows * H;
+  const int ns = mine ? partial_count(p, H, w / H, w % H) : 0;  // plan data: before the wait
   pdl_wait_primary();       // partials of the prefix and private grids are complete
   pdl_launch_dependents();  // the next layer's first kernel may start (other partial half)
 #ifdef FK_TIMELINE
   if (threadIdx.x == 0 && blockIdx.x < 1024) fk_tl_cta_merge[layer & 1][blockIdx.x][0] = global_ns();
 #endif
-  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int H = a.num_heads;
-  if (w < p.num_rows * H) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane);
+  if (mine) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane, ns);
   CTA_TL_END(fk_tl_cta_merge, layer);
 }
 
