@@ -80,11 +80,6 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                                  uint64_t* bar, uint64_t pol) {
   asm volatile(
@@ -335,12 +330,16 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
 }
 
 // ------------------------------------------------------------ fused merge
-// Every partial writer counts its arrival on (row, head) with an acq_rel
-// atomic (release: its partial stores -- and, through the warp / CTA barrier
-// before it, its partners' -- precede the count; acquire: the last one sees
-// every other partial).  Who merges:
-//  * a private warp whose arrival was the last merges the row (the atomic's
-//    result is consumed one piece later, so its latency hides under the next
+// (FK_OPT_FUSED_MERGE=1; measured slower than the merge kernel.)
+// Every partial counts as an arrival on its (row, head) counter, released
+// after the partial's stores (and, through the warp / CTA barrier before
+// it, its partners') and acquired by whoever sees the final count: private
+// warps count a piece one piece late behind an acq_rel fence
+// (fused_private_step), tcgen05 CTAs count their static chunks' rows in one
+// batch behind a fence at the end, and a dynamic chunk's rows at its end
+// with acq_rel atomics.  Who merges:
+//  * a private warp whose arrival was the last merges the row (the count's
+//    result is read one piece later, so its latency hides under the next
 //    piece's loads);
 //  * a row completed by a tcgen05 piece is merged by its owner, private warp
 //    rh % grid_warps, when that warp leaves -- unless the owner has already
