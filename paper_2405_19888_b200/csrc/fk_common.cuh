@@ -238,15 +238,16 @@ __device__ __forceinline__ int partial_count(const PlanDev& p, int H, int row, i
 // Merge all partials of (row, head) into the bf16 (and optional fp32)
 // output; one warp, 4 head-dim elements per lane.  Rows with no token at
 // all (no partial) produce zeros.
+template <int kMergeEarly = 8>
 __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
                                                     __nv_bfloat16* out, float* out_f32, int lane, int ns) {
-  // two dependent rounds: (m, l) of every slot lane-parallel (slot k in lane
-  // k % 32 of round k / 32, up to kMergeRounds rounds in registers), then
-  // every slot's o (4 dims per lane), 8 slots' loads in flight at a time
+  // (m, l) of every slot lane-parallel (slot k in lane k % 32 of round k /
+  // 32, up to kMergeRounds rounds in registers) and the o (4 dims per lane)
+  // of the first kMergeEarly slots in one memory round trip; any further
+  // slots' o 8 at a time
   constexpr int kMergeRounds = 4;  // up to 128 partials per (row, head)
   const int H = a.num_heads;
   const long long base = part_index(p, H, row, 0, head);  // slot stride is H
-  constexpr int kMergeEarly = 8;
   float4 v0[kMergeEarly];
 #pragma unroll
   for (int k = 0; k < kMergeEarly; ++k)
@@ -326,7 +327,7 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
 }
 __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const PlanDev& p, int row, int head,
                                                     __nv_bfloat16* out, float* out_f32, int lane) {
-  merge_row_head_warp(a, p, row, head, out, out_f32, lane, partial_count(p, a.num_heads, row, head));
+  merge_row_head_warp<8>(a, p, row, head, out, out_f32, lane, partial_count(p, a.num_heads, row, head));
 }
 
 // ------------------------------------------------------------ fused merge
