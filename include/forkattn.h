@@ -115,7 +115,7 @@ enum {
   FK_OPT_TC_MIN_CHUNK = 10,   /* chunk size (128-token tiles) of the tcgen05 prefix kernel's dynamic
                                  tail, 1..24 (default 4) */
   FK_OPT_PRIV_WARPS = 11,     /* private CTA shape: 10 warps x 2 stages (default), 6 x 4, 7 x 4,
-                                 8 x 3, 9 x 3, 12 x 2 or 14 x 2 */
+                                 8 x 3, 9 x 3, 11 x 2, 12 x 2 or 14 x 2 */
   FK_OPT_GRAPH = 12,          /* 1 (default): fk_attn_decode_layers replays its launches as a CUDA
                                  graph (captured once per launch structure, parameters updated in
                                  place afterwards); 0: direct launches */

@@ -721,6 +721,7 @@ cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const
     case 6: return launch_private_shape<4, 6>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 7: return launch_private_shape<4, 7>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 9: return launch_private_shape<3, 9>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 11: return launch_private_shape<2, 11>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 12: return launch_private_shape<2, 12>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 14: return launch_private_shape<2, 14>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
     case 8: return launch_private_shape<3, 8>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);

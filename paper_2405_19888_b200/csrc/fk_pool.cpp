@@ -426,8 +426,8 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_GRAPH: p->use_graph = value != 0; break;
     case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
     case FK_OPT_PRIV_WARPS:
-      if (value != 6 && value != 7 && value != 8 && value != 9 && value != 10 && value != 12 && value != 14)
-        return fail(FK_INVALID_ARGUMENT, "private warps must be 6, 7, 8, 9, 10, 12 or 14");
+      if (value < 6 || value > 14 || value == 13)
+        return fail(FK_INVALID_ARGUMENT, "private warps must be 6 to 12 or 14");
       p->priv_wpc = value;
       break;
     case FK_OPT_TC_MIN_CHUNK: p->tc_min_chunk = std::min<int64_t>(kTcMaxChunk, std::max<int64_t>(1, value)); break;

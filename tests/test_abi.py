@@ -166,4 +166,8 @@ def test_options_validate():
                      (_lib.FK_OPT_TC_DYN_PCT, 20), (_lib.FK_OPT_TC_BOUNDARY_COST, 2), (_lib.FK_OPT_FUSED_MERGE, 0)):
         assert L.fk_pool_set_option(h, opt, val) == _lib.FK_OK
     assert L.fk_pool_set_option(h, 999, 1) == _lib.FK_INVALID_ARGUMENT
+    for warps in (6, 7, 8, 9, 10, 11, 12, 14):
+        assert L.fk_pool_set_option(h, _lib.FK_OPT_PRIV_WARPS, warps) == _lib.FK_OK
+    for warps in (5, 13, 15):
+        assert L.fk_pool_set_option(h, _lib.FK_OPT_PRIV_WARPS, warps) == _lib.FK_INVALID_ARGUMENT
     L.fk_pool_destroy(h)

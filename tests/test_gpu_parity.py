@@ -426,10 +426,10 @@ def test_prefix_chunk_queue_wraps(cuda_device, min_chunk):
     check_history(eng)
 
 
-@pytest.mark.parametrize("warps", [6, 7, 8, 9, 12, 14])
+@pytest.mark.parametrize("warps", [6, 7, 8, 9, 11, 12, 14])
 def test_private_ring_shapes(cuda_device, warps):
     """FK_OPT_PRIV_WARPS: every private CTA shape besides the default 10 x 2
-    (6/7 warps x 4 stages, 8/9 x 3, 12/14 x 2) gives the same attention."""
+    (6/7 warps x 4 stages, 8/9 x 3, 11/12/14 x 2) gives the same attention."""
     eng = make_engine(cuda_device, H=4, L=2)
     eng.set_option(_lib.FK_OPT_PRIV_WARPS, warps)
     fork_group(eng, 400, [33, 100, 7, 260], out_len=3)
