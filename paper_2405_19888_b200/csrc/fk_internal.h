@@ -54,6 +54,7 @@ struct PlanDev {
   int fused;                      // fused merge on this launch (set per launch)
   const int* tc_chunk_rowbase;    // [tc_nchunks + 1]: first orphan slot of each chunk (prefix sums of nq)
   int tc_active_ctas;             // tcgen05 CTAs with at least one static chunk
+  int tc_l2_share;                // CTAs b, b + X/k stream the same tiles together: default L2 policy
   unsigned fused_epoch;           // this launch's "left" value (fk_common.cuh; set per launch)
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]

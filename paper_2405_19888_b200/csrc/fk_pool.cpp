@@ -721,6 +721,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   std::vector<int32_t> ch_item, ch_t0, ch_t1, cta_chunk0;
   std::vector<int32_t> it_first_chunk(items.size(), 0);
   int64_t tc_ctas = 0, n_static = 0;
+  bool tc_l2_share = false;
   if (tc_units > 0) {
     // at least ~4 tiles per CTA unless FK_OPT_PREFIX_TARGET_CTAS says
     // otherwise: a CTA's start-up (TMEM, barriers, first loads) costs about that
@@ -741,39 +742,68 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
         ++i;
       }
     };
-    // cost-balanced static ranges over [0, u_s)
+    // cost-balanced static ranges over [lo, hi) for nx CTAs -> cut points
     const double bc = (double)p->tc_boundary_cost;
-    int64_t n_bound = 0;  // item starts strictly inside (0, u_s)
-    for (size_t i = num_mma + 1; i < items.size(); ++i) n_bound += it_unit_off[i] < u_s;
-    double rest = (double)u_s + bc * (double)n_bound;
-    std::vector<int64_t> cut{0};
-    double cost = 0.0;
-    size_t nxt_item = num_mma + 1;
-    for (int64_t u = 0; u < u_s;) {
-      const int64_t b = (int64_t)cut.size() - 1;  // current CTA
-      const double target = rest / (double)std::max<int64_t>(1, X - b);
-      const int64_t item_end = nxt_item < items.size() ? std::min<int64_t>(u_s, it_unit_off[nxt_item]) : u_s;
-      const bool last = (int64_t)cut.size() == X;
-      int64_t take = last ? item_end - u
-                          : std::min<int64_t>(item_end - u, std::max<int64_t>(1, std::llround(target - cost)));
-      u += take;
-      cost += (double)take;
-      if (u == item_end && nxt_item < items.size() && it_unit_off[nxt_item] == u && u < u_s) {
-        ++nxt_item;
-        if (!last && target - cost < 0.5) {  // close the CTA at the item boundary
-          rest -= cost + bc;
+    auto split = [&](int64_t lo, int64_t hi, int64_t nx, std::vector<int64_t>& cut) {
+      size_t nxt_item = num_mma;
+      while (nxt_item < items.size() && it_unit_off[nxt_item] <= lo) ++nxt_item;
+      int64_t n_bound = 0;  // item starts strictly inside (lo, hi)
+      for (size_t i = nxt_item; i < items.size(); ++i) n_bound += it_unit_off[i] < hi;
+      double rest = (double)(hi - lo) + bc * (double)n_bound;
+      const size_t first = cut.size();
+      cut.push_back(lo);
+      double cost = 0.0;
+      int64_t u = lo;
+      while (u < hi) {
+        const int64_t b = (int64_t)(cut.size() - first) - 1;  // current CTA
+        const double target = rest / (double)std::max<int64_t>(1, nx - b);
+        const int64_t item_end = nxt_item < items.size() ? std::min<int64_t>(hi, it_unit_off[nxt_item]) : hi;
+        const bool last = (int64_t)(cut.size() - first) == nx;
+        int64_t take = last ? item_end - u
+                            : std::min<int64_t>(item_end - u, std::max<int64_t>(1, std::llround(target - cost)));
+        u += take;
+        cost += (double)take;
+        if (u == item_end && nxt_item < items.size() && it_unit_off[nxt_item] == u && u < hi) {
+          ++nxt_item;
+          if (!last && target - cost < 0.5) {  // close the CTA at the item boundary
+            rest -= cost + bc;
+            cut.push_back(u);
+            cost = 0.0;
+          } else {
+            cost += bc;  // this CTA starts another piece
+          }
+        } else if (!last && u < hi && target - cost < 0.5) {
+          rest -= cost;
           cut.push_back(u);
           cost = 0.0;
-        } else {
-          cost += bc;  // this CTA starts another piece
         }
-      } else if (!last && u < u_s && target - cost < 0.5) {
-        rest -= cost;
-        cut.push_back(u);
-        cost = 0.0;
       }
+    };
+    // One shared context with k >= 2 query blocks (> 128 forks): its unit
+    // list is k identical groups (block-major item order above).  Split
+    // group 0 over X / k CTAs and give group g the same ranges on CTAs
+    // b + g X / k, so the k CTAs reading a tile read it at about the same
+    // time and all but the first hit L2 (the loads then keep the default
+    // L2 policy: PlanDev::tc_l2_share).
+    int64_t mirror_k = 0;
+    if (p->tc_dyn_pct == 0 && shared.size() == 1 && shared[0].tc && shared[0].splits == 1) {
+      const int64_t k = ((int64_t)shared[0].rows.size() + kTcQBlock - 1) / kTcQBlock;
+      if (k >= 2 && X >= 2 * k && (int64_t)(items.size() - num_mma) == k * H && tc_units % k == 0) mirror_k = k;
     }
-    cut.push_back(u_s);
+    std::vector<int64_t> cut;
+    if (mirror_k) {
+      const int64_t ug = tc_units / mirror_k, xg = X / mirror_k;
+      std::vector<int64_t> c0;
+      split(0, ug, xg, c0);
+      c0.push_back(ug);
+      for (int64_t g = 0; g < mirror_k; ++g)
+        for (size_t j = 0; j + 1 < c0.size(); ++j) cut.push_back(c0[j] + g * ug);
+      cut.push_back(tc_units);
+    } else {
+      split(0, u_s, X, cut);
+      cut.push_back(u_s);
+    }
+    tc_l2_share = mirror_k > 0;
     tc_ctas = (int64_t)cut.size() - 1;
     for (int64_t b = 0; b < tc_ctas; ++b) {
       cta_chunk0.push_back((int32_t)ch_item.size());
@@ -1115,6 +1145,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.fused = 0;
   pd.tc_chunk_rowbase = (const int32_t*)(d + o_crb);
   pd.tc_active_ctas = tc_active;
+  pd.tc_l2_share = tc_l2_share ? 1 : 0;
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
   pd.row_priv_npages = drb + nb;

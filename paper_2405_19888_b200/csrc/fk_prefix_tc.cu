@@ -279,10 +279,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         for (int j = 1; j < kTcTilePages; ++j) run = run && pl[j] == pl[0] + j;
         auto load_tile = [&](uint8_t* st, int plane, uint64_t* bar) {
           mbar_expect_tx(bar, kTcTilePages * 2 * 2048);
-          // evict-first: a tile is read once per layer (with more than one
-          // query block, by CTAs streaming it at about the same time);
-          // measured +3-4 % per step
-          const uint64_t pol = l2_policy_evict_first();
+          // evict-first: a tile is read once per layer (measured +3-4 % per
+          // step); with mirrored query-block CTAs (tc_l2_share) the default
+          // policy, so the partner CTA's read of the tile hits L2
+          const uint64_t pol = p.tc_l2_share ? l2_policy_evict_normal() : l2_policy_evict_first();
           if (run) {
             tma_load_3d_hint(st, &tmap_run, 0, pl[0] * kPage, plane, bar, pol);
             tma_load_3d_hint(st + kTcHalf, &tmap_run, 64, pl[0] * kPage, plane, bar, pol);
