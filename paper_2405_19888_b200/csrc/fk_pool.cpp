@@ -659,11 +659,9 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       const int nq = (int)s.rows.size();
       const int psr = s.tc ? np : ((np + s.splits - 1) / s.splits + kMmaTilePages - 1) / kMmaTilePages * kMmaTilePages;
       // items are (query block, head) with the head innermost: with more than
-      // one query block (> 128 forks) the cost-balanced split puts block k of
-      // head h on a CTA as far into its range as block 0 of head h is on
-      // another, so both stream the same pages at about the same time and the
-      // second read can hit L2 (measured +1.5 % at B = 256 against blocks of
-      // one head back to back, whose re-read comes ~47 us later, past L2)
+      // one query block (> 128 forks) the unit list is k identical groups,
+      // which the static split below mirrors so that the k CTAs reading a
+      // tile read it together (the later reads hit L2)
       for (int sp = 0; sp < s.splits; ++sp) {
         const int p0 = sp * psr, p1 = std::min(np, p0 + psr);
         const int64_t t1 = std::min<int64_t>(c.tokens, (int64_t)p1 * kPage);
