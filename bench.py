@@ -46,6 +46,11 @@ CONFIGS = {
     "mapreduce_13b": dict(model="LLaMA-13B", L=40, H=40, P=2000, B=32, S=None, groups=2),
     # BASELINE.json configs[4]: nested 4k -> 1k -> 64 users x 256 per GPU
     "nested_13b": dict(model="LLaMA-13B", L=40, H=40, P=4096, B=64, S=256, app=1024),
+    # the same two workloads at the BASELINE totals, dealt over the ranks
+    # (strong scaling): 16 map-reduce groups of 32 forks; 8 apps x 64 users
+    # (512 requests) under one 4k system prompt, replicated per GPU
+    "mapreduce_13b_16x32": dict(model="LLaMA-13B", L=40, H=40, P=2000, B=32, S=None, groups=16, strong=True),
+    "nested_13b_8apps": dict(model="LLaMA-13B", L=40, H=40, P=4096, B=64, S=256, app=1024, apps=8, strong=True),
 }
 DEFAULT_CONFIG = "llama13b_p6000_b64"
 
@@ -121,7 +126,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
-def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=4096):
+def rank_units(cfg, rank=0, world=1):
+    """Fork groups (map-reduce) or apps (nested) this rank serves: every one
+    at the per-GPU configs, a round-robin deal of the BASELINE totals over the
+    ranks at the strong-scaling ones (cluster.rank_groups)."""
+    from paper_2405_19888_b200.cluster import rank_groups
+
+    n = cfg.get("groups") or cfg.get("apps") or 1
+    return rank_groups(rank, n, world) if cfg.get("strong") else list(range(n))
+
+
+def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=4096, rank=0, world=1):
     import paper_2405_19888_b200 as P
     from paper_2405_19888_b200.workloads import drain_fills, fork_group, nested_forest
 
@@ -129,18 +144,23 @@ def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=409
     geo = P.ModelGeometry(L, H, 128)
     eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 30, device=device, geometry=geo,
                       model=P.SyntheticDecodeModel(seed))
+    units = rank_units(cfg, rank, world)
     if "app" in cfg:
-        nested_forest(eng, cfg["P"], cfg["app"], 1, cfg["S"], cfg["B"], out_len=out_len, seed=seed)
+        nested_forest(eng, cfg["P"], cfg["app"], len(units), cfg["S"], cfg["B"], out_len=out_len, seed=seed)
     elif cfg.get("groups"):
         import random
         rng = random.Random(0)
-        for gi in range(cfg["groups"]):
-            fork_group(eng, cfg["P"], [rng.randint(128, 1024) for _ in range(cfg["B"])], out_len=out_len,
-                       tag=f"g{gi}", seed=seed + gi)
+        lens = [[rng.randint(128, 1024) for _ in range(cfg["B"])] for _ in range(cfg["groups"])]
+        for gi in units:
+            fork_group(eng, cfg["P"], lens[gi], out_len=out_len, tag=f"g{gi}", seed=seed + gi)
     else:
         fork_group(eng, cfg["P"], [cfg["S"]] * cfg["B"], out_len=out_len, seed=seed)
     drain_fills(eng)
     rows = len(eng.gens)
+    # leaf tokens when the model rows take over (the parity check's oracle:
+    # positions >= n0 of a request's leaf hold its model K/V row)
+    eng.bench_leaf_n0 = {eng.contexts[g.context_id].uid: (eng.contexts[g.context_id].token_count, r)
+                         for r, g in enumerate(eng.gens.values())}
     # back the whole run's decode growth now, so no arena growth (a device-wide
     # copy) lands in the timed region
     st = eng.pool_stats()
@@ -207,6 +227,79 @@ def time_layers(eng, steps, torch):
     return start.elapsed_time(end) / 1e3 / (steps * L)
 
 
+def time_layers_isolated(eng, reps, torch):
+    """Per-layer attention as a model sees it: one fk_attn_decode per layer
+    (direct launches, no graph), PDL only between the layer's own kernels
+    (FK_OPT_PDL=1), and a foreign kernel between consecutive layers (the rest
+    of the transformer layer), so nothing of layer l+1 overlaps layer l.  The
+    foreign kernel's own time is measured alone and subtracted."""
+    from paper_2405_19888_b200 import _lib
+
+    L = eng.geometry.num_layers
+    rows = eng.last_plan.num_rows
+    H = eng.geometry.num_heads
+    q = eng.model.q
+    out = torch.empty_like(q)
+    le = rows * H * 128 * 2
+    st = eng.stream
+    sp = ctypes.c_void_p(st.cuda_stream)
+    foreign = torch.empty(1 << 16, dtype=torch.float32, device=q.device)
+    eng.set_option(_lib.FK_OPT_PDL, 1)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def one_pass(attn=True):
+        for layer in range(L):
+            if attn:
+                _lib.check(_lib.lib.fk_attn_decode(eng._pool.handle, layer, ctypes.c_void_p(q.data_ptr() + layer * le),
+                                                   ctypes.c_void_p(out.data_ptr() + layer * le), None, sp))
+            foreign.add_(1.0)
+
+    try:
+        with torch.cuda.stream(st):
+            one_pass()
+            start.record(st)
+            for _ in range(reps):
+                one_pass()
+            end.record(st)
+            end.synchronize()
+            t_all = start.elapsed_time(end) / 1e3
+            start.record(st)
+            for _ in range(reps):
+                one_pass(attn=False)
+            end.record(st)
+            end.synchronize()
+            t_foreign = start.elapsed_time(end) / 1e3
+    finally:
+        eng.set_option(_lib.FK_OPT_PDL, 2)
+    return (t_all - t_foreign) / (reps * L), t_foreign / (reps * L)
+
+
+def parity_check(eng, torch):
+    """Outside the timed region: one more GpuEngine.step on the benchmarked
+    engine (same plan path, kernels and CUDA graph as the timed steps) with the
+    fp32 pre-cast output captured; layers 0 and L-1 against the fp64 oracle
+    (the engine's synthetic prefill rows + the model's appended K/V rows)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from gpu_check import MAX_ABS, MEAN_REL_F32, REL_L2, check_history, tensor_model_oracle
+
+    eng.capture_f32, eng.keep_history = True, True
+    eng.history.clear()
+    eng.step()
+    eng.stream.synchronize()
+    eng.capture_f32, eng.keep_history = False, False
+    L = eng.geometry.num_layers
+    kv, queries = tensor_model_oracle(eng, eng.bench_leaf_n0)
+    t0 = time.perf_counter()
+    w = check_history(eng, layers=[0, L - 1], kv=kv, queries=queries, strict=False)
+    eng.history.clear()
+    return {"max_abs": w["max_abs"], "rel_l2": w["rel_l2"], "mean_rel_f32": w["mean_rel_f32"], "pass": w["pass"],
+            "layers": [0, L - 1], "rows": eng.last_plan.num_rows, "batch_tokens": int(eng.last_plan.batch_tokens),
+            "tolerance": {"max_abs": MAX_ABS, "rel_l2": REL_L2, "mean_rel_f32": MEAN_REL_F32},
+            "oracle": "fp64 un-decomposed softmax over each row's chain (oracle/forkattn_oracle.py attend_forest)",
+            "step": "one GpuEngine.step after the timed region (same plan path and graph)",
+            "check_s": round(time.perf_counter() - t0, 1)}
+
+
 def cpu_baseline(cfg, budget_s=12.0, impl_steps=None):
     """numpy fp32 oracle (matmul form) on the host cores for one layer of the
     workload; tokens/s extrapolated x L.  Returns (tokens/s, sample, cores, secs)."""
@@ -251,6 +344,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the post-run parity check against the oracle")
+    ap.add_argument("--no-isolated", action="store_true", help="skip the isolated-layer timing")
     ap.add_argument("--tc-min-fanout", type=int, default=None)
     ap.add_argument("--corun", type=int, default=None, help="FK_OPT_CORUN (default: library default, 1)")
     ap.add_argument("--prefix-rate-pct", type=int, default=None)
@@ -260,24 +355,36 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    strong = bool(cfg.get("strong"))
+    units = cfg.get("groups") or cfg.get("apps") or 1
     workload = dict(workload=args.config, model=cfg["model"], layers=cfg["L"], heads=cfg["H"], head_dim=128,
-                    prefix_tokens=cfg["P"], forks=cfg["B"] * cfg.get("groups", 1),
+                    prefix_tokens=cfg["P"], forks=cfg["B"] * units,
                     suffix_tokens=cfg["S"] if cfg["S"] else "U[128,1024]",
-                    per_gpu="one prefix-affinity group set per GPU (weak scaling)",
+                    per_gpu=("BASELINE totals dealt over the GPUs by whole fork group / app (strong scaling)"
+                             if strong else "one prefix-affinity group set per GPU (weak scaling)"),
                     l2="inputs larger than L2 (KV per layer >> 126 MB; layers stream distinct pages)",
                     parallelism=f"dp{args.gpus} (independent engines, no collective)")
+    if "app" in cfg:
+        workload["app_tokens"] = cfg["app"]
     metric = "shared-prefix decode attn tokens/s + HBM GB/s vs roofline, 1/2/4/8 B200"
 
     if args.impl == "reference":
         if rank != 0:
             return
-        rows = cfg["B"] * cfg.get("groups", 1)
+        rows = cfg["B"] * units
         c = dict(cfg, B=rows)
+        t0 = time.perf_counter()
         tok_s, sample, cores, t_layer = cpu_baseline(c, impl_steps=max(1, args.steps) + max(0, args.warmup))
+        # one "step" of this arm is one sampled layer (the whole 40-layer step
+        # would take minutes per step on the host); tokens/s is extrapolated
+        # to all L layers and says so
         line = {"metric": metric, "value": tok_s, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_layer * cfg["L"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "config": workload,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_layer,
+                "step_is": f"one sampled layer of the {cfg['L']}-layer step (median); value extrapolated x{cfg['L']}",
+                "extrapolated": True, "layer_ms": 1e3 * t_layer, "layers": cfg["L"],
+                "wall_s": round(time.perf_counter() - t0, 2),
+                "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic", "config": workload,
                 "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
                 "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -287,15 +394,20 @@ def main():
 
     dist = None
     if world > 1:
+        # the process group only carries the barrier and the out-of-region
+        # timing reductions (no collective on the data path): gloo on the
+        # host, so several ranks can even share one GPU (smoke tests)
         import torch.distributed as dist  # noqa: F811
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = local
+        dist.init_process_group("gloo")
+    device = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(device)
     from paper_2405_19888_b200 import _lib
+    from paper_2405_19888_b200.cluster import max_over_ranks, sum_over_ranks
 
-    eng, rows = build_engine(cfg, device, torch, out_len=2 * (args.steps + args.warmup) + 64)
+    out_len = 2 * (args.steps + args.warmup) + 64
+    eng, rows = build_engine(cfg, device, torch, out_len=out_len, rank=rank, world=world)
+
     def apply_options(e):
         if args.tc_min_fanout is not None:
             e.set_option(_lib.FK_OPT_TC_MIN_FANOUT, args.tc_min_fanout)
@@ -315,37 +427,38 @@ def main():
     torch.cuda.synchronize(device)
 
     def barrier():
+        torch.cuda.synchronize(device)
         if dist is not None:
             dist.barrier()
-        torch.cuda.synchronize(device)
-
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=torch.device("cuda", device))
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     barrier()
     clocks.mark()
     t_steps = time_steps(eng, args.steps, torch)
     barrier()
+    info = eng.last_plan
+    batch_tokens = int(info.batch_tokens)
+    bytes_layer = alg_bytes_per_layer(info, rows, H)
+    plan_line = {"rows": info.num_rows, "shared_ctx": info.num_shared_ctx, "prefix_ctas": info.num_prefix_ctas,
+                 "max_slots": info.max_slots, "tc_items": info.num_tc_items, "mma_items": info.num_mma_items}
     # per-layer attention alone for the roofline (same plan as the last step)
     t_layer = time_layers(eng, max(args.steps // 2, 3), torch)
     barrier()
     clk = clocks.stop()
+    iso = None
+    if not args.no_isolated:
+        t_iso, t_foreign = time_layers_isolated(eng, 3, torch)
+        iso = (max_over_ranks(t_iso), t_foreign)
+    parity = None if args.no_check else parity_check(eng, torch)
     t_steps = max_over_ranks(t_steps)
     t_layer = max_over_ranks(t_layer)
-    info = eng.last_plan
-    bytes_layer = alg_bytes_per_layer(info, rows, H)
+    total_rows = int(sum_over_ranks(rows))
     peak, peak_kind = load_peaks()
     achieved = bytes_layer / t_layer / 1e9
-    value = world * rows * args.steps / t_steps
+    value = total_rows * args.steps / t_steps
     # per layer: prefix kernel(s) + private + merge (none with the fused merge);
     # per step: one K/V append
     launches_per_step = L * (1 + int(info.num_mma_items > 0) + int(info.num_tc_items > 0)
                              + int(not info.fused_merge)) + 1
-    batch_tokens = info.batch_tokens
 
     # ---- e2e: host (pinned) inputs through the engine API
     e2e = None
@@ -353,8 +466,7 @@ def main():
         eng.close()
         del eng
         torch.cuda.empty_cache()
-        eng2, rows2 = build_engine(cfg, device, torch, host_inputs=True,
-                                   out_len=2 * (args.steps + args.warmup) + 64)
+        eng2, rows2 = build_engine(cfg, device, torch, host_inputs=True, out_len=out_len, rank=rank, world=world)
         apply_options(eng2)
         for _ in range(max(args.warmup, 3)):
             eng2.step()
@@ -366,18 +478,21 @@ def main():
         t_e2e = max_over_ranks(max(t_e2e, wall))
         bi = 3 * L * rows2 * H * 128 * 2
         bo = L * rows2 * H * 128 * 2
-        e2e = {"value": world * rows2 * args.steps / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": bi,
+        e2e = {"value": total_rows * args.steps / t_e2e, "unit": "tokens/s", "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo, "ms_per_step": 1e3 * t_e2e / args.steps}
         eng2.close()
     else:
         eng.close()
 
-    traffic, traffic_src = None, None
+    traffic, traffic_src, traffic_tok = None, None, None
     try:  # DRAM bytes per layer (prefix + private + merge) from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f).get(args.config)
         if tr:
-            traffic, traffic_src = tr["layer_bytes"], tr["source"]
+            traffic_src = tr["source"]
+            if tr.get("batch_tokens") == batch_tokens:  # captured at this run's final plan
+                traffic = tr["layer_bytes"]
+            traffic_tok = tr.get("bytes_per_token")
     except Exception:
         pass
 
@@ -386,6 +501,19 @@ def main():
         if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 figure
             tok_s, sample, cores, _ = cpu_baseline(dict(cfg, B=rows))
             cpu = {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_bytes_per_token": traffic_tok,
+                "alg_bytes_per_token": H * 128 * 2 * 2, "peak_kind": peak_kind,
+                "kernel": "fk_attn_decode (prefix + private/merge kernels, one layer)",
+                "alg_bytes_per_layer": bytes_layer, "layer_us": t_layer * 1e6,
+                "batch_tokens": batch_tokens,
+                "roofline_tokens_per_s": rows * peak * 1e9 / (L * bytes_layer)}
+        if iso is not None:
+            roof["layer_us_isolated"] = iso[0] * 1e6
+            roof["frac_isolated"] = bytes_layer / iso[0] / 1e9 / peak
+            roof["isolated_mode"] = ("one fk_attn_decode per layer, PDL within the layer only, a foreign kernel "
+                                     f"between layers ({iso[1] * 1e6:.2f} us, subtracted)")
         line = {
             "metric": metric,
             "value": value,
@@ -395,25 +523,21 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": 1e3 * t_steps / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic",
             "config": workload,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_kind": peak_kind,
-                         "kernel": "fk_attn_decode (prefix + private/merge kernels, one layer)",
-                         "alg_bytes_per_layer": bytes_layer, "layer_us": t_layer * 1e6,
-                         "batch_tokens": batch_tokens,
-                         "roofline_tokens_per_s": rows * peak * 1e9 / (L * bytes_layer)},
+            "roofline": roof,
+            "parity": parity,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
-            "plan": {"rows": info.num_rows, "shared_ctx": info.num_shared_ctx, "prefix_ctas": info.num_prefix_ctas,
-                     "max_slots": info.max_slots, "tc_items": info.num_tc_items, "mma_items": info.num_mma_items},
+            "plan": plan_line,
         }
+        if world > 1:
+            line["rows_total"] = total_rows
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

@@ -201,18 +201,75 @@ def attend(q: np.ndarray, k: np.ndarray, v: np.ndarray, dtype=np.float64) -> np.
     return np.einsum("ht,thd->hd", p, vd)
 
 
-class KVCache:
-    """Generated K/V per (context uid, layer), grown on demand."""
+_C_LIB = None
 
-    def __init__(self, seed: int, heads: int, k_scale: float = 1.0):
+
+def c_lib():
+    """oracle_c.c (the C restatement, built by oracle/Makefile) via ctypes, or
+    None when it cannot be built (numpy restatement then)."""
+    global _C_LIB
+    if _C_LIB is None:
+        import ctypes
+        import os
+        import subprocess
+
+        here = os.path.dirname(os.path.abspath(__file__))
+        path = os.path.join(here, "build", "liboracle_c.so")
+        if not os.path.exists(path):
+            subprocess.run(["make", "-s", "-C", here], check=False)
+        try:
+            lib = ctypes.CDLL(path)
+            lib.oracle_synth_rows.restype = None
+            lib.oracle_synth_rows.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_float,
+                                              ctypes.c_void_p]
+            _C_LIB = lib
+        except OSError:
+            _C_LIB = False
+    return _C_LIB or None
+
+
+def synth_rows_range(seed: int, tag: int, uid: int, pos0: int, n: int, layer: int, heads: int,
+                     scale: float = 1.0) -> np.ndarray:
+    """synth_rows for the contiguous positions [pos0, pos0 + n), through the C
+    restatement when available (same values, pinned by test_oracle)."""
+    lib = c_lib()
+    if lib is None or n == 0:
+        return synth_rows(seed, tag, uid, np.arange(pos0, pos0 + n), layer, heads, scale)
+    out = np.empty((n, heads, 128), dtype=np.float32)
+    lib.oracle_synth_rows(int(seed) & MASK64, tag, int(uid), int(pos0), int(n), int(layer), int(heads),
+                          float(scale), out.ctypes.data)
+    return out
+
+
+class KVCache:
+    """Generated K/V per (context uid, layer), grown on demand.
+
+    `appended[uid] = (n0, rows)`: positions >= n0 of that context hold model
+    rows instead of generated ones (the K/V a TensorDecodeModel appended
+    during decode); rows(layer, kv, positions) -> [n, H, 128] float32."""
+
+    def __init__(self, seed: int, heads: int, k_scale: float = 1.0, appended=None):
         self.seed, self.heads, self.k_scale = seed, heads, k_scale
+        self.appended = appended or {}
         self._c: Dict[Tuple[int, int], Tuple[np.ndarray, np.ndarray]] = {}
+
+    def _gen(self, uid: int, ntok: int, layer: int):
+        n0, rows = self.appended.get(uid, (ntok, None))
+        n0 = min(n0, ntok)
+        k = synth_rows_range(self.seed, TAG_K, uid, 0, n0, layer, self.heads, self.k_scale)
+        v = synth_rows_range(self.seed, TAG_V, uid, 0, n0, layer, self.heads, 1.0)
+        if ntok > n0:
+            pos = np.arange(n0, ntok)
+            k = np.concatenate([k, np.asarray(rows(layer, 0, pos), dtype=np.float32)])
+            v = np.concatenate([v, np.asarray(rows(layer, 1, pos), dtype=np.float32)])
+        return k, v
 
     def get(self, uid: int, ntok: int, layer: int):
         key = (uid, layer)
         have = self._c.get(key)
         if have is None or have[0].shape[0] < ntok:
-            have = context_kv(self.seed, uid, max(ntok, 1), layer, self.heads, self.k_scale)
+            have = self._gen(uid, max(ntok, 1), layer)
             self._c[key] = have
         return have[0][:ntok], have[1][:ntok]
 
@@ -232,6 +289,46 @@ def attend_rows(chains: Sequence[Sequence[Tuple[int, int]]], q: np.ndarray, kv: 
         if ks:
             out[b] = attend(q[b], np.concatenate(ks), np.concatenate(vs), dtype)
     return out
+
+
+def attend_forest(chains: Sequence[Sequence[Tuple[int, int]]], q: np.ndarray, kv: KVCache, layer: int,
+                  dtype=np.float64) -> np.ndarray:
+    """Same math as attend_rows -- one exact softmax over each row's whole
+    concatenated chain, no split-K / partial merging -- with the products
+    batched per context: every context's K/V is multiplied once with the
+    queries of all rows that read it (BLAS), the max and the sum are taken over
+    the row's full score vector.  For full-size checks (6k-token prefixes,
+    40 heads, 64-256 rows)."""
+    B, H, D = q.shape
+    scale = dtype(1.0 / math.sqrt(D))
+    qh = np.ascontiguousarray(q.astype(dtype).transpose(1, 0, 2))  # [H, B, D]
+    users: Dict[int, List[int]] = {}
+    ntok: Dict[int, int] = {}
+    for b, chain in enumerate(chains):
+        for uid, n in chain:
+            if n > 0:
+                users.setdefault(uid, []).append(b)
+                ntok[uid] = n
+    scores = {}
+    m = np.full((H, B), -np.inf, dtype=dtype)
+    for uid, rows in users.items():
+        k, _ = kv.get(uid, ntok[uid], layer)
+        kt = np.ascontiguousarray(k.astype(dtype).transpose(1, 2, 0))  # [H, D, T]
+        idx = np.asarray(rows)
+        s = np.matmul(qh[:, idx, :], kt) * scale  # [H, nr, T]
+        scores[uid] = (idx, s)
+        m[:, idx] = np.maximum(m[:, idx], s.max(axis=2))  # (a row reads a context once)
+    mm = np.where(np.isfinite(m), m, 0.0)
+    l = np.zeros((H, B), dtype=dtype)
+    o = np.zeros((H, B, D), dtype=dtype)
+    for uid, (idx, s) in scores.items():
+        _, v = kv.get(uid, ntok[uid], layer)
+        p = np.exp(s - mm[:, idx, None])
+        vh = np.ascontiguousarray(v.astype(dtype).transpose(1, 0, 2))  # [H, T, D]
+        l[:, idx] += p.sum(axis=2)
+        o[:, idx] += np.matmul(p, vh)
+    out = np.where(l[:, :, None] > 0, o / np.where(l > 0, l, 1.0)[:, :, None], 0.0)
+    return out.transpose(1, 0, 2)
 
 
 def attend_shared_batch(q: np.ndarray, prefix_k: np.ndarray, prefix_v: np.ndarray,

@@ -61,3 +61,27 @@ void oracle_synth_chunk(uint64_t seed, uint64_t tag, int64_t uid, int64_t pos, i
     out[i] = to_bf16(v);
   }
 }
+
+/* Rows [pos0, pos0 + n) of one context for one layer, all heads: out is
+ * [n][heads][128] float32 holding the bf16 values (the numpy restatement
+ * synth_rows, forkattn_oracle.py, in bulk for full-size checks). */
+void oracle_synth_rows(uint64_t seed, uint64_t tag, int64_t uid, int64_t pos0, int64_t n, int32_t layer,
+                       int32_t heads, float scale, float* out) {
+  const uint64_t k0 = mix(mix(seed ^ (tag << 56)) ^ (uint64_t)uid);
+  for (int64_t t = 0; t < n; ++t) {
+    const uint64_t kp = mix(mix(k0 ^ (uint64_t)(pos0 + t)) ^ (uint64_t)(int64_t)layer);
+    for (int32_t h = 0; h < heads; ++h) {
+      const uint64_t kh = mix(kp ^ (uint64_t)(int64_t)h);
+      float* o = out + ((size_t)t * heads + h) * 128;
+      for (int j = 0; j < 32; ++j) {
+        const uint64_t w = mix(kh ^ (uint64_t)j);
+        for (int i = 0; i < 4; ++i) {
+          const int u = (int)((w >> (16 * i)) & 0xFFFF);
+          const float v = (float)(u - 32768) * 5.340576171875e-05f * scale;
+          const uint32_t b = (uint32_t)to_bf16(v) << 16;
+          memcpy(&o[4 * j + i], &b, 4);
+        }
+      }
+    }
+  }
+}

@@ -23,6 +23,7 @@ from .engine import (
     StepReport,
     SyntheticDecodeModel,
     TensorDecodeModel,
+    engine_factory,
     format_ms,
     hash_token_ids,
 )
@@ -31,6 +32,6 @@ from .errors import ContextBusy, KernelError, OutOfMemory, UnknownContext, Unkno
 __all__ = [
     "GpuEngine", "Engine", "GpuKvStore", "CostModel", "Context", "ContextPlan", "FillTask",
     "GenerationTask", "StepReport", "ModelGeometry", "LLAMA_7B", "LLAMA_13B", "TINY",
-    "SyntheticDecodeModel", "TensorDecodeModel", "format_ms", "hash_token_ids",
+    "SyntheticDecodeModel", "TensorDecodeModel", "engine_factory", "format_ms", "hash_token_ids",
     "OutOfMemory", "UnknownContext", "UnknownParentContext", "ContextBusy", "KernelError",
 ]

@@ -238,10 +238,12 @@ int reserve_pages(fk_pool* p, int64_t pages) {
     return fail(FK_CUDA_ERROR, "KV arena of %zu bytes (%lld pages): %s", new_bytes,
                 (long long)pages, cudaGetErrorString(e));
   }
-  // zero so every byte a kernel may touch is a finite bf16
+  // zero so every byte a kernel may touch is a finite bf16.  cudaMemset runs
+  // on the legacy default stream, which the pool's (non-blocking) streams do
+  // not wait for: synchronize before any fill can write the new pages.
   FK_CUDA(cudaMemset(nkv, 0, new_bytes));
+  FK_CUDA(cudaDeviceSynchronize());
   if (p->kv) {
-    FK_CUDA(cudaDeviceSynchronize());
     const size_t old_plane = (size_t)p->num_pages * kPage * D * 2;
     const size_t new_plane = (size_t)pages * kPage * D * 2;
     FK_CUDA(cudaMemcpy2D(nkv, new_plane, p->kv, old_plane, old_plane, planes,
@@ -285,6 +287,7 @@ int ensure_scratch(fk_pool* p, int rows, int slots, int64_t orphan_slots) {
     p->mctl = nullptr;
     FK_CUDA(cudaMalloc(&p->mctl, bytes));
     FK_CUDA(cudaMemset(p->mctl, 0, bytes));
+    FK_CUDA(cudaDeviceSynchronize());  // (legacy-stream memset; see reserve_pages)
     p->mctl_rh = cap_rh;
     p->mctl_q = cap_q;
   }
@@ -1281,13 +1284,36 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   const double t0 = timing ? now_us() : 0.0;
-  // 1. record the launches (same code path: tickets and partial halves advance)
+  // 1. record the launches (same code path: tickets and partial halves advance).
+  // Recording advances the host ticket bases, the partial-half parity and the
+  // fused epoch before anything runs; if the graph is not launched they go
+  // back, so the host bases keep matching the device counters.
+  const unsigned long long tb0 = p->ticket_base, ttb0 = p->ticket_tc_base;
+  const int par0 = p->launch_parity;
+  const unsigned ep0 = p->fused_epoch;
+  struct Rollback {
+    fk_pool* p;
+    unsigned long long tb, ttb;
+    int par;
+    unsigned ep;
+    bool armed = true;
+    ~Rollback() {
+      if (!armed) return;
+      p->ticket_base = tb;
+      p->ticket_tc_base = ttb;
+      p->launch_parity = par;
+      p->fused_epoch = ep;
+    }
+  } rollback{p, tb0, ttb0, par0, ep0};
   std::vector<fk::LaunchRec> recs;
   fk::g_launch_rec = &recs;
   const int rc = run();
   fk::g_launch_rec = nullptr;
   if (rc != FK_OK) return rc;
-  if (recs.empty()) return FK_OK;
+  if (recs.empty()) {
+    rollback.armed = false;
+    return FK_OK;
+  }
   for (auto& r : recs) r.finalize();
   cudaStream_t st = (cudaStream_t)stream;
   GraphCache& G = p->graphs[std::make_tuple(layer0, nlayers, st)];
@@ -1354,6 +1380,7 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   }
   const double t2 = timing ? now_us() : 0.0;
   FK_CUDA(cudaGraphLaunch(G.exec, st));
+  rollback.armed = false;
   if (timing)
     fprintf(stderr, "fk graph: %zu launches, record %.1f us, %s %.1f us, launch %.1f us\n", recs.size(), t1 - t0,
             same ? "update" : "capture", t2 - t1, now_us() - t2);

@@ -523,7 +523,19 @@ class GpuEngine:
         return task
 
     def _discard_context(self, ctx: Context) -> None:
-        if self.device is not None:  # fills into the recycled pages wait for this point
+        if self.device is not None:
+            # Pages freed here may be handed out again by decode growth (their
+            # new rows are written on the engine stream) or by a fill (which
+            # waits for _release_event): the engine stream first waits for any
+            # fill still writing the discarded contexts, so both reuses are
+            # ordered after it.
+            c = ctx
+            while c is not None:
+                ev = self._fill_pending.pop(c.context_id, None)
+                if ev is not None:
+                    self._stream.wait_event(ev)
+                parent = self.contexts.get(c.parent_id) if c.parent_id is not None else None
+                c = parent if (parent is not None and parent.refcount == 1 and parent.dropped) else None
             self._release_event = self._torch.cuda.Event()
             self._release_event.record(self._stream)
         while ctx is not None:
@@ -764,11 +776,17 @@ class GpuEngine:
         if isinstance(model, TensorDecodeModel) and model.q.device.type != "cuda" and not self.capture_f32:
             self._decode_attention_host(running)
             return
+        caller = torch.cuda.current_stream(self._dev)
         with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
             if isinstance(model, TensorDecodeModel):
                 q = model.q
                 if q.device.type != "cuda":
                     q = q.to(self._dev, non_blocking=True)
+                elif caller != self._stream:
+                    # the caller's producer of q ran on its own stream; keep q
+                    # alive until the engine stream has read it
+                    self._stream.wait_stream(caller)
+                    q.record_stream(self._stream)
             else:
                 q = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
                 _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed,
@@ -798,6 +816,7 @@ class GpuEngine:
         model = self.model
         if isinstance(model, TensorDecodeModel) and model.k is not None:
             geo = self.geometry
+            caller = torch.cuda.current_stream(self._dev)
             with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
                 k, v = model.k, model.v
                 hp = getattr(self, "_hp", None)
@@ -808,6 +827,10 @@ class GpuEngine:
                 elif k.device.type != "cuda":
                     k = k.to(self._dev, non_blocking=True)
                     v = v.to(self._dev, non_blocking=True)
+                elif caller != self._stream:  # the caller's producer ran on its own stream
+                    self._stream.wait_stream(caller)
+                    k.record_stream(self._stream)
+                    v.record_stream(self._stream)
                 _lib.check(_lib.lib.fk_append_kv_layers(self._pool.handle, 0, geo.num_layers,
                                                         ctypes.c_void_p(k.data_ptr()),
                                                         ctypes.c_void_p(v.data_ptr()), self._sp()))
@@ -994,3 +1017,32 @@ class GpuEngine:
 
 # Alias so a maintainer can rebind `semflow.engine.Engine = Engine`.
 Engine = GpuEngine
+
+
+def engine_factory(geometry: ModelGeometry = LLAMA_13B, devices: Optional[Sequence[int]] = None, **kw):
+    """A constructor with `Engine`'s signature for SemanticManager's one
+    construction site (manager.py:130-139: `Engine(eid, cost, kv_tokens=...,
+    token_capacity=...)` for eid = e0 .. e{engines-1}), mapping engine eI to
+    GPU devices[I mod len(devices)] (default: every visible GPU), so
+    `Config(engines=N)` spreads the prefix-affinity scheduler's groups
+    (scheduler.py:198-222) over the GPUs of one process.  Extra keyword
+    arguments (model, capture_f32, keep_history, ...) go to every GpuEngine;
+    devices=[] builds host-only engines (the integer twin).
+
+        import semflow.manager
+        semflow.manager.Engine = engine_factory(LLAMA_13B)
+    """
+    if devices is None:
+        import torch
+
+        devices = list(range(torch.cuda.device_count()))
+    devices = list(devices)
+
+    def make(engine_id: str, cost: Any, kv_tokens: int = 120_000, token_capacity: int = 64_000) -> GpuEngine:
+        digits = engine_id.lstrip("e")
+        idx = int(digits) if digits.isdigit() else 0
+        dev = devices[idx % len(devices)] if devices else None
+        return GpuEngine(engine_id, cost, kv_tokens, token_capacity, device=dev, geometry=geometry, **kw)
+
+    make.devices = devices
+    return make

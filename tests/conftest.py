@@ -15,11 +15,17 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REFERENCE_SRC = os.environ.get("FK_REFERENCE", "/root/reference/pkg/src")
 HAVE_REFERENCE = os.path.isdir(os.path.join(REFERENCE_SRC, "semflow"))
+# the reference package installed unmodified into baseline/_ref (travels to
+# the GPU box, where /root/reference does not exist): the runtime the
+# manager-driven GPU tests put above the B200 engine
+BASELINE_REF = os.path.join(ROOT, "baseline", "_ref")
+if not HAVE_REFERENCE and os.path.isdir(os.path.join(BASELINE_REF, "semflow")):
+    REFERENCE_SRC = BASELINE_REF
 
 for p in (ROOT, os.path.join(ROOT, "tests", "golden")):
     if p not in sys.path:
         sys.path.insert(0, p)
-if HAVE_REFERENCE and REFERENCE_SRC not in sys.path:
+if os.path.isdir(os.path.join(REFERENCE_SRC, "semflow")) and REFERENCE_SRC not in sys.path:
     sys.path.insert(1, REFERENCE_SRC)
 
 

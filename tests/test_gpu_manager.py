@@ -1,0 +1,84 @@
+"""The reference runtime drives the B200 path.
+
+semflow's SemanticManager builds its engines at one site
+(manager.py:130-139); rebinding `semflow.manager.Engine` to
+`engine_factory(...)` puts a GpuEngine per engine id on the GPUs
+(eI -> cuda:(I mod ndev)).  The reference's own experiment harness then runs
+a shared-prompt serving workload end to end -- `_place_one` forks every
+request from the 6k system prompt (manager.py:465-511), `_step_engine`
+steps the engines (manager.py:623-636), `_complete_request` finishes them --
+and every decode step executes the attention kernels on the device.
+
+Checked: the manager's view (traces, step reports, end time, peak blocks)
+is identical to the unmodified reference Engine's run, and every recorded
+decode step's attention agrees with the fp64 oracle.  semflow comes from
+/root/reference (build container) or baseline/_ref (the unmodified install
+that travels to the GPU box).
+"""
+
+import dataclasses
+
+import pytest
+
+import paper_2405_19888_b200 as P
+
+from gpu_check import check_history
+
+pytestmark = pytest.mark.gpu
+
+semflow = pytest.importorskip("semflow", reason="the reference runtime (semflow) is not importable")
+
+
+def run_manager(factory, engines=1):
+    import semflow.manager as sm
+    from semflow.config import Config
+    from semflow.experiments import run_workload_manager
+    from semflow.workloads import shared_prompt_serving
+
+    wl = shared_prompt_serving(1, users=64, system_prompt_len=6000, unique_len=200, output_len=8)
+    saved = sm.Engine
+    if factory is not None:
+        sm.Engine = factory
+    try:
+        mgr, runners, end_ns = run_workload_manager(wl, "semflow", Config(total_blocks=30000, engines=engines))
+    finally:
+        sm.Engine = saved
+    return mgr, end_ns
+
+
+def manager_view(mgr, end_ns):
+    view = {"end_ns": end_ns}
+    for eid, e in sorted(mgr.engines.items()):
+        view[eid] = {
+            "trace": list(e.trace),
+            "reports": [dataclasses.astuple(r) for r in e.reports],
+            "peak": e.store.peak_used,
+            "emitted": e.total_emitted,
+            "clock": e.clock_ns,
+        }
+    return view
+
+
+@pytest.mark.parametrize("engines", [1, 2])
+def test_reference_manager_drives_gpu_engines(cuda_device, engines):
+    import torch
+
+    want = manager_view(*run_manager(None, engines))
+    factory = P.engine_factory(P.ModelGeometry(2, 8, 128), capture_f32=True, keep_history=True)
+    mgr, end_ns = run_manager(factory, engines)
+    got = manager_view(mgr, end_ns)
+    assert got == want
+    ndev = torch.cuda.device_count()
+    decode_steps = 0
+    for i, (eid, eng) in enumerate(sorted(mgr.engines.items())):
+        assert isinstance(eng, P.GpuEngine) and eng.device == i % ndev
+        if not eng.history:
+            continue
+        eng.stream.synchronize()
+        decode_steps += len(eng.history)
+        # the 6000-token system prompt is one shared context read by the forks
+        assert max(r["batch_tokens"] for r in eng.history) >= 6000
+        check_history(eng)
+    assert decode_steps >= 8
+    assert sum(e.kv_tokens_streamed for e in mgr.engines.values()) == sum(
+        r.batch_tokens for e in mgr.engines.values() for r in e.reports)

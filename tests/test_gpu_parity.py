@@ -398,6 +398,23 @@ def test_fill_while_decoding(cuda_device):
     assert_plan_matches_walk(eng)
 
 
+def test_discarded_fill_then_decode_growth_into_its_pages(cuda_device):
+    """A context freed while its fill may still be writing (the manager frees
+    just-filled contexts on OutOfMemory, manager.py:489-492): its pages go
+    back to the free stack and the next decode growth hands them to running
+    leaves, whose new K/V rows must land after the old fill (the engine
+    stream waits for it at discard time)."""
+    eng = make_engine(cuda_device, H=8, L=4)
+    fork_group(eng, 64, [16, 32, 48], out_len=4)  # leaves end on page boundaries: step 1 grows
+    eng.fill([1] * 4000, "junk", None)  # 250 pages, filled on the fill stream
+    junk_pages = set(eng.context_pages("junk")[1])
+    eng.free_context("junk")            # back on the free stack, fill possibly still running
+    run_steps(eng, 4)
+    grown = {eng.context_pages(leaf)[1][-1] for leaf in ("e0.c1", "e0.c2", "e0.c3")}
+    assert grown <= junk_pages  # decode growth took the recycled pages
+    check_history(eng)
+
+
 @pytest.mark.parametrize("suffix", [600, 2100])
 def test_merge_many_partials(cuda_device, suffix):
     """One-page private chunks cut a long suffix into one partial per page:

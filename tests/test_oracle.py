@@ -152,3 +152,32 @@ def test_attend_matches_torch_sdpa_fp64():
         tv = torch.from_numpy(v.astype(np.float64)).permute(1, 0, 2)
         want = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv)[:, 0, :].numpy()
         assert np.abs(got - want).max() < 1e-12, (T, kscale)
+
+
+def test_bulk_c_rows_match_numpy_generator():
+    """oracle_synth_rows (C, used for full-size checks) == synth_rows (numpy)."""
+    for seed, tag, uid, pos0, n, layer, heads, scale in ((1, 1, 0, 0, 33, 0, 3, 1.0),
+                                                         (0x5EED, 2, 77, 6000, 17, 39, 40, 1.0),
+                                                         (12345, 1, 5, 1 << 41, 4, 7, 2, 8.0)):
+        want = O.synth_rows(seed, tag, uid, np.arange(pos0, pos0 + n), layer, heads, scale)
+        got = O.synth_rows_range(seed, tag, uid, pos0, n, layer, heads, scale)
+        assert np.array_equal(want, got)
+
+
+def test_forest_form_equals_per_row_form():
+    """attend_forest (context-batched products, one softmax per whole row)
+    == attend_rows (per-row concatenated chain) on nested, ragged, empty and
+    shared-leaf forests, with model-appended rows."""
+    rng = np.random.default_rng(2)
+    app = {3: (10, lambda layer, kv, pos: np.full((len(pos), 4, 128), 0.25 * (kv + 1) + layer, np.float32)),
+           5: (0, lambda layer, kv, pos: rng.standard_normal((len(pos), 4, 128)).astype(np.float32))}
+    for k_scale in (1.0, 8.0):
+        kv = O.KVCache(11, 4, k_scale, appended=app)
+        chains = [[(0, 300), (1, 33)], [(0, 300), (2, 0)], [(0, 300), (3, 17), (4, 5)],
+                  [(0, 300), (3, 17), (5, 40)], [(6, 0)], [(7, 64)], [(0, 300), (1, 33)]]
+        q = O.bf16_round(rng.standard_normal((len(chains), 4, 128), dtype=np.float32))
+        for layer in (0, 2):
+            a = O.attend_rows(chains, q, kv, layer)
+            b = O.attend_forest(chains, q, kv, layer)
+            assert np.abs(a - b).max() < 1e-12
+            assert np.abs(b[4]).max() == 0.0  # empty chain -> zeros
