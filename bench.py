@@ -51,6 +51,10 @@ CONFIGS = {
     # (512 requests) under one 4k system prompt, replicated per GPU
     "mapreduce_13b_16x32": dict(model="LLaMA-13B", L=40, H=40, P=2000, B=32, S=None, groups=16, strong=True),
     "nested_13b_8apps": dict(model="LLaMA-13B", L=40, H=40, P=4096, B=64, S=256, app=1024, apps=8, strong=True),
+    # launcher smoke (tests): the strong deal at a 2-layer, 8-head shape, so
+    # several ranks fit on one GPU
+    "nested_smoke_8apps": dict(model="smoke (2 layers x 8 heads)", L=2, H=8, P=4096, B=64, S=256, app=1024, apps=8,
+                               strong=True),
 }
 DEFAULT_CONFIG = "llama13b_p6000_b64"
 
@@ -145,6 +149,17 @@ def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=409
     eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 30, device=device, geometry=geo,
                       model=P.SyntheticDecodeModel(seed))
     units = rank_units(cfg, rank, world)
+    # back every page the run will use up front: growing the arena later is
+    # a device-wide copy with old and new arenas live at once
+    pg = lambda n: -(-n // 16)  # noqa: E731
+    grow = pg(out_len) + 1
+    if "app" in cfg:
+        pages = pg(cfg["P"]) + len(units) * (pg(cfg["app"]) + cfg["B"] * (pg(cfg["S"]) + grow))
+    elif cfg.get("groups"):
+        pages = len(units) * (pg(cfg["P"]) + cfg["B"] * (pg(1024) + grow))
+    else:
+        pages = pg(cfg["P"]) + cfg["B"] * (pg(cfg["S"]) + grow)
+    eng.reserve_pages(pages)
     if "app" in cfg:
         nested_forest(eng, cfg["P"], cfg["app"], len(units), cfg["S"], cfg["B"], out_len=out_len, seed=seed)
     elif cfg.get("groups"):

@@ -80,6 +80,8 @@ typedef struct {
   int32_t num_mma_items;   /* prefix items routed to the warp-level mma.sync kernel */
   int32_t fused_merge;     /* 1: each (row, head) is merged by its last partial's writer
                               (no merge kernel); see FK_OPT_FUSED_MERGE */
+  int64_t streamed_tokens; /* KV tokens the kernels stream per layer: batch_tokens, plus the
+                              step's new tokens under FK_OPT_APPEND_FIRST */
 } fk_plan_info;
 
 /* ---- pool ---------------------------------------------------------------- */
@@ -127,7 +129,14 @@ enum {
                                  the row's owning private warp as it leaves, or by the tcgen05 CTA
                                  if the owner has left); needs tcgen05 and private work, no mma.sync
                                  items, launch order 0.  0 (default): a merge kernel after every
-                                 layer -- measured faster */
+                                 layer -- measured faster */,
+  FK_OPT_APPEND_FIRST = 16    /* 1: attend to the step's own token (a real decoder): fk_step_plan does
+                                 the step's one-token growth (row order, sequential OOM rule) and
+                                 plans spans that include it; the caller then takes the growth from
+                                 fk_step_grow, commits and appends the new K/V rows, and only then
+                                 runs fk_attn_decode.  fk_plan_info.batch_tokens stays the
+                                 reference's pre-growth count.  0 (default): the reference's span
+                                 (chain tokens at step start, engine.py:416-434), append after */
 };
 
 /* ---- context forest ------------------------------------------------------ */

@@ -40,6 +40,7 @@ FK_OPT_GRAPH = 12
 FK_OPT_TC_DYN_PCT = 13
 FK_OPT_TC_BOUNDARY_COST = 14
 FK_OPT_FUSED_MERGE = 15
+FK_OPT_APPEND_FIRST = 16
 
 
 class PoolDesc(ctypes.Structure):
@@ -80,6 +81,7 @@ class PlanInfo(ctypes.Structure):
         ("num_tc_items", c_int32),
         ("num_mma_items", c_int32),
         ("fused_merge", c_int32),
+        ("streamed_tokens", c_int64),
     ]
 
 

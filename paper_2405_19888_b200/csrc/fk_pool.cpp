@@ -165,6 +165,9 @@ struct fk_pool {
   unsigned fused_epoch = 0;  // "left" value of the latest fused launch
   size_t mctl_left_cap() const { return (size_t)std::max(num_sms, 1) * 12; }  // private grid warps
   int64_t fused_merge = 0;   // FK_OPT_FUSED_MERGE (measured slower than the merge kernel: off)
+  int64_t append_first = 0;  // FK_OPT_APPEND_FIRST: fk_step_plan grows the rows first (attend own token)
+  bool plan_grew = false;    // the current plan already did the step's growth (fk_step_grow returns it)
+  std::vector<int64_t> grow_pos, grow_ids;
   bool plan_fused_ok = false;  // the current plan admits the fused merge
   unsigned long long* ticket = nullptr;  // device: private chunk tickets (never reset)
   unsigned long long ticket_base = 0;    // tickets consumed by earlier private launches
@@ -441,6 +444,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_CORUN: p->corun = value; break;
     case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
     case FK_OPT_FUSED_MERGE: p->fused_merge = value != 0; break;
+    case FK_OPT_APPEND_FIRST: p->append_first = value != 0; break;
     default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
   }
   return FK_OK;
@@ -482,10 +486,13 @@ int fk_ctx_grow(fk_pool* p, int64_t ctx, int64_t new_tokens, int64_t* new_ids, i
                 (long long)need);
   if (need > 0 && p->on_device && need > (int64_t)p->free_pages.size()) {
     // the logical pool admits it: back it with more device pages
-    int64_t want = std::max<int64_t>(p->num_pages + need - (int64_t)p->free_pages.size(),
-                                     std::min<int64_t>(p->total_blocks,
-                                                       std::max<int64_t>(64, p->num_pages * 2)));
+    // grow geometrically (x1.5), but fall back to exactly what is needed when
+    // the device cannot hold the old and the larger new arena at once
+    const int64_t exact = p->num_pages + need - (int64_t)p->free_pages.size();
+    const int64_t want = std::max<int64_t>(exact, std::min<int64_t>(p->total_blocks,
+                                                                   std::max<int64_t>(64, p->num_pages * 3 / 2)));
     int rc = reserve_pages(p, want);
+    if (rc != FK_OK && want > exact) rc = reserve_pages(p, exact);
     if (rc != FK_OK) return fail(FK_OUT_OF_MEMORY, "device arena: %s", g_last_error.c_str());
   }
   for (int64_t i = 0; i < need; ++i) {
@@ -586,13 +593,40 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       cur = ci->second.parent;
     }
   }
-  int64_t batch_tokens = 0, shared_tokens = 0, private_tokens = 0;
-  if (dedup) {
-    for (int64_t c : order) batch_tokens += p->ctxs[c].tokens;
-  } else {
-    for (int r = 0; r < B; ++r)
-      for (int64_t c : chain[r]) batch_tokens += p->ctxs[c].tokens;
+  int64_t shared_tokens = 0, private_tokens = 0;
+  auto count_tokens = [&]() {
+    int64_t n = 0;
+    if (dedup) {
+      for (int64_t c : order) n += p->ctxs[c].tokens;
+    } else {
+      for (int r = 0; r < B; ++r)
+        for (int64_t c : chain[r]) n += p->ctxs[c].tokens;
+    }
+    return n;
+  };
+  // the reference's count, before the step's growth (engine.py:416-417)
+  const int64_t batch_tokens = count_tokens();
+  std::vector<int64_t> leaf_tokens_pre(B);
+  for (int r = 0; r < B; ++r) leaf_tokens_pre[r] = p->ctxs[leaves[r]].tokens;
+  // FK_OPT_APPEND_FIRST: the step's one-token growth happens now, in row
+  // (gens) order with the sequential OOM rule of fk_step_grow, and the
+  // kernels' spans include the new token (a decoder attends to its own key)
+  p->plan_grew = false;
+  if (p->append_first) {
+    p->grow_pos.assign(B, -1);
+    p->grow_ids.assign(B, -1);
+    for (int r = 0; r < B; ++r) {
+      const int64_t pos = p->ctxs[leaves[r]].tokens;
+      int64_t n = 0, id = -1;
+      const int rc = fk_ctx_grow(p, leaves[r], pos + 1, &id, 1, &n);
+      if (rc == FK_OUT_OF_MEMORY) continue;
+      if (rc != FK_OK) return rc;
+      p->grow_pos[r] = pos;
+      p->grow_ids[r] = n > 0 ? id : -1;
+    }
+    p->plan_grew = true;
   }
+  const int64_t streamed_tokens = p->append_first ? count_tokens() : batch_tokens;
   auto is_shared = [&](int64_t c) { return dedup && fan[c] >= 2 && p->ctxs[c].tokens > 0; };
 
   PT(T1);
@@ -980,17 +1014,17 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       const int64_t leaf = leaves[r];
       const int k = rank[leaf]++;
       row_uid[r] = leaf;
-      p->plan_leaf_tokens[r] = p->ctxs[leaf].tokens;
-      row_pos[r] = p->ctxs[leaf].tokens + ((int64_t)k << 40);
+      p->plan_leaf_tokens[r] = leaf_tokens_pre[r];
+      row_pos[r] = leaf_tokens_pre[r] + ((int64_t)k << 40);
     }
   }
 
   // the work-list invariant: the KV tokens the kernels stream
   // per layer -- shared contexts once, private contexts per row -- are exactly
   // Engine._batch_tokens(running) (engine.py:470-484)
-  if (shared_tokens + private_tokens != batch_tokens)
+  if (shared_tokens + private_tokens != streamed_tokens)
     return fail(FK_INVALID_ARGUMENT, "work-list invariant violated: %lld shared + %lld private != %lld batch tokens",
-                (long long)shared_tokens, (long long)private_tokens, (long long)batch_tokens);
+                (long long)shared_tokens, (long long)private_tokens, (long long)streamed_tokens);
   const int n_items = (int)items.size();
   // fused merge: every (row, head) must receive a partial, every tcgen05
   // item a chunk, and the private warps (the queue's drainers) must exist
@@ -1014,6 +1048,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     info->num_tc_items = num_tc;
     info->num_mma_items = num_mma;
     info->fused_merge = (fused_ok && p->fused_merge && p->launch_order == 0) ? 1 : 0;
+    info->streamed_tokens = streamed_tokens;
   }
   p->committed = false;
   if (plan_timing) {
@@ -1392,6 +1427,14 @@ int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids) {
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   const int B = (int)p->plan_leaves.size();
   if (B > 0 && (!positions || !new_ids)) return fail(FK_INVALID_ARGUMENT, "null output");
+  if (p->plan_grew) {  // FK_OPT_APPEND_FIRST: the plan did this step's growth
+    for (int r = 0; r < B; ++r) {
+      positions[r] = p->grow_pos[r];
+      new_ids[r] = p->grow_ids[r];
+    }
+    p->plan_grew = false;
+    return FK_OK;
+  }
   for (int r = 0; r < B; ++r) {  // gens order, one token each (engine.py:431-443)
     auto it = p->ctxs.find(p->plan_leaves[r]);
     if (it == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "leaf of row %d vanished", r);

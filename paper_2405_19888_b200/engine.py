@@ -293,6 +293,7 @@ class GpuEngine:
         num_pages: int = 0,
         capture_f32: bool = False,
         keep_history: bool = False,
+        attend_own_token: bool = False,
     ):
         self.engine_id = engine_id
         self.cost = cost
@@ -333,6 +334,7 @@ class GpuEngine:
         self.kv_tokens_streamed = 0  # sum of batch_tokens over decode steps (per layer)
         self._stream = None
         self._leaf_buf = (ctypes.c_int64 * 64)()
+        self._leaf_pos0 = (ctypes.c_int64 * 64)()
         self._pos_buf = (ctypes.c_int64 * 64)()
         self._id_buf = (ctypes.c_int64 * 64)()
         if device is not None:
@@ -351,6 +353,12 @@ class GpuEngine:
             # stream events), so a layer's kernels may start under the previous
             # layer's merge (cross-layer programmatic dependent launch).
             self._pool.set_option(_lib.FK_OPT_PDL, 2)
+        # FK_OPT_APPEND_FIRST: each row's new K/V row is
+        # appended before attention and is part of its span, as in a real
+        # decoder; the default is the reference's span (engine.py:416-434)
+        self.attend_own_token = bool(attend_own_token)
+        if self.attend_own_token:
+            self._pool.set_option(_lib.FK_OPT_APPEND_FIRST, 1)
 
     # -- device plumbing ------------------------------------------------------
 
@@ -659,10 +667,13 @@ class GpuEngine:
         B = len(running)
         if B > len(self._leaf_buf):
             self._leaf_buf = (ctypes.c_int64 * (2 * B))()
+            self._leaf_pos0 = (ctypes.c_int64 * (2 * B))()
             self._pos_buf = (ctypes.c_int64 * (2 * B))()
             self._id_buf = (ctypes.c_int64 * (2 * B))()
         for i, g in enumerate(running):
-            self._leaf_buf[i] = self.contexts[g.context_id].uid
+            ctx = self.contexts[g.context_id]
+            self._leaf_buf[i] = ctx.uid
+            self._leaf_pos0[i] = ctx.token_count
         _lib.check(_lib.lib.fk_step_plan(self._pool.handle, self._leaf_buf, B,
                                          1 if self.cost.shared_kernel else 0, self._sp(),
                                          ctypes.byref(self.last_plan)))
@@ -745,7 +756,7 @@ class GpuEngine:
                 for ci, (a, b) in enumerate(chunks):
                     hp["q"][a:b].copy_(model.q[a:b], non_blocking=True)
                     hp["ev_q"][ci].record(h2d)
-                if model.k is not None:
+                if model.k is not None and not self.attend_own_token:  # (appended before attention otherwise)
                     hp["k"].copy_(model.k, non_blocking=True)
                     hp["v"].copy_(model.v, non_blocking=True)
                     hp["ev_kv"].record(h2d)
@@ -820,7 +831,8 @@ class GpuEngine:
             with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
                 k, v = model.k, model.v
                 hp = getattr(self, "_hp", None)
-                if k.device.type != "cuda" and hp is not None and hp["shape"] == tuple(k.shape):
+                if (k.device.type != "cuda" and hp is not None and hp["shape"] == tuple(k.shape)
+                        and not self.attend_own_token):
                     # copied in under this step's attention (_decode_attention_host)
                     self._stream.wait_event(hp["ev_kv"])
                     k, v = hp["k"], hp["v"]
@@ -889,10 +901,23 @@ class GpuEngine:
         batch_tokens = self._plan(running) if running else 0
         if running and self.device is not None and self._fill_pending:
             self._wait_fills(running)
-        snapshot = self._snapshot(running) if (self.keep_history and running) else None
+        snapshot = None
+        positions: List[int] = []
+        if self.attend_own_token:
+            # real-decoder order: grow (the plan already did, fk_step_plan
+            # under FK_OPT_APPEND_FIRST), write the new K/V rows, then attend
+            # over spans that include them
+            positions = self._grow_rows(running, emitted, finished, failed) if running else []
+            snapshot = self._snapshot(running) if (self.keep_history and running) else None
+            if running and self.device is not None:
+                self._append(running, positions)
+                self._decode_attention(running)
+        else:
+            snapshot = self._snapshot(running) if (self.keep_history and running) else None
+            if running and self.device is not None:
+                self._decode_attention(running)
         if running and self.device is not None:
-            self._decode_attention(running)
-            self.kv_tokens_streamed += batch_tokens
+            self.kv_tokens_streamed += int(self.last_plan.streamed_tokens)
 
         elapsed = 0
         if fill_tokens > 0:
@@ -906,9 +931,32 @@ class GpuEngine:
         self.clock_ns += elapsed
         self.busy_ns += elapsed
 
+        if not self.attend_own_token:
+            positions = self._grow_rows(running, emitted, finished, failed) if running else []
+            if running and self.device is not None:
+                self._append(running, positions)
+
+        for rid in fill_completed:  # fills done this step decode next step
+            g = self.gens.get(rid)
+            if g is not None:
+                g.started = True
+
+        self.total_emitted += len(emitted)
+        self.trace.append("t=%s engine=%s fill=%d batch=%d emitted=%d"
+                          % (format_ms(self.clock_ns), self.engine_id, fill_tokens, batch_tokens, len(emitted)))
+        report = StepReport(self.engine_id, started_ns, elapsed, fill_tokens, batch_tokens, emitted,
+                            finished, failed, fill_completed)
+        self.reports.append(report)
+        if snapshot is not None:
+            self.history.append(self._history_record(running, snapshot, batch_tokens, positions))
+        return report
+
+    def _grow_rows(self, running: List[GenerationTask], emitted: Dict[str, int], finished: List[str],
+                   failed: List[Tuple[str, str]]) -> List[int]:
+        """One token per running generation, gens order, sequential OOM rule
+        (engine.py:431-443), in one C call; mirrors the block ids."""
+        _lib.check(_lib.lib.fk_step_grow(self._pool.handle, self._pos_buf, self._id_buf))
         positions: List[int] = []
-        if running:  # one token per running generation, gens order (engine.py:431-443), in one C call
-            _lib.check(_lib.lib.fk_step_grow(self._pool.handle, self._pos_buf, self._id_buf))
         for i, g in enumerate(running):
             ctx = self.contexts[g.context_id]
             pos = int(self._pos_buf[i])
@@ -930,23 +978,7 @@ class GpuEngine:
             if g.remaining == 0:
                 g.done = True
                 finished.append(g.request_id)
-        if running and self.device is not None:
-            self._append(running, positions)
-
-        for rid in fill_completed:  # fills done this step decode next step
-            g = self.gens.get(rid)
-            if g is not None:
-                g.started = True
-
-        self.total_emitted += len(emitted)
-        self.trace.append("t=%s engine=%s fill=%d batch=%d emitted=%d"
-                          % (format_ms(self.clock_ns), self.engine_id, fill_tokens, batch_tokens, len(emitted)))
-        report = StepReport(self.engine_id, started_ns, elapsed, fill_tokens, batch_tokens, emitted,
-                            finished, failed, fill_completed)
-        self.reports.append(report)
-        if snapshot is not None:
-            self.history.append(self._history_record(running, snapshot, batch_tokens, positions))
-        return report
+        return positions
 
     def _history_record(self, running, snapshot, batch_tokens, positions) -> Dict[str, Any]:
         """Snapshot for the parity tests: the outputs are copied to the host on
@@ -963,6 +995,9 @@ class GpuEngine:
             "leaf_uid": [self.contexts[g.context_id].uid if g.context_id in self.contexts else -1
                          for g in running],
             "batch_tokens": batch_tokens,
+            "streamed_tokens": int(self.last_plan.streamed_tokens),
+            # leaf tokens before this step's growth: the synthetic query key
+            "qpos": [int(self._leaf_pos0[i]) for i in range(len(running))],
             "output": host(self.last_output),
             "output_f32": host(self.last_output_f32),
             "positions": positions,

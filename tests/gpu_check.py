@@ -24,9 +24,12 @@ def to_np(t):
 
 
 def synthetic_queries(eng, rec, layer):
+    """Q rows of the synthetic model, keyed by (leaf uid, leaf tokens before
+    the step's growth): the chains' leaf count, or rec["qpos"] when the span
+    already includes the step's own token (attend_own_token)."""
     chains = rec["chains"]
-    return O.row_queries(eng.model_seed, [c[-1][0] for c in chains], [c[-1][1] for c in chains], layer,
-                         eng.geometry.num_heads)
+    qpos = rec.get("qpos") or [c[-1][1] for c in chains]
+    return O.row_queries(eng.model_seed, [c[-1][0] for c in chains], qpos, layer, eng.geometry.num_heads)
 
 
 def tensor_model_oracle(eng, leaf_n0):

@@ -59,7 +59,7 @@ def test_two_rank_torchrun_on_one_gpu():
     rank, no collective on the data path (gloo only for the barrier and the
     max-over-ranks timing), rank 0 prints one line with the whole-job rows;
     the strong-scaling config deals the 8 nested apps over the ranks."""
-    for config, rows in (("llama7b_p6000_b64", 128), ("nested_13b_8apps", 512)):
+    for config, rows in (("llama7b_p6000_b64", 128), ("nested_smoke_8apps", 512)):
         res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                               "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"),
                               "--gpus", "2", "--steps", "3", "--warmup", "3", "--config", config, "--no-e2e",

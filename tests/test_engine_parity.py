@@ -29,12 +29,19 @@ def normalise(rec):
     return json.loads(json.dumps(rec))
 
 
-def test_golden_streams_bit_exact():
+@pytest.mark.parametrize("own_token", [False, True])
+def test_golden_streams_bit_exact(own_token):
+    """Also with attend_own_token (FK_OPT_APPEND_FIRST: the plan does the
+    step's growth before attention): the integer side is unchanged."""
     data = json.load(open(os.path.join(GOLDEN, "engine_streams.json")))
     assert len(data) >= 20
     outcomes = set()
+
+    def factory(kv, shared):
+        return P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=kv, attend_own_token=own_token)
+
     for case in data:
-        got = normalise(streams.record_stream(gpu_engine_factory, case["spec"]))
+        got = normalise(streams.record_stream(factory, case["spec"]))
         want = case["record"]
         for i, (g, w) in enumerate(zip(got, want)):
             assert g == w, (case["spec"]["seed"], i, case["spec"]["ops"][i] if i < len(case["spec"]["ops"]) else "final")

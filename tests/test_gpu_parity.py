@@ -614,3 +614,70 @@ def test_fused_merge_matches_merge_kernel(cuda_device, shape, pdl, graph):
     for (a16, a32), (b16, b32) in zip(*outs):
         assert torch.equal(a16.view(torch.int16), b16.view(torch.int16))
         assert torch.equal(a32, b32)
+
+
+@pytest.mark.parametrize("shape", ["ragged", "nested", "shared_leaf", "oom"])
+def test_attend_own_token_synthetic(cuda_device, shape):
+    """attend_own_token (FK_OPT_APPEND_FIRST): each row's new K/V row is
+    written before attention and is part of its span (a real decoder); the
+    oracle attends over the chain including the step's own token."""
+    if shape == "oom":
+        eng = make_engine(cuda_device, H=4, L=2, kv_tokens=16 * 12, attend_own_token=True)
+        eng.fill([1] * 16 * 10, "root", None)
+        eng.fill([1] * 16, "a", "root")
+        eng.fill([1] * 15, "b", "root")
+        eng.generate("ra", "a", [1] * 3, "")
+        eng.generate("rb", "b", [1] * 3, "")
+        reps = [eng.step() for _ in range(3)]
+        eng.stream.synchronize()
+        assert any(r.failed for r in reps)
+    else:
+        eng = make_engine(cuda_device, H=8, L=2, attend_own_token=True)
+        if shape == "ragged":
+            fork_group(eng, 100, [0, 1, 15, 16, 17, 40], out_len=18, seed=3)
+            run_steps(eng, 18)
+        elif shape == "nested":
+            nested_forest(eng, root_len=300, app_len=50, n_apps=2, user_len=33, users_per_app=3, out_len=4)
+            run_steps(eng, 4)
+        else:
+            eng.fill([1] * 200, "root", None, boundary_hash=1)
+            eng.fill([1] * 30, "leaf", "root", boundary_hash=2)
+            eng.generate("a", "leaf", [1] * 4, "")
+            eng.generate("b", "leaf", [1] * 4, "")
+            run_steps(eng, 4)
+    for rec in eng.history:
+        # the span includes the step's new tokens; the reference count does not
+        assert rec["streamed_tokens"] == rec["batch_tokens"] + sum(p >= 0 for p in rec["positions"])
+    check_history(eng)
+
+
+def test_attend_own_token_model_rows(cuda_device):
+    """attend_own_token with model K/V rows: the output of a step includes
+    the row the model produced for that very step (compared with the oracle
+    over prefill rows + every appended model row so far)."""
+    import torch
+
+    from gpu_check import tensor_model_oracle
+    from paper_2405_19888_b200.workloads import drain_fills
+
+    H, L = 8, 3
+    eng = make_engine(cuda_device, H=H, L=L, attend_own_token=True)
+    fork_group(eng, 900, [30, 64, 5, 100, 0], out_len=4)
+    drain_fills(eng)
+    rows = len(eng.gens)
+    n0 = {eng.contexts[g.context_id].uid: (eng.contexts[g.context_id].token_count, r)
+          for r, g in enumerate(eng.gens.values())}
+    g = torch.Generator().manual_seed(9)
+    dev = torch.device("cuda", cuda_device)
+    q, k, v = (torch.randn((L, rows, H, 128), generator=g).to(torch.bfloat16).to(dev) for _ in range(3))
+    eng.model = P.TensorDecodeModel(q, k, v)
+    run_steps(eng, 3)
+    kv, queries = tensor_model_oracle(eng, n0)
+    check_history(eng, kv=kv, queries=queries)
+    # and it differs from the reference span (the own token matters)
+    eng2 = make_engine(cuda_device, H=H, L=L)
+    fork_group(eng2, 900, [30, 64, 5, 100, 0], out_len=4)
+    drain_fills(eng2)
+    eng2.model = P.TensorDecodeModel(q, k, v)
+    run_steps(eng2, 1)
+    assert not torch.equal(eng.history[0]["output"], eng2.history[0]["output"])
