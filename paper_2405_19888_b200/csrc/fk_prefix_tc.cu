@@ -37,7 +37,7 @@ constexpr int kTcTileBytes = 2 * kTcHalf;          // one K or V tile (32 KiB)
 constexpr int kTcChunkQ = 16;                      // chunk queue entries (producer lead <= ~6 chunks)
 struct TcMisc {
   uint64_t k_full[kTcKStages], k_empty[kTcKStages], v_full[kTcVStages], v_empty[kTcVStages];
-  uint64_t s_full[2], p_full[2], o_done, q_full;
+  uint64_t s_full[2], p_full[2], q_full;
   uint64_t cq_full[kTcChunkQ];  // chunk queue: the producer posts each chunk id it streams
   int cq[kTcChunkQ];
   uint32_t tmem_base;
@@ -103,7 +103,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   uint64_t* v_empty = ms.v_empty;
   uint64_t* s_full = ms.s_full;
   uint64_t* p_full = ms.p_full;
-  uint64_t& o_done = ms.o_done;
   uint64_t& q_full = ms.q_full;
   uint32_t& tmem_base_sh = ms.tmem_base;
   auto& s_max = ms.s_max;
@@ -150,7 +149,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], kTcSoftmaxWarps);
     }
-    mbar_init(&o_done, 1);
     mbar_init(&q_full, kTcSoftmaxWarps);
     for (int i = 0; i < kTcChunkQ; ++i) mbar_init(&ms.cq_full[i], 1);
     fence_mbar_init();
@@ -360,8 +358,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
               mma_ts(tm + 256, p_tm + kk * 16, bdesc, kIdescPV, (!p_new || kk > 0) ? 1u : 0u);
               mma_ts(tm + 256, p_tm + kk * 16 + 8, bdesc, kIdescPV, 1u);
             }
-            mma_commit(&o_done);
-            mma_commit(&v_empty[s]);
+            mma_commit(&v_empty[s]);  // also "O includes PV(tp)" for the softmax warps
             if (tp < 16) TL(48 + tp);
             ++tp;
             p_new = false;
@@ -460,11 +457,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       mbar_wait(&s_full[sb], (t >> 1) & 1);
       if (warp == 4 && lane == 0 && t < 16) TL(64 + t);
       tc_fence_after();
-      // o_done completes once per PV.  s_full(t) implies PV(t-2) is done
-      // (issued before S(t), in-order pipe) and PV(t) needs P(t), so here
-      // the barrier has completed phase t-2 or t-1: a parity wait for t-1
-      // is unambiguous.  A piece end must retire PV(t-1) before P(t) is
-      // released, so its later wait for PV(t) is unambiguous too.
+      // "O includes PV(u)" is v_empty[u % kTcVStages] completing its phase
+      // u / kTcVStages (committed right after PV(u); the producer waits for
+      // every phase before it reuses the stage, so no phase goes unobserved).
+      // s_full(t) implies PV(t-2) is done (issued before S(t), in-order
+      // pipe), so the phases before the awaited one have completed and the
+      // next one cannot (it needs P(u + kTcVStages)): the parity waits for
+      // PV(t-1) here and PV(t) at a piece end are unambiguous.
       if (active) {
         auto tile = [&](auto mode) {
           constexpr bool R16 = decltype(mode)::value;
@@ -511,7 +510,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
           // it (alpha = 1 for the others).
           const bool rescale = tile_max > m + kRescaleThreshold;
           const bool warp_rescale = __any_sync(0xffffffffu, rescale) && !chunk_start;
-          if (t > 0 && (warp_rescale || piece_end)) mbar_wait(&o_done, (t - 1) & 1);
+          if (t > 0 && (warp_rescale || piece_end))
+            mbar_wait(&v_empty[(t - 1) % kTcVStages], ((t - 1) / kTcVStages) & 1);
           if (warp_rescale) {
             const float alpha = rescale ? ex2(m - tile_max) : 1.f;
             l *= alpha;
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
         if (warp == 4 && lane == 0) TL(243 + min(c.qi, 3) * 4);
         if (next >= 0) stage_q(p.tc_chunk_item[next], c.qi + 1);
         if (warp == 2 && lane == 0) CTA_TL_NOTE(fk_tl_cta_prefix, layer, 3, c.qi + 1);
-        mbar_wait(&o_done, t & 1);
+        mbar_wait(&v_empty[t % kTcVStages], (t / kTcVStages) & 1);
         if (warp == 4 && lane == 0 && t < 16) TL(96 + t);
         tc_fence_after();
         if (active) {
