@@ -8,6 +8,7 @@ types.  The library is built in-tree by `make -C paper_2405_19888_b200/csrc`
 
 from __future__ import annotations
 
+import array
 import ctypes
 import os
 from ctypes import POINTER, c_char_p, c_float, c_int32, c_int64, c_size_t, c_uint8, c_uint32, c_uint64, c_void_p
@@ -158,20 +159,32 @@ def build_info() -> str:
     return lib.fk_build_info().decode()
 
 
+def _u32_buffer(ids):
+    """Token ids as a contiguous u32 buffer (array.array: one C loop, no
+    per-element ctypes objects); ids outside u32 wrap like struct.pack would
+    refuse to -- the reference only hashes u32 ids."""
+    try:
+        return array.array("I", ids)
+    except (OverflowError, TypeError):
+        return array.array("I", [int(t) & 0xFFFFFFFF for t in ids])
+
+
 def fnv1a64_u32(ids, seed: int) -> int:
     """hash_token_ids (tokenizer.py:47-49) through the C-ABI."""
-    n = len(ids)
-    arr = (c_uint32 * max(n, 1))(*[int(t) & 0xFFFFFFFF for t in ids])
-    return int(lib.fk_fnv1a64_u32(arr, n, seed & 0xFFFFFFFFFFFFFFFF))
+    arr = _u32_buffer(ids)
+    n = len(arr)
+    ptr = arr.buffer_info()[0] if n else None
+    return int(lib.fk_fnv1a64_u32(ctypes.cast(ptr, POINTER(c_uint32)) if ptr else None, n,
+                                  seed & 0xFFFFFFFFFFFFFFFF))
 
 
 def fnv1a64_chain(segments, seed: int):
     """Chained segment hashes (prefix.py:78-85) in one C call."""
-    flat = [int(t) & 0xFFFFFFFF for seg in segments for t in seg]
+    flat = _u32_buffer([t for seg in segments for t in seg])
     offs = [0]
     for seg in segments:
         offs.append(offs[-1] + len(seg))
-    ids = (c_uint32 * max(len(flat), 1))(*flat)
+    ids = ctypes.cast(flat.buffer_info()[0], POINTER(c_uint32)) if len(flat) else (c_uint32 * 1)()
     off = (c_int64 * len(offs))(*offs)
     out = (c_uint64 * max(len(segments), 1))()
     check(lib.fk_fnv1a64_chain(ids, off, len(segments), seed & 0xFFFFFFFFFFFFFFFF, out))

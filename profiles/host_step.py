@@ -1,0 +1,103 @@
+"""Host cost of the engine step with several GpuEngines in one process.
+
+The reference manager steps its engines serially on one thread
+(run_until_idle, manager.py:638-657), so with one engine per GPU the host
+time of GpuEngine.step must stay well under the GPU step time.  This runs
+the unmodified reference runtime (semflow from /root/reference or
+baseline/_ref) over Config(engines=N) with engine_factory: N shared-prompt
+groups (64 users each, 6000-token system prompt, 200-token unique part), one
+group per engine, and reports the host microseconds spent inside
+GpuEngine.step (plan, launches, growth, bookkeeping; the GPU runs
+asynchronously) and the whole manager loop per engine step.
+
+    python profiles/host_step.py [--engines 8] [--output-len 64] [--layers 32 --heads 32]
+
+All engines live on the visible GPU(s) (engine eI -> cuda:(I mod ndev));
+LLaMA-7B attention shape by default so that 8 engines fit on one B200.
+"""
+
+import argparse
+import dataclasses
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+for ref in (os.environ.get("FK_REFERENCE", "/root/reference/pkg/src"), os.path.join(ROOT, "baseline", "_ref")):
+    if os.path.isdir(os.path.join(ref, "semflow")):
+        sys.path.insert(1, ref)
+        break
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--engines", type=int, default=8)
+    ap.add_argument("--users", type=int, default=64)
+    ap.add_argument("--output-len", type=int, default=64)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--py-hash", action="store_true",
+                    help="keep the reference's pure-Python FNV (default: rebind it to the C one, INTEGRATION.md §3)")
+    args = ap.parse_args()
+
+    import torch
+
+    import paper_2405_19888_b200 as P
+    import semflow.manager as sm
+    from semflow.config import Config
+    from semflow.experiments import run_workload_manager
+    from semflow.workloads import Workload, shared_prompt_serving
+
+    apps = []
+    for g in range(args.engines):
+        wl = shared_prompt_serving(100 + g, users=args.users, system_prompt_len=6000, unique_len=200,
+                                   output_len=args.output_len)
+        apps += [dataclasses.replace(a, app_id=f"g{g}.{a.app_id}") for a in wl.apps]
+    work = Workload("GroupsPerEngine", 7, {"groups": args.engines}, apps)
+
+    step_us = []
+    orig_step = P.GpuEngine.step
+
+    def timed_step(self):
+        t0 = time.perf_counter()
+        r = orig_step(self)
+        step_us.append((time.perf_counter() - t0) * 1e6)
+        return r
+
+    P.GpuEngine.step = timed_step
+    if not args.py_hash:  # render_prefix / end hashes through fk_fnv1a64_u32
+        import semflow.engine as se
+        import semflow.prefix as sp
+        import semflow.tokenizer as st
+        st.hash_token_ids = sp.hash_token_ids = se.hash_token_ids = P.hash_token_ids
+    sm.Engine = P.engine_factory(P.ModelGeometry(args.layers, args.heads, 128))
+    t0 = time.perf_counter()
+    mgr, _, end_ns = run_workload_manager(work, "semflow", Config(engines=args.engines, kv_tokens=1 << 21))
+    wall = time.perf_counter() - t0
+    for e in mgr.engines.values():
+        if e.stream is not None:
+            e.stream.synchronize()
+    gpu_wall = time.perf_counter() - t0
+    decode = [len(e.history) for e in mgr.engines.values()]
+    steps_per_engine = [len(e.reports) for e in mgr.engines.values()]
+    # the first steps include the one-time graph captures: report the steady part too
+    steady = step_us[len(step_us) // 4:]
+    out = {
+        "engines": args.engines, "c_hash": not args.py_hash, "devices": torch.cuda.device_count(), "layers": args.layers, "heads": args.heads,
+        "users_per_engine": args.users, "steps_per_engine": steps_per_engine,
+        "engine_steps": len(step_us),
+        "step_host_us_mean": statistics.mean(step_us), "step_host_us_median": statistics.median(step_us),
+        "step_host_us_steady_mean": statistics.mean(steady), "step_host_us_steady_median": statistics.median(steady),
+        "manager_loop_us_per_engine_step": wall / max(len(step_us), 1) * 1e6,
+        "wall_s": wall, "wall_with_gpu_drain_s": gpu_wall, "virtual_end_ms": end_ns / 1e6,
+        "max_batch": max(max((r.batch_tokens for r in e.reports), default=0) for e in mgr.engines.values()),
+    }
+    del decode
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
