@@ -65,6 +65,8 @@ typedef struct {
   int64_t num_pages;    /* physical pages in the arena (0 when host-only) */
   int64_t free_pages;   /* physical pages on the free stack */
   int64_t arena_bytes;  /* device bytes of the KV arena */
+  int64_t host_wait_ns; /* host time fk_step_plan spent waiting for the GPU to release a plan
+                           slot (the host runs at most one step ahead) */
 } fk_pool_stats;
 
 /* Per-step plan summary returned by fk_step_plan. */

@@ -67,6 +67,7 @@ class PoolStats(ctypes.Structure):
         ("num_pages", c_int64),
         ("free_pages", c_int64),
         ("arena_bytes", c_int64),
+        ("host_wait_ns", c_int64),
     ]
 
 

@@ -165,6 +165,7 @@ struct fk_pool {
   unsigned fused_epoch = 0;  // "left" value of the latest fused launch
   size_t mctl_left_cap() const { return (size_t)std::max(num_sms, 1) * 12; }  // private grid warps
   int64_t fused_merge = 0;   // FK_OPT_FUSED_MERGE (measured slower than the merge kernel: off)
+  int64_t host_wait_ns = 0;  // time fk_step_plan blocked on the GPU (plan slot reuse)
   int64_t append_first = 0;  // FK_OPT_APPEND_FIRST: fk_step_plan grows the rows first (attend own token)
   bool plan_grew = false;    // the current plan already did the step's growth (fk_step_grow returns it)
   std::vector<int64_t> grow_pos, grow_ids;
@@ -419,6 +420,7 @@ int fk_pool_stats_get(const fk_pool* p, fk_pool_stats* out) {
   out->num_pages = p->num_pages;
   out->free_pages = (int64_t)p->free_pages.size();
   out->arena_bytes = (int64_t)p->arena_bytes;
+  out->host_wait_ns = p->host_wait_ns;
   return FK_OK;
 }
 
@@ -1098,7 +1100,11 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   p->cur = (p->cur + 1) & 1;
   PlanSlot& slot = p->slots[p->cur];
-  if (slot.armed) FK_CUDA(cudaEventSynchronize(slot.done));
+  if (slot.armed) {
+    const auto w0 = std::chrono::steady_clock::now();
+    FK_CUDA(cudaEventSynchronize(slot.done));
+    p->host_wait_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - w0).count();
+  }
   rc = ensure_slot(p, slot, L.size);
   if (rc != FK_OK) return rc;
   char* h = (char*)slot.host;

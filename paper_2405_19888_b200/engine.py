@@ -24,6 +24,8 @@ from __future__ import annotations
 
 import ctypes
 import itertools
+import os
+import time
 from collections import deque
 from dataclasses import dataclass, field
 from typing import Any, Deque, Dict, List, Optional, Sequence, Set, Tuple
@@ -32,6 +34,7 @@ from . import _lib
 from .errors import ContextBusy, OutOfMemory, UnknownContext, UnknownParentContext
 
 MS = 1_000_000  # ns per millisecond
+_PHASES = bool(os.environ.get("FK_DEBUG_TIMING"))  # per-phase host time of step() (profiles/host_step.py)
 FNV64_EMPTY = 0xCBF29CE484222325
 
 
@@ -898,7 +901,11 @@ class GpuEngine:
                     fill_completed.append(task.request_id)
 
         running = [g for g in self.gens.values() if g.started and not g.done]
+        if _PHASES:
+            tm = [time.perf_counter()]
         batch_tokens = self._plan(running) if running else 0
+        if _PHASES:
+            tm.append(time.perf_counter())
         if running and self.device is not None and self._fill_pending:
             self._wait_fills(running)
         snapshot = None
@@ -918,6 +925,8 @@ class GpuEngine:
                 self._decode_attention(running)
         if running and self.device is not None:
             self.kv_tokens_streamed += int(self.last_plan.streamed_tokens)
+        if _PHASES:
+            tm.append(time.perf_counter())
 
         elapsed = 0
         if fill_tokens > 0:
@@ -936,6 +945,13 @@ class GpuEngine:
             if running and self.device is not None:
                 self._append(running, positions)
 
+        if _PHASES:
+            tm.append(time.perf_counter())
+            acc = self.__dict__.setdefault("phase_us", {"plan": 0.0, "attention": 0.0, "grow_append": 0.0, "n": 0})
+            acc["plan"] += (tm[1] - tm[0]) * 1e6
+            acc["attention"] += (tm[2] - tm[1]) * 1e6
+            acc["grow_append"] += (tm[3] - tm[2]) * 1e6
+            acc["n"] += 1
         for rid in fill_completed:  # fills done this step decode next step
             g = self.gens.get(rid)
             if g is not None:

@@ -62,9 +62,14 @@ def main():
     orig_step = P.GpuEngine.step
 
     def timed_step(self):
+        w0 = self.pool_stats().host_wait_ns if self.device is not None else 0
         t0 = time.perf_counter()
         r = orig_step(self)
-        step_us.append((time.perf_counter() - t0) * 1e6)
+        t1 = time.perf_counter()
+        w1 = self.pool_stats().host_wait_ns if self.device is not None else 0
+        # host CPU time of the step: wall time minus the time the plan waited
+        # for the GPU to release a plan slot (the host runs <= 1 step ahead)
+        step_us.append((t1 - t0) * 1e6 - (w1 - w0) / 1e3)
         return r
 
     P.GpuEngine.step = timed_step
@@ -96,6 +101,13 @@ def main():
         "max_batch": max(max((r.batch_tokens for r in e.reports), default=0) for e in mgr.engines.values()),
     }
     del decode
+    ph = [e.__dict__.get("phase_us") for e in mgr.engines.values()]
+    ph = [x for x in ph if x]
+    if ph:  # FK_DEBUG_TIMING=1: per-phase host us per step (plan includes its GPU wait)
+        n = sum(x["n"] for x in ph)
+        out["phase_us"] = {k: sum(x[k] for x in ph) / n for k in ("plan", "attention", "grow_append")}
+        waits = sum(e.pool_stats().host_wait_ns for e in mgr.engines.values() if e.device is not None)
+        out["phase_us"]["plan_gpu_wait"] = waits / 1e3 / n
     print(json.dumps(out))
 
 
