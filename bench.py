@@ -470,10 +470,8 @@ def main():
     peak, peak_kind = load_peaks()
     achieved = bytes_layer / t_layer / 1e9
     value = total_rows * args.steps / t_steps
-    # per layer: prefix kernel(s) + private + merge (none with the fused merge);
-    # per step: one K/V append
-    launches_per_step = L * (1 + int(info.num_mma_items > 0) + int(info.num_tc_items > 0)
-                             + int(not info.fused_merge)) + 1
+    # per layer: prefix kernel(s) + private + merge; per step: one K/V append
+    launches_per_step = L * (2 + int(info.num_mma_items > 0) + int(info.num_tc_items > 0)) + 1
 
     # ---- e2e: host (pinned) inputs through the engine API
     e2e = None

@@ -80,8 +80,8 @@ typedef struct {
   int32_t max_slots;       /* partial slots per (row, head) incl. the private one */
   int32_t num_tc_items;    /* prefix items routed to the tcgen05 kernel */
   int32_t num_mma_items;   /* prefix items routed to the warp-level mma.sync kernel */
-  int32_t fused_merge;     /* 1: each (row, head) is merged by its last partial's writer
-                              (no merge kernel); see FK_OPT_FUSED_MERGE */
+  int32_t fused_merge;     /* always 0 since round 2 (the fused merge was removed: every
+                              launch merges with fk_merge_kernel) */
   int64_t streamed_tokens; /* KV tokens the kernels stream per layer: batch_tokens, plus the
                               step's new tokens under FK_OPT_APPEND_FIRST */
 } fk_plan_info;
@@ -116,22 +116,13 @@ enum {
                                  schedule, 1..32 (default 2): the granularity of its tail */
   FK_OPT_PRIV_STATIC_FIRST = 9, /* 1 (default): the private warps that start at once take their
                                  first chunk by warp index instead of a ticket */
-  FK_OPT_TC_MIN_CHUNK = 10,   /* chunk size (128-token tiles) of the tcgen05 prefix kernel's dynamic
-                                 tail, 1..24 (default 4) */
-  FK_OPT_PRIV_WARPS = 11,     /* private CTA shape: 10 warps x 2 stages (default), 6 x 4, 7 x 4,
-                                 8 x 3, 9 x 3, 11 x 2, 12 x 2 or 14 x 2 */
+  FK_OPT_PRIV_WARPS = 11,     /* private CTA shape: 10 warps x 2 stages (default), 8 x 3 or 12 x 2 */
   FK_OPT_GRAPH = 12,          /* 1 (default): fk_attn_decode_layers replays its launches as a CUDA
                                  graph (captured once per launch structure, parameters updated in
                                  place afterwards); 0: direct launches */
-  FK_OPT_TC_DYN_PCT = 13,     /* share (%) of the prefix tiles the tcgen05 CTAs take dynamically after
-                                 their cost-balanced static ranges (default 0: measured, an epilogue per chunk costs more than the balance gains) */
   FK_OPT_TC_BOUNDARY_COST = 14, /* static split: tiles a piece start mid-range costs a CTA (default 4) */
-  FK_OPT_FUSED_MERGE = 15     /* 1: no merge kernel -- the writer of the last partial of a (row, head)
-                                 merges it (private warps at once; rows a tcgen05 piece completes by
-                                 the row's owning private warp as it leaves, or by the tcgen05 CTA
-                                 if the owner has left); needs tcgen05 and private work, no mma.sync
-                                 items, launch order 0.  0 (default): a merge kernel after every
-                                 layer -- measured faster */,
+  /* 10, 13 (tcgen05 dynamic tail) and 15 (fused merge) were removed in round 2:
+     measured slower than what they replace; setting them fails */
   FK_OPT_APPEND_FIRST = 16    /* 1: attend to the step's own token (a real decoder): fk_step_plan does
                                  the step's one-token growth (row order, sequential OOM rule) and
                                  plans spans that include it; the caller then takes the growth from

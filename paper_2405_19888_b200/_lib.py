@@ -35,12 +35,9 @@ FK_OPT_PREFIX_RATE_PCT = 6
 FK_OPT_PDL = 7
 FK_OPT_PRIV_MIN_CHUNK = 8
 FK_OPT_PRIV_STATIC_FIRST = 9
-FK_OPT_TC_MIN_CHUNK = 10
 FK_OPT_PRIV_WARPS = 11
 FK_OPT_GRAPH = 12
-FK_OPT_TC_DYN_PCT = 13
 FK_OPT_TC_BOUNDARY_COST = 14
-FK_OPT_FUSED_MERGE = 15
 FK_OPT_APPEND_FIRST = 16
 
 

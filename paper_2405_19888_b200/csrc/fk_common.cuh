@@ -138,14 +138,13 @@ template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
                             Args&&... args) {
   if (g_launch_rec) {
-    LaunchRec r;
+    LaunchRec& r = g_launch_rec->push();
     r.func = (const void*)kernel;
     r.grid = grid;
     r.block = block;
     r.smem = smem;
     r.pdl = pdl;
     (rec_push_arg<KArgs>(r, static_cast<KArgs>(args)), ...);
-    g_launch_rec->push_back(std::move(r));
     return cudaSuccess;
   }
   cudaLaunchConfig_t cfg = {};
@@ -229,6 +228,10 @@ __device__ __forceinline__ uint2 synth_chunk(unsigned long long key, int j, floa
   }
   return make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
 }
+
+// ------------------------------------------------------------ the plan
+// Per translation unit (static): uploaded by upload_plan_main / _tc.
+static __constant__ PlanDev fk_plan_c[kPlanSlots];
 
 // ------------------------------------------------------ partial bookkeeping
 __device__ __forceinline__ long long part_index(const PlanDev& p, int H, int row, int slot, int head) {
@@ -335,129 +338,4 @@ __device__ __forceinline__ void merge_row_head_warp(const ArenaDev& a, const Pla
   merge_row_head_warp<8>(a, p, row, head, out, out_f32, lane, partial_count(p, a.num_heads, row, head));
 }
 
-// ------------------------------------------------------------ fused merge
-// (FK_OPT_FUSED_MERGE=1; measured slower than the merge kernel.)
-// Every partial counts as an arrival on its (row, head) counter, released
-// after the partial's stores (and, through the warp / CTA barrier before
-// it, its partners') and acquired by whoever sees the final count: private
-// warps count a piece one piece late behind an acq_rel fence
-// (fused_private_step), tcgen05 CTAs count their static chunks' rows in one
-// batch behind a fence at the end, and a dynamic chunk's rows at its end
-// with acq_rel atomics.  Who merges:
-//  * a private warp whose arrival was the last merges the row (the count's
-//    result is read one piece later, so its latency hides under the next
-//    piece's loads);
-//  * a row completed by a tcgen05 piece is merged by its owner, private warp
-//    rh % grid_warps, when that warp leaves -- unless the owner has already
-//    left, in which case the tcgen05 CTA marks the row's orphan slot and
-//    merges it when the CTA finishes.  Leaving = store "left" (this launch's
-//    epoch), SC fence, then read the owned rows' counters; the tcgen05 side
-//    does its arrival, SC fence, then reads the owner's "left": at least one
-//    side sees the other (store-buffering with fences), so every row is
-//    merged at least once.  A second merge of a row rewrites identical bytes.
-// ArenaDev::mctl (per launch half): from [4] the mctl_rh arrival counters,
-// then one orphan slot per (tcgen05 chunk, query row)
-// (PlanDev::tc_chunk_rowbase), then the private warps' "left" epochs.
-// Counters and slots return to 0 within the launch (their mergers); epochs
-// only grow.
-__device__ __forceinline__ unsigned* mctl_cnt(const ArenaDev& a) { return a.mctl + 4; }
-__device__ __forceinline__ unsigned* mctl_orphans(const ArenaDev& a) { return a.mctl + 4 + a.mctl_rh; }
-__device__ __forceinline__ unsigned* mctl_left(const ArenaDev& a) { return a.mctl + 4 + a.mctl_rh + a.mctl_q; }
-
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_sc() { asm volatile("fence.sc.gpu;" ::: "memory"); }
-
-// merge rh and zero its counter for the launch after next (a concurrent
-// second merger writes the same bytes and zeroes it again)
-__device__ __forceinline__ void fused_merge_rh(const ArenaDev& a, const PlanDev& p, int rh, int lane) {
-  merge_row_head_warp(a, p, rh / a.num_heads, rh % a.num_heads, a.out, a.out_f32, lane);
-  if (lane == 0) mctl_cnt(a)[rh] = 0u;
-}
-
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-
-// Private warps count their pieces one piece late, so neither the release
-// (its stores long complete) nor the atomic's result (returned a piece ago)
-// stalls the stream.  At a piece end, before that piece's loads and stores:
-// read the result of the previous count (`pend`), fence (release for the
-// stored-but-uncounted piece `unrel`, acquire for `pend`), count `unrel`,
-// and merge `pend`'s row if its count was the last.
-__device__ __forceinline__ void fused_private_step(const ArenaDev& a, const PlanDev& p, int& unrel_rh, int& pend_rh,
-                                                   unsigned& pend_old, int lane) {
-  int last = lane == 0 && pend_rh >= 0 && pend_old + 1u == (unsigned)p.row_head_count[pend_rh];
-  const int merge_rh = pend_rh;
-  __syncwarp();
-  fence_acq_rel();
-  pend_rh = unrel_rh;
-  unrel_rh = -1;
-  if (pend_rh >= 0 && lane == 0) pend_old = atomicAdd(mctl_cnt(a) + pend_rh, 1u);
-  last = __shfl_sync(0xffffffffu, last, 0);
-  __syncwarp();
-  if (last) fused_merge_rh(a, p, merge_rh, lane);
-}
-
-// a private warp leaves: announce it, then merge the owned rows that are
-// complete (rh = gw + k * grid_warps)
-__device__ __forceinline__ void fused_leave(const ArenaDev& a, const PlanDev& p, int gw, int grid_warps, int lane) {
-  if (lane == 0) {
-    *(volatile unsigned*)(mctl_left(a) + gw) = p.fused_epoch;
-    fence_sc();
-  }
-  __syncwarp();
-  const int nrh = p.num_rows * a.num_heads;
-  for (int base = gw; base < nrh; base += 32 * grid_warps) {
-    const int rh = base + lane * grid_warps;
-    bool done = false;
-    if (rh < nrh) done = ld_acquire(mctl_cnt(a) + rh) == (unsigned)p.row_head_count[rh];
-    unsigned m = __ballot_sync(0xffffffffu, done);
-    __syncwarp();
-    while (m) {
-      const int l = __ffs(m) - 1;
-      m &= m - 1;
-      fused_merge_rh(a, p, base + l * grid_warps, lane);
-    }
-  }
-}
-
-// a tcgen05 piece row's partial is written (both halves' stores precede
-// this, bar.sync): count it; if it completed the row and the row's owner
-// has left, mark the orphan slot for this CTA's end
-__device__ __forceinline__ void fused_arrive_tc_row(const ArenaDev& a, const PlanDev& p, int rh, int slot) {
-  if (atom_add_acq_rel(mctl_cnt(a) + rh, 1u) + 1u != (unsigned)p.row_head_count[rh]) return;
-  fence_sc();
-  if (*(volatile unsigned*)(mctl_left(a) + rh % p.priv_warps) == p.fused_epoch)
-    mctl_orphans(a)[slot] = (unsigned)rh + 1u;
-}
-
-// end of a tcgen05 CTA: merge the marked slots [s0, s1); orphan k (in slot
-// order) goes to warp k % nw.  Marks were written before a CTA barrier; the
-// caller zeroes the slots after another one.
-__device__ __forceinline__ void fused_merge_orphans(const ArenaDev& a, const PlanDev& p, int s0, int s1, int warp,
-                                                    int nw, int lane) {
-  unsigned* slots = mctl_orphans(a);
-  int k0 = 0;  // orphans before this group
-  for (int g = s0; g < s1; g += 32) {
-    const unsigned v = g + lane < s1 ? __ldcg(slots + g + lane) : 0u;
-    const unsigned m = __ballot_sync(0xffffffffu, v != 0u);
-    unsigned mine = 0u;  // lanes whose orphan ordinal falls on this warp
-    for (unsigned mm = m; mm; mm &= mm - 1) {
-      const int l = __ffs(mm) - 1;
-      if ((k0 + __popc(m & ((1u << l) - 1u))) % nw == warp) mine |= 1u << l;
-    }
-    for (; mine; mine &= mine - 1) {
-      const int l = __ffs(mine) - 1;
-      fused_merge_rh(a, p, (int)__shfl_sync(0xffffffffu, v, l) - 1, lane);
-    }
-    k0 += __popc(m);
-  }
-}
 }  // namespace fk

@@ -41,21 +41,14 @@ struct PlanDev {
   const int* qrows;        // request rows
   const int* qslot;        // slot of piece 0 for each (item, query)
   // tcgen05 schedule: chunks of consecutive tiles of one item, in unit
-  // order; CTA b streams its static chunks, then takes dynamic ones by ticket
-  // (ArenaDev::ticket_tc - tc_ticket_base).
+  // order; CTA b streams chunks [tc_cta_chunk0[b], tc_cta_chunk0[b + 1]).
   int tc_units, tc_ctas, tc_nchunks;
-  unsigned long long tc_ticket_base;
   const int* tc_chunk_item;       // [tc_nchunks]
   const int* tc_chunk_tile0;      // [tc_nchunks] first tile within the item
   const int* tc_chunk_tile1;      // [tc_nchunks] end tile (exclusive)
   const int* it_first_chunk;      // per item: its first chunk (piece 0)
-  const int* tc_cta_chunk0;       // [tc_ctas + 1]: CTA b's static chunks are [chunk0[b], chunk0[b + 1])
-  int tc_static_chunks;           // dynamic chunk = tc_static_chunks + ticket
-  int fused;                      // fused merge on this launch (set per launch)
-  const int* tc_chunk_rowbase;    // [tc_nchunks + 1]: first orphan slot of each chunk (prefix sums of nq)
-  int tc_active_ctas;             // tcgen05 CTAs with at least one static chunk
+  const int* tc_cta_chunk0;       // [tc_ctas + 1]
   int tc_l2_share;                // CTAs b, b + X/k stream the same tiles together: default L2 policy
-  unsigned fused_epoch;           // this launch's "left" value (fk_common.cuh; set per launch)
   // rows
   const int* row_priv_off;     // offset into pages[] / page_ntok[]
   const int* row_priv_npages;
@@ -93,17 +86,20 @@ struct ArenaDev {
   long long num_pages;
   int num_layers;
   int num_heads;
-  float* part_o;          // [rows][max_slots][H][D]
+  float* part_o;          // [rows][max_slots][H][D]  (this launch's half)
   float2* part_ml;        // [rows][max_slots][H]  (m in log2 domain, l)
-  unsigned long long* ticket;     // private chunk ticket counter (never reset)
-  unsigned long long* ticket_tc;  // tcgen05 prefix chunk ticket counter (never reset)
-  // fused merge (this launch's half; layout in fk_common.cuh): control
-  // words, arrival counters per (row, head), orphan slots per tcgen05 row piece
-  unsigned* mctl;
-  int mctl_rh, mctl_q;
-  __nv_bfloat16* out;     // this launch's outputs (fused merge)
-  float* out_f32;
+  // private chunk ticket counter of this launch's half: counts from 0, and
+  // the launch's merge kernel zeroes it once every CTA of the launch is done
+  // (the next launch on this half is two launches later and cannot start
+  // before that merge completed: see fk_merge_kernel)
+  unsigned* tick;
 };
+
+// The step plan lives in __constant__ memory (one entry per pool plan slot,
+// uploaded with the plan, fk_common.cuh), so a layer's kernel parameters are
+// the same from step to step and the step's CUDA graph replays without
+// parameter updates.
+constexpr int kPlanSlots = 128;  // 64 device pools per process x 2 plan slots
 
 inline __host__ __device__ long long plane_index(int layer, int kv, int head, int H) {
   return ((long long)layer * 2 + kv) * H + head;
@@ -126,22 +122,39 @@ struct LaunchRec {
     for (size_t i = 0; i < offs.size(); ++i) args[i] = bytes.data() + offs[i];
   }
 };
+// Recorded launches; entries are reused across calls (their vectors keep
+// their capacity), n = how many are valid.
+struct RecBuf {
+  std::vector<LaunchRec> v;
+  size_t n = 0;
+  LaunchRec& push() {
+    if (n == v.size()) v.emplace_back();
+    LaunchRec& r = v[n++];
+    r.bytes.clear();
+    r.offs.clear();
+    return r;
+  }
+};
 // Non-null while fk_attn_decode_layers records: launch_k appends instead of launching.
-extern thread_local std::vector<LaunchRec>* g_launch_rec;
+extern thread_local RecBuf* g_launch_rec;
 
 
-// Launchers (fk_kernels.cu).  All return cudaError_t of the launch.
-cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
-                           float scale_log2, const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl,
-                           cudaStream_t s);
-cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
+// Launchers (fk_kernels.cu, fk_prefix_tc.cu).  All return cudaError_t of the
+// launch.  `ps` is the plan's constant-memory slot; `p` the host copy of the
+// same plan (grid sizes).
+// the plan's constant-memory copy in each translation unit that reads it
+cudaError_t upload_plan_main(int ps, const PlanDev* host_pinned, cudaStream_t s);  // fk_kernels.cu
+cudaError_t upload_plan_tc(int ps, const PlanDev* host_pinned, cudaStream_t s);    // fk_prefix_tc.cu
+cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,
+                           float scale_log2, const CUtensorMap* tmap, int grid, bool pdl, cudaStream_t s);
+cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,
                               float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
-cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
+cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,
                              float scale_log2, const CUtensorMap* tmap, const CUtensorMap* tmap_run,
-                             bool pdl, bool after_private, bool trig_late, cudaStream_t s);
-cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, int layer, bool pdl,
+                             bool pdl, bool after_private, cudaStream_t s);
+cudaError_t launch_merge(const ArenaDev& a, int ps, void* out, float* out_f32, int layer, int grid, bool pdl,
                          cudaStream_t s);
-cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers,
+cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int ps, int layer0, int nlayers,
                           const void* k, const void* v, cudaStream_t s);
 cudaError_t launch_synth_fill(const ArenaDev& a, const int* pages_dev, int npages_first,
                               long long uid, long long pos0, long long pos1,
@@ -150,9 +163,9 @@ cudaError_t launch_fill_kv(const ArenaDev& a, const int* pages_dev, int first_pa
                            int layer0, int nlayers, const void* k, const void* v, cudaStream_t s);
 cudaError_t launch_copy_pages(const ArenaDev& dst, const void* src_kv, long long src_num_pages, const int* pages_dev,
                               int npages, cudaStream_t s);
-cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p,
+cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p, int ps,
                                  unsigned long long seed, void* q_all, cudaStream_t s);
-cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p,
+cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p, int ps,
                                 unsigned long long seed, float k_scale, cudaStream_t s);
 
 }  // namespace fk

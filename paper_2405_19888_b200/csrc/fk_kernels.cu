@@ -19,7 +19,7 @@
 
 namespace fk {
 
-thread_local std::vector<LaunchRec>* g_launch_rec = nullptr;
+thread_local RecBuf* g_launch_rec = nullptr;
 
 // =========================================================== private (n_c=1)
 // Units u = (head, flat private page entry e), head-major.  The plan cuts the
@@ -63,11 +63,11 @@ struct PdlTail {
   }
 };
 template <int STAGES, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, PlanDev p, int layer,
+__global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, int ps, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
                                                                    float scale_log2,
-                                                                   const __grid_constant__ CUtensorMap tmap,
-                                                                   unsigned long long ticket_base) {
+                                                                   const __grid_constant__ CUtensorMap tmap) {
+  const PlanDev& p = fk_plan_c[ps];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[WARPS][STAGES];
@@ -86,20 +86,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   // The warps of the CTAs that start at once (the first priv_static of the
   // grid) begin on chunk = their global warp index, with no ticket round trip
   // before their first loads; every later chunk comes from a ticket:
-  // chunk = priv_static + ticket.  Each warp stops after its first failing
-  // ticket, so a launch consumes nchunks - priv_static + (grid warps) tickets
-  // (the host advances ticket_base by that).
+  // chunk = priv_static + ticket, the counter (this launch's half) starting
+  // at 0 and reset by the launch's merge kernel.  Each warp stops after its
+  // first failing ticket.
   const int gw = blockIdx.x * WARPS + warp;
   auto grab = [&]() -> int {
     int c = 0;
-    if (lane == 0) c = p.priv_static + (int)(atomicAdd(a.ticket, 1ull) - ticket_base);
+    if (lane == 0) c = p.priv_static + (int)atomicAdd(a.tick, 1u);
     return __shfl_sync(0xffffffffu, c, 0);
   };
   int ca = gw < p.priv_static ? gw : grab();
-  if (ca >= nch) {
-    if (p.fused) fused_leave(a, p, gw, gridDim.x * WARPS, lane);
-    return;
-  }
+  if (ca >= nch) return;
 
   uint8_t* ring = smem + warp * STAGES * kPwStageBytes;
   if (lane == 0) {
@@ -186,10 +183,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   for (int k = 0; k < 8; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
   float m = -INFINITY, l = 0.f;
   const int mi = lane >> 3, ri = lane & 7;
-  // fused merge (fk_common.cuh): the stored-but-uncounted piece's (row, head),
-  // and the counted one's with its count
-  int unrel_rh = -1, pend_rh = -1;
-  unsigned pend_old = 0u;
 
   while (true) {
     // the unit after this one (next in A, else first of B) decides the piece end
@@ -197,15 +190,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
     const bool have_next = !chunk_last || lb > 0;
     const UnitMeta nxt = !chunk_last ? sh(ma, i + 1) : (lb > 0 ? sh(mb, 0) : cur);
     const bool piece_end = chunk_last || nxt.row != cur.row || nxt.head != cur.head;
-    if (p.fused && piece_end && (unrel_rh >= 0 || pend_rh >= 0)) {
-#ifdef FK_TIMELINE
-      const unsigned long long tf0 = global_ns();
-#endif
-      fused_private_step(a, p, unrel_rh, pend_rh, pend_old, lane);
-#ifdef FK_TIMELINE
-      if (lane == 0 && blockIdx.x < 1024) atomicAdd(&fk_tl_cta_priv[layer & 1][blockIdx.x][3], global_ns() - tf0);
-#endif
-    }
     if (piece_end && have_next) fetch_q(qn, nxt.row, nxt.head);
     const int s = (int)(seq % STAGES);
     mbar_wait(&full[warp][s], (seq / STAGES) & 1);
@@ -283,7 +267,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
         }
         if (g == 0) a.part_ml[pi] = make_float2(m, lsum);
       }
-      unrel_rh = (int)rh;
       m = -INFINITY;
       l = 0.f;
 #pragma unroll
@@ -310,17 +293,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, P
   }
 #ifdef FK_TIMELINE
   if (lane == 0) CTA_TL_NOTE(fk_tl_cta_priv, layer, 2, global_ns());
-#endif
-#ifdef FK_TIMELINE
-  const unsigned long long tl0 = global_ns();
-#endif
-  if (p.fused) {
-    fused_private_step(a, p, unrel_rh, pend_rh, pend_old, lane);  // count the last piece
-    fused_private_step(a, p, unrel_rh, pend_rh, pend_old, lane);  // settle it
-    fused_leave(a, p, gw, gridDim.x * WARPS, lane);
-  }
-#ifdef FK_TIMELINE
-  if (lane == 0 && blockIdx.x < 1024) atomicAdd(&fk_tl_cta_priv[layer & 1][blockIdx.x][3], (global_ns() - tl0) << 32);
 #endif
   CTA_TL_END(fk_tl_cta_priv, layer);
 }
@@ -352,8 +324,9 @@ __device__ __forceinline__ uint32_t sw128(int row, int c16) {
 }
 
 __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
-    ArenaDev a, PlanDev p, int layer, const __nv_bfloat16* __restrict__ q, float scale_log2,
+    ArenaDev a, int ps, int layer, const __nv_bfloat16* __restrict__ q, float scale_log2,
     const __grid_constant__ CUtensorMap tmap) {
+  const PlanDev& p = fk_plan_c[ps];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kPmStages];
@@ -533,21 +506,30 @@ __global__ void __launch_bounds__(kPmThreads) fk_prefix_mma_kernel(
 // ================================================================== merge
 // K4: one warp per (row, head) combines every partial (shared-prefix splits
 // + private pieces) in log2 space and writes the bf16 row (fp32 optional).
+// The grid is fixed (a multiple of the SM count, warps loop over (row,
+// head)), so its launch does not change with the batch.
 CTA_TL_DECL(fk_tl_cta_merge);
 
-__global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, PlanDev p, __nv_bfloat16* __restrict__ out,
+__global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, int ps, __nv_bfloat16* __restrict__ out,
                                                       float* __restrict__ out_f32, int layer) {
+  const PlanDev& p = fk_plan_c[ps];
   CTA_TL_START(fk_tl_cta_merge, layer);  // (timeline builds: [0] = after the wait)
-  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int H = a.num_heads;
-  const bool mine = w < p.num_rows * H;
-  const int ns = mine ? partial_count(p, H, w / H, w % H) : 0;  // plan data: before the wait
+  const int lane = threadIdx.x & 31;
+  const int H = a.num_heads, nrh = p.num_rows * H, stride = gridDim.x * 8;
+  int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int ns = w < nrh ? partial_count(p, H, w / H, w % H) : 0;  // plan data: before the wait
   pdl_wait_primary();       // partials of the prefix and private grids are complete
   pdl_launch_dependents();  // the next layer's first kernel may start (other partial half)
+  // Every CTA of this launch's prefix and private grids has finished, so
+  // nobody takes a ticket from this half any more: reset it for the launch
+  // after next (which cannot start before this grid completes -- its first
+  // kernel waits, directly or through the kernels in between, for this one).
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.tick = 0u;
 #ifdef FK_TIMELINE
   if (threadIdx.x == 0 && blockIdx.x < 1024) fk_tl_cta_merge[layer & 1][blockIdx.x][0] = global_ns();
 #endif
-  if (mine) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane, ns);  // (8 early slots: 12 / 16 measured slower)
+  if (w < nrh) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane, ns);  // (8 early slots: 12 / 16 measured slower)
+  for (w += stride; w < nrh; w += stride) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane);
   CTA_TL_END(fk_tl_cta_merge, layer);
 }
 
@@ -568,8 +550,9 @@ extern "C" int fk_debug_cta_timeline_merge(unsigned long long* out, int n) {
 // kAppendLayers layers: lanes 0-15 move K, 16-31 V, 16 B each; all of a
 // warp's loads are issued before its stores.
 constexpr int kAppendLayers = 8;
-__global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, PlanDev p, int layer0, int nlayers,
+__global__ void __launch_bounds__(256) fk_append_kernel(ArenaDev a, int ps, int layer0, int nlayers,
                                                        const uint4* __restrict__ k, const uint4* __restrict__ v) {
+  const PlanDev& p = fk_plan_c[ps];
   const int H = a.num_heads;
   const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (w >= p.num_rows * H) return;
@@ -666,7 +649,8 @@ __global__ void fk_synth_fill_kernel(ArenaDev a, const int* __restrict__ pages, 
   }
 }
 
-__global__ void fk_synth_queries_kernel(ArenaDev a, PlanDev p, unsigned long long seed, uint2* q_all) {
+__global__ void fk_synth_queries_kernel(ArenaDev a, int ps, unsigned long long seed, uint2* q_all) {
+  const PlanDev& p = fk_plan_c[ps];
   const int row = blockIdx.x, layer = blockIdx.y;
   const int H = a.num_heads, B = p.num_rows;
   for (int i = threadIdx.x; i < H * 32; i += blockDim.x) {
@@ -676,7 +660,8 @@ __global__ void fk_synth_queries_kernel(ArenaDev a, PlanDev p, unsigned long lon
   }
 }
 
-__global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long seed, float k_scale) {
+__global__ void fk_synth_append_kernel(ArenaDev a, int ps, unsigned long long seed, float k_scale) {
+  const PlanDev& p = fk_plan_c[ps];
   const int row = blockIdx.x, layer = blockIdx.y;
   const int pg = p.app_page[row];
   if (pg < 0) return;
@@ -696,10 +681,14 @@ __global__ void fk_synth_append_kernel(ArenaDev a, PlanDev p, unsigned long long
 }
 
 // ============================================================== launchers
+cudaError_t upload_plan_main(int ps, const PlanDev* host_pinned, cudaStream_t s) {
+  return cudaMemcpyToSymbolAsync(fk_plan_c, host_pinned, sizeof(PlanDev), (size_t)ps * sizeof(PlanDev),
+                                 cudaMemcpyHostToDevice, s);
+}
+
 template <int STAGES, int WARPS>
-static cudaError_t launch_private_shape(const ArenaDev& a, const PlanDev& p, int layer, const void* q,
-                                       float scale_log2, const CUtensorMap* tmap, unsigned long long ticket_base,
-                                       bool pdl, cudaStream_t s) {
+static cudaError_t launch_private_shape(const ArenaDev& a, int ps, int layer, const void* q, float scale_log2,
+                                       const CUtensorMap* tmap, int grid_ctas, bool pdl, cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   constexpr int smem = priv_smem<STAGES, WARPS>();
   if (!attr_set_on_device(attr_devices)) {
@@ -707,50 +696,42 @@ static cudaError_t launch_private_shape(const ArenaDev& a, const PlanDev& p, int
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  const int grid = p.priv_warps / WARPS;
-  return launch_k(fk_private_kernel<STAGES, WARPS>, dim3(grid), dim3(WARPS * 32), smem, s, pdl, a, p, layer,
-                  (const __nv_bfloat16*)q, scale_log2, *tmap, ticket_base);
+  return launch_k(fk_private_kernel<STAGES, WARPS>, dim3(grid_ctas), dim3(WARPS * 32), smem, s, pdl, a, ps, layer,
+                  (const __nv_bfloat16*)q, scale_log2, *tmap);
 }
 
-cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                           const CUtensorMap* tmap, unsigned long long ticket_base, bool pdl, cudaStream_t s) {
+cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q, float scale_log2,
+                           const CUtensorMap* tmap, int grid, bool pdl, cudaStream_t s) {
   if (p.priv_units == 0) return cudaSuccess;
-  // ring shapes: per-warp stages x warps per CTA (8 KiB stages: 10 x 2 = 160 KiB, the
-  // default; 8 x 3 and 12 x 2 = 192 KiB; 7 x 4 = 224 KiB)
+  // ring shapes: per-warp stages x warps per CTA (8 KiB stages): 10 x 2 = 160 KiB
+  // (the default, measured best), 8 x 3 and 12 x 2 = 192 KiB
   switch (p.priv_wpc) {
-    case 6: return launch_private_shape<4, 6>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    case 7: return launch_private_shape<4, 7>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    case 9: return launch_private_shape<3, 9>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    case 11: return launch_private_shape<2, 11>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    case 12: return launch_private_shape<2, 12>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    case 14: return launch_private_shape<2, 14>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    case 8: return launch_private_shape<3, 8>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
-    default: return launch_private_shape<2, 10>(a, p, layer, q, scale_log2, tmap, ticket_base, pdl, s);
+    case 8: return launch_private_shape<3, 8>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+    case 12: return launch_private_shape<2, 12>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+    default: return launch_private_shape<2, 10>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
   }
 }
 
-cudaError_t launch_merge(const ArenaDev& a, const PlanDev& p, void* out, float* out_f32, int layer, bool pdl,
+cudaError_t launch_merge(const ArenaDev& a, int ps, void* out, float* out_f32, int layer, int grid, bool pdl,
                          cudaStream_t s) {
-  const int warps = p.num_rows * a.num_heads;
-  return launch_k(fk_merge_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, pdl, a, p, (__nv_bfloat16*)out,
-                  out_f32, layer);
+  return launch_k(fk_merge_kernel, dim3(grid), dim3(256), 0, s, pdl, a, ps, (__nv_bfloat16*)out, out_f32, layer);
 }
 
-cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
-                              const CUtensorMap* tmap, cudaStream_t s) {
+cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,
+                              float scale_log2, const CUtensorMap* tmap, cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   if (!attr_set_on_device(attr_devices)) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPmSmem);
     if (e != cudaSuccess) return e;
   }
-  return launch_k(fk_prefix_mma_kernel, dim3(p.tc_begin), dim3(kPmThreads), kPmSmem, s, false, a, p, layer,
+  return launch_k(fk_prefix_mma_kernel, dim3(p.tc_begin), dim3(kPmThreads), kPmSmem, s, false, a, ps, layer,
                   (const __nv_bfloat16*)q, scale_log2, *tmap);
 }
 
-cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int layer0, int nlayers, const void* k,
+cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int ps, int layer0, int nlayers, const void* k,
                           const void* v, cudaStream_t s) {
   dim3 grid((p.num_rows * a.num_heads + 7) / 8, (nlayers + kAppendLayers - 1) / kAppendLayers);
-  fk_append_kernel<<<grid, 256, 0, s>>>(a, p, layer0, nlayers, (const uint4*)k, (const uint4*)v);
+  fk_append_kernel<<<grid, 256, 0, s>>>(a, ps, layer0, nlayers, (const uint4*)k, (const uint4*)v);
   return cudaGetLastError();
 }
 
@@ -770,17 +751,17 @@ cudaError_t launch_fill_kv(const ArenaDev& a, const int* pages_dev, int first_pa
   return cudaGetLastError();
 }
 
-cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p, unsigned long long seed, void* q_all,
+cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p, int ps, unsigned long long seed, void* q_all,
                                  cudaStream_t s) {
   dim3 grid(p.num_rows, a.num_layers);
-  fk_synth_queries_kernel<<<grid, 256, 0, s>>>(a, p, seed, (uint2*)q_all);
+  fk_synth_queries_kernel<<<grid, 256, 0, s>>>(a, ps, seed, (uint2*)q_all);
   return cudaGetLastError();
 }
 
-cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p, unsigned long long seed, float k_scale,
+cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p, int ps, unsigned long long seed, float k_scale,
                                 cudaStream_t s) {
   dim3 grid(p.num_rows, a.num_layers);
-  fk_synth_append_kernel<<<grid, 256, 0, s>>>(a, p, seed, k_scale);
+  fk_synth_append_kernel<<<grid, 256, 0, s>>>(a, ps, seed, k_scale);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <climits>
 #include <cmath>
@@ -135,12 +136,11 @@ struct fk_pool {
   int64_t priv_min_chunk = kPrivMinChunk;  // smallest private chunk (pages): the tail granularity
   int64_t priv_wpc = kPrivWarpsPerCta;  // private CTA shape (warps; stages follow)
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
-  int64_t tc_min_chunk = 4;      // tcgen05 dynamic-tail chunk (tiles)
-  int64_t tc_dyn_pct = 0;        // share of the prefix tiles left to the dynamic tail (measured: 0 best)
   int64_t tc_boundary_cost = 4;  // tiles a piece start mid-range costs a tcgen05 CTA (static split)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t use_graph = 1;  // fk_attn_decode_layers replays a CUDA graph
-  std::map<std::tuple<int32_t, int32_t, cudaStream_t>, GraphCache> graphs;  // per (layer0, nlayers, stream)
+  std::map<std::tuple<int32_t, int32_t, cudaStream_t, int>, GraphCache> graphs;  // (layer0, nlayers, stream, slot/half)
+  fk::RecBuf rec_buf;  // launches recorded by fk_attn_decode_layers (storage reused)
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
   int64_t prefix_rate_pct = 50;  // prefix KV bytes/s per SM relative to the private stream's (measured optimum, headline)
@@ -160,19 +160,13 @@ struct fk_pool {
   float2* part_ml = nullptr;
   size_t part_cap = 0;     // entries (rows*slots*H) per half
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
-  unsigned* mctl = nullptr;  // fused merge words, two halves of 4 + mctl_rh + mctl_q (ArenaDev::mctl)
-  size_t mctl_rh = 0, mctl_q = 0;
-  unsigned fused_epoch = 0;  // "left" value of the latest fused launch
-  size_t mctl_left_cap() const { return (size_t)std::max(num_sms, 1) * 12; }  // private grid warps
-  int64_t fused_merge = 0;   // FK_OPT_FUSED_MERGE (measured slower than the merge kernel: off)
   int64_t host_wait_ns = 0;  // time fk_step_plan blocked on the GPU (plan slot reuse)
   int64_t append_first = 0;  // FK_OPT_APPEND_FIRST: fk_step_plan grows the rows first (attend own token)
   bool plan_grew = false;    // the current plan already did the step's growth (fk_step_grow returns it)
   std::vector<int64_t> grow_pos, grow_ids;
-  bool plan_fused_ok = false;  // the current plan admits the fused merge
-  unsigned long long* ticket = nullptr;  // device: private chunk tickets (never reset)
-  unsigned long long ticket_base = 0;    // tickets consumed by earlier private launches
-  unsigned long long ticket_tc_base = 0; // ... and by earlier tcgen05 prefix launches
+  unsigned* tick = nullptr;  // device: private chunk tickets, one counter per partial half
+  int plan_base = -1;        // first of this pool's two __constant__ plan slots (fk_plan_c)
+  int priv_grid = 0;         // private grid (CTAs) of the current plan
 
   ArenaDev arena() const {
     ArenaDev a;
@@ -182,14 +176,8 @@ struct fk_pool {
     a.num_heads = desc.num_heads;
     a.part_o = part_o;
     a.part_ml = part_ml;
-    a.ticket = ticket;
-    a.ticket_tc = ticket ? ticket + 1 : nullptr;
-    a.mctl = mctl;
-    a.mctl_rh = (int)mctl_rh;
-    a.mctl_q = (int)mctl_q;
-    a.out = nullptr;
-    a.out_f32 = nullptr;
-      return a;
+    a.tick = tick;
+    return a;
   }
 };
 
@@ -266,7 +254,7 @@ int reserve_pages(fk_pool* p, int64_t pages) {
   return encode_tmap(p);
 }
 
-int ensure_scratch(fk_pool* p, int rows, int slots, int64_t orphan_slots) {
+int ensure_scratch(fk_pool* p, int rows, int slots) {
   const size_t H = p->desc.num_heads, D = p->desc.head_dim;
   const size_t need = (size_t)std::max(rows, 1) * std::max(slots, 1) * H;
   if (need > p->part_cap) {
@@ -282,18 +270,6 @@ int ensure_scratch(fk_pool* p, int rows, int slots, int64_t orphan_slots) {
     FK_CUDA(cudaMalloc(&p->part_o, 2 * cap * D * sizeof(float)));
     FK_CUDA(cudaMalloc(&p->part_ml, 2 * cap * sizeof(float2)));
     p->part_cap = cap;
-  }
-  const size_t rh = (size_t)std::max(rows, 1) * H, oq = (size_t)std::max<int64_t>(orphan_slots, 1);
-  if (rh > p->mctl_rh || oq > p->mctl_q) {
-    const size_t cap_rh = std::max(rh + rh / 2, p->mctl_rh), cap_q = std::max(oq + oq / 2, p->mctl_q);
-    const size_t bytes = 2 * (4 + cap_rh + cap_q + p->mctl_left_cap()) * sizeof(unsigned);
-    if (p->mctl) FK_CUDA(cudaFree(p->mctl));
-    p->mctl = nullptr;
-    FK_CUDA(cudaMalloc(&p->mctl, bytes));
-    FK_CUDA(cudaMemset(p->mctl, 0, bytes));
-    FK_CUDA(cudaDeviceSynchronize());  // (legacy-stream memset; see reserve_pages)
-    p->mctl_rh = cap_rh;
-    p->mctl_q = cap_q;
   }
   return FK_OK;
 }
@@ -322,6 +298,25 @@ struct Layout {
     return off;
   }
 };
+
+// Process-wide allocator of the __constant__ plan slots (fk_plan_c): two
+// per device pool.
+std::mutex g_slot_mu;
+std::vector<bool> g_slot_used(kPlanSlots, false);
+int alloc_plan_slots() {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  for (int i = 0; i + 1 < kPlanSlots; i += 2)
+    if (!g_slot_used[i]) {
+      g_slot_used[i] = g_slot_used[i + 1] = true;
+      return i;
+    }
+  return -1;
+}
+void free_plan_slots(int base) {
+  if (base < 0) return;
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_slot_used[base] = g_slot_used[base + 1] = false;
+}
 
 }  // namespace
 
@@ -362,11 +357,16 @@ int fk_pool_create(const fk_pool_desc* desc, fk_pool** out) {
         return fail(FK_CUDA_ERROR, "cudaEventCreate failed");
       }
     }
-    if (cudaMalloc(&p->ticket, 2 * sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMemset(p->ticket, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    if (cudaMalloc(&p->tick, 2 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(p->tick, 0, 2 * sizeof(unsigned)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
       cudaGetLastError();
       fk_pool_destroy(p);
       return fail(FK_CUDA_ERROR, "ticket counter allocation failed");
+    }
+    p->plan_base = alloc_plan_slots();
+    if (p->plan_base < 0) {
+      fk_pool_destroy(p);
+      return fail(FK_INVALID_ARGUMENT, "more than %d device pools in one process", kPlanSlots / 2);
     }
     int rc = reserve_pages(p, desc->num_pages);
     if (rc != FK_OK) {
@@ -391,8 +391,8 @@ int fk_pool_destroy(fk_pool* p) {
     if (p->kv) cudaFree(p->kv);
     if (p->part_o) cudaFree(p->part_o);
     if (p->part_ml) cudaFree(p->part_ml);
-    if (p->mctl) cudaFree(p->mctl);
-    if (p->ticket) cudaFree(p->ticket);
+    if (p->tick) cudaFree(p->tick);
+    free_plan_slots(p->plan_base);
     for (auto& kv : p->graphs) kv.second.reset();
   }
   delete p;
@@ -434,18 +434,15 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_GRAPH: p->use_graph = value != 0; break;
     case FK_OPT_PRIV_STATIC_FIRST: p->priv_static_first = value != 0; break;
     case FK_OPT_PRIV_WARPS:
-      if (value < 6 || value > 14 || value == 13)
-        return fail(FK_INVALID_ARGUMENT, "private warps must be 6 to 12 or 14");
+      if (value != 8 && value != 10 && value != 12)
+        return fail(FK_INVALID_ARGUMENT, "private warps must be 8, 10 or 12");
       p->priv_wpc = value;
       break;
-    case FK_OPT_TC_MIN_CHUNK: p->tc_min_chunk = std::min<int64_t>(kTcMaxChunk, std::max<int64_t>(1, value)); break;
-    case FK_OPT_TC_DYN_PCT: p->tc_dyn_pct = std::min<int64_t>(100, std::max<int64_t>(0, value)); break;
     case FK_OPT_TC_BOUNDARY_COST: p->tc_boundary_cost = std::max<int64_t>(0, value); break;
     case FK_OPT_PRIV_MIN_CHUNK: p->priv_min_chunk = std::min<int64_t>(kPrivMaxChunk, std::max<int64_t>(1, value)); break;
     case FK_OPT_MIN_SPLIT_PAGES: p->min_split_pages = std::max<int64_t>(1, value); break;
     case FK_OPT_CORUN: p->corun = value; break;
     case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
-    case FK_OPT_FUSED_MERGE: p->fused_merge = value != 0; break;
     case FK_OPT_APPEND_FIRST: p->append_first = value != 0; break;
     default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
   }
@@ -748,24 +745,21 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     const double wv = (double)priv_tok_heads;
     tc_target = std::min<int64_t>(p->num_sms - 1, std::max<int64_t>(1, std::llround(p->num_sms * wp / (wp + wv))));
   }
-  // tcgen05 schedule, static + dynamic: the first (100 - tc_dyn_pct)% of the
-  // tile units are split into one cost-balanced range per CTA (a piece start
-  // mid-range costs tc_boundary_cost tiles), the rest into small chunks the
-  // CTAs that finish first take from a ticket counter, so per-SM speed
-  // differences even out without paying an epilogue per small chunk
-  // everywhere.  Chunks never cross an item and are listed in unit order (an
-  // item's chunks are contiguous: chunk - it_first_chunk = piece index).
+  // tcgen05 schedule: the tile units are split into one cost-balanced range
+  // per CTA (a piece start mid-range costs tc_boundary_cost tiles).  (A
+  // ticketed dynamic tail of small chunks was measured in round 1: an
+  // epilogue per chunk costs more than the balance gains -- removed.)
+  // Chunks never cross an item and are listed in unit order (an item's
+  // chunks are contiguous: chunk - it_first_chunk = piece index).
   std::vector<int32_t> ch_item, ch_t0, ch_t1, cta_chunk0;
   std::vector<int32_t> it_first_chunk(items.size(), 0);
-  int64_t tc_ctas = 0, n_static = 0;
+  int64_t tc_ctas = 0;
   bool tc_l2_share = false;
   if (tc_units > 0) {
     // at least ~4 tiles per CTA unless FK_OPT_PREFIX_TARGET_CTAS says
     // otherwise: a CTA's start-up (TMEM, barriers, first loads) costs about that
     const int64_t cap = p->prefix_target_ctas > 0 ? tc_units : (tc_units + 3) / 4;
     const int64_t X = std::max<int64_t>(1, std::min<int64_t>(tc_target, cap));
-    const int64_t u_dyn = std::min<int64_t>(tc_units - X, tc_units * p->tc_dyn_pct / 100);
-    const int64_t u_s = tc_units - std::max<int64_t>(0, u_dyn);
     // item of each unit boundary
     auto emit = [&](int64_t a, int64_t b) {  // chunks for units [a, b), split at items
       size_t i = num_mma;
@@ -823,7 +817,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     // time and all but the first hit L2 (the loads then keep the default
     // L2 policy: PlanDev::tc_l2_share).
     int64_t mirror_k = 0;
-    if (p->tc_dyn_pct == 0 && shared.size() == 1 && shared[0].tc && shared[0].splits == 1) {
+    if (shared.size() == 1 && shared[0].tc && shared[0].splits == 1) {
       const int64_t k = ((int64_t)shared[0].rows.size() + kTcQBlock - 1) / kTcQBlock;
       if (k >= 2 && X >= 2 * k && (int64_t)(items.size() - num_mma) == k * H && tc_units % k == 0) mirror_k = k;
     }
@@ -837,8 +831,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
         for (size_t j = 0; j + 1 < c0.size(); ++j) cut.push_back(c0[j] + g * ug);
       cut.push_back(tc_units);
     } else {
-      split(0, u_s, X, cut);
-      cut.push_back(u_s);
+      split(0, tc_units, X, cut);
+      cut.push_back(tc_units);
     }
     tc_l2_share = mirror_k > 0;
     tc_ctas = (int64_t)cut.size() - 1;
@@ -846,16 +840,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       cta_chunk0.push_back((int32_t)ch_item.size());
       emit(cut[b], cut[b + 1]);
     }
-    n_static = (int64_t)ch_item.size();
-    cta_chunk0.push_back((int32_t)n_static);
-    // dynamic tail: small chunks within items
-    for (int64_t u = u_s; u < tc_units;) {
-      size_t i = num_mma;
-      while (i + 1 < items.size() && it_unit_off[i + 1] <= u) ++i;
-      const int64_t end = std::min<int64_t>(u + p->tc_min_chunk, it_unit_off[i] + items[i].units);
-      emit(u, end);
-      u = end;
-    }
+    cta_chunk0.push_back((int32_t)ch_item.size());
     for (size_t i = num_mma, k = 0; i < items.size(); ++i) {
       while (k < ch_item.size() && ch_item[k] != (int32_t)i) ++k;
       it_first_chunk[i] = (int32_t)k;
@@ -863,8 +848,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   const int64_t tc_nchunks = (int64_t)ch_item.size();
   if (getenv("FK_DEBUG_PLAN")) {
-    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs, %lld chunks (%lld static):", (long long)tc_units,
-            (long long)tc_ctas, (long long)tc_nchunks, (long long)n_static);
+    fprintf(stderr, "fk plan: %lld tc units, %lld CTAs, %lld chunks:", (long long)tc_units, (long long)tc_ctas,
+            (long long)tc_nchunks);
     for (size_t k = 0; k < ch_item.size(); ++k) fprintf(stderr, " %d:%d-%d", ch_item[k], ch_t0[k], ch_t1[k]);
     fprintf(stderr, "\n");
   }
@@ -974,9 +959,9 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int64_t nchunks = (int64_t)chunk_start.size();
   chunk_start.push_back((int32_t)U);
   // launched first (order 1) the private grid must leave the prefix its SMs
-  const int64_t grid_sms = (corun && p->launch_order == 1) ? priv_sms : p->num_sms;
-  const int64_t grid_ctas = std::max<int64_t>(
-      1, std::min<int64_t>(grid_sms, (nchunks + wpc - 1) / wpc));
+  // The grid is the SM count whatever the work (warps without a chunk exit at
+  // once), so its launch stays the same from step to step.
+  const int64_t grid_ctas = (corun && p->launch_order == 1) ? priv_sms : p->num_sms;
   const int64_t G = grid_ctas * wpc;
   // items (row, head) are contiguous unit ranges in unit order (head-major,
   // rows by their offset), so one forward sweep finds every item's chunks
@@ -1028,17 +1013,6 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     return fail(FK_INVALID_ARGUMENT, "work-list invariant violated: %lld shared + %lld private != %lld batch tokens",
                 (long long)shared_tokens, (long long)private_tokens, (long long)streamed_tokens);
   const int n_items = (int)items.size();
-  // fused merge: every (row, head) must receive a partial, every tcgen05
-  // item a chunk, and the private warps (the queue's drainers) must exist
-  // orphan slot of (tcgen05 chunk, query row): prefix sums of the chunks' rows
-  std::vector<int32_t> ch_rowbase(ch_item.size() + 1, 0);
-  for (size_t k = 0; k < ch_item.size(); ++k) ch_rowbase[k + 1] = ch_rowbase[k] + items[ch_item[k]].nq;
-  int tc_active = 0;
-  for (int64_t b = 0; b + 1 < (int64_t)cta_chunk0.size(); ++b) tc_active += cta_chunk0[b] < cta_chunk0[b + 1];
-  bool fused_ok = num_mma == 0 && tc_nchunks > 0 && U > 0 && B > 0;
-  for (size_t i = num_mma; i < items.size() && fused_ok; ++i) fused_ok = items[i].units > 0;
-  for (int64_t i = 0; i < B * H && fused_ok; ++i) fused_ok = row_head_count[i] > 0;
-  p->plan_fused_ok = fused_ok;
   if (info) {
     info->batch_tokens = batch_tokens;
     info->shared_tokens = shared_tokens;
@@ -1049,7 +1023,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     info->max_slots = max_slots;
     info->num_tc_items = num_tc;
     info->num_mma_items = num_mma;
-    info->fused_merge = (fused_ok && p->fused_merge && p->launch_order == 0) ? 1 : 0;
+    info->fused_merge = 0;  // (the fused form was removed in round 2: always the merge kernel)
     info->streamed_tokens = streamed_tokens;
   }
   p->committed = false;
@@ -1066,7 +1040,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   PT(T7);
   // ---- upload ---------------------------------------------------------------
   FK_ON_DEVICE(p->desc.device);
-  int rc = ensure_scratch(p, B, max_slots, ch_rowbase.back());
+  int rc = ensure_scratch(p, B, max_slots);
   if (rc != FK_OK) return rc;
   const size_t ni = (size_t)std::max(n_items, 1);
   const size_t nb = (size_t)std::max(B, 1);
@@ -1092,7 +1066,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_ch1 = L.add(nchb);
   const size_t o_ifc = L.add(sizeof(int32_t) * ni);
   const size_t o_cc0 = L.add(sizeof(int32_t) * std::max<size_t>(cta_chunk0.size(), 1));
-  const size_t o_crb = L.add(sizeof(int32_t) * ch_rowbase.size());
+  const size_t o_pd = L.add(sizeof(PlanDev));  // the plan struct itself (pinned source of the constant upload)
   // rotate slots; wait until the GPU finished with the one we reuse
   if (p->cur >= 0 && p->slots[p->cur].dev) {
     FK_CUDA(cudaEventRecord(p->slots[p->cur].done, st));
@@ -1153,7 +1127,6 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   put(o_ch1, ch_t1.data(), ch_t1.size() * 4);
   put(o_ifc, it_first_chunk.data(), it_first_chunk.size() * 4);
   put(o_cc0, cta_chunk0.data(), cta_chunk0.size() * 4);
-  put(o_crb, ch_rowbase.data(), ch_rowbase.size() * 4);
   FK_CUDA(cudaMemcpyAsync(slot.dev, slot.host, L.size, cudaMemcpyHostToDevice, st));
 
   const char* d = (const char*)slot.dev;
@@ -1177,16 +1150,11 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.tc_units = (int)tc_units;
   pd.tc_ctas = (int)tc_ctas;
   pd.tc_nchunks = (int)tc_nchunks;
-  pd.tc_ticket_base = 0;  // set per launch
   pd.tc_chunk_item = (const int32_t*)(d + o_chi);
   pd.tc_chunk_tile0 = (const int32_t*)(d + o_ch0);
   pd.tc_chunk_tile1 = (const int32_t*)(d + o_ch1);
   pd.it_first_chunk = (const int32_t*)(d + o_ifc);
   pd.tc_cta_chunk0 = (const int32_t*)(d + o_cc0);
-  pd.tc_static_chunks = (int)n_static;
-  pd.fused = 0;
-  pd.tc_chunk_rowbase = (const int32_t*)(d + o_crb);
-  pd.tc_active_ctas = tc_active;
   pd.tc_l2_share = tc_l2_share ? 1 : 0;
   const int32_t* drb = (const int32_t*)(d + o_rows);
   pd.row_priv_off = drb;
@@ -1214,6 +1182,12 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   p->off_app_page = o_app;
   p->off_app_slot = o_app + nb * 4;
   p->off_app_pos = o_apos;
+  p->priv_grid = (int)grid_ctas;
+  // the plan struct into this slot's __constant__ entry of both kernel units
+  memcpy(h + o_pd, &pd, sizeof(PlanDev));
+  const int ps = p->plan_base + p->cur;
+  FK_CUDA(upload_plan_main(ps, (const PlanDev*)(h + o_pd), st));
+  FK_CUDA(upload_plan_tc(ps, (const PlanDev*)(h + o_pd), st));
   p->have_plan = true;
   return FK_OK;
 }
@@ -1233,44 +1207,38 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_parity) {
     a.part_o += p->part_cap * p->desc.head_dim;
     a.part_ml += p->part_cap;
-    a.mctl += 4 + p->mctl_rh + p->mctl_q + p->mctl_left_cap();
+    a.tick += 1;
   }
   p->launch_parity ^= 1;
+  const int ps = p->plan_base + p->cur;  // the plan's __constant__ slot
   const bool has_mma = p->plan.tc_begin > 0;
   const bool has_tc = p->plan.num_items > p->plan.tc_begin;
   // cross-layer PDL: this layer's first kernel may start while the previous
   // layer's merge runs (it writes the other half of the partials and reads
   // q only after griddepcontrol.wait); never behind the mma prefix kernel
   const bool xl = p->pdl >= 2 && !has_mma;
-  // fused merge: the partial writers merge (fk_common.cuh); no K4
-  const bool fused = p->plan_fused_ok && p->fused_merge && p->launch_order == 0 && has_tc && !has_mma &&
-                     p->plan.priv_units > 0;
-  p->plan.fused = fused ? 1 : 0;
-  if (fused) p->plan.fused_epoch = ++p->fused_epoch;
-  a.out = (__nv_bfloat16*)out;
-  a.out_f32 = out_f32;
   if (!p->tmap_ok) return fail(FK_CUDA_ERROR, "tensor map not encoded");
   // K2 (shared prefixes) and K3 (private streams) only write partials, so
-  // their order is free; K4 merges every (row, head) afterwards.
-  // tickets a tcgen05 launch consumes (fk_prefix_tc_kernel): every dynamic
-  // chunk once, plus one failing ticket per CTA
-  if (has_tc) {
-    p->plan.tc_ticket_base = p->ticket_tc_base;
-    p->ticket_tc_base += (unsigned long long)(p->plan.tc_nchunks - p->plan.tc_static_chunks + p->plan.tc_ctas);
-  }
-  auto run_prefix = [&](bool pdl_tc, bool after_private) -> int {
-    if (has_mma) FK_CUDA(launch_prefix_mma(a, p->plan, layer, q, scale_log2, &p->tmap, st));
-    if (has_tc)
-      FK_CUDA(launch_prefix_tc(a, p->plan, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc, after_private,
-                               fused, st));
-    return FK_OK;
+  // their order is free; K4 merges every (row, head) afterwards and resets
+  // this half's ticket counter.  If a launch fails after others went out,
+  // the counter is reset behind them so the half starts clean next time.
+  bool launched = false;
+  auto bail = [&](cudaError_t e, const char* what) -> int {
+    if (launched && !g_launch_rec) cudaMemsetAsync(a.tick, 0, sizeof(unsigned), st);
+    return fail(FK_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
   };
-  // tickets a private launch consumes (fk_private_kernel): nchunks - static + grid warps
-  auto take_tickets = [&]() -> unsigned long long {
-    const unsigned long long base = p->ticket_base;
-    if (p->plan.priv_units > 0)
-      p->ticket_base += (unsigned long long)(p->plan.priv_nchunks - p->plan.priv_static + p->plan.priv_warps);
-    return base;
+#define FK_LAUNCH(expr, what)                          \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return bail(_e, what);      \
+    launched = true;                                   \
+  } while (0)
+  auto run_prefix = [&](bool pdl_tc, bool after_private) -> int {
+    if (has_mma) FK_LAUNCH(launch_prefix_mma(a, p->plan, ps, layer, q, scale_log2, &p->tmap, st), "prefix (mma)");
+    if (has_tc)
+      FK_LAUNCH(launch_prefix_tc(a, p->plan, ps, layer, q, scale_log2, &p->tmap, &p->tmap_run, pdl_tc,
+                                 after_private, st), "prefix (tcgen05)");
+    return FK_OK;
   };
   // Launch order 0: prefix -> private (PDL: private fills the SMs the prefix
   // grid leaves free; its CTAs wait for the prefix grid on exit).  Order 1:
@@ -1280,26 +1248,17 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_order == 0) {
     int rc = run_prefix(xl, false);
     if (rc != FK_OK) return rc;
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, take_tickets(),
-                           (p->pdl && (has_mma || has_tc)) || (xl && !has_tc), st));
+    FK_LAUNCH(launch_private(a, p->plan, ps, layer, q, scale_log2, &p->tmap, p->priv_grid,
+                             (p->pdl && (has_mma || has_tc)) || (xl && !has_tc), st), "private");
   } else {
-    FK_CUDA(launch_private(a, p->plan, layer, q, scale_log2, &p->tmap, take_tickets(), xl, st));
+    FK_LAUNCH(launch_private(a, p->plan, ps, layer, q, scale_log2, &p->tmap, p->priv_grid, xl, st), "private");
     const bool chained = p->pdl && has_tc && !has_mma && p->plan.priv_units > 0;
     int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;
   }
-  if (!fused) FK_CUDA(launch_merge(a, p->plan, out, out_f32, layer, p->pdl != 0, st));
-  return FK_OK;
-}
-
-// debug (not in the C ABI): both halves of the fused-merge control block
-extern "C" int fk_debug_mctl(fk_pool* p, unsigned* out, int64_t n, int64_t* rh_cap) {
-  if (!p || !p->mctl) return FK_INVALID_ARGUMENT;
-  *rh_cap = (int64_t)p->mctl_rh;
-  const int64_t total = 2 * (4 + (int64_t)p->mctl_rh + (int64_t)p->mctl_q + (int64_t)p->mctl_left_cap());
-  FK_ON_DEVICE(p->desc.device);
-  FK_CUDA(cudaDeviceSynchronize());
-  FK_CUDA(cudaMemcpy(out, p->mctl, sizeof(unsigned) * std::min(n, total), cudaMemcpyDeviceToHost));
+  // fixed merge grid (warps loop over (row, head)): 4 CTAs of 8 warps per SM
+  FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, 4 * p->num_sms, p->pdl != 0, st), "merge");
+#undef FK_LAUNCH
   return FK_OK;
 }
 
@@ -1325,63 +1284,70 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   const double t0 = timing ? now_us() : 0.0;
-  // 1. record the launches (same code path: tickets and partial halves advance).
-  // Recording advances the host ticket bases, the partial-half parity and the
-  // fused epoch before anything runs; if the graph is not launched they go
-  // back, so the host bases keep matching the device counters.
-  const unsigned long long tb0 = p->ticket_base, ttb0 = p->ticket_tc_base;
+  // 1. record the launches (same code path; the partial-half parity advances
+  // before anything runs, and goes back if the graph is not launched)
   const int par0 = p->launch_parity;
-  const unsigned ep0 = p->fused_epoch;
   struct Rollback {
     fk_pool* p;
-    unsigned long long tb, ttb;
     int par;
-    unsigned ep;
     bool armed = true;
     ~Rollback() {
-      if (!armed) return;
-      p->ticket_base = tb;
-      p->ticket_tc_base = ttb;
-      p->launch_parity = par;
-      p->fused_epoch = ep;
+      if (armed) p->launch_parity = par;
     }
-  } rollback{p, tb0, ttb0, par0, ep0};
-  std::vector<fk::LaunchRec> recs;
+  } rollback{p, par0};
+  fk::RecBuf& recs = p->rec_buf;
+  recs.n = 0;
   fk::g_launch_rec = &recs;
   const int rc = run();
   fk::g_launch_rec = nullptr;
   if (rc != FK_OK) return rc;
-  if (recs.empty()) {
+  if (recs.n == 0) {
     rollback.armed = false;
     return FK_OK;
   }
-  for (auto& r : recs) r.finalize();
   cudaStream_t st = (cudaStream_t)stream;
-  GraphCache& G = p->graphs[std::make_tuple(layer0, nlayers, st)];
-  bool same = G.exec && G.stream == st && G.shape.size() == recs.size();
-  for (size_t i = 0; same && i < recs.size(); ++i) {
-    const fk::LaunchRec &a = G.shape[i], &b = recs[i];
-    same = a.func == b.func && a.grid.x == b.grid.x && a.grid.y == b.grid.y && a.block.x == b.block.x &&
-           a.smem == b.smem && a.pdl == b.pdl && a.offs == b.offs;
+  // One graph per (layer range, stream, plan slot, starting partial half):
+  // with the plan in __constant__ memory the kernel arguments then repeat
+  // from step to step, and a replay needs no parameter update at all.
+  GraphCache& G = p->graphs[std::make_tuple(layer0, nlayers, st, p->cur * 2 + par0)];
+  bool same = G.exec && G.stream == st && G.shape.size() == recs.n;
+  for (size_t i = 0; same && i < recs.n; ++i) {
+    const fk::LaunchRec &a = G.shape[i], &b = recs.v[i];
+    same = a.func == b.func && a.pdl == b.pdl && a.offs == b.offs;
   }
   const double t1 = timing ? now_us() : 0.0;
+  int updated = 0;
   if (same) {
-    // 2a. known structure: new arguments into the instantiated graph
-    for (size_t i = 0; i < recs.size(); ++i) {
+    // 2a. known structure: refresh only the nodes whose grid or arguments
+    // changed (a grid may change in place; the function and PDL edges not)
+    for (size_t i = 0; i < recs.n; ++i) {
+      fk::LaunchRec& r = recs.v[i];
+      fk::LaunchRec& c = G.shape[i];
+      if (c.grid.x == r.grid.x && c.grid.y == r.grid.y && c.block.x == r.block.x && c.smem == r.smem &&
+          c.bytes == r.bytes)
+        continue;
+      r.finalize();
       cudaKernelNodeParams kp = {};
-      kp.func = const_cast<void*>(recs[i].func);
-      kp.gridDim = recs[i].grid;
-      kp.blockDim = recs[i].block;
-      kp.sharedMemBytes = (unsigned)recs[i].smem;
-      kp.kernelParams = recs[i].args.data();
+      kp.func = const_cast<void*>(r.func);
+      kp.gridDim = r.grid;
+      kp.blockDim = r.block;
+      kp.sharedMemBytes = (unsigned)r.smem;
+      kp.kernelParams = r.args.data();
       FK_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nodes[i], &kp));
+      c.grid = r.grid;
+      c.block = r.block;
+      c.smem = r.smem;
+      c.bytes = r.bytes;
+      ++updated;
     }
   } else {
     // 2b. new structure: capture the launches (PDL attributes become
     // programmatic edges) and instantiate
     G.reset();
     FK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
-    for (auto& r : recs) {
+    for (size_t k = 0; k < recs.n; ++k) {
+      fk::LaunchRec& r = recs.v[k];
+      r.finalize();
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = r.grid;
       cfg.blockDim = r.block;
@@ -1402,29 +1368,27 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
         cudaStreamEndCapture(st, &g);
         if (g) cudaGraphDestroy(g);
         cudaGetLastError();
+        G.reset();
         return fail(FK_CUDA_ERROR, "graph capture: %s (%zu dependencies)", cudaGetErrorString(e), nd);
       }
       G.nodes.push_back(deps[0]);
     }
-    FK_CUDA(cudaStreamEndCapture(st, &G.graph));
-    FK_CUDA(cudaGraphInstantiate(&G.exec, G.graph, 0));
-    G.stream = st;
-    G.shape.resize(recs.size());
-    for (size_t i = 0; i < recs.size(); ++i) {
-      G.shape[i].func = recs[i].func;
-      G.shape[i].grid = recs[i].grid;
-      G.shape[i].block = recs[i].block;
-      G.shape[i].smem = recs[i].smem;
-      G.shape[i].pdl = recs[i].pdl;
-      G.shape[i].offs = recs[i].offs;
+    cudaError_t e = cudaStreamEndCapture(st, &G.graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&G.exec, G.graph, 0);
+    if (e != cudaSuccess) {
+      G.reset();
+      return fail(FK_CUDA_ERROR, "graph instantiate: %s", cudaGetErrorString(e));
     }
+    G.stream = st;
+    G.shape.assign(recs.v.begin(), recs.v.begin() + recs.n);
+    updated = (int)recs.n;
   }
   const double t2 = timing ? now_us() : 0.0;
   FK_CUDA(cudaGraphLaunch(G.exec, st));
   rollback.armed = false;
   if (timing)
-    fprintf(stderr, "fk graph: %zu launches, record %.1f us, %s %.1f us, launch %.1f us\n", recs.size(), t1 - t0,
-            same ? "update" : "capture", t2 - t1, now_us() - t2);
+    fprintf(stderr, "fk graph: %zu launches, record %.1f us, %s %.1f us (%d nodes), launch %.1f us\n", recs.n,
+            t1 - t0, same ? "update" : "capture", t2 - t1, updated, now_us() - t2);
   return FK_OK;
 }
 
@@ -1512,7 +1476,7 @@ int fk_append_kv_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void*
   if (p->plan.num_rows == 0) return FK_OK;
   if (!k || !v) return fail(FK_INVALID_ARGUMENT, "null k/v");
   FK_ON_DEVICE(p->desc.device);
-  FK_CUDA(launch_append(p->arena(), p->plan, layer0, nlayers, k, v, (cudaStream_t)stream));
+  FK_CUDA(launch_append(p->arena(), p->plan, p->plan_base + p->cur, layer0, nlayers, k, v, (cudaStream_t)stream));
   return FK_OK;
 }
 
@@ -1612,7 +1576,7 @@ int fk_synth_queries(fk_pool* p, uint64_t seed, void* q_all, void* stream) {
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   if (p->plan.num_rows == 0) return FK_OK;
   FK_ON_DEVICE(p->desc.device);
-  FK_CUDA(launch_synth_queries(p->arena(), p->plan, seed, q_all, (cudaStream_t)stream));
+  FK_CUDA(launch_synth_queries(p->arena(), p->plan, p->plan_base + p->cur, seed, q_all, (cudaStream_t)stream));
   return FK_OK;
 }
 
@@ -1622,7 +1586,7 @@ int fk_synth_append(fk_pool* p, uint64_t seed, float k_scale, void* stream) {
   if (!p->committed) return fail(FK_INVALID_ARGUMENT, "fk_step_commit not called for this plan");
   if (p->plan.num_rows == 0) return FK_OK;
   FK_ON_DEVICE(p->desc.device);
-  FK_CUDA(launch_synth_append(p->arena(), p->plan, seed, k_scale, (cudaStream_t)stream));
+  FK_CUDA(launch_synth_append(p->arena(), p->plan, p->plan_base + p->cur, seed, k_scale, (cudaStream_t)stream));
   return FK_OK;
 }
 

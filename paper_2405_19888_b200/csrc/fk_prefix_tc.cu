@@ -85,12 +85,13 @@ __device__ __forceinline__ int tc_read_queue(uint64_t* cq_full, const int* cq, i
   return ((volatile const int*)cq)[i % kTcChunkQ];
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a, PlanDev p, int layer,
+__global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a, int ps, int layer,
                                                                      const __nv_bfloat16* __restrict__ q,
                                                                      float scale_log2,
                                                                      const __grid_constant__ CUtensorMap tmap,
                                                                      const __grid_constant__ CUtensorMap tmap_run,
-                                                                     int after_private, int trig_late) {
+                                                                     int after_private) {
+  const PlanDev& p = fk_plan_c[ps];
   // all shared state is dynamic (no static smem), so the buffer starts at
   // the 1 KiB-aligned base SWIZZLE_128B needs
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -111,21 +112,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.num_heads;
-  const int nch = p.tc_nchunks;
-  // The private grid may start on the SMs we leave free: at once, or (fused
-  // merge, trig_late) once every thread has waited for the previous launch --
-  // the private grid then starts only after the previous layer completed, and
-  // every CTA of this grid is resident before any private warp can wait on
-  // its reports.
-  if (!trig_late) pdl_launch_dependents();
-  bool dep_done = !trig_late;
-  auto dep = [&]() {
-    if (!dep_done) {
-      pdl_wait_primary();
-      pdl_launch_dependents();
-      dep_done = true;
-    }
-  };
+  // the private grid may start at once on the SMs this grid leaves free
+  pdl_launch_dependents();
   // Launched behind the private grid (launch order 1), this grid's completion
   // must imply that grid's: thread 0 waits for it on exit.
   if ((int)blockIdx.x >= p.tc_ctas || p.tc_cta_chunk0[blockIdx.x] == p.tc_cta_chunk0[blockIdx.x + 1]) {
@@ -167,9 +155,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    // Chunks: the CTA's static range first, then tickets (chunk =
-    // tc_static_chunks + ticket); lane 0 posts each chunk id in the queue
-    // one chunk ahead of streaming it.  Page ids are prefetched lane-parallel
+    // Chunks: the CTA's range of the plan's chunk list; lane 0 posts each
+    // chunk id in the queue one chunk ahead of streaming it.  Page ids are prefetched lane-parallel
     // into a 2 x 32-entry register window; the next chunk's item metadata and
     // first window are fetched over the following two tiles, so a chunk
     // switch never waits on a dependent global load.  Lane 0 issues the TMA.
@@ -177,19 +164,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       prefetch_tmap(&tmap);
       prefetch_tmap(&tmap_run);
     }
-    // static chunks first, then tickets (a CTA stops after its first failing one)
     int sidx = p.tc_cta_chunk0[blockIdx.x];
     const int send = p.tc_cta_chunk0[blockIdx.x + 1];
-    auto grab = [&]() -> int {
-      if (sidx < send) return sidx++;
-      dep();  // tickets of the previous launch are all taken once it completed
-      int c = 0;
-      if (lane == 0) {
-        c = p.tc_static_chunks + (int)(atomicAdd(a.ticket_tc, 1ull) - p.tc_ticket_base);
-        if (c >= nch) c = -1;
-      }
-      return __shfl_sync(0xffffffffu, c, 0);
-    };
+    auto grab = [&]() -> int { return sidx < send ? sidx++ : -1; };
     auto post = [&](int i, int chunk) {
       if (lane == 0) {
         ((volatile int*)cq)[i % kTcChunkQ] = chunk;
@@ -209,8 +186,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     int n_item = 0, n_tile0 = 0, n_tile1 = 0, n_head = 0, n_npi = 0, n_poff = 0, n_win = 0, n_nwin = 0;
     int n_stage = 0;  // 0 nothing, 1 metadata, 2 metadata + first window of chunk `nxt`
     for (int t = 0;; ++t) {
-      // a full ring: loads past it need the MMA, which needs the previous launch
-      if (t == (kTcKStages < kTcVStages ? kTcKStages : kTcVStages)) dep();
       if (c.tile == c.tile1) {  // current chunk done: switch to `nxt`
         if (nxt < 0) break;
         if (n_stage < 1) {
@@ -302,9 +277,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
       __syncwarp();
       ++c.tile;
     }
-    dep();
   } else if (warp == 1) {
-    dep();
     // ------------------------------------------------------------ MMA issuer
     // Two in-order streams polled by one thread: S(t) = Q.K^T as soon as K(t)
     // lands (and, at a chunk start, its Q is staged), PV(t) as soon as P(t)
@@ -430,7 +403,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     // under cross-layer PDL the previous layer's merge may still be running:
     // q and the partials are touched only after it has completed
     if (!after_private) pdl_wait_primary();
-    dep();
     TcCursor c;
     c.qi = 0;
     tc_load_chunk(p, c, tc_read_queue(cq_full, cq, 0));
@@ -619,14 +591,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
             if (half == 1 && lead) s_l[my_row] = lr;
             asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
             if (warp == 4 && lane == 0) TL(242 + min(c.qi, 3) * 4);
-            if (half == 0 && lead && real) {
-              a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
-              // fused merge: a dynamic chunk's rows are counted here (both
-              // halves' stores precede this release: bar.sync); the static
-              // chunks' rows at the end of the CTA, in one batch
-              if (p.fused && chunk >= p.tc_static_chunks)
-                fused_arrive_tc_row(a, p, r * H + head, p.tc_chunk_rowbase[chunk] + my_q);
-            }
+            if (half == 0 && lead && real) a.part_ml[pi] = make_float2(m, lr + s_l[my_row]);
           };
           if (r16) epilogue(BoolC<true>{});
           else epilogue(BoolC<false>{});
@@ -648,43 +613,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm) : "memory");
-  }
-  if (p.fused) {
-    // rows this CTA completed after their owners had left (fk_common.cuh):
-    // its static chunks' slots, and (last CTA out) the dynamic chunks'
-    const int b = blockIdx.x;
-    const int c0 = p.tc_cta_chunk0[b], c1 = p.tc_cta_chunk0[b + 1];
-    const int s0 = p.tc_chunk_rowbase[c0], s1 = p.tc_chunk_rowbase[c1];
-    // count the static chunks' rows (their partials were stored before the
-    // __syncthreads above; the fence releases them), one row per thread
-    fence_acq_rel();
-    for (int sl = s0 + (int)threadIdx.x; sl < s1; sl += kTcThreads) {
-      int ck = c0;
-      while (p.tc_chunk_rowbase[ck + 1] <= sl) ++ck;
-      const int it = p.tc_chunk_item[ck];
-      const int rh = p.qrows[p.it_q_off[it] + (sl - p.tc_chunk_rowbase[ck])] * H + p.it_head[it];
-      if (atomicAdd(mctl_cnt(a) + rh, 1u) + 1u == (unsigned)p.row_head_count[rh]) {
-        fence_sc();
-        if (*(volatile unsigned*)(mctl_left(a) + rh % p.priv_warps) == p.fused_epoch)
-          mctl_orphans(a)[sl] = (unsigned)rh + 1u;
-      }
-    }
-    __syncthreads();
-    fused_merge_orphans(a, p, s0, s1, warp, kTcThreads / 32, lane);
-    __syncthreads();  // every warp has read the slots; this CTA's marks precede thread 0's release
-    for (int i = s0 + (int)threadIdx.x; i < s1; i += kTcThreads) mctl_orphans(a)[i] = 0u;
-    if (p.tc_nchunks > p.tc_static_chunks) {
-      if (threadIdx.x == 0)
-        ms.cq[0] = atom_add_acq_rel(a.mctl + 2, 1u) + 1u == (unsigned)p.tc_active_ctas;
-      __syncthreads();
-      if (ms.cq[0]) {
-        const int d0 = p.tc_chunk_rowbase[p.tc_static_chunks], d1 = p.tc_chunk_rowbase[p.tc_nchunks];
-        fused_merge_orphans(a, p, d0, d1, warp, kTcThreads / 32, lane);
-        __syncthreads();
-        for (int i = d0 + (int)threadIdx.x; i < d1; i += kTcThreads) mctl_orphans(a)[i] = 0u;
-        if (threadIdx.x == 0) a.mctl[2] = 0u;
-      }
-    }
   }
   if (after_private && threadIdx.x == 0) pdl_wait_primary();
 }
@@ -711,9 +639,14 @@ extern "C" int fk_debug_timeline(unsigned long long* out, int n) {
 #endif
 }
 
-cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, const void* q, float scale_log2,
+cudaError_t upload_plan_tc(int ps, const PlanDev* host_pinned, cudaStream_t s) {
+  return cudaMemcpyToSymbolAsync(fk_plan_c, host_pinned, sizeof(PlanDev), (size_t)ps * sizeof(PlanDev),
+                                 cudaMemcpyHostToDevice, s);
+}
+
+cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q, float scale_log2,
                              const CUtensorMap* tmap, const CUtensorMap* tmap_run, bool pdl, bool after_private,
-                             bool trig_late, cudaStream_t s) {
+                             cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   if (!attr_set_on_device(attr_devices)) {
     cudaError_t e = cudaFuncSetAttribute(fk_prefix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
@@ -729,20 +662,8 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int layer, con
     }
   }
   if (p.tc_ctas == 0) return cudaSuccess;
-  cudaError_t e = launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, p, layer,
-                           (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run, after_private ? 1 : 0,
-                           trig_late ? 1 : 0);
-  if (e != cudaSuccess) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, fk_prefix_tc_kernel);
-    int optin = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    fprintf(stderr, "fk_prefix_tc launch: %s (static smem %zu, dyn %d, max dyn attr %d, optin %d, regs %d, threads %d)\n",
-            cudaGetErrorString(e), fa.sharedSizeBytes, kTcSmem, fa.maxDynamicSharedSizeBytes, optin, fa.numRegs,
-            fa.maxThreadsPerBlock);
-  }
-  return e;
+  return launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, ps, layer,
+                  (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run, after_private ? 1 : 0);
 }
 
 }  // namespace fk

@@ -32,8 +32,40 @@ for ref in (os.environ.get("FK_REFERENCE", "/root/reference/pkg/src"), os.path.j
         break
 
 
+def direct(args):
+    """One engine built exactly as bench.py builds it (headline shape by
+    default), stepped in a loop: per-step host time minus the plan's GPU
+    waits, and the per-phase split."""
+    import torch
+
+    import bench
+
+    cfg = bench.CONFIGS[args.config]
+    eng, rows = bench.build_engine(cfg, 0, torch, out_len=args.steps + 16)
+    for _ in range(5):
+        eng.step()
+    torch.cuda.synchronize()
+    us = []
+    for _ in range(args.steps):
+        w0 = eng.pool_stats().host_wait_ns
+        t0 = time.perf_counter()
+        eng.step()
+        t1 = time.perf_counter()
+        us.append((t1 - t0) * 1e6 - (eng.pool_stats().host_wait_ns - w0) / 1e3)
+    torch.cuda.synchronize()
+    out = {"mode": "direct", "config": args.config, "rows": rows, "steps": args.steps,
+           "step_host_us_median": statistics.median(us), "step_host_us_mean": statistics.mean(us)}
+    ph = eng.__dict__.get("phase_us")
+    if ph:
+        out["phase_us"] = {k: ph[k] / ph["n"] for k in ("plan", "attention", "grow_append")}
+    print(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--direct", action="store_true", help="one bench.py engine, no manager")
+    ap.add_argument("--config", default="llama13b_p6000_b64")
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--engines", type=int, default=8)
     ap.add_argument("--users", type=int, default=64)
     ap.add_argument("--output-len", type=int, default=64)
@@ -42,6 +74,8 @@ def main():
     ap.add_argument("--py-hash", action="store_true",
                     help="keep the reference's pure-Python FNV (default: rebind it to the C one, INTEGRATION.md §3)")
     args = ap.parse_args()
+    if args.direct:
+        return direct(args)
 
     import torch
 

@@ -145,8 +145,7 @@ def test_large_fanout_multiple_query_blocks(cuda_device):
 def test_many_splits(cuda_device):
     eng = make_engine(cuda_device, H=2)
     eng.set_option(_lib.FK_OPT_MIN_SPLIT_PAGES, 1)  # mma path: one split per page
-    eng.set_option(_lib.FK_OPT_TC_MIN_CHUNK, 1)     # tcgen05 path: one-tile chunks
-    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4096)
+    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4096)  # tcgen05 path: one-tile ranges
     fork_group(eng, 1000, [20, 21], out_len=2)
     run_steps(eng, 2)
     assert eng.last_plan.max_slots > 5
@@ -428,25 +427,24 @@ def test_merge_many_partials(cuda_device, suffix):
     check_history(eng)
 
 
-@pytest.mark.parametrize("min_chunk", [1, 3])
-def test_prefix_chunk_queue_wraps(cuda_device, min_chunk):
-    """Few tcgen05 CTAs, small chunks: each CTA streams 20+ chunks, so the
+@pytest.mark.parametrize("ctas", [1, 3])
+def test_prefix_chunk_queue_wraps(cuda_device, ctas):
+    """Few tcgen05 CTAs over many items: each CTA streams 20+ chunks, so the
     producer's chunk queue (16 entries) wraps several times, chunks of
-    several heads and both query-block layouts interleave per CTA."""
-    eng = make_engine(cuda_device, H=6, L=1)
-    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, 4)
-    eng.set_option(_lib.FK_OPT_TC_DYN_PCT, 60)  # most tiles through the dynamic tail
-    eng.set_option(_lib.FK_OPT_TC_MIN_CHUNK, min_chunk)
-    fork_group(eng, 2300, [9] * 70, out_len=2, tag="a", seed=1)   # 70 rows: 32-lane layout
-    fork_group(eng, 1100, [4] * 20, out_len=2, tag="b", seed=2)   # 20 rows: 16-lane layout
+    several heads and both query-block layouts (32- and 16-lane) interleave."""
+    eng = make_engine(cuda_device, H=16, L=1)
+    eng.set_option(_lib.FK_OPT_PREFIX_TARGET_CTAS, ctas)
+    fork_group(eng, 700, [9] * 70, out_len=2, tag="a", seed=1)   # 70 rows: 32-lane layout
+    fork_group(eng, 300, [4] * 20, out_len=2, tag="b", seed=2)   # 20 rows: 16-lane layout
+    fork_group(eng, 140, [4] * 3, out_len=2, tag="c", seed=3)
     run_steps(eng, 2)
     check_history(eng)
 
 
-@pytest.mark.parametrize("warps", [6, 7, 8, 9, 11, 12, 14])
+@pytest.mark.parametrize("warps", [8, 12])
 def test_private_ring_shapes(cuda_device, warps):
-    """FK_OPT_PRIV_WARPS: every private CTA shape besides the default 10 x 2
-    (6/7 warps x 4 stages, 8/9 x 3, 11/12/14 x 2) gives the same attention."""
+    """FK_OPT_PRIV_WARPS: the private CTA shapes besides the default 10 x 2
+    (8 warps x 3 stages, 12 x 2) give the same attention."""
     eng = make_engine(cuda_device, H=4, L=2)
     eng.set_option(_lib.FK_OPT_PRIV_WARPS, warps)
     fork_group(eng, 400, [33, 100, 7, 260], out_len=3)
@@ -454,13 +452,12 @@ def test_private_ring_shapes(cuda_device, warps):
     check_history(eng)
 
 
-@pytest.mark.parametrize("dyn", [0, 100])
-def test_prefix_static_and_dynamic_schedules(cuda_device, dyn):
-    """FK_OPT_TC_DYN_PCT 0: only cost-balanced static ranges; 100: every
-    tcgen05 tile through ticketed 4-tile chunks (no static range beyond the
-    first chunk per CTA)."""
+@pytest.mark.parametrize("cost", [0, 8])
+def test_prefix_boundary_cost(cuda_device, cost):
+    """FK_OPT_TC_BOUNDARY_COST 0 / 8: the cost-balanced static ranges cut
+    items at different points (more or fewer pieces per head)."""
     eng = make_engine(cuda_device, H=8, L=2)
-    eng.set_option(_lib.FK_OPT_TC_DYN_PCT, dyn)
+    eng.set_option(_lib.FK_OPT_TC_BOUNDARY_COST, cost)
     fork_group(eng, 3000, [40] * 50, out_len=2, tag="a", seed=4)
     fork_group(eng, 900, [5, 77, 130], out_len=2, tag="b", seed=5)
     run_steps(eng, 2)
@@ -568,52 +565,6 @@ def test_full_size_fork_permutation(cuda_device):
     b = run(list(reversed(range(n))))
     d = (a - b).abs()
     assert d.max().item() <= 1e-2 and (d.norm() / a.norm()).item() <= 4e-3, (d.max().item(),)
-
-
-FUSED_SHAPES = {
-    # prefix rows finish last (long prefix, short private streams)
-    "prefix_last": dict(P=3000, lens=[5, 17, 33, 1] * 4, H=8, L=3),
-    # private rows finish last (short prefix, long private streams)
-    "private_last": dict(P=160, lens=[700, 300, 64, 900, 20], H=8, L=3),
-    # 129 forks: two query blocks per head, 32-lane epilogue
-    "two_qblocks": dict(P=520, lens=[3, 40, 130] * 43, H=4, L=2),
-    # most prefix tiles in one-tile dynamic chunks: the last tcgen05 CTA out
-    # merges the orphans of the dynamic chunks
-    "dynamic_chunks": dict(P=2600, lens=[9, 2, 30, 1] * 3, H=4, L=2,
-                           opts=dict(TC_DYN_PCT=60, TC_MIN_CHUNK=1, PREFIX_TARGET_CTAS=6)),
-}
-
-
-@pytest.mark.parametrize("shape", sorted(FUSED_SHAPES))
-@pytest.mark.parametrize("pdl,graph", [(2, 1), (1, 0), (0, 1)])
-def test_fused_merge_matches_merge_kernel(cuda_device, shape, pdl, graph):
-    """FK_OPT_FUSED_MERGE=1: the last partial's writer merges (private warps at
-    once, prefix-completed rows by their owning private warp or the tcgen05
-    CTA) -- the same LSE merge over the same partials as the merge kernel,
-    so the outputs are bit-identical; both agree with the oracle."""
-    if PATH["path"] != "tc":
-        pytest.skip("the fused merge runs with tcgen05 prefix items")
-    s = FUSED_SHAPES[shape]
-    outs = []
-    for fused in (1, 0):
-        eng = make_engine(cuda_device, H=s["H"], L=s["L"])
-        eng.set_option(_lib.FK_OPT_FUSED_MERGE, fused)
-        eng.set_option(_lib.FK_OPT_PDL, pdl)
-        eng.set_option(_lib.FK_OPT_GRAPH, graph)
-        for k, v in s.get("opts", {}).items():
-            eng.set_option(getattr(_lib, "FK_OPT_" + k), v)
-        fork_group(eng, s["P"], s["lens"], out_len=4, seed=11)
-        run_steps(eng, 4)
-        assert eng.last_plan.fused_merge == fused
-        if fused:
-            check_history(eng)
-        outs.append([(r["output"], r["output_f32"]) for r in eng.history])
-    import torch
-
-    assert len(outs[0]) == len(outs[1]) == 4
-    for (a16, a32), (b16, b32) in zip(*outs):
-        assert torch.equal(a16.view(torch.int16), b16.view(torch.int16))
-        assert torch.equal(a32, b32)
 
 
 @pytest.mark.parametrize("shape", ["ragged", "nested", "shared_leaf", "oom"])

@@ -78,25 +78,3 @@ def test_nested_plan_counts_every_level_once():
     running = list(eng.gens.values())
     assert eng._plan(running) == 4096 + 8 * 1024 + 64 * 256
     assert eng.last_plan.num_shared_ctx == 9
-
-
-def test_fused_merge_admission():
-    """FK_OPT_FUSED_MERGE=1: the plan reports the fused merge for a fork group
-    (tcgen05 prefix + private streams); launch order 1, the mma.sync prefix
-    path and a plan without private streams keep the merge kernel."""
-    from paper_2405_19888_b200 import _lib
-    from paper_2405_19888_b200.workloads import fork_group
-
-    def plan(suffix, **opts):
-        eng = P.GpuEngine("e0", P.CostModel(), kv_tokens=1 << 22, geometry=P.LLAMA_13B)
-        for k, v in opts.items():
-            eng.set_option(getattr(_lib, "FK_OPT_" + k), v)
-        fork_group(eng, 2000, [suffix] * 8, out_len=2)
-        eng._plan(list(eng.gens.values()))
-        return eng.last_plan
-
-    assert plan(100).fused_merge == 0  # default: the merge kernel
-    assert plan(100, FUSED_MERGE=1).fused_merge == 1
-    assert plan(100, FUSED_MERGE=1, LAUNCH_ORDER=1).fused_merge == 0
-    assert plan(100, FUSED_MERGE=1, TC_MIN_FANOUT=0).fused_merge == 0  # mma.sync prefix items
-    assert plan(0, FUSED_MERGE=1).fused_merge == 0  # no private warps to own the rows
