@@ -146,6 +146,9 @@ int fk_ctx_grow(fk_pool* pool, int64_t ctx, int64_t new_token_count,
 int fk_ctx_release(fk_pool* pool, int64_t ctx);
 int fk_ctx_info(const fk_pool* pool, int64_t ctx, int64_t* token_count,
                 int64_t* num_blocks, int64_t* parent);
+/* Token count of ctx (Context.token_count, engine.py:53-63), or -1 if unknown:
+ * the pool is authoritative, the Python mirror reads it on demand. */
+int64_t fk_ctx_tokens(const fk_pool* pool, int64_t ctx);
 /* Parity readback: logical ids and the physical pages backing them. */
 int fk_ctx_blocks(const fk_pool* pool, int64_t ctx, int64_t* logical,
                   int32_t* physical, int64_t cap, int64_t* n);
@@ -176,8 +179,9 @@ int fk_attn_decode_layers(fk_pool* pool, int32_t layer0, int32_t nlayers, const 
  * sequential OOM rule of engine.py:431-438: positions[r] = token index of
  * row r's new token, or -1 if its grow failed (OutOfMemory: that request
  * fails, the others continue); new_ids[r] = the logical block id the grow
- * allocated, or -1.  Host-only pools use it too (no device work). */
-int fk_step_grow(fk_pool* pool, int64_t* positions, int64_t* new_ids);
+ * allocated, or -1; *n_failed = rows whose grow failed.  Host-only pools use
+ * it too (no device work). */
+int fk_step_grow(fk_pool* pool, int64_t* positions, int64_t* new_ids, int32_t* n_failed /* nullable */);
 /* After the Python mirror grew each leaf by one token (engine.py:431-438):
  * positions[r] = slot index (token count before the grow) of row r's new
  * token, or -1 when that grow failed (OOM).  Uploads append targets. */

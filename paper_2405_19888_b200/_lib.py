@@ -97,12 +97,13 @@ SIGNATURES = [
     ("fk_ctx_grow", c_int32, [c_void_p, c_int64, c_int64, POINTER(c_int64), c_int64, POINTER(c_int64)]),
     ("fk_ctx_release", c_int32, [c_void_p, c_int64]),
     ("fk_ctx_info", c_int32, [c_void_p, c_int64, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
+    ("fk_ctx_tokens", c_int64, [c_void_p, c_int64]),
     ("fk_ctx_blocks", c_int32, [c_void_p, c_int64, POINTER(c_int64), POINTER(c_int32), c_int64, POINTER(c_int64)]),
     ("fk_step_plan", c_int32, [c_void_p, POINTER(c_int64), c_int32, c_int32, c_void_p, POINTER(PlanInfo)]),
     ("fk_attn_decode", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("fk_attn_decode_layers", c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                         c_int64, c_void_p]),
-    ("fk_step_grow", c_int32, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),
+    ("fk_step_grow", c_int32, [c_void_p, POINTER(c_int64), POINTER(c_int64), POINTER(c_int32)]),
     ("fk_step_commit", c_int32, [c_void_p, POINTER(c_int64), c_void_p]),
     ("fk_append_kv", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("fk_append_kv_layers", c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),

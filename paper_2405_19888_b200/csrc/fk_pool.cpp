@@ -141,6 +141,7 @@ struct fk_pool {
   int64_t use_graph = 1;  // fk_attn_decode_layers replays a CUDA graph
   std::map<std::tuple<int32_t, int32_t, cudaStream_t, int>, GraphCache> graphs;  // (layer0, nlayers, stream, slot/half)
   fk::RecBuf rec_buf;  // launches recorded by fk_attn_decode_layers (storage reused)
+  std::vector<int32_t> scratch_chunks;  // planner scratch (capacity reused across steps)
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
   int64_t prefix_rate_pct = 50;  // prefix KV bytes/s per SM relative to the private stream's (measured optimum, headline)
@@ -540,6 +541,12 @@ int fk_ctx_info(const fk_pool* p, int64_t ctx, int64_t* tokens, int64_t* nblocks
   if (nblocks) *nblocks = (int64_t)it->second.logical.size();
   if (parent) *parent = it->second.parent;
   return FK_OK;
+}
+
+int64_t fk_ctx_tokens(const fk_pool* p, int64_t ctx) {
+  if (!p) return -1;
+  auto it = p->ctxs.find(ctx);
+  return it == p->ctxs.end() ? -1 : it->second.tokens;
 }
 
 int fk_ctx_blocks(const fk_pool* p, int64_t ctx, int64_t* logical, int32_t* physical, int64_t cap,
@@ -948,13 +955,24 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int64_t priv_sms = corun ? std::max<int64_t>(1, p->num_sms - tc_ctas) : p->num_sms;
   const int64_t wpc = p->priv_wpc;
   const int64_t w_active = priv_sms * wpc;
-  std::vector<int32_t> chunk_start;
-  for (int64_t pos = 0; pos < U;) {
-    int64_t sz = (U - pos + 2 * w_active - 1) / (2 * w_active);
-    sz = std::min<int64_t>(std::max<int64_t>(sz, p->priv_min_chunk), kPrivMaxChunk);
-    sz = std::min<int64_t>(sz, U - pos);
-    chunk_start.push_back((int32_t)pos);
-    pos += sz;
+  // size(pos) = clamp(ceil((U - pos) / 2W), min_chunk, 32), generated run by
+  // run: one division per distinct size, then plain adds (this runs every step)
+  std::vector<int32_t>& chunk_start = p->scratch_chunks;
+  chunk_start.clear();
+  {
+    const int64_t w2 = 2 * w_active, mc = p->priv_min_chunk;
+    int64_t pos = 0;
+    while (pos < U) {
+      const int64_t R = U - pos;
+      int64_t sz = std::min<int64_t>(std::max<int64_t>((R + w2 - 1) / w2, mc), kPrivMaxChunk);
+      // the size holds while ceil(R / 2W) stays >= sz (capped) or == sz
+      const int64_t floor_r = sz > mc ? (sz - 1) * w2 : 0;  // R must stay above this
+      int64_t k = sz > mc ? (R - floor_r + sz - 1) / sz : (R + sz - 1) / sz;
+      for (; k > 0 && pos < U; --k) {
+        chunk_start.push_back((int32_t)pos);
+        pos += std::min<int64_t>(sz, U - pos);
+      }
+    }
   }
   const int64_t nchunks = (int64_t)chunk_start.size();
   chunk_start.push_back((int32_t)U);
@@ -1392,17 +1410,20 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   return FK_OK;
 }
 
-int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids) {
+int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids, int32_t* n_failed) {
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   const int B = (int)p->plan_leaves.size();
   if (B > 0 && (!positions || !new_ids)) return fail(FK_INVALID_ARGUMENT, "null output");
+  int32_t nf = 0;
   if (p->plan_grew) {  // FK_OPT_APPEND_FIRST: the plan did this step's growth
     for (int r = 0; r < B; ++r) {
       positions[r] = p->grow_pos[r];
       new_ids[r] = p->grow_ids[r];
+      nf += positions[r] < 0;
     }
     p->plan_grew = false;
+    if (n_failed) *n_failed = nf;
     return FK_OK;
   }
   for (int r = 0; r < B; ++r) {  // gens order, one token each (engine.py:431-443)
@@ -1414,12 +1435,14 @@ int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids) {
     if (rc == FK_OUT_OF_MEMORY) {
       positions[r] = -1;
       new_ids[r] = -1;
+      ++nf;
       continue;
     }
     if (rc != FK_OK) return rc;
     positions[r] = pos;
     if (n == 0) new_ids[r] = -1;
   }
+  if (n_failed) *n_failed = nf;
   return FK_OK;
 }
 

@@ -79,20 +79,45 @@ class CostModel:
         return self.iteration_ns(capacity) / MS
 
 
-@dataclass
 class Context:
-    """Forest node (engine.py:53-63) plus the pool uid that keys it in C++."""
+    """Forest node (engine.py:53-63) plus the pool uid that keys it in C++.
 
-    context_id: str
-    engine_id: str
-    parent_id: Optional[str]
-    token_count: int = 0
-    block_ids: List[int] = field(default_factory=list)
-    refcount: int = 0
-    dropped: bool = False
-    chain_hashes: List[int] = field(default_factory=list)
-    registered_hashes: List[int] = field(default_factory=list)
-    uid: int = -1
+    The C++ pool is authoritative for the block accounting: token_count and
+    block_ids are read from it on demand (a decode step then touches no
+    Python object per row); refcount, dropped and the hashes live here."""
+
+    __slots__ = ("context_id", "engine_id", "parent_id", "refcount", "dropped", "chain_hashes",
+                 "registered_hashes", "uid", "_pool", "_released")
+
+    def __init__(self, context_id: str, engine_id: str, parent_id: Optional[str], refcount: int = 0,
+                 dropped: bool = False, chain_hashes: Optional[List[int]] = None,
+                 registered_hashes: Optional[List[int]] = None, uid: int = -1, pool: Any = None):
+        self.context_id = context_id
+        self.engine_id = engine_id
+        self.parent_id = parent_id
+        self.refcount = refcount
+        self.dropped = dropped
+        self.chain_hashes = [] if chain_hashes is None else chain_hashes
+        self.registered_hashes = [] if registered_hashes is None else registered_hashes
+        self.uid = uid
+        self._pool = pool
+        self._released = False
+
+    @property
+    def token_count(self) -> int:
+        if self._released or self._pool is None:
+            return 0
+        return int(_lib.lib.fk_ctx_tokens(self._pool.handle, self.uid))
+
+    @property
+    def block_ids(self) -> List[int]:
+        if self._released or self._pool is None:
+            return []
+        return self._pool.blocks(self.uid)[0]
+
+    def __repr__(self) -> str:
+        return (f"Context({self.context_id!r}, parent={self.parent_id!r}, tokens={self.token_count}, "
+                f"refcount={self.refcount}, dropped={self.dropped})")
 
 
 @dataclass
@@ -102,19 +127,42 @@ class FillTask:
     token_ids: List[int]
 
 
-@dataclass
 class GenerationTask:
-    request_id: str
-    context_id: str
-    token_ids: List[int]
-    value_text: str
-    emitted: int = 0
-    started: bool = False
-    done: bool = False
+    """engine.py:116-128.  `emitted` is derived from the engine's decode
+    counter: a running generation emits one token per decode iteration until
+    it finishes or fails (engine.py:431-443), so the step updates no
+    per-row Python state -- only the rows that finish or fail."""
+
+    __slots__ = ("request_id", "context_id", "token_ids", "value_text", "started", "done",
+                 "_base", "_clock", "_t0", "_t_end")
+
+    def __init__(self, request_id: str, context_id: str, token_ids: List[int], value_text: str,
+                 emitted: int = 0, started: bool = False, done: bool = False, clock: Optional[List[int]] = None):
+        self.request_id = request_id
+        self.context_id = context_id
+        self.token_ids = token_ids
+        self.value_text = value_text
+        self.started = started
+        self.done = done
+        self._base = emitted
+        self._clock = clock if clock is not None else [0]
+        self._t0 = -1      # decode counter when it first ran (-1: never)
+        self._t_end = -1   # decode counter when it stopped (-1: still running)
+
+    @property
+    def emitted(self) -> int:
+        if self._t0 < 0:
+            return self._base
+        end = self._t_end if self._t_end >= 0 else self._clock[0]
+        return self._base + end - self._t0
 
     @property
     def remaining(self) -> int:
         return len(self.token_ids) - self.emitted
+
+    def __repr__(self) -> str:
+        return (f"GenerationTask({self.request_id!r}, ctx={self.context_id!r}, emitted={self.emitted}/"
+                f"{len(self.token_ids)}, started={self.started}, done={self.done})")
 
 
 @dataclass
@@ -157,15 +205,19 @@ TINY = ModelGeometry(1, 32, 128)
 class GpuKvStore:
     """PagedKvStore (engine.py:66-106) over the C++ pool.
 
-    `owner` stays a live dict (the reference's conservation oracle reads it,
-    tests/oracles.py:543-553); logical ids come from the pool's monotonic
-    counter and are never recycled, physical pages are.
-    """
+    Logical ids come from the pool's monotonic counter and are never
+    recycled, physical pages are.  `owner` (block id -> context id, read by
+    the reference's conservation oracle, tests/oracles.py:543-553) is built
+    from the pool on demand."""
 
-    def __init__(self, pool: "_Pool", block_size: int):
+    def __init__(self, pool: "_Pool", block_size: int, contexts: Dict[str, "Context"]):
         self._pool = pool
         self.block_size = block_size
-        self.owner: Dict[int, str] = {}
+        self._contexts = contexts
+
+    @property
+    def owner(self) -> Dict[int, str]:
+        return {bid: ctx.context_id for ctx in self._contexts.values() for bid in ctx.block_ids}
 
     @property
     def total_blocks(self) -> int:
@@ -191,27 +243,15 @@ class GpuKvStore:
         return -(-tokens // self.block_size)
 
     def grow(self, ctx: Context, new_token_count: int) -> None:
-        need = self.blocks_for(new_token_count) - len(ctx.block_ids)
-        buf = self._pool.id_buffer(max(need, 0))
-        n = ctypes.c_int64(0)
-        status = _lib.lib.fk_ctx_grow(
-            self._pool.handle, ctx.uid, int(new_token_count), buf, max(need, 0), ctypes.byref(n)
-        )
+        status = _lib.lib.fk_ctx_grow(self._pool.handle, ctx.uid, int(new_token_count), None, 0, None)
         if status == _lib.FK_OUT_OF_MEMORY:
+            need = self.blocks_for(new_token_count) - len(ctx.block_ids)
             raise OutOfMemory(f"engine {ctx.engine_id}: need {need} blocks, {self.free_blocks} free")
         _lib.check(status)
-        for i in range(n.value):
-            bid = int(buf[i])
-            self.owner[bid] = ctx.context_id
-            ctx.block_ids.append(bid)
-        ctx.token_count = new_token_count
 
     def release(self, ctx: Context) -> None:
         _lib.check(_lib.lib.fk_ctx_release(self._pool.handle, ctx.uid))
-        for bid in ctx.block_ids:
-            del self.owner[bid]
-        ctx.block_ids = []
-        ctx.token_count = 0
+        ctx._released = True
 
 
 class _Pool:
@@ -239,6 +279,15 @@ class _Pool:
         if n > len(self._ids):
             self._ids = (ctypes.c_int64 * max(n, 2 * len(self._ids)))()
         return self._ids
+
+    def blocks(self, uid: int) -> Tuple[List[int], List[int]]:
+        """(logical ids, physical pages) of a context, read back from C++."""
+        n = ctypes.c_int64(0)
+        _lib.check(_lib.lib.fk_ctx_blocks(self.handle, uid, None, None, 0, ctypes.byref(n)))
+        lg = (ctypes.c_int64 * max(n.value, 1))()
+        ph = (ctypes.c_int32 * max(n.value, 1))()
+        _lib.check(_lib.lib.fk_ctx_blocks(self.handle, uid, lg, ph, n.value, ctypes.byref(n)))
+        return lg[:n.value], ph[:n.value]
 
     def stats(self) -> _lib.PoolStats:
         _lib.check(_lib.lib.fk_pool_stats_get(self.handle, ctypes.byref(self._stats)))
@@ -306,9 +355,9 @@ class GpuEngine:
         self.geometry = geometry
         self.device = device
         self._pool = _Pool(geometry, block_size, -(-kv_tokens // block_size), device, num_pages)
-        self.store = GpuKvStore(self._pool, block_size)
-        self.clock_ns = 0
         self.contexts: Dict[str, Context] = {}
+        self.store = GpuKvStore(self._pool, block_size, self.contexts)
+        self.clock_ns = 0
         self.registry: Dict[int, str] = {}
         self.fill_queue: Deque[FillTask] = deque()
         self.gens: Dict[str, GenerationTask] = {}
@@ -325,6 +374,13 @@ class GpuEngine:
         self.total_emitted = 0
         self._ctx_counter = itertools.count()
         self._uid_counter = itertools.count()
+        # decode iterations so far (GenerationTask.emitted derives from it), the
+        # running rows in gens order (rebuilt only when the set changes) and
+        # the running generations by the counter value they finish at
+        self._dclock = [0]
+        self._running: Optional[List[GenerationTask]] = None
+        self._running_rids: List[str] = []
+        self._finish_at: Dict[int, List[GenerationTask]] = {}
         # device state
         self.model = model if model is not None else SyntheticDecodeModel()
         self.capture_f32 = capture_f32
@@ -332,10 +388,13 @@ class GpuEngine:
         self.history: List[Dict[str, Any]] = []
         self.last_output = None
         self.last_output_f32 = None
-        self.last_rows: List[str] = []
+        self._last_running: List[GenerationTask] = []
         self.last_plan = _lib.PlanInfo()
         self.kv_tokens_streamed = 0  # sum of batch_tokens over decode steps (per layer)
         self._stream = None
+        self._plan_rows: List[GenerationTask] = []  # rows of _leaf_buf
+        self._nfail = ctypes.c_int32(0)
+        self._zero_len: List[GenerationTask] = []
         self._leaf_buf = (ctypes.c_int64 * 64)()
         self._leaf_pos0 = (ctypes.c_int64 * 64)()
         self._pos_buf = (ctypes.c_int64 * 64)()
@@ -350,6 +409,8 @@ class GpuEngine:
                 # fills (prefill KV writes, prefix migrations) run on their own
                 # stream: decode waits only for the fills of contexts it reads
                 self._fill_stream = torch.cuda.Stream(self._dev)
+            self._spv = self._stream.cuda_stream  # (plain int: ctypes passes it as void*)
+            self._ev_caller = torch.cuda.Event()  # the caller's stream position, per step
             self._fill_pending: Dict[str, Any] = {}  # context id -> event of its last fill
             self._release_event = None  # engine-stream fence of the last page release
             # The engine owns Q's producer side (its own buffers, ordered by
@@ -386,13 +447,7 @@ class GpuEngine:
 
     def context_pages(self, context_id: str) -> Tuple[List[int], List[int]]:
         """(logical ids, physical pages) of a context, read back from C++."""
-        ctx = self.get_context(context_id)
-        n = ctypes.c_int64(0)
-        _lib.check(_lib.lib.fk_ctx_blocks(self._pool.handle, ctx.uid, None, None, 0, ctypes.byref(n)))
-        lg = (ctypes.c_int64 * max(n.value, 1))()
-        ph = (ctypes.c_int32 * max(n.value, 1))()
-        _lib.check(_lib.lib.fk_ctx_blocks(self._pool.handle, ctx.uid, lg, ph, n.value, ctypes.byref(n)))
-        return [int(lg[i]) for i in range(n.value)], [int(ph[i]) for i in range(n.value)]
+        return self._pool.blocks(self.get_context(context_id).uid)
 
     def close(self) -> None:
         if self._stream is not None:
@@ -422,7 +477,7 @@ class GpuEngine:
             inherited = list(parent.chain_hashes)
             parent_uid = parent.uid
         ctx = Context(context_id, self.engine_id, parent_context_id, chain_hashes=inherited,
-                      uid=next(self._uid_counter))
+                      uid=next(self._uid_counter), pool=self._pool)
         _lib.check(_lib.lib.fk_ctx_create(self._pool.handle, ctx.uid, parent_uid))
         self.contexts[context_id] = ctx
         if request_id is not None:
@@ -528,9 +583,12 @@ class GpuEngine:
         ctx = self.get_context(context_id)
         ctx.refcount += 1  # the active generation holds its leaf
         self.request_leaf[request_id] = context_id
-        task = GenerationTask(request_id, context_id, list(token_ids), value_text)
+        task = GenerationTask(request_id, context_id, list(token_ids), value_text, clock=self._dclock)
         task.started = self.pending_fills.get(request_id, 0) == 0
+        if not task.token_ids:
+            self._zero_len.append(task)
         self.gens[request_id] = task
+        self._running = None
         return task
 
     def _discard_context(self, ctx: Context) -> None:
@@ -669,14 +727,20 @@ class GpuEngine:
     def _plan(self, running: List[GenerationTask]) -> int:
         B = len(running)
         if B > len(self._leaf_buf):
+            self._plan_rows = []
             self._leaf_buf = (ctypes.c_int64 * (2 * B))()
             self._leaf_pos0 = (ctypes.c_int64 * (2 * B))()
             self._pos_buf = (ctypes.c_int64 * (2 * B))()
             self._id_buf = (ctypes.c_int64 * (2 * B))()
-        for i, g in enumerate(running):
-            ctx = self.contexts[g.context_id]
-            self._leaf_buf[i] = ctx.uid
-            self._leaf_pos0[i] = ctx.token_count
+        prev = self._plan_rows
+        if prev is not running and (len(prev) != B or any(a is not b for a, b in zip(prev, running))):
+            # the running set changed: new leaf list (a generation keeps its leaf)
+            for i, g in enumerate(running):
+                self._leaf_buf[i] = self.contexts[g.context_id].uid
+            self._plan_rows = running
+        if self.keep_history:  # leaf tokens before the step (the synthetic query key)
+            for i, g in enumerate(running):
+                self._leaf_pos0[i] = self.contexts[g.context_id].token_count
         _lib.check(_lib.lib.fk_step_plan(self._pool.handle, self._leaf_buf, B,
                                          1 if self.cost.shared_kernel else 0, self._sp(),
                                          ctypes.byref(self.last_plan)))
@@ -779,54 +843,66 @@ class GpuEngine:
             st.wait_event(hp["ev_d2h"])  # the step completes with its output on the host
         self.last_output = out
         self.last_output_f32 = None
-        self.last_rows = [g.request_id for g in running]
+        self._last_running = running
 
     def _decode_attention(self, running: List[GenerationTask]) -> None:
         torch = self._torch
+        model = self.model
+        tensor_model = isinstance(model, TensorDecodeModel)
+        if tensor_model and model.q.device.type != "cuda" and not self.capture_f32:
+            self._decode_attention_host(running)
+            return
         geo = self.geometry
         B = len(running)
         shape = (geo.num_layers, B, geo.num_heads, geo.head_dim)
-        model = self.model
-        if isinstance(model, TensorDecodeModel) and model.q.device.type != "cuda" and not self.capture_f32:
-            self._decode_attention_host(running)
-            return
+        st = self._stream
         caller = torch.cuda.current_stream(self._dev)
-        with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
-            if isinstance(model, TensorDecodeModel):
+        # The step's buffers are allocated on the engine stream (so the caching
+        # allocator never hands the engine memory another stream still uses);
+        # caller tensors are read only after the caller's stream reached this
+        # point.  (set_stream instead of the context managers: this is the
+        # per-step host path.)
+        torch.cuda.set_stream(st)
+        try:
+            if tensor_model:
                 q = model.q
                 if q.device.type != "cuda":
                     q = q.to(self._dev, non_blocking=True)
-                elif caller != self._stream:
-                    # the caller's producer of q ran on its own stream; keep q
-                    # alive until the engine stream has read it
-                    self._stream.wait_stream(caller)
-                    q.record_stream(self._stream)
+                elif caller != st:
+                    self._ev_caller.record(caller)
+                    st.wait_event(self._ev_caller)
+                    q.record_stream(st)
             else:
                 q = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
-                _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed,
-                                                     ctypes.c_void_p(q.data_ptr()), self._sp()))
+                _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed, q.data_ptr(), self._spv))
             out = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
             f32 = torch.empty(shape, dtype=torch.float32, device=self._dev) if self.capture_f32 else None
             # every layer's queries are already on the device: one C call
-            # launches the layers' kernels back to back (fk_attn_decode_layers)
-            layer_elems = B * geo.num_heads * geo.head_dim
+            # replays the layers' kernels (fk_attn_decode_layers, a CUDA graph)
+            layer_bytes = B * geo.num_heads * geo.head_dim * 2
             _lib.check(_lib.lib.fk_attn_decode_layers(
-                self._pool.handle, 0, geo.num_layers, ctypes.c_void_p(q.data_ptr()), layer_elems * 2,
-                ctypes.c_void_p(out.data_ptr()), layer_elems * 2,
-                ctypes.c_void_p(f32.data_ptr()) if f32 is not None else None, layer_elems * 4, self._sp()))
+                self._pool.handle, 0, geo.num_layers, q.data_ptr(), layer_bytes, out.data_ptr(), layer_bytes,
+                f32.data_ptr() if f32 is not None else None, layer_bytes * 2, self._spv))
             self.last_output = out
             self.last_output_f32 = f32
-            if isinstance(model, TensorDecodeModel) and model.copy_out:
+            if tensor_model and model.copy_out:
                 if model.host_out is None or tuple(model.host_out.shape) != shape:
                     model.host_out = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
                 model.host_out.copy_(out, non_blocking=True)
-        self.last_rows = [g.request_id for g in running]
+        finally:
+            torch.cuda.set_stream(caller)
+        self._last_running = running
 
-    def _append(self, running: List[GenerationTask], positions: List[int]) -> None:
+    @property
+    def last_rows(self) -> List[str]:
+        """Request ids of the rows of last_output, in row order."""
+        return [g.request_id for g in self._last_running]
+
+    def _append(self, running: List[GenerationTask]) -> None:
+        """The step's new K/V rows into their (page, slot), positions from
+        fk_step_grow (still in _pos_buf)."""
         torch = self._torch
-        for i, pos in enumerate(positions):
-            self._pos_buf[i] = pos
-        _lib.check(_lib.lib.fk_step_commit(self._pool.handle, self._pos_buf, self._sp()))
+        _lib.check(_lib.lib.fk_step_commit(self._pool.handle, self._pos_buf, self._spv))
         model = self.model
         if isinstance(model, TensorDecodeModel) and model.k is not None:
             geo = self.geometry
@@ -885,10 +961,13 @@ class GpuEngine:
         failed: List[Tuple[str, str]] = []
         fill_completed: List[str] = []
 
-        for g in list(self.gens.values()):  # zero-length generations (engine.py:398-402)
-            if g.started and not g.done and not g.token_ids:
-                g.done = True
-                finished.append(g.request_id)
+        if self._zero_len:  # zero-length generations (engine.py:398-402)
+            for g in list(self.gens.values()):
+                if g.started and not g.done and not g.token_ids:
+                    g.done = True
+                    finished.append(g.request_id)
+                    self._running = None
+            self._zero_len = [g for g in self._zero_len if not g.done]
 
         fill_tokens = 0
         if self.fill_queue:  # one fill chunk per step, FIFO (engine.py:404-414)
@@ -900,7 +979,7 @@ class GpuEngine:
                 if left <= 0:
                     fill_completed.append(task.request_id)
 
-        running = [g for g in self.gens.values() if g.started and not g.done]
+        running = self._running_rows()
         if _PHASES:
             tm = [time.perf_counter()]
         batch_tokens = self._plan(running) if running else 0
@@ -909,15 +988,16 @@ class GpuEngine:
         if running and self.device is not None and self._fill_pending:
             self._wait_fills(running)
         snapshot = None
-        positions: List[int] = []
+        emitted: Dict[str, int] = {}
         if self.attend_own_token:
             # real-decoder order: grow (the plan already did, fk_step_plan
             # under FK_OPT_APPEND_FIRST), write the new K/V rows, then attend
             # over spans that include them
-            positions = self._grow_rows(running, emitted, finished, failed) if running else []
+            if running:
+                emitted = self._grow_rows(running, finished, failed)
             snapshot = self._snapshot(running) if (self.keep_history and running) else None
             if running and self.device is not None:
-                self._append(running, positions)
+                self._append(running)
                 self._decode_attention(running)
         else:
             snapshot = self._snapshot(running) if (self.keep_history and running) else None
@@ -940,10 +1020,10 @@ class GpuEngine:
         self.clock_ns += elapsed
         self.busy_ns += elapsed
 
-        if not self.attend_own_token:
-            positions = self._grow_rows(running, emitted, finished, failed) if running else []
-            if running and self.device is not None:
-                self._append(running, positions)
+        if not self.attend_own_token and running:
+            emitted = self._grow_rows(running, finished, failed)
+            if self.device is not None:
+                self._append(running)
 
         if _PHASES:
             tm.append(time.perf_counter())
@@ -954,8 +1034,9 @@ class GpuEngine:
             acc["n"] += 1
         for rid in fill_completed:  # fills done this step decode next step
             g = self.gens.get(rid)
-            if g is not None:
+            if g is not None and not g.started:
                 g.started = True
+                self._running = None
 
         self.total_emitted += len(emitted)
         self.trace.append("t=%s engine=%s fill=%d batch=%d emitted=%d"
@@ -964,37 +1045,62 @@ class GpuEngine:
                             finished, failed, fill_completed)
         self.reports.append(report)
         if snapshot is not None:
+            positions = [int(self._pos_buf[i]) for i in range(len(running))]
             self.history.append(self._history_record(running, snapshot, batch_tokens, positions))
         return report
 
-    def _grow_rows(self, running: List[GenerationTask], emitted: Dict[str, int], finished: List[str],
-                   failed: List[Tuple[str, str]]) -> List[int]:
+    def _running_rows(self) -> List[GenerationTask]:
+        """Started, not done, in gens order (engine.py:416) -- cached until the
+        set changes.  A generation's first decode iteration fixes where it
+        finishes on the decode counter (one token per iteration)."""
+        run = self._running
+        if run is None:
+            run = [g for g in self.gens.values() if g.started and not g.done]
+            t = self._dclock[0]
+            for g in run:
+                if g._t0 < 0:
+                    g._t0 = t
+                    self._finish_at.setdefault(t + len(g.token_ids) - g._base, []).append(g)
+            self._running = run
+            self._running_rids = [g.request_id for g in run]
+        return run
+
+    def _grow_rows(self, running: List[GenerationTask], finished: List[str],
+                   failed: List[Tuple[str, str]]) -> Dict[str, int]:
         """One token per running generation, gens order, sequential OOM rule
-        (engine.py:431-443), in one C call; mirrors the block ids."""
-        _lib.check(_lib.lib.fk_step_grow(self._pool.handle, self._pos_buf, self._id_buf))
-        positions: List[int] = []
-        for i, g in enumerate(running):
-            ctx = self.contexts[g.context_id]
-            pos = int(self._pos_buf[i])
-            if pos < 0:  # OutOfMemory: only this request fails (PagedKvStore.grow message)
-                need = self.store.blocks_for(ctx.token_count + 1) - len(ctx.block_ids)
+        (engine.py:431-443), in one C call; returns StepReport.emitted.  Token
+        counts and block ids live in the pool, emitted counts derive from the
+        decode counter: only failing and finishing rows are touched here."""
+        nf = self._nfail
+        _lib.check(_lib.lib.fk_step_grow(self._pool.handle, self._pos_buf, self._id_buf, ctypes.byref(nf)))
+        t = self._dclock[0]
+        if nf.value:
+            for i, g in enumerate(running):
+                if self._pos_buf[i] < 0:  # OutOfMemory: only this request fails (PagedKvStore.grow message)
+                    ctx = self.contexts[g.context_id]
+                    need = self.store.blocks_for(ctx.token_count + 1) - len(ctx.block_ids)
+                    g.done = True
+                    g._t_end = t
+                    failed.append((g.request_id, f"engine {ctx.engine_id}: need {need} blocks, "
+                                                 f"{self.store.free_blocks} free"))
+            emitted = {g.request_id: 1 for g in running if g._t_end < 0}
+            self._running = None
+        else:
+            emitted = dict.fromkeys(self._running_rids, 1)
+        self._dclock[0] = t + 1
+        fin = self._finish_at.pop(t + 1, None)
+        if fin:
+            live = [g for g in fin if not g.done and self.gens.get(g.request_id) is g]
+            if len(live) > 1:
+                order = {id(g): i for i, g in enumerate(running)}
+                live.sort(key=lambda g: order.get(id(g), len(order)))
+            for g in live:
                 g.done = True
-                failed.append((g.request_id, f"engine {ctx.engine_id}: need {need} blocks, "
-                                             f"{self.store.free_blocks} free"))
-                positions.append(-1)
-                continue
-            bid = int(self._id_buf[i])
-            if bid >= 0:
-                self.store.owner[bid] = ctx.context_id
-                ctx.block_ids.append(bid)
-            ctx.token_count = pos + 1
-            positions.append(pos)
-            g.emitted += 1
-            emitted[g.request_id] = 1
-            if g.remaining == 0:
-                g.done = True
+                g._t_end = t + 1
                 finished.append(g.request_id)
-        return positions
+            if live:
+                self._running = None
+        return emitted
 
     def _history_record(self, running, snapshot, batch_tokens, positions) -> Dict[str, Any]:
         """Snapshot for the parity tests: the outputs are copied to the host on
@@ -1021,10 +1127,18 @@ class GpuEngine:
 
     # -- request lifecycle (engine.py:488-538) -------------------------------------
 
+    def _forget(self, g: GenerationTask) -> None:
+        """A generation leaves gens: freeze its emitted count, drop it from
+        the running rows."""
+        if g._t0 >= 0 and g._t_end < 0:
+            g._t_end = self._dclock[0]
+        self._running = None
+
     def finish_generation(self, request_id: str) -> Optional[int]:
         g = self.gens.pop(request_id, None)
         if g is None:
             return None
+        self._forget(g)
         for d in (self.pending_fills, self.charges, self.holder_class, self.request_leaf):
             d.pop(request_id, None)
         ctx = self.contexts.get(g.context_id)
@@ -1051,6 +1165,7 @@ class GpuEngine:
         g = self.gens.pop(request_id, None)
         if g is None:
             return
+        self._forget(g)
         ctx = self.contexts.get(g.context_id)
         if ctx is not None:
             ctx.refcount -= 1

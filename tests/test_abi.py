@@ -128,15 +128,17 @@ def test_step_grow_sequential_oom_rule():
     assert info.batch_tokens == 16 + 16 + 5 + 16
     pos = (ctypes.c_int64 * 3)()
     new = (ctypes.c_int64 * 3)()
-    assert L.fk_step_grow(h, pos, new) == _lib.FK_OK
+    nf = ctypes.c_int32()
+    assert L.fk_step_grow(h, pos, new, ctypes.byref(nf)) == _lib.FK_OK
     # row 0 (ctx 2) needs a new page -> OOM; row 1 (ctx 3) fits its page; row 2 needs one -> OOM
-    assert list(pos) == [-1, 5, -1]
+    assert list(pos) == [-1, 5, -1] and nf.value == 2
     assert list(new) == [-1, -1, -1]
     tok = ctypes.c_int64()
     nb = ctypes.c_int64()
     par = ctypes.c_int64()
     L.fk_ctx_info(h, 3, ctypes.byref(tok), ctypes.byref(nb), ctypes.byref(par))
     assert (tok.value, nb.value, par.value) == (6, 1, 1)
+    assert L.fk_ctx_tokens(h, 3) == 6 and L.fk_ctx_tokens(h, 99) == -1
     L.fk_pool_destroy(h)
 
 
