@@ -123,13 +123,15 @@ enum {
   FK_OPT_TC_BOUNDARY_COST = 14, /* static split: tiles a piece start mid-range costs a CTA (default 4) */
   /* 10, 13 (tcgen05 dynamic tail) and 15 (fused merge) were removed in round 2:
      measured slower than what they replace; setting them fails */
-  FK_OPT_APPEND_FIRST = 16    /* 1: attend to the step's own token (a real decoder): fk_step_plan does
+  FK_OPT_APPEND_FIRST = 16,   /* 1: attend to the step's own token (a real decoder): fk_step_plan does
                                  the step's one-token growth (row order, sequential OOM rule) and
                                  plans spans that include it; the caller then takes the growth from
                                  fk_step_grow, commits and appends the new K/V rows, and only then
                                  runs fk_attn_decode.  fk_plan_info.batch_tokens stays the
                                  reference's pre-growth count.  0 (default): the reference's span
                                  (chain tokens at step start, engine.py:416-434), append after */
+  FK_OPT_DEBUG_SKIP_MERGE = 90 /* diagnostic only: 1 = do not launch the LSE merge (outputs are NOT
+                                 written); bounds the time the merge adds to a layer */
 };
 
 /* ---- context forest ------------------------------------------------------ */

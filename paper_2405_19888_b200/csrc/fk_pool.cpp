@@ -162,6 +162,7 @@ struct fk_pool {
   size_t part_cap = 0;     // entries (rows*slots*H) per half
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
   int64_t host_wait_ns = 0;  // time fk_step_plan blocked on the GPU (plan slot reuse)
+  int64_t skip_merge = 0;    // FK_OPT_DEBUG_SKIP_MERGE (diagnostic)
   int64_t append_first = 0;  // FK_OPT_APPEND_FIRST: fk_step_plan grows the rows first (attend own token)
   bool plan_grew = false;    // the current plan already did the step's growth (fk_step_grow returns it)
   std::vector<int64_t> grow_pos, grow_ids;
@@ -445,6 +446,7 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_CORUN: p->corun = value; break;
     case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
     case FK_OPT_APPEND_FIRST: p->append_first = value != 0; break;
+    case FK_OPT_DEBUG_SKIP_MERGE: p->skip_merge = value != 0; break;
     default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
   }
   return FK_OK;
@@ -1275,6 +1277,11 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
     if (rc != FK_OK) return rc;
   }
   // fixed merge grid (warps loop over (row, head)): 4 CTAs of 8 warps per SM
+  if (p->skip_merge) {  // diagnostic: no merge (and the ticket half reset by a memset)
+    if (fk::g_launch_rec) return fail(FK_INVALID_ARGUMENT, "FK_OPT_DEBUG_SKIP_MERGE needs FK_OPT_GRAPH=0");
+    FK_CUDA(cudaMemsetAsync(a.tick, 0, sizeof(unsigned), st));
+    return FK_OK;
+  }
   FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, 4 * p->num_sms, p->pdl != 0, st), "merge");
 #undef FK_LAUNCH
   return FK_OK;
