@@ -39,6 +39,7 @@ def main():
         for name, opts in zip(args.set, sets):
             for k, v in opts:
                 eng.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
+            eng.step()  # plan-time options take effect with a new plan
             t, tf = bench.time_layers_isolated(eng, args.reps, torch)
             res[name].append(t * 1e6)
             for k, v in opts:  # back to defaults for the next set
