@@ -191,7 +191,8 @@ def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=409
         eng.model.seed = seed
     else:
         dev = torch.device("cuda", device)
-        eng.model = P.TensorDecodeModel(q.to(dev), k.to(dev), v.to(dev))
+        q = q.to(dev)
+        eng.model = P.TensorDecodeModel(q, k.to(dev), v.to(dev), out=torch.empty_like(q))
         eng.model.seed = seed
     torch.cuda.synchronize(device)
     return eng, rows

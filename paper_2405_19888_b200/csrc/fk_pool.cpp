@@ -1052,6 +1052,14 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     fprintf(stderr, "fk plan us: walk %.0f shared %.0f tc %.0f slots %.0f priv %.0f sched %.0f keys %.0f\n",
             pt[1] - pt[0], pt[2] - pt[1], pt[3] - pt[2], pt[4] - pt[3], pt[5] - pt[4], pt[6] - pt[5], pt[7] - pt[6]);
   }
+  static const bool plan_debug = getenv("FK_DEBUG_PLAN") != nullptr;
+  if (plan_debug) {
+    int64_t parts = 0, priv_parts = 0;
+    for (int64_t k = 0; k < B * H; ++k) parts += row_head_count[k];
+    for (int64_t k = 0; k < B * H; ++k) priv_parts += row_head_count[k] - row_head_base[k];
+    fprintf(stderr, "fk plan: %d rows, %lld private units, %lld chunks, partials %lld (private %lld), max slots %d\n",
+            B, (long long)U, (long long)nchunks, (long long)parts, (long long)priv_parts, max_slots);
+  }
   if (!p->on_device) {
     p->have_plan = true;
     return FK_OK;

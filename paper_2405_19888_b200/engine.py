@@ -321,12 +321,16 @@ class SyntheticDecodeModel:
 class TensorDecodeModel:
     """Caller-supplied rows: q[L][B][H][D] and k/v[L][B][H][D] bf16, device
     resident or host (pinned) — host tensors are copied in the step, and the
-    output is copied back, which is the end-to-end path of bench.py."""
+    output is copied back, which is the end-to-end path of bench.py.
+    `out` (device, same shape as q) is the model's own attention-output
+    buffer: the step writes it in place (on the engine stream) instead of
+    allocating a new tensor every step."""
 
-    def __init__(self, q, k=None, v=None, copy_out: bool = False):
+    def __init__(self, q, k=None, v=None, copy_out: bool = False, out=None):
         self.q, self.k, self.v = q, k, v
         self.copy_out = copy_out
         self.host_out = None
+        self.out = out
 
 
 class GpuEngine:
@@ -411,6 +415,9 @@ class GpuEngine:
                 self._fill_stream = torch.cuda.Stream(self._dev)
             self._spv = self._stream.cuda_stream  # (plain int: ctypes passes it as void*)
             self._ev_caller = torch.cuda.Event()  # the caller's stream position, per step
+            self._dev_index = int(device)
+            self._caller_raw = None  # the caller's stream (cached Stream object, by raw handle)
+            self._caller = None
             self._fill_pending: Dict[str, Any] = {}  # context id -> event of its last fill
             self._release_event = None  # engine-stream fence of the last page release
             # The engine owns Q's producer side (its own buffers, ordered by
@@ -856,26 +863,34 @@ class GpuEngine:
         B = len(running)
         shape = (geo.num_layers, B, geo.num_heads, geo.head_dim)
         st = self._stream
-        caller = torch.cuda.current_stream(self._dev)
+        caller = self._caller  # (_caller_sync: the engine stream is past the caller's producers)
         # The step's buffers are allocated on the engine stream (so the caching
-        # allocator never hands the engine memory another stream still uses);
-        # caller tensors are read only after the caller's stream reached this
-        # point.  (set_stream instead of the context managers: this is the
-        # per-step host path.)
+        # allocator never hands the engine memory another stream still uses).
+        # (set_stream instead of the context managers: this is the per-step
+        # host path.)
         torch.cuda.set_stream(st)
         try:
             if tensor_model:
                 q = model.q
                 if q.device.type != "cuda":
                     q = q.to(self._dev, non_blocking=True)
-                elif caller != st:
-                    self._ev_caller.record(caller)
-                    st.wait_event(self._ev_caller)
-                    q.record_stream(st)
-            else:
-                q = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
+            else:  # synthetic queries into an engine-owned buffer (only the engine stream touches it)
+                q = self.__dict__.get("_synth_q")
+                if q is None or tuple(q.shape) != shape:
+                    q = self._synth_q = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
                 _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed, q.data_ptr(), self._spv))
-            out = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
+            out = model.out if tensor_model else None
+            if out is None or tuple(out.shape) != shape or out.dtype != torch.bfloat16 or out.device != self._dev:
+                # engine-owned outputs: a ring of two, alternating with the
+                # plan slots, so a step's graph sees the same pointers as the
+                # step two before it (no node updates); last_output stays
+                # valid until two steps later (pass TensorDecodeModel(out=...)
+                # to own the buffer)
+                ring = self.__dict__.setdefault("_out_ring", [None, None])
+                i = self._ring_i = self.__dict__.get("_ring_i", 1) ^ 1
+                out = ring[i]
+                if out is None or tuple(out.shape) != shape:
+                    out = ring[i] = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
             f32 = torch.empty(shape, dtype=torch.float32, device=self._dev) if self.capture_f32 else None
             # every layer's queries are already on the device: one C call
             # replays the layers' kernels (fk_attn_decode_layers, a CUDA graph)
@@ -904,9 +919,13 @@ class GpuEngine:
         torch = self._torch
         _lib.check(_lib.lib.fk_step_commit(self._pool.handle, self._pos_buf, self._spv))
         model = self.model
-        if isinstance(model, TensorDecodeModel) and model.k is not None:
+        if isinstance(model, TensorDecodeModel) and model.k is not None and model.k.device.type == "cuda":
+            # (the engine stream already waits for the caller: _caller_sync)
             geo = self.geometry
-            caller = torch.cuda.current_stream(self._dev)
+            _lib.check(_lib.lib.fk_append_kv_layers(self._pool.handle, 0, geo.num_layers,
+                                                    model.k.data_ptr(), model.v.data_ptr(), self._spv))
+        elif isinstance(model, TensorDecodeModel) and model.k is not None:
+            geo = self.geometry
             with torch.cuda.device(self._dev), torch.cuda.stream(self._stream):
                 k, v = model.k, model.v
                 hp = getattr(self, "_hp", None)
@@ -915,19 +934,39 @@ class GpuEngine:
                     # copied in under this step's attention (_decode_attention_host)
                     self._stream.wait_event(hp["ev_kv"])
                     k, v = hp["k"], hp["v"]
-                elif k.device.type != "cuda":
+                else:
                     k = k.to(self._dev, non_blocking=True)
                     v = v.to(self._dev, non_blocking=True)
-                elif caller != self._stream:  # the caller's producer ran on its own stream
-                    self._stream.wait_stream(caller)
-                    k.record_stream(self._stream)
-                    v.record_stream(self._stream)
                 _lib.check(_lib.lib.fk_append_kv_layers(self._pool.handle, 0, geo.num_layers,
                                                         ctypes.c_void_p(k.data_ptr()),
                                                         ctypes.c_void_p(v.data_ptr()), self._sp()))
         else:
             _lib.check(_lib.lib.fk_synth_append(self._pool.handle, self.model_seed, self.model_k_scale,
                                                 self._sp()))
+
+    def _caller_sync(self) -> None:
+        """Once per step: the engine stream waits for the caller's current
+        stream (where a TensorDecodeModel's q/k/v were produced), and device
+        model tensors are marked as used by the engine stream (caching
+        allocator).  The attention and the append read them afterwards."""
+        torch = self._torch
+        raw = torch._C._cuda_getCurrentRawStream(self._dev_index)
+        if raw != self._caller_raw:
+            self._caller = torch.cuda.current_stream(self._dev)
+            self._caller_raw = raw
+        if raw == self._spv:
+            return
+        model = self.model
+        if isinstance(model, TensorDecodeModel) and model.q.device.type == "cuda":
+            self._ev_caller.record(self._caller)
+            self._stream.wait_event(self._ev_caller)
+            st = self._stream
+            model.q.record_stream(st)
+            if model.k is not None:
+                model.k.record_stream(st)
+                model.v.record_stream(st)
+            if model.out is not None:
+                model.out.record_stream(st)
 
     def _wait_fills(self, running: List[GenerationTask]) -> None:
         """The decode stream waits for the pending fills of the contexts this
@@ -985,8 +1024,10 @@ class GpuEngine:
         batch_tokens = self._plan(running) if running else 0
         if _PHASES:
             tm.append(time.perf_counter())
-        if running and self.device is not None and self._fill_pending:
-            self._wait_fills(running)
+        if running and self.device is not None:
+            self._caller_sync()
+            if self._fill_pending:
+                self._wait_fills(running)
         snapshot = None
         emitted: Dict[str, int] = {}
         if self.attend_own_token:

@@ -41,10 +41,20 @@ def direct(args):
     import bench
 
     cfg = bench.CONFIGS[args.config]
-    eng, rows = bench.build_engine(cfg, 0, torch, out_len=args.steps + 16)
+    eng, rows = bench.build_engine(cfg, 0, torch, out_len=2 * args.steps + 16)
     for _ in range(5):
         eng.step()
     torch.cuda.synchronize()
+    if args.cprofile:  # where the host time goes (tottime per function)
+        import cProfile
+        import pstats
+        pr = cProfile.Profile()
+        pr.enable()
+        for _ in range(args.steps):
+            eng.step()
+        pr.disable()
+        torch.cuda.synchronize()
+        pstats.Stats(pr).sort_stats("tottime").print_stats(25)
     us = []
     for _ in range(args.steps):
         w0 = eng.pool_stats().host_wait_ns
@@ -64,9 +74,11 @@ def direct(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--direct", action="store_true", help="one bench.py engine, no manager")
+    ap.add_argument("--cprofile", action="store_true", help="(direct) cProfile the steps first")
     ap.add_argument("--config", default="llama13b_p6000_b64")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--engines", type=int, default=8)
+    ap.add_argument("--pages", type=int, default=0, help="KV arena pages per engine (default: the workload's need)")
     ap.add_argument("--users", type=int, default=64)
     ap.add_argument("--output-len", type=int, default=64)
     ap.add_argument("--layers", type=int, default=32)
@@ -92,7 +104,7 @@ def main():
         apps += [dataclasses.replace(a, app_id=f"g{g}.{a.app_id}") for a in wl.apps]
     work = Workload("GroupsPerEngine", 7, {"groups": args.engines}, apps)
 
-    step_us = []
+    step_us, full = [], []
     orig_step = P.GpuEngine.step
 
     def timed_step(self):
@@ -104,6 +116,7 @@ def main():
         # host CPU time of the step: wall time minus the time the plan waited
         # for the GPU to release a plan slot (the host runs <= 1 step ahead)
         step_us.append((t1 - t0) * 1e6 - (w1 - w0) / 1e3)
+        full.append(r is not None and r.batch_tokens > 0 and self.last_plan.num_rows == args.users)
         return r
 
     P.GpuEngine.step = timed_step
@@ -112,10 +125,23 @@ def main():
         import semflow.prefix as sp
         import semflow.tokenizer as st
         st.hash_token_ids = sp.hash_token_ids = se.hash_token_ids = P.hash_token_ids
-    sm.Engine = P.engine_factory(P.ModelGeometry(args.layers, args.heads, 128))
+    # the KV arena sized up front (a serving deployment sizes its pool at
+    # start-up; growing it is a device-wide copy): prompt + users x (unique +
+    # output) tokens per engine, in 16-token pages
+    pages = args.pages or (-(-6000 // 16) + args.users * (-(-(200 + args.output_len) // 16) + 2) + 64)
+    sm.Engine = P.engine_factory(P.ModelGeometry(args.layers, args.heads, 128), num_pages=pages)
     t0 = time.perf_counter()
+    if args.cprofile:
+        import cProfile
+        import pstats
+        pr = cProfile.Profile()
+        pr.enable()
     mgr, _, end_ns = run_workload_manager(work, "semflow", Config(engines=args.engines, kv_tokens=1 << 21))
     wall = time.perf_counter() - t0
+    if args.cprofile:
+        pr.disable()
+        st_ = pstats.Stats(pr)
+        st_.sort_stats("tottime").print_stats("paper_2405_19888_b200|torch", 30)
     for e in mgr.engines.values():
         if e.stream is not None:
             e.stream.synchronize()
@@ -130,6 +156,10 @@ def main():
         "engine_steps": len(step_us),
         "step_host_us_mean": statistics.mean(step_us), "step_host_us_median": statistics.median(step_us),
         "step_host_us_steady_mean": statistics.mean(steady), "step_host_us_steady_median": statistics.median(steady),
+        # decode steps with every user of the engine's group in the batch (B = users)
+        "full_batch_steps": sum(full),
+        "full_batch_step_host_us_median": statistics.median([u for u, f in zip(step_us, full) if f] or [0.0]),
+        "full_batch_step_host_us_mean": statistics.mean([u for u, f in zip(step_us, full) if f] or [0.0]),
         "manager_loop_us_per_engine_step": wall / max(len(step_us), 1) * 1e6,
         "wall_s": wall, "wall_with_gpu_drain_s": gpu_wall, "virtual_end_ms": end_ns / 1e6,
         "max_batch": max(max((r.batch_tokens for r in e.reports), default=0) for e in mgr.engines.values()),
