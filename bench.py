@@ -247,8 +247,11 @@ def time_layers_isolated(eng, reps, torch):
     """Per-layer attention as a model sees it: one fk_attn_decode per layer
     (direct launches, no graph), PDL only between the layer's own kernels
     (FK_OPT_PDL=1), and a foreign kernel between consecutive layers (the rest
-    of the transformer layer), so nothing of layer l+1 overlaps layer l.  The
-    foreign kernel's own time is measured alone and subtracted."""
+    of the transformer layer), so nothing of layer l+1 overlaps layer l.
+    Each layer is bracketed by CUDA events on the engine stream (recorded
+    after the foreign kernel, and after the layer's last kernel): the time
+    from the layer's first kernel start to its completion.  Returns (mean
+    layer seconds, foreign-kernel GPU seconds per layer)."""
     from paper_2405_19888_b200 import _lib
 
     L = eng.geometry.num_layers
@@ -261,33 +264,52 @@ def time_layers_isolated(eng, reps, torch):
     sp = ctypes.c_void_p(st.cuda_stream)
     foreign = torch.empty(1 << 16, dtype=torch.float32, device=q.device)
     eng.set_option(_lib.FK_OPT_PDL, 1)
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
+    fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(L)]
 
-    def one_pass(attn=True):
+    def one_pass(times, ftimes):
         for layer in range(L):
-            if attn:
-                _lib.check(_lib.lib.fk_attn_decode(eng._pool.handle, layer, ctypes.c_void_p(q.data_ptr() + layer * le),
-                                                   ctypes.c_void_p(out.data_ptr() + layer * le), None, sp))
+            fev[layer][0].record(st)
             foreign.add_(1.0)
+            fev[layer][1].record(st)
+            ev[layer][0].record(st)
+            _lib.check(_lib.lib.fk_attn_decode(eng._pool.handle, layer, ctypes.c_void_p(q.data_ptr() + layer * le),
+                                               ctypes.c_void_p(out.data_ptr() + layer * le), None, sp))
+            ev[layer][1].record(st)
+        st.synchronize()
+        if times is not None:
+            times += [a.elapsed_time(b) / 1e3 for a, b in ev]
+            ftimes += [a.elapsed_time(b) / 1e3 for a, b in fev]
 
     try:
         with torch.cuda.stream(st):
-            one_pass()
-            start.record(st)
+            one_pass(None, None)
+            times, ftimes = [], []
             for _ in range(reps):
-                one_pass()
-            end.record(st)
-            end.synchronize()
-            t_all = start.elapsed_time(end) / 1e3
-            start.record(st)
-            for _ in range(reps):
-                one_pass(attn=False)
-            end.record(st)
-            end.synchronize()
-            t_foreign = start.elapsed_time(end) / 1e3
+                one_pass(times, ftimes)
     finally:
         eng.set_option(_lib.FK_OPT_PDL, 2)
-    return (t_all - t_foreign) / (reps * L), t_foreign / (reps * L)
+    return sum(times) / len(times), sum(ftimes) / len(ftimes)
+
+
+def ncu_layer(eng, torch, batch_tokens, bytes_layer):
+    """One layer's kernels inside a cudaProfilerStart/Stop range, on the plan
+    the roofline is timed on, so an `ncu --profile-from-start off` run of
+    bench.py measures DRAM traffic at exactly this batch_tokens (written with
+    the algorithmic bytes to gpurun_out/ncu_layer.json)."""
+    from paper_2405_19888_b200 import _lib
+
+    q = eng.model.q
+    out = torch.empty_like(q)
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    _lib.check(_lib.lib.fk_attn_decode(eng._pool.handle, 0, ctypes.c_void_p(q.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr()), None, ctypes.c_void_p(eng.stream.cuda_stream)))
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "ncu_layer.json"), "w") as f:
+        json.dump({"batch_tokens": batch_tokens, "alg_bytes_per_layer": bytes_layer}, f)
 
 
 def parity_check(eng, torch):
@@ -459,6 +481,8 @@ def main():
     # per-layer attention alone for the roofline (same plan as the last step)
     t_layer = time_layers(eng, max(args.steps // 2, 3), torch)
     barrier()
+    if os.environ.get("FK_NCU_LAYER"):  # profiles/traffic_all.sh: ncu --profile-from-start off
+        ncu_layer(eng, torch, batch_tokens, bytes_layer)
     clk = clocks.stop()
     iso = None
     if not args.no_isolated:
@@ -504,9 +528,12 @@ def main():
             tr = json.load(f).get(args.config)
         if tr:
             traffic_src = tr["source"]
+            traffic_tok = tr.get("bytes_per_token")
             if tr.get("batch_tokens") == batch_tokens:  # captured at this run's final plan
                 traffic = tr["layer_bytes"]
-            traffic_tok = tr.get("bytes_per_token")
+            elif traffic_tok:  # another run length: the measured bytes per streamed token, scaled
+                traffic = traffic_tok * batch_tokens
+                traffic_src += f" (captured at {tr.get('batch_tokens')} tokens, scaled per token)"
     except Exception:
         pass
 
@@ -527,7 +554,8 @@ def main():
             roof["layer_us_isolated"] = iso[0] * 1e6
             roof["frac_isolated"] = bytes_layer / iso[0] / 1e9 / peak
             roof["isolated_mode"] = ("one fk_attn_decode per layer, PDL within the layer only, a foreign kernel "
-                                     f"between layers ({iso[1] * 1e6:.2f} us, subtracted)")
+                                     f"between layers ({iso[1] * 1e6:.2f} us); each layer timed by CUDA events "
+                                     "around its own launches")
         line = {
             "metric": metric,
             "value": value,
