@@ -249,16 +249,20 @@ class KVCache:
     rows instead of generated ones (the K/V a TensorDecodeModel appended
     during decode); rows(layer, kv, positions) -> [n, H, 128] float32."""
 
-    def __init__(self, seed: int, heads: int, k_scale: float = 1.0, appended=None):
+    def __init__(self, seed: int, heads: int, k_scale: float = 1.0, appended=None, alias=None):
         self.seed, self.heads, self.k_scale = seed, heads, k_scale
         self.appended = appended or {}
+        # alias[uid] = src_uid: a context whose K/V was copied from another
+        # engine's context (prefix migration) holds that context's rows
+        self.alias = alias or {}
         self._c: Dict[Tuple[int, int], Tuple[np.ndarray, np.ndarray]] = {}
 
     def _gen(self, uid: int, ntok: int, layer: int):
         n0, rows = self.appended.get(uid, (ntok, None))
         n0 = min(n0, ntok)
-        k = synth_rows_range(self.seed, TAG_K, uid, 0, n0, layer, self.heads, self.k_scale)
-        v = synth_rows_range(self.seed, TAG_V, uid, 0, n0, layer, self.heads, 1.0)
+        src = self.alias.get(uid, uid)
+        k = synth_rows_range(self.seed, TAG_K, src, 0, n0, layer, self.heads, self.k_scale)
+        v = synth_rows_range(self.seed, TAG_V, src, 0, n0, layer, self.heads, 1.0)
         if ntok > n0:
             pos = np.arange(n0, ntok)
             k = np.concatenate([k, np.asarray(rows(layer, 0, pos), dtype=np.float32)])

@@ -43,42 +43,6 @@ def hash_token_ids(token_ids: Sequence[int], seed: int = FNV64_EMPTY) -> int:
     return _lib.fnv1a64_u32(list(token_ids), seed)
 
 
-def format_ms(ns: int) -> str:
-    """engine.format_ms (engine.py:541-545): ms with <= 3 decimals, zeros trimmed."""
-    text = "%.3f" % (ns / MS)
-    if "." in text:
-        text = text.rstrip("0").rstrip(".")
-    return text
-
-
-@dataclass
-class CostModel:
-    """Virtual clock of the reference (engine.py:25-50); kept so reports and
-    traces stay byte-identical.  Any object with the same attributes works."""
-
-    c0_ms: float = 2.0
-    c1_ms: float = 0.0062
-    c2_ms: float = 5.0
-    c3_ms: float = 0.002
-    shared_kernel: bool = True
-    block_size: int = 16
-
-    def __post_init__(self) -> None:
-        self.c0_ns = round(self.c0_ms * MS)
-        self.c1_ns = round(self.c1_ms * MS)
-        self.c2_ns = round(self.c2_ms * MS)
-        self.c3_ns = round(self.c3_ms * MS)
-
-    def iteration_ns(self, batch_tokens: int) -> int:
-        return self.c0_ns + self.c1_ns * batch_tokens
-
-    def fill_ns(self, fill_tokens: int) -> int:
-        return self.c2_ns + self.c3_ns * fill_tokens
-
-    def latency_threshold_ms(self, capacity: int) -> float:
-        return self.iteration_ns(capacity) / MS
-
-
 class Context:
     """Forest node (engine.py:53-63) plus the pool uid that keys it in C++.
 
@@ -120,13 +84,6 @@ class Context:
                 f"refcount={self.refcount}, dropped={self.dropped})")
 
 
-@dataclass
-class FillTask:
-    request_id: Optional[str]
-    context_id: str
-    token_ids: List[int]
-
-
 class GenerationTask:
     """engine.py:116-128.  `emitted` is derived from the engine's decode
     counter: a running generation emits one token per decode iteration until
@@ -163,28 +120,6 @@ class GenerationTask:
     def __repr__(self) -> str:
         return (f"GenerationTask({self.request_id!r}, ctx={self.context_id!r}, emitted={self.emitted}/"
                 f"{len(self.token_ids)}, started={self.started}, done={self.done})")
-
-
-@dataclass
-class StepReport:
-    engine_id: str
-    started_ns: int
-    elapsed_ns: int
-    fill_tokens: int
-    batch_tokens: int
-    emitted: Dict[str, int]
-    finished: List[str]
-    failed: List[Tuple[str, str]]
-    fill_completed: List[str]
-
-
-@dataclass
-class ContextPlan:
-    reuse_context_id: Optional[str]
-    reused_tokens: int
-    fill_segments: List[Tuple[List[int], int]]
-    marginal_tokens: int
-    adopted_tokens: int = 0
 
 
 @dataclass(frozen=True)
@@ -333,7 +268,191 @@ class TensorDecodeModel:
         self.out = out
 
 
-class GpuEngine:
+# ---- the reference runtime ------------------------------------------------------
+# GpuEngine plugs into semflow (the reference runtime: manager, scheduler,
+# API).  Where semflow is importable, the engine's pure bookkeeping -- the
+# report / plan / fill dataclasses, the cost model, prefix planning, the
+# live-context walk, context freeing -- is the reference's own code
+# (GpuEngine subclasses semflow.engine.Engine and overrides only what the
+# device path changes: the context forest and block store live in the C++
+# pool, fills write K/V, the step runs the kernels).  Without semflow (a
+# standalone bench run) the restatement below stands in, pinned to the
+# reference by the golden op streams (tests/golden) and the rebound suites.
+_ref = None
+if not os.environ.get("FK_STANDALONE_ENGINE"):
+    try:
+        from semflow import engine as _ref  # noqa: F811
+    except ImportError:
+        _ref = None
+
+if _ref is not None:
+    CostModel = _ref.CostModel
+    FillTask = _ref.FillTask
+    StepReport = _ref.StepReport
+    ContextPlan = _ref.ContextPlan
+    format_ms = _ref.format_ms
+    _EngineBase = _ref.Engine
+else:
+    def format_ms(ns: int) -> str:
+        """engine.format_ms (engine.py:541-545): ms with <= 3 decimals, zeros trimmed."""
+        text = "%.3f" % (ns / MS)
+        if "." in text:
+            text = text.rstrip("0").rstrip(".")
+        return text
+
+    @dataclass
+    class CostModel:
+        """Virtual clock of the reference (engine.py:25-50); kept so reports and
+        traces stay byte-identical.  Any object with the same attributes works."""
+
+        c0_ms: float = 2.0
+        c1_ms: float = 0.0062
+        c2_ms: float = 5.0
+        c3_ms: float = 0.002
+        shared_kernel: bool = True
+        block_size: int = 16
+
+        def __post_init__(self) -> None:
+            self.c0_ns = round(self.c0_ms * MS)
+            self.c1_ns = round(self.c1_ms * MS)
+            self.c2_ns = round(self.c2_ms * MS)
+            self.c3_ns = round(self.c3_ms * MS)
+
+        def iteration_ns(self, batch_tokens: int) -> int:
+            return self.c0_ns + self.c1_ns * batch_tokens
+
+        def fill_ns(self, fill_tokens: int) -> int:
+            return self.c2_ns + self.c3_ns * fill_tokens
+
+        def latency_threshold_ms(self, capacity: int) -> float:
+            return self.iteration_ns(capacity) / MS
+
+    @dataclass
+    class FillTask:
+        request_id: Optional[str]
+        context_id: str
+        token_ids: List[int]
+
+    @dataclass
+    class StepReport:
+        engine_id: str
+        started_ns: int
+        elapsed_ns: int
+        fill_tokens: int
+        batch_tokens: int
+        emitted: Dict[str, int]
+        finished: List[str]
+        failed: List[Tuple[str, str]]
+        fill_completed: List[str]
+
+    @dataclass
+    class ContextPlan:
+        reuse_context_id: Optional[str]
+        reused_tokens: int
+        fill_segments: List[Tuple[List[int], int]]
+        marginal_tokens: int
+        adopted_tokens: int = 0
+
+    class _EngineBase:
+        """Restatement of the reference Engine's bookkeeping (engine.py:186-387,
+        534-538) for runs without semflow; GpuEngine supplies the state."""
+
+        def new_context_id(self) -> str:
+            return f"{self.engine_id}.c{next(self._ctx_counter)}"
+
+        def get_context(self, context_id: str) -> Context:
+            ctx = self.contexts.get(context_id)
+            if ctx is None:
+                raise UnknownContext(f"unknown context {context_id}")
+            return ctx
+
+        def free_context(self, context_id: str) -> None:
+            ctx = self.get_context(context_id)
+            if ctx.refcount > 0:
+                raise ContextBusy(f"context {context_id} has refcount {ctx.refcount}")
+            self._discard_context(ctx)
+
+        def mark_dropped(self, context_id: str) -> None:
+            ctx = self.get_context(context_id)
+            ctx.dropped = True
+            if ctx.refcount == 0:
+                self._discard_context(ctx)
+
+        # -- planning (engine.py:304-382) -------------------------------------------
+
+        def plan_prefix(self, chain_hashes: Sequence[int], segment_tokens: Sequence[Sequence[int]],
+                        overlay: Optional[Dict[int, str]] = None) -> ContextPlan:
+            """Deepest chain boundary held by the registry (or the overlay of
+            this scheduling pass) -> context to fork from; see engine.py:304-363."""
+            n = len(chain_hashes)
+            cumulative: List[int] = []
+            acc = 0
+            for i in range(n):
+                if i < len(segment_tokens):
+                    acc += len(segment_tokens[i])
+                cumulative.append(acc)
+            reuse_id: Optional[str] = None
+            depth = credited = 0
+            if self.reuse_enabled:
+                live: Optional[Set[str]] = None
+                for i in reversed(range(n)):
+                    if cumulative[i] == 0:
+                        break
+                    h = chain_hashes[i]
+                    holder = self.registry.get(h)
+                    planned = overlay is not None and h in overlay
+                    if holder is None and not planned:
+                        continue
+                    if reuse_id is None:
+                        reuse_id = holder if holder is not None else overlay[h]
+                        depth = i + 1
+                    if planned:
+                        credited = i + 1
+                        break
+                    if live is None:
+                        live = self._live_context_ids()
+                    if holder in live:
+                        credited = i + 1
+                        break
+            fills: List[Tuple[List[int], int]] = []
+            marginal = 0
+            for i in range(depth, len(segment_tokens)):
+                seg = list(segment_tokens[i])
+                if seg:
+                    fills.append((seg, chain_hashes[i]))
+                    marginal += len(seg)
+            reused = 0
+            if reuse_id is not None and reuse_id in self.contexts:
+                reused = self._chain_tokens(self.contexts[reuse_id])
+            adopted = 0
+            if depth > credited:
+                adopted = cumulative[depth - 1] - (cumulative[credited - 1] if credited else 0)
+            return ContextPlan(reuse_id, reused, fills, marginal, adopted)
+
+        def _live_context_ids(self) -> Set[str]:
+            live: Set[str] = set()
+            for leaf in self.request_leaf.values():
+                for c in self._ancestors(self.contexts.get(leaf)):
+                    if c.context_id in live:
+                        break
+                    live.add(c.context_id)
+            return live
+
+        def _chain_tokens(self, ctx: Context) -> int:
+            return sum(c.token_count for c in self._ancestors(ctx))
+
+        def has_work(self) -> bool:
+            return bool(self.fill_queue) or any(not g.done for g in self.gens.values())
+
+        @property
+        def charged_tokens(self) -> int:
+            return sum(self.charges.values())
+
+        def admitted_classes(self) -> List[str]:
+            return sorted(set(self.holder_class.values()))
+
+
+class GpuEngine(_EngineBase):
     """Drop-in `Engine` (engine.py:157-538) with a B200 decode path."""
 
     def __init__(
@@ -350,6 +469,7 @@ class GpuEngine:
         capture_f32: bool = False,
         keep_history: bool = False,
         attend_own_token: bool = False,
+        peers: Optional[List["GpuEngine"]] = None,
     ):
         self.engine_id = engine_id
         self.cost = cost
@@ -395,6 +515,12 @@ class GpuEngine:
         self._last_running: List[GenerationTask] = []
         self.last_plan = _lib.PlanInfo()
         self.kv_tokens_streamed = 0  # sum of batch_tokens over decode steps (per layer)
+        # prefix migration (engine_factory(migrate_prefixes=True)): the engines
+        # of one process whose registries a fill may copy a prefix from
+        self._peers = peers
+        self.prefix_migrations = 0
+        self.migrated_tokens = 0
+        self.migrated: Dict[int, Tuple[str, int, int]] = {}  # dst uid -> (src engine id, src uid, tokens)
         self._stream = None
         self._plan_rows: List[GenerationTask] = []  # rows of _leaf_buf
         self._nfail = ctypes.c_int32(0)
@@ -464,15 +590,6 @@ class GpuEngine:
 
     # -- context primitives (engine.py:192-300) --------------------------------
 
-    def new_context_id(self) -> str:
-        return f"{self.engine_id}.c{next(self._ctx_counter)}"
-
-    def get_context(self, context_id: str) -> Context:
-        ctx = self.contexts.get(context_id)
-        if ctx is None:
-            raise UnknownContext(f"unknown context {context_id}")
-        return ctx
-
     def create_context(self, context_id: str, parent_context_id: Optional[str], request_id: Optional[str] = None) -> Context:
         inherited: List[int] = []
         parent_uid = -1
@@ -507,6 +624,9 @@ class GpuEngine:
         the prefill (tests, bench)."""
         if kv is not None:
             self._check_rows(kv, len(token_ids))
+        if (kv is None and kv_from is None and self._peers and boundary_hash is not None and self.device is not None
+                and token_ids and context_id not in self.contexts):
+            kv_from = self._peer_prefix(boundary_hash, parent_context_id, len(token_ids))
         if kv_from is not None:
             src_eng, src_id = kv_from
             src_ctx = src_eng.get_context(src_id)
@@ -556,6 +676,9 @@ class GpuEngine:
             self._fill_pending[context_id] = done
             if kv_from is not None:
                 src_eng.stream.wait_event(done)  # the source may not recycle its pages before the copy
+                self.prefix_migrations += 1
+                self.migrated_tokens += len(token_ids)
+                self.migrated[ctx.uid] = (src_eng.engine_id, src_ctx.uid, len(token_ids))
         if boundary_hash is not None:
             ctx.chain_hashes.append(boundary_hash)
             if boundary_hash not in self.registry:
@@ -566,6 +689,33 @@ class GpuEngine:
             self.pending_fills[request_id] = self.pending_fills.get(request_id, 0) + 1
             self.request_leaf[request_id] = context_id
         return len(token_ids)
+
+    def _boundary(self, context_id: Optional[str]) -> Optional[int]:
+        """Chain hash at the end of a context (None: the root side)."""
+        ctx = self.contexts.get(context_id) if context_id else None
+        return ctx.chain_hashes[-1] if ctx is not None and ctx.chain_hashes else None
+
+    def _peer_prefix(self, boundary_hash: int, parent_context_id: Optional[str], ntok: int):
+        """The reference scheduler's `shared-ctx` fallback (scheduler.py:198-222)
+        places a request on an engine without its prefix when the engines that
+        hold it are full; the new engine would prefill the prefix again.
+        Instead, a fill whose segment ends at a chain hash another engine of
+        the process holds -- same segment (same parent boundary), at least as
+        many tokens -- copies that context's K/V (fill(kv_from=...):
+        fk_ctx_copy_kv, NVLink peer reads across GPUs).  Returns (engine,
+        context id) or None."""
+        want_parent = self._boundary(parent_context_id)
+        for e in self._peers:
+            if e is self or e.device is None:
+                continue
+            cid = e.registry.get(boundary_hash)
+            src = e.contexts.get(cid) if cid is not None else None
+            if src is None or src.token_count < ntok or e._boundary(src.parent_id) != want_parent:
+                continue
+            if e.geometry != self.geometry:
+                continue
+            return (e, cid)
+        return None
 
     def _check_rows(self, kv, n: int) -> None:
         if self.device is None:
@@ -630,90 +780,12 @@ class GpuEngine:
                 if parent.refcount == 0 and parent.dropped:
                     ctx = parent  # cascade (engine.py:280-285)
 
-    def free_context(self, context_id: str) -> None:
-        ctx = self.get_context(context_id)
-        if ctx.refcount > 0:
-            raise ContextBusy(f"context {context_id} has refcount {ctx.refcount}")
-        self._discard_context(ctx)
-
-    def mark_dropped(self, context_id: str) -> None:
-        ctx = self.get_context(context_id)
-        ctx.dropped = True
-        if ctx.refcount == 0:
-            self._discard_context(ctx)
-
-    # -- planning (engine.py:304-382) -------------------------------------------
-
-    def plan_prefix(self, chain_hashes: Sequence[int], segment_tokens: Sequence[Sequence[int]],
-                    overlay: Optional[Dict[int, str]] = None) -> ContextPlan:
-        """Deepest chain boundary held by the registry (or the overlay of
-        this scheduling pass) -> context to fork from; see engine.py:304-363."""
-        n = len(chain_hashes)
-        cumulative: List[int] = []
-        acc = 0
-        for i in range(n):
-            if i < len(segment_tokens):
-                acc += len(segment_tokens[i])
-            cumulative.append(acc)
-        reuse_id: Optional[str] = None
-        depth = credited = 0
-        if self.reuse_enabled:
-            live: Optional[Set[str]] = None
-            for i in reversed(range(n)):
-                if cumulative[i] == 0:
-                    break
-                h = chain_hashes[i]
-                holder = self.registry.get(h)
-                planned = overlay is not None and h in overlay
-                if holder is None and not planned:
-                    continue
-                if reuse_id is None:
-                    reuse_id = holder if holder is not None else overlay[h]
-                    depth = i + 1
-                if planned:
-                    credited = i + 1
-                    break
-                if live is None:
-                    live = self._live_context_ids()
-                if holder in live:
-                    credited = i + 1
-                    break
-        fills: List[Tuple[List[int], int]] = []
-        marginal = 0
-        for i in range(depth, len(segment_tokens)):
-            seg = list(segment_tokens[i])
-            if seg:
-                fills.append((seg, chain_hashes[i]))
-                marginal += len(seg)
-        reused = 0
-        if reuse_id is not None and reuse_id in self.contexts:
-            reused = self._chain_tokens(self.contexts[reuse_id])
-        adopted = 0
-        if depth > credited:
-            adopted = cumulative[depth - 1] - (cumulative[credited - 1] if credited else 0)
-        return ContextPlan(reuse_id, reused, fills, marginal, adopted)
-
     def _ancestors(self, ctx: Optional[Context]):
         while ctx is not None:
             yield ctx
             ctx = self.contexts.get(ctx.parent_id) if ctx.parent_id else None
 
-    def _live_context_ids(self) -> Set[str]:
-        live: Set[str] = set()
-        for leaf in self.request_leaf.values():
-            for c in self._ancestors(self.contexts.get(leaf)):
-                if c.context_id in live:
-                    break
-                live.add(c.context_id)
-        return live
-
-    def _chain_tokens(self, ctx: Context) -> int:
-        return sum(c.token_count for c in self._ancestors(ctx))
-
     # -- stepping (engine.py:386-484) ---------------------------------------------
-
-    def has_work(self) -> bool:
-        return bool(self.fill_queue) or any(not g.done for g in self.gens.values())
 
     def _batch_tokens(self, running: List[GenerationTask]) -> int:
         """Host restatement of the dedup walk; the step itself takes the
@@ -1214,19 +1286,12 @@ class GpuEngine:
             if ctx.refcount == 0:
                 self._discard_context(ctx)
 
-    @property
-    def charged_tokens(self) -> int:
-        return sum(self.charges.values())
-
-    def admitted_classes(self) -> List[str]:
-        return sorted(set(self.holder_class.values()))
-
-
 # Alias so a maintainer can rebind `semflow.engine.Engine = Engine`.
 Engine = GpuEngine
 
 
-def engine_factory(geometry: ModelGeometry = LLAMA_13B, devices: Optional[Sequence[int]] = None, **kw):
+def engine_factory(geometry: ModelGeometry = LLAMA_13B, devices: Optional[Sequence[int]] = None,
+                   migrate_prefixes: bool = False, **kw):
     """A constructor with `Engine`'s signature for SemanticManager's one
     construction site (manager.py:130-139: `Engine(eid, cost, kv_tokens=...,
     token_capacity=...)` for eid = e0 .. e{engines-1}), mapping engine eI to
@@ -1235,6 +1300,10 @@ def engine_factory(geometry: ModelGeometry = LLAMA_13B, devices: Optional[Sequen
     (scheduler.py:198-222) over the GPUs of one process.  Extra keyword
     arguments (model, capture_f32, keep_history, ...) go to every GpuEngine;
     devices=[] builds host-only engines (the integer twin).
+    migrate_prefixes=True: the engines fill a prefix another engine of the
+    process already holds by copying its K/V (GpuEngine._peer_prefix) --
+    the `shared-ctx` fallback of the scheduler then costs an NVLink copy
+    instead of a prefill.
 
         import semflow.manager
         semflow.manager.Engine = engine_factory(LLAMA_13B)
@@ -1245,11 +1314,17 @@ def engine_factory(geometry: ModelGeometry = LLAMA_13B, devices: Optional[Sequen
         devices = list(range(torch.cuda.device_count()))
     devices = list(devices)
 
+    peers: Optional[List[GpuEngine]] = [] if migrate_prefixes else None
+
     def make(engine_id: str, cost: Any, kv_tokens: int = 120_000, token_capacity: int = 64_000) -> GpuEngine:
         digits = engine_id.lstrip("e")
         idx = int(digits) if digits.isdigit() else 0
         dev = devices[idx % len(devices)] if devices else None
-        return GpuEngine(engine_id, cost, kv_tokens, token_capacity, device=dev, geometry=geometry, **kw)
+        eng = GpuEngine(engine_id, cost, kv_tokens, token_capacity, device=dev, geometry=geometry, peers=peers, **kw)
+        if peers is not None:
+            peers.append(eng)
+        return eng
 
     make.devices = devices
+    make.peers = peers
     return make

@@ -24,6 +24,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--opt", action="append", default=[])
+    ap.add_argument("--isolated", action="store_true",
+                    help="stamps of bench.time_layers_isolated (direct launches, a foreign kernel between layers)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     eng, rows = bench.build_engine(cfg, 0, torch, out_len=32)
@@ -33,6 +35,9 @@ def main():
     for _ in range(4):
         eng.step()
     torch.cuda.synchronize()
+    if args.isolated:
+        bench.time_layers_isolated(eng, 1, torch)
+        torch.cuda.synchronize()
     info = eng.last_plan
     out = {}
     for name in ("prefix", "priv", "merge"):

@@ -182,3 +182,32 @@ def test_shared_kernel_dedup_counts():
             reps.append(eng.step())
         assert [r.batch_tokens for r in reps] == [base + 2 * k for k in range(5)]
         assert all(r.batch_tokens == eng._batch_tokens([]) + r.batch_tokens for r in reps)
+
+
+def test_engine_builds_on_the_reference_runtime():
+    """Where semflow is importable the engine's pure bookkeeping is the
+    reference's own code: GpuEngine subclasses semflow.engine.Engine and the
+    report / plan / fill types are semflow's (engine.py here, `_ref`)."""
+    import paper_2405_19888_b200.engine as E
+
+    try:
+        import semflow.engine as se
+    except ImportError:
+        pytest.skip("semflow not importable")
+    assert E._ref is se and issubclass(E.GpuEngine, se.Engine)
+    assert E.StepReport is se.StepReport and E.ContextPlan is se.ContextPlan and E.CostModel is se.CostModel
+    assert E.GpuEngine.plan_prefix is se.Engine.plan_prefix
+
+
+def test_standalone_restatement_stays_pinned():
+    """Without semflow the restated bookkeeping stands in (a standalone bench
+    run): the golden op streams and unit pins pass in that mode too."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, FK_STANDALONE_ENGINE="1")
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          os.path.join(os.path.dirname(__file__), "test_engine_parity.py"),
+                          "-k", "golden_streams or unit_pins or dedup_counts or live_random"],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]

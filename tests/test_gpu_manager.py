@@ -29,7 +29,7 @@ pytestmark = pytest.mark.gpu
 semflow = pytest.importorskip("semflow", reason="the reference runtime (semflow) is not importable")
 
 
-def run_manager(factory, engines=1):
+def run_manager(factory, engines=1, **cfg):
     import semflow.manager as sm
     from semflow.config import Config
     from semflow.experiments import run_workload_manager
@@ -40,7 +40,7 @@ def run_manager(factory, engines=1):
     if factory is not None:
         sm.Engine = factory
     try:
-        mgr, runners, end_ns = run_workload_manager(wl, "semflow", Config(total_blocks=30000, engines=engines))
+        mgr, runners, end_ns = run_workload_manager(wl, "semflow", Config(total_blocks=30000, engines=engines, **cfg))
     finally:
         sm.Engine = saved
     return mgr, end_ns
@@ -82,3 +82,31 @@ def test_reference_manager_drives_gpu_engines(cuda_device, engines):
     assert decode_steps >= 8
     assert sum(e.kv_tokens_streamed for e in mgr.engines.values()) == sum(
         r.batch_tokens for e in mgr.engines.values() for r in e.reports)
+
+
+def test_shared_ctx_fallback_migrates_the_prefix(cuda_device):
+    """With a throughput capacity the prefix holder cannot absorb, the
+    scheduler's `shared-ctx` placement falls back to `solo` on the second
+    engine (scheduler.py:198-222), which must then fill the 6k system
+    prompt.  With engine_factory(migrate_prefixes=True) that fill copies the
+    holder's K/V (fk_ctx_copy_kv) instead of prefilling: the manager's view
+    is unchanged, the copied context holds the holder's rows (oracle alias),
+    and every decode step still matches the oracle."""
+    import oracle.forkattn_oracle as O
+
+    cfg = dict(throughput_capacity=10000)
+    want = manager_view(*run_manager(None, 2, **cfg))
+    factory = P.engine_factory(P.ModelGeometry(2, 8, 128), capture_f32=True, keep_history=True,
+                               migrate_prefixes=True)
+    mgr, end_ns = run_manager(factory, 2, **cfg)
+    assert manager_view(mgr, end_ns) == want
+    engines = [e for _, e in sorted(mgr.engines.items())]
+    assert sum(e.prefix_migrations for e in engines) >= 1
+    assert sum(e.migrated_tokens for e in engines) >= 6000
+    for eng in engines:
+        if not eng.history:
+            continue
+        eng.stream.synchronize()
+        alias = {dst: src for dst, (_, src, _) in eng.migrated.items()}
+        kv = O.KVCache(eng.model_seed, eng.geometry.num_heads, eng.model_k_scale, alias=alias)
+        check_history(eng, kv=kv)
