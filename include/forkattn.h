@@ -67,6 +67,8 @@ typedef struct {
   int64_t arena_bytes;  /* device bytes of the KV arena */
   int64_t host_wait_ns; /* host time fk_step_plan spent waiting for the GPU to release a plan
                            slot (the host runs at most one step ahead) */
+  int64_t graph_replays; /* fk_attn_decode_layers calls that replayed a cached CUDA graph
+                            without recording (nothing the launches depend on changed) */
 } fk_pool_stats;
 
 /* Per-step plan summary returned by fk_step_plan. */
@@ -222,9 +224,10 @@ int fk_ctx_copy_kv(fk_pool* dst, int64_t dst_ctx, const fk_pool* src, int64_t sr
  * generator.  k_scale multiplies K (stress). */
 int fk_synth_fill(fk_pool* pool, int64_t ctx, int64_t pos0, int64_t pos1,
                   uint64_t seed, float k_scale, void* stream);
-/* Q rows for the current plan: q_all[L][num_rows][H][D] bf16, row r keyed by
- * (leaf uid, leaf tokens at plan time, rank of r among rows on that leaf). */
-int fk_synth_queries(fk_pool* pool, uint64_t seed, void* q_all, void* stream);
+/* Q rows for the current plan: q_all[L][rows_cap][H][D] bf16 (rows_cap >=
+ * num_rows; 0 = num_rows), row r keyed by (leaf uid, leaf tokens at plan
+ * time, rank of r among rows on that leaf). */
+int fk_synth_queries(fk_pool* pool, uint64_t seed, void* q_all, int32_t rows_cap, void* stream);
 /* Append the step's synthetic K/V rows (keyed by (leaf uid, position)) for
  * all layers, using the targets of fk_step_commit. */
 int fk_synth_append(fk_pool* pool, uint64_t seed, float k_scale, void* stream);

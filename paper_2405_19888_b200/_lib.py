@@ -66,6 +66,7 @@ class PoolStats(ctypes.Structure):
         ("free_pages", c_int64),
         ("arena_bytes", c_int64),
         ("host_wait_ns", c_int64),
+        ("graph_replays", c_int64),
     ]
 
 
@@ -111,7 +112,7 @@ SIGNATURES = [
     ("fk_fill_kv", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     ("fk_ctx_copy_kv", c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_void_p]),
     ("fk_synth_fill", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_float, c_void_p]),
-    ("fk_synth_queries", c_int32, [c_void_p, c_uint64, c_void_p, c_void_p]),
+    ("fk_synth_queries", c_int32, [c_void_p, c_uint64, c_void_p, c_int32, c_void_p]),
     ("fk_synth_append", c_int32, [c_void_p, c_uint64, c_float, c_void_p]),
     ("fk_fnv1a64_u32", c_uint64, [POINTER(c_uint32), c_size_t, c_uint64]),
     ("fk_fnv1a64_chain", c_int32, [POINTER(c_uint32), POINTER(c_int64), c_int32, c_uint64, POINTER(c_uint64)]),

@@ -43,6 +43,7 @@ struct PlanDev {
   // tcgen05 schedule: chunks of consecutive tiles of one item, in unit
   // order; CTA b streams chunks [tc_cta_chunk0[b], tc_cta_chunk0[b + 1]).
   int tc_units, tc_ctas, tc_nchunks;
+  int tc_grid;                    // launched CTAs (>= tc_ctas, kept across steps: the extra CTAs exit at once)
   const int* tc_chunk_item;       // [tc_nchunks]
   const int* tc_chunk_tile0;      // [tc_nchunks] first tile within the item
   const int* tc_chunk_tile1;      // [tc_nchunks] end tile (exclusive)
@@ -163,8 +164,8 @@ cudaError_t launch_fill_kv(const ArenaDev& a, const int* pages_dev, int first_pa
                            int layer0, int nlayers, const void* k, const void* v, cudaStream_t s);
 cudaError_t launch_copy_pages(const ArenaDev& dst, const void* src_kv, long long src_num_pages, const int* pages_dev,
                               int npages, cudaStream_t s);
-cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p, int ps,
-                                 unsigned long long seed, void* q_all, cudaStream_t s);
+cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p, int ps, unsigned long long seed, void* q_all,
+                                 int rows_cap, cudaStream_t s);
 cudaError_t launch_synth_append(const ArenaDev& a, const PlanDev& p, int ps,
                                 unsigned long long seed, float k_scale, cudaStream_t s);
 

@@ -649,10 +649,10 @@ __global__ void fk_synth_fill_kernel(ArenaDev a, const int* __restrict__ pages, 
   }
 }
 
-__global__ void fk_synth_queries_kernel(ArenaDev a, int ps, unsigned long long seed, uint2* q_all) {
+__global__ void fk_synth_queries_kernel(ArenaDev a, int ps, unsigned long long seed, uint2* q_all, int B) {
   const PlanDev& p = fk_plan_c[ps];
   const int row = blockIdx.x, layer = blockIdx.y;
-  const int H = a.num_heads, B = p.num_rows;
+  const int H = a.num_heads;  // q_all: [layers][B (>= rows)][H][D]
   for (int i = threadIdx.x; i < H * 32; i += blockDim.x) {
     const int h = i / 32, j = i % 32;
     const unsigned long long key = synth_key(seed, kTagQ, p.row_uid[row], p.row_pos[row], layer, h);
@@ -752,9 +752,9 @@ cudaError_t launch_fill_kv(const ArenaDev& a, const int* pages_dev, int first_pa
 }
 
 cudaError_t launch_synth_queries(const ArenaDev& a, const PlanDev& p, int ps, unsigned long long seed, void* q_all,
-                                 cudaStream_t s) {
+                                 int rows_cap, cudaStream_t s) {
   dim3 grid(p.num_rows, a.num_layers);
-  fk_synth_queries_kernel<<<grid, 256, 0, s>>>(a, ps, seed, (uint2*)q_all);
+  fk_synth_queries_kernel<<<grid, 256, 0, s>>>(a, ps, seed, (uint2*)q_all, rows_cap);
   return cudaGetLastError();
 }
 

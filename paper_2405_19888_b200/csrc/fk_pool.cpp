@@ -47,10 +47,42 @@ int fail(int code, const char* fmt, ...) {
 
 struct Ctx {
   int64_t parent = -1;
+  Ctx* par = nullptr;  // the parent's node (unordered_map nodes never move; a parent outlives its children)
   int64_t tokens = 0;
   int32_t children = 0;
   std::vector<int64_t> logical;  // logical block ids (itertools.count order)
   std::vector<int32_t> phys;     // physical pages backing them
+  // planner state, valid while mark == the pool's plan epoch
+  uint32_t mark = 0;
+  int32_t fan = 0;      // rows whose chain holds this context
+  int32_t sidx = -1;    // index among the step's shared contexts, or -1
+  int32_t rank = 0;     // rows planned so far with this context as their leaf
+  bool shared = false;  // fan-out >= 2 with tokens (dedup mode)
+};
+
+// Planner scratch, reused from step to step (fk_step_plan).
+struct PlanItem {
+  int sh, split, q0, nq, head, page0, npages, ntok, units;
+};
+struct PlanShared {
+  Ctx* ctx;
+  int nrows = 0;   // descendant rows (at srows[row0 ..], row order)
+  int row0 = 0;
+  int seen = 0;
+  bool tc = false;
+  int splits = 1;  // mma path: head-independent page splits
+  int page_off = 0;
+  int q_off = 0;
+};
+struct PlanScratch {
+  std::vector<Ctx*> chain, order;
+  std::vector<int32_t> chain_off, srows, pages, page_ntok, qrows, it_unit_off, ch_item, ch_t0, ch_t1, cta_chunk0,
+      it_first_chunk, pieces_of, rs_off, rs_sh, rs_qb, row_head_base, base_at, it_qslot_off, qslot, row_priv_off,
+      row_priv_np, row_unit_off, page_row, chunk_start, row_head_count, rh_chunk0, srow_e, acc;
+  std::vector<int64_t> leaf_tokens_pre, cut, cut0, qb_off, row_uid, row_pos;
+  int64_t n_chunks = 0;  // chunk_start holds n_chunks + 1 entries in use
+  std::vector<PlanShared> shared;
+  std::vector<PlanItem> items;
 };
 
 // One plan slot: pinned staging + device copy + the event that guards reuse.
@@ -94,7 +126,25 @@ struct DeviceGuard {
 // A step's attention launches as one CUDA graph: captured the first time a
 // launch structure is seen, afterwards only its kernel-node parameters are
 // updated (the structure -- functions, grids, PDL edges -- stays).
+// Everything the recorded launches of fk_attn_decode_layers depend on
+// (functions, grids, argument bytes): when it repeats, the cached graph is
+// replayed without re-recording.  FK_DEBUG_GRAPH_CHECK=1 records anyway and
+// fails if the launches differ (tests/test_gpu_manager.py).
+struct ReplayKey {
+  const void* kv;
+  int64_t num_pages;
+  const void *part_o, *part_ml, *tick;
+  size_t part_cap;
+  const void *q, *out, *out_f32;
+  int64_t q_stride, out_stride, f32_stride;
+  int32_t tc_begin, num_items, tc_grid, tc_ctas, priv_any, priv_wpc, priv_grid, num_sms, pdl, launch_order, plan_slot;
+  int32_t pad;
+};
+static_assert(sizeof(ReplayKey) % 8 == 0, "ReplayKey is compared bytewise");
+
 struct GraphCache {
+  ReplayKey key{};
+  bool key_ok = false;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::vector<cudaGraphNode_t> nodes;   // kernel nodes in launch order
@@ -107,6 +157,7 @@ struct GraphCache {
     graph = nullptr;
     nodes.clear();
     shape.clear();
+    key_ok = false;
   }
 };
 
@@ -141,7 +192,8 @@ struct fk_pool {
   int64_t use_graph = 1;  // fk_attn_decode_layers replays a CUDA graph
   std::map<std::tuple<int32_t, int32_t, cudaStream_t, int>, GraphCache> graphs;  // (layer0, nlayers, stream, slot/half)
   fk::RecBuf rec_buf;  // launches recorded by fk_attn_decode_layers (storage reused)
-  std::vector<int32_t> scratch_chunks;  // planner scratch (capacity reused across steps)
+  PlanScratch ps;                   // planner scratch (capacity reused across steps)
+  uint32_t plan_epoch = 0;
   int64_t min_split_pages = 8;
   int64_t corun = 1;             // tcgen05 prefix and private stream share the SMs spatially
   int64_t prefix_rate_pct = 50;  // prefix KV bytes/s per SM relative to the private stream's (measured optimum, headline)
@@ -162,6 +214,7 @@ struct fk_pool {
   size_t part_cap = 0;     // entries (rows*slots*H) per half
   int launch_parity = 0;   // which half of the partials the next fk_attn_decode uses
   int64_t host_wait_ns = 0;  // time fk_step_plan blocked on the GPU (plan slot reuse)
+  int64_t graph_replays = 0; // fk_attn_decode_layers calls replayed without recording
   int64_t skip_merge = 0;    // FK_OPT_DEBUG_SKIP_MERGE (diagnostic)
   int64_t append_first = 0;  // FK_OPT_APPEND_FIRST: fk_step_plan grows the rows first (attend own token)
   bool plan_grew = false;    // the current plan already did the step's growth (fk_step_grow returns it)
@@ -169,6 +222,8 @@ struct fk_pool {
   unsigned* tick = nullptr;  // device: private chunk tickets, one counter per partial half
   int plan_base = -1;        // first of this pool's two __constant__ plan slots (fk_plan_c)
   int priv_grid = 0;         // private grid (CTAs) of the current plan
+  int tc_grid = 0;           // tcgen05 prefix grid, kept while the plan's CTA count moves a little
+  uint64_t plan_digest = 0;  // FK_DEBUG_PLAN_DIGEST: hash of the last plan's arrays
 
   ArenaDev arena() const {
     ArenaDev a;
@@ -186,6 +241,33 @@ struct fk_pool {
 namespace {
 
 int64_t blocks_for(int64_t tokens, int64_t bs) { return (tokens + bs - 1) / bs; }
+
+// FNV-1a over every array and scalar a plan uploads (FK_DEBUG_PLAN_DIGEST=1):
+// pins the planner's output across rewrites (tests/test_plan.py).
+bool plan_digest_on() {
+  static const bool on = getenv("FK_DEBUG_PLAN_DIGEST") != nullptr;
+  return on;
+}
+struct PlanDigest {
+  uint64_t h = 0xcbf29ce484222325ull;
+  void bytes(const void* d, size_t n) {
+    const unsigned char* b = (const unsigned char*)d;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+  }
+  void scalars(std::initializer_list<int64_t> xs) {
+    for (int64_t x : xs) bytes(&x, 8);
+  }
+  template <class T>
+  void span(const T* v, int64_t n) {
+    bytes(&n, 8);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t y = (int64_t)v[i];
+      bytes(&y, 8);
+    }
+  }
+  template <class T>
+  void vec(const std::vector<T>& v) { span(v.data(), (int64_t)v.size()); }
+};
 
 int encode_tmap(fk_pool* p) {
   p->tmap_ok = false;
@@ -256,21 +338,26 @@ int reserve_pages(fk_pool* p, int64_t pages) {
   return encode_tmap(p);
 }
 
-int ensure_scratch(fk_pool* p, int rows, int slots) {
+int ensure_scratch(fk_pool* p, int rows, int slots, cudaStream_t st) {
   const size_t H = p->desc.num_heads, D = p->desc.head_dim;
   const size_t need = (size_t)std::max(rows, 1) * std::max(slots, 1) * H;
   if (need > p->part_cap) {
-    // headroom: max_slots moves by one as suffixes cross page boundaries, and
-    // every reallocation is a device-wide sync (cudaFree)
-    size_t cap = std::max(need + need / 2, p->part_cap * 2);
-    if (p->part_o) FK_CUDA(cudaFree(p->part_o));
-    if (p->part_ml) FK_CUDA(cudaFree(p->part_ml));
+    // headroom: max_slots moves by one as suffixes cross page boundaries.
+    // Stream-ordered (re)allocation on the plan's stream -- the stream the
+    // step's kernels run on -- so growing the partials never syncs the device
+    // (a cudaFree would wait for every engine sharing the GPU).
+    // (first allocation: room for 64 rows x 16 slots, so a batch that builds
+    // up request by request does not reallocate -- and update every graph
+    // node -- at every few rows)
+    size_t cap = std::max({need + need / 2, p->part_cap * 2, (size_t)64 * 16 * H});
+    if (p->part_o) FK_CUDA(cudaFreeAsync(p->part_o, st));
+    if (p->part_ml) FK_CUDA(cudaFreeAsync(p->part_ml, st));
     p->part_o = nullptr;
     p->part_ml = nullptr;
     // two halves: consecutive fk_attn_decode launches alternate, so a layer's
     // kernels may start (PDL) while the previous layer's merge still reads
-    FK_CUDA(cudaMalloc(&p->part_o, 2 * cap * D * sizeof(float)));
-    FK_CUDA(cudaMalloc(&p->part_ml, 2 * cap * sizeof(float2)));
+    FK_CUDA(cudaMallocAsync((void**)&p->part_o, 2 * cap * D * sizeof(float), st));
+    FK_CUDA(cudaMallocAsync((void**)&p->part_ml, 2 * cap * sizeof(float2), st));
     p->part_cap = cap;
   }
   return FK_OK;
@@ -423,6 +510,7 @@ int fk_pool_stats_get(const fk_pool* p, fk_pool_stats* out) {
   out->free_pages = (int64_t)p->free_pages.size();
   out->arena_bytes = (int64_t)p->arena_bytes;
   out->host_wait_ns = p->host_wait_ns;
+  out->graph_replays = p->graph_replays;
   return FK_OK;
 }
 
@@ -465,6 +553,7 @@ int fk_ctx_create(fk_pool* p, int64_t ctx, int64_t parent) {
   }
   Ctx c;
   c.parent = parent >= 0 ? parent : -1;
+  c.par = parent >= 0 ? &p->ctxs.find(parent)->second : nullptr;
   p->ctxs.emplace(ctx, std::move(c));
   return FK_OK;
 }
@@ -580,42 +669,52 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int64_t H = p->desc.num_heads;
 
   PT(T0);
+  // Everything below reuses the pool's scratch (no per-step allocation once
+  // warm) and reaches contexts through pointers (one hash lookup per leaf);
+  // tests/test_plan.py::test_plan_digests_pinned holds the output to the
+  // round-1 planner's bit for bit.
+  PlanScratch& S = p->ps;
+  const uint32_t epoch = ++p->plan_epoch;
   // chains leaf -> root, fan-out per context (engine.py:476-482 walk)
-  std::vector<std::vector<int64_t>> chain(B);
-  std::unordered_map<int64_t, int> fan;
-  std::vector<int64_t> order;  // unique contexts, first-seen (row order, leaf->root)
+  std::vector<Ctx*>& chain = S.chain;
+  std::vector<int32_t>& chain_off = S.chain_off;
+  std::vector<Ctx*>& order = S.order;  // unique contexts, first-seen (row order, leaf->root)
+  chain.clear();
+  order.clear();
+  chain_off.resize(B + 1);
   for (int r = 0; r < B; ++r) {
-    int64_t cur = leaves[r];
-    if (!p->ctxs.count(cur)) return fail(FK_UNKNOWN_CONTEXT, "unknown leaf context %lld", (long long)cur);
-    while (cur >= 0) {
-      auto ci = p->ctxs.find(cur);
-      if (ci == p->ctxs.end()) break;  // engine.py:482 contexts.get() -> None
-      chain[r].push_back(cur);
-      auto f = fan.find(cur);
-      if (f == fan.end()) {
-        fan.emplace(cur, 1);
-        order.push_back(cur);
+    chain_off[r] = (int32_t)chain.size();
+    auto li = p->ctxs.find(leaves[r]);
+    if (li == p->ctxs.end()) return fail(FK_UNKNOWN_CONTEXT, "unknown leaf context %lld", (long long)leaves[r]);
+    for (Ctx* c = &li->second; c; c = c->par) {
+      chain.push_back(c);
+      if (c->mark != epoch) {
+        c->mark = epoch;
+        c->fan = 1;
+        c->sidx = -1;
+        c->rank = 0;
+        order.push_back(c);
       } else {
-        f->second += 1;
+        c->fan += 1;
       }
-      cur = ci->second.parent;
     }
   }
-  int64_t shared_tokens = 0, private_tokens = 0;
+  chain_off[B] = (int32_t)chain.size();
   auto count_tokens = [&]() {
     int64_t n = 0;
     if (dedup) {
-      for (int64_t c : order) n += p->ctxs[c].tokens;
+      for (const Ctx* c : order) n += c->tokens;
     } else {
-      for (int r = 0; r < B; ++r)
-        for (int64_t c : chain[r]) n += p->ctxs[c].tokens;
+      for (const Ctx* c : chain) n += c->tokens;
     }
     return n;
   };
+  int64_t shared_tokens = 0, private_tokens = 0;
   // the reference's count, before the step's growth (engine.py:416-417)
   const int64_t batch_tokens = count_tokens();
-  std::vector<int64_t> leaf_tokens_pre(B);
-  for (int r = 0; r < B; ++r) leaf_tokens_pre[r] = p->ctxs[leaves[r]].tokens;
+  std::vector<int64_t>& leaf_tokens_pre = S.leaf_tokens_pre;
+  leaf_tokens_pre.resize(B);
+  for (int r = 0; r < B; ++r) leaf_tokens_pre[r] = chain[chain_off[r]]->tokens;
   // FK_OPT_APPEND_FIRST: the step's one-token growth happens now, in row
   // (gens) order with the sequential OOM rule of fk_step_grow, and the
   // kernels' spans include the new token (a decoder attends to its own key)
@@ -624,7 +723,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     p->grow_pos.assign(B, -1);
     p->grow_ids.assign(B, -1);
     for (int r = 0; r < B; ++r) {
-      const int64_t pos = p->ctxs[leaves[r]].tokens;
+      const int64_t pos = chain[chain_off[r]]->tokens;
       int64_t n = 0, id = -1;
       const int rc = fk_ctx_grow(p, leaves[r], pos + 1, &id, 1, &n);
       if (rc == FK_OUT_OF_MEMORY) continue;
@@ -635,73 +734,83 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     p->plan_grew = true;
   }
   const int64_t streamed_tokens = p->append_first ? count_tokens() : batch_tokens;
-  auto is_shared = [&](int64_t c) { return dedup && fan[c] >= 2 && p->ctxs[c].tokens > 0; };
+  // (after the growth: a leaf two generations share becomes shared once it has a token)
+  for (Ctx* c : order) c->shared = dedup && c->fan >= 2 && c->tokens > 0;
 
   PT(T1);
   // ---- shared contexts (K2 work) --------------------------------------------
-  struct Shared {
-    int64_t ctx;
-    std::vector<int> rows;  // descendant rows, row order
-    bool tc;
-    int splits = 1;         // mma path: head-independent page splits
-    int page_off = 0;
-    int q_off = 0;
-  };
-  std::vector<Shared> shared;
-  std::unordered_map<int64_t, int> shared_idx;
-  for (int64_t c : order) {
-    if (!is_shared(c)) continue;
-    shared_idx[c] = (int)shared.size();
-    Shared s;
+  std::vector<PlanShared>& shared = S.shared;
+  shared.clear();
+  for (Ctx* c : order) {
+    if (!c->shared) continue;
+    c->sidx = (int32_t)shared.size();
+    PlanShared s;
     s.ctx = c;
-    s.tc = p->tc_min_fanout > 0 && fan[c] >= p->tc_min_fanout;
-    shared.push_back(std::move(s));
-    shared_tokens += p->ctxs[c].tokens;
+    s.tc = p->tc_min_fanout > 0 && c->fan >= p->tc_min_fanout;
+    s.nrows = 0;
+    shared.push_back(s);
+    shared_tokens += c->tokens;
+  }
+  const int nsh_real = (int)shared.size();
+  // descendant rows of each shared context, row order (counted, then placed)
+  std::vector<int32_t>& srows = S.srows;
+  for (const Ctx* c : chain)
+    if (c->sidx >= 0) shared[c->sidx].nrows += 1;
+  {
+    int32_t acc = 0;
+    for (auto& s : shared) {
+      s.row0 = acc;
+      acc += s.nrows;
+      s.nrows = 0;
+    }
+    srows.resize(acc);
   }
   for (int r = 0; r < B; ++r)
-    for (int64_t c : chain[r]) {
-      auto si = shared_idx.find(c);
-      if (si != shared_idx.end()) shared[si->second].rows.push_back(r);
+    for (int32_t k = chain_off[r]; k < chain_off[r + 1]; ++k) {
+      const int32_t si = chain[k]->sidx;
+      if (si >= 0) srows[shared[si].row0 + shared[si].nrows++] = r;
     }
-  std::vector<int32_t> pages, page_ntok, qrows;
+  std::vector<int32_t>& pages = S.pages;
+  std::vector<int32_t>& page_ntok = S.page_ntok;
+  std::vector<int32_t>& qrows = S.qrows;
+  pages.clear();
+  page_ntok.clear();
+  qrows.clear();
   for (auto& s : shared) {
-    const Ctx& c = p->ctxs[s.ctx];
+    const Ctx& c = *s.ctx;
     s.page_off = (int)pages.size();
     for (size_t k = 0; k < c.phys.size(); ++k) {
       pages.push_back(c.phys[k]);
       page_ntok.push_back((int32_t)std::min<int64_t>(kPage, c.tokens - (int64_t)k * kPage));
     }
     s.q_off = (int)qrows.size();
-    for (int r : s.rows) qrows.push_back(r);
+    qrows.insert(qrows.end(), srows.begin() + s.row0, srows.begin() + s.row0 + s.nrows);
   }
   // mma split policy: ~one wave of CTAs over the mma-class prefix work
   {
     int64_t total = 0;
     for (auto& s : shared)
-      if (!s.tc)
-        total += (int64_t)p->ctxs[s.ctx].phys.size() * ((s.rows.size() + kMmaQBlock - 1) / kMmaQBlock) * H;
+      if (!s.tc) total += (int64_t)s.ctx->phys.size() * ((s.nrows + kMmaQBlock - 1) / kMmaQBlock) * H;
     const int64_t target = p->prefix_target_ctas > 0 ? p->prefix_target_ctas : p->num_sms;
     const int64_t per = std::max<int64_t>(p->min_split_pages, (total + target - 1) / std::max<int64_t>(target, 1));
     const int64_t ps = (per + kMmaTilePages - 1) / kMmaTilePages * kMmaTilePages;
     for (auto& s : shared) {
-      const int64_t np = (int64_t)p->ctxs[s.ctx].phys.size();
+      const int64_t np = (int64_t)s.ctx->phys.size();
       s.splits = s.tc ? 1 : (int)std::max<int64_t>(1, (np + ps - 1) / ps);
     }
   }
   // items: mma (ctx, split, qblock, head) then tcgen05 (ctx, qblock, head)
-  struct Item {
-    int sh, split, q0, nq, head, page0, npages, ntok, units;
-  };
-  std::vector<Item> items;
+  std::vector<PlanItem>& items = S.items;
+  items.clear();
   int num_mma = 0, num_tc = 0;
   for (int pass = 0; pass < 2; ++pass)
-    for (int si = 0; si < (int)shared.size(); ++si) {
-      const Shared& s = shared[si];
+    for (int si = 0; si < nsh_real; ++si) {
+      const PlanShared& s = shared[si];
       if ((int)s.tc != pass) continue;
-      const Ctx& c = p->ctxs[s.ctx];
+      const Ctx& c = *s.ctx;
       const int np = (int)c.phys.size();
       const int qb = s.tc ? kTcQBlock : kMmaQBlock;
-      const int nq = (int)s.rows.size();
+      const int nq = s.nrows;
       const int psr = s.tc ? np : ((np + s.splits - 1) / s.splits + kMmaTilePages - 1) / kMmaTilePages * kMmaTilePages;
       // items are (query block, head) with the head innermost: with more than
       // one query block (> 128 forks) the unit list is k identical groups,
@@ -712,7 +821,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
         const int64_t t1 = std::min<int64_t>(c.tokens, (int64_t)p1 * kPage);
         for (int q0 = 0; q0 < nq; q0 += qb)
           for (int h = 0; h < H; ++h) {
-            Item it;
+            PlanItem it;
             it.sh = si;
             it.split = sp;
             it.q0 = q0;
@@ -729,7 +838,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     }
   PT(T2);
   // tcgen05 stream-K: tile units of all tc items over <= one wave of CTAs
-  std::vector<int32_t> it_unit_off(items.size(), 0);
+  std::vector<int32_t>& it_unit_off = S.it_unit_off;
+  it_unit_off.assign(items.size(), 0);
   int64_t tc_units = 0;
   for (size_t i = num_mma; i < items.size(); ++i) {
     it_unit_off[i] = (int32_t)tc_units;
@@ -740,9 +850,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // S - X, launched back to back (PDL) so both stream HBM at once.  X splits
   // the SMs in proportion to each side's bytes over its per-SM rate.
   int64_t priv_tok_heads = 0;
-  for (int r = 0; r < B; ++r)
-    for (int64_t c : chain[r])
-      if (!is_shared(c)) priv_tok_heads += p->ctxs[c].tokens * H;
+  for (const Ctx* c : chain)
+    if (!c->shared) priv_tok_heads += c->tokens * H;
   // a 128-query block costs the softmax ~4/3 of a <= 64-query block per tile
   // (the 16-lane layout only covers fan-outs <= 64; measured 2.5 vs 1.9 us)
   double tc_tok_heads = 0.0;
@@ -760,8 +869,16 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // epilogue per chunk costs more than the balance gains -- removed.)
   // Chunks never cross an item and are listed in unit order (an item's
   // chunks are contiguous: chunk - it_first_chunk = piece index).
-  std::vector<int32_t> ch_item, ch_t0, ch_t1, cta_chunk0;
-  std::vector<int32_t> it_first_chunk(items.size(), 0);
+  std::vector<int32_t>& ch_item = S.ch_item;
+  std::vector<int32_t>& ch_t0 = S.ch_t0;
+  std::vector<int32_t>& ch_t1 = S.ch_t1;
+  std::vector<int32_t>& cta_chunk0 = S.cta_chunk0;
+  std::vector<int32_t>& it_first_chunk = S.it_first_chunk;
+  ch_item.clear();
+  ch_t0.clear();
+  ch_t1.clear();
+  cta_chunk0.clear();
+  it_first_chunk.assign(items.size(), 0);
   int64_t tc_ctas = 0;
   bool tc_l2_share = false;
   if (tc_units > 0) {
@@ -826,14 +943,16 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     // time and all but the first hit L2 (the loads then keep the default
     // L2 policy: PlanDev::tc_l2_share).
     int64_t mirror_k = 0;
-    if (shared.size() == 1 && shared[0].tc && shared[0].splits == 1) {
-      const int64_t k = ((int64_t)shared[0].rows.size() + kTcQBlock - 1) / kTcQBlock;
+    if (nsh_real == 1 && shared[0].tc && shared[0].splits == 1) {
+      const int64_t k = ((int64_t)shared[0].nrows + kTcQBlock - 1) / kTcQBlock;
       if (k >= 2 && X >= 2 * k && (int64_t)(items.size() - num_mma) == k * H && tc_units % k == 0) mirror_k = k;
     }
-    std::vector<int64_t> cut;
+    std::vector<int64_t>& cut = S.cut;
+    cut.clear();
     if (mirror_k) {
       const int64_t ug = tc_units / mirror_k, xg = X / mirror_k;
-      std::vector<int64_t> c0;
+      std::vector<int64_t>& c0 = S.cut0;
+      c0.clear();
       split(0, ug, xg, c0);
       c0.push_back(ug);
       for (int64_t g = 0; g < mirror_k; ++g)
@@ -870,70 +989,99 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   PT(T3);
   // per (shared ctx, qblock, head): pieces contributed to each of its rows
   // (dense tables: this runs every step on the host)
-  const int64_t nsh = std::max<int64_t>((int64_t)shared.size(), 1);
-  std::vector<int64_t> qb_off(shared.size() + 1, 0);  // first (qblock, head) slot of each shared ctx
+  std::vector<int64_t>& qb_off = S.qb_off;  // first (qblock, head) slot of each shared ctx
+  qb_off.assign(shared.size() + 1, 0);
   for (size_t si = 0; si < shared.size(); ++si) {
     const int qbs = shared[si].tc ? kTcQBlock : kMmaQBlock;
-    qb_off[si + 1] = qb_off[si] + (int64_t)((shared[si].rows.size() + qbs - 1) / qbs) * H;
+    qb_off[si + 1] = qb_off[si] + (int64_t)((shared[si].nrows + qbs - 1) / qbs) * H;
   }
-  std::vector<int32_t> pieces_of(std::max<int64_t>(qb_off.back(), 1), 0);
+  std::vector<int32_t>& pieces_of = S.pieces_of;
+  pieces_of.assign(std::max<int64_t>(qb_off.back(), 1), 0);
   for (size_t i = 0; i < items.size(); ++i) {
-    const Item& it = items[i];
+    const PlanItem& it = items[i];
     const int qb = it.q0 / (shared[it.sh].tc ? kTcQBlock : kMmaQBlock);
     pieces_of[qb_off[it.sh] + (int64_t)qb * H + it.head] += item_pieces(i);
   }
-  // each row's shared contexts root -> leaf, with its query block in each
-  std::vector<std::vector<std::pair<int, int>>> row_shared(B);
+  // each row's shared contexts root -> leaf with its query block in each
+  // (rs[rs_off[r] ..]), and the slot base of each at every head
+  std::vector<int32_t>& rs_off = S.rs_off;
+  std::vector<int32_t>& rs_sh = S.rs_sh;
+  std::vector<int32_t>& rs_qb = S.rs_qb;
+  std::vector<int32_t>& srow_e = S.srow_e;  // rs entry of each (shared ctx, row) in srows order
+  rs_off.resize(B + 1);
+  rs_sh.clear();
+  rs_qb.clear();
   {
-    std::vector<int32_t> pos(shared.size() * (size_t)B, -1);  // [shared][row] -> position in s.rows
-    for (size_t si = 0; si < shared.size(); ++si)
-      for (size_t j = 0; j < shared[si].rows.size(); ++j) pos[si * B + shared[si].rows[j]] = (int32_t)j;
-    for (int r = 0; r < B; ++r)
-      for (auto ci = chain[r].rbegin(); ci != chain[r].rend(); ++ci) {
-        auto si = shared_idx.find(*ci);
-        if (si == shared_idx.end()) continue;
-        const Shared& sc = shared[si->second];
-        row_shared[r].emplace_back(si->second, pos[(size_t)si->second * B + r] / (sc.tc ? kTcQBlock : kMmaQBlock));
+    // position of each row among a shared context's rows: the rows are
+    // placed in row order, so a running counter per context gives it
+    for (auto& s : shared) s.seen = 0;
+    srow_e.resize(srows.size());
+    for (int r = 0; r < B; ++r) {
+      rs_off[r] = (int32_t)rs_sh.size();
+      for (int32_t k = chain_off[r + 1] - 1; k >= chain_off[r]; --k) {  // root -> leaf
+        const int32_t si = chain[k]->sidx;
+        if (si < 0) continue;
+        PlanShared& sc = shared[si];
+        srow_e[sc.row0 + sc.seen] = (int32_t)rs_sh.size();
+        rs_sh.push_back(si);
+        rs_qb.push_back(sc.seen++ / (sc.tc ? kTcQBlock : kMmaQBlock));
       }
+    }
+    rs_off[B] = (int32_t)rs_sh.size();
   }
   // slot bases: per (row, head) walk the shared chain root -> leaf
-  std::vector<int32_t> row_head_base(std::max<int64_t>(B * H, 1), 0);
-  std::vector<int32_t> base_at((size_t)std::max<int64_t>(B * H * nsh, 1), 0);  // [(row * H + h) * nsh + sh]
+  std::vector<int32_t>& row_head_base = S.row_head_base;
+  std::vector<int32_t>& base_at = S.base_at;  // [rs entry][H]
+  row_head_base.assign(std::max<int64_t>((int64_t)B * H, 1), 0);
+  base_at.resize(std::max<size_t>(rs_sh.size() * (size_t)H, 1));
+  std::vector<int32_t>& acc = S.acc;
+  acc.resize(H);
   for (int r = 0; r < B; ++r) {
-    for (int h = 0; h < H; ++h) {
-      int acc = 0;
-      for (const auto& sq : row_shared[r]) {
-        base_at[((int64_t)r * H + h) * nsh + sq.first] = acc;
-        acc += pieces_of[qb_off[sq.first] + (int64_t)sq.second * H + h];
+    std::fill(acc.begin(), acc.end(), 0);
+    for (int32_t e = rs_off[r]; e < rs_off[r + 1]; ++e) {
+      const int32_t* po = pieces_of.data() + qb_off[rs_sh[e]] + (int64_t)rs_qb[e] * H;
+      int32_t* ba = base_at.data() + (size_t)e * H;
+      for (int h = 0; h < H; ++h) {
+        ba[h] = acc[h];
+        acc[h] += po[h];
       }
-      row_head_base[(int64_t)r * H + h] = acc;
     }
+    std::copy(acc.begin(), acc.end(), row_head_base.begin() + (int64_t)r * H);
   }
-  std::vector<int32_t> it_qslot_off(items.size()), qslot;
-  for (size_t i = 0; i < items.size(); ++i) {
-    const Item& it = items[i];
-    const Shared& sc = shared[it.sh];
-    it_qslot_off[i] = (int32_t)qslot.size();
-    for (int j = 0; j < it.nq; ++j) {
-      const int r = sc.rows[it.q0 + j];
-      qslot.push_back(base_at[((int64_t)r * H + it.head) * nsh + it.sh] + ((int)i < num_mma ? it.split : 0));
-    }
+  std::vector<int32_t>& it_qslot_off = S.it_qslot_off;
+  std::vector<int32_t>& qslot = S.qslot;
+  it_qslot_off.resize(items.size());
+  {
+    size_t nq_all = 0;
+    for (const PlanItem& it : items) nq_all += it.nq;
+    qslot.resize(nq_all);
+  }
+  for (size_t i = 0, o = 0; i < items.size(); ++i) {
+    const PlanItem& it = items[i];
+    const int32_t* re = srow_e.data() + shared[it.sh].row0 + it.q0;
+    const int32_t* ba = base_at.data() + it.head;
+    it_qslot_off[i] = (int32_t)o;
+    const int add = (int)i < num_mma ? it.split : 0;
+    for (int j = 0; j < it.nq; ++j) qslot[o + j] = ba[(size_t)re[j] * H] + add;
+    o += it.nq;
   }
 
   PT(T4);
   // ---- private streams (K3 work) ----------------------------------------------
-  std::vector<int32_t> row_priv_off(B), row_priv_np(B);
+  std::vector<int32_t>& row_priv_off = S.row_priv_off;
+  std::vector<int32_t>& row_priv_np = S.row_priv_np;
+  row_priv_off.resize(B);
+  row_priv_np.resize(B);
   for (int r = 0; r < B; ++r) {
     row_priv_off[r] = (int32_t)pages.size();
-    for (auto ci = chain[r].rbegin(); ci != chain[r].rend(); ++ci) {  // root -> leaf
-      if (is_shared(*ci)) continue;
-      const Ctx& c = p->ctxs[*ci];
-      if (c.tokens <= 0) continue;
+    for (int32_t k = chain_off[r + 1] - 1; k >= chain_off[r]; --k) {  // root -> leaf
+      const Ctx& c = *chain[k];
+      if (c.shared || c.tokens <= 0) continue;
       private_tokens += c.tokens;
-      for (size_t k = 0; k < c.phys.size(); ++k) {
-        const int64_t nt = std::min<int64_t>(kPage, c.tokens - (int64_t)k * kPage);
+      for (size_t j = 0; j < c.phys.size(); ++j) {
+        const int64_t nt = std::min<int64_t>(kPage, c.tokens - (int64_t)j * kPage);
         if (nt <= 0) break;
-        pages.push_back(c.phys[k]);
+        pages.push_back(c.phys[j]);
         page_ntok.push_back((int32_t)nt);
       }
     }
@@ -942,10 +1090,14 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // private units (head, flat private entry), head-major
   const int64_t priv_base = B > 0 ? row_priv_off[0] : (int64_t)pages.size();
   const int64_t NPT = (int64_t)pages.size() - priv_base;
-  std::vector<int32_t> row_unit_off(std::max(B, 1), 0), page_row(std::max<int64_t>(NPT, 1), 0);
+  std::vector<int32_t>& row_unit_off = S.row_unit_off;
+  std::vector<int32_t>& page_row = S.page_row;
+  row_unit_off.assign(std::max(B, 1), 0);
+  page_row.resize(std::max<int64_t>(NPT, 1));
+  page_row[0] = 0;
   for (int r = 0; r < B; ++r) {
     row_unit_off[r] = (int32_t)(row_priv_off[r] - priv_base);
-    for (int k = 0; k < row_priv_np[r]; ++k) page_row[row_unit_off[r] + k] = r;
+    std::fill_n(page_row.begin() + row_unit_off[r], row_priv_np[r], r);
   }
   const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
@@ -958,50 +1110,58 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int64_t wpc = p->priv_wpc;
   const int64_t w_active = priv_sms * wpc;
   // size(pos) = clamp(ceil((U - pos) / 2W), min_chunk, 32), generated run by
-  // run: one division per distinct size, then plain adds (this runs every step)
-  std::vector<int32_t>& chunk_start = p->scratch_chunks;
-  chunk_start.clear();
+  // run: one division per distinct size, then plain stores (this runs every step)
+  std::vector<int32_t>& chunk_start = S.chunk_start;
   {
     const int64_t w2 = 2 * w_active, mc = p->priv_min_chunk;
-    int64_t pos = 0;
+    // upper bound of the chunk count: every chunk but the last has >= mc
+    // units (grown only: a resize down and up again would zero-fill)
+    const size_t bound = (size_t)(U / std::max<int64_t>(mc, 1) + 2);
+    if (chunk_start.size() < bound) chunk_start.resize(bound);
+    int32_t* cs = chunk_start.data();
+    int64_t n = 0, pos = 0;
     while (pos < U) {
       const int64_t R = U - pos;
       int64_t sz = std::min<int64_t>(std::max<int64_t>((R + w2 - 1) / w2, mc), kPrivMaxChunk);
       // the size holds while ceil(R / 2W) stays >= sz (capped) or == sz
       const int64_t floor_r = sz > mc ? (sz - 1) * w2 : 0;  // R must stay above this
       int64_t k = sz > mc ? (R - floor_r + sz - 1) / sz : (R + sz - 1) / sz;
-      for (; k > 0 && pos < U; --k) {
-        chunk_start.push_back((int32_t)pos);
-        pos += std::min<int64_t>(sz, U - pos);
-      }
+      // k chunks of sz units from pos, the last one cut at U
+      k = std::min<int64_t>(k, (R + sz - 1) / sz);
+      const int32_t p0 = (int32_t)pos, s32 = (int32_t)sz;
+      for (int32_t j = 0; j < (int32_t)k; ++j) cs[n + j] = p0 + j * s32;
+      n += k;
+      pos = std::min<int64_t>(U, pos + k * sz);
     }
+    cs[n] = (int32_t)U;
+    S.n_chunks = n;
   }
-  const int64_t nchunks = (int64_t)chunk_start.size();
-  chunk_start.push_back((int32_t)U);
+  const int64_t nchunks = S.n_chunks;
   // launched first (order 1) the private grid must leave the prefix its SMs
   // The grid is the SM count whatever the work (warps without a chunk exit at
   // once), so its launch stays the same from step to step.
   const int64_t grid_ctas = (corun && p->launch_order == 1) ? priv_sms : p->num_sms;
   const int64_t G = grid_ctas * wpc;
   // items (row, head) are contiguous unit ranges in unit order (head-major,
-  // rows by their offset), so one forward sweep finds every item's chunks
-  std::vector<int32_t> row_head_count(std::max<int64_t>(B * H, 1), 0), rh_chunk0(std::max<int64_t>(B * H, 1), 0);
+  // rows in row order: their offsets only grow), so one forward sweep finds
+  // every item's chunks
+  std::vector<int32_t>& row_head_count = S.row_head_count;
+  std::vector<int32_t>& rh_chunk0 = S.rh_chunk0;
+  row_head_count.assign(std::max<int64_t>((int64_t)B * H, 1), 0);
+  rh_chunk0.assign(std::max<int64_t>((int64_t)B * H, 1), 0);
   int max_slots = 1;
   {
-    std::vector<int> rows_by_off(B);
-    for (int r = 0; r < B; ++r) rows_by_off[r] = r;
-    std::sort(rows_by_off.begin(), rows_by_off.end(),
-              [&](int x, int y) { return row_unit_off[x] < row_unit_off[y]; });
+    const int32_t* cs = chunk_start.data();
     int64_t c = 0;  // chunk holding the current unit
     for (int64_t h = 0; h < H; ++h)
-      for (int r : rows_by_off) {
+      for (int r = 0; r < B; ++r) {
         const int64_t np = row_priv_np[r];
         int pieces = 0;
         if (np > 0) {
           const int64_t a0 = h * NPT + row_unit_off[r], b0 = a0 + np;
-          while (chunk_start[c + 1] <= a0) ++c;
+          while (cs[c + 1] <= a0) ++c;
           const int64_t c0 = c;
-          while (chunk_start[c + 1] <= b0 - 1) ++c;
+          while (cs[c + 1] <= b0 - 1) ++c;
           rh_chunk0[r * H + h] = (int32_t)c0;
           pieces = (int)(c - c0 + 1);
         }
@@ -1012,18 +1172,17 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   PT(T6);
   // synthetic keys: (leaf uid, leaf tokens at plan time + rank << 40)
-  std::vector<int64_t> row_uid(B), row_pos(B);
+  std::vector<int64_t>& row_uid = S.row_uid;
+  std::vector<int64_t>& row_pos = S.row_pos;
+  row_uid.resize(B);
+  row_pos.resize(B);
   p->plan_leaves.assign(leaves, leaves + B);
   p->plan_leaf_tokens.resize(B);
-  {
-    std::unordered_map<int64_t, int> rank;
-    for (int r = 0; r < B; ++r) {
-      const int64_t leaf = leaves[r];
-      const int k = rank[leaf]++;
-      row_uid[r] = leaf;
-      p->plan_leaf_tokens[r] = leaf_tokens_pre[r];
-      row_pos[r] = leaf_tokens_pre[r] + ((int64_t)k << 40);
-    }
+  for (int r = 0; r < B; ++r) {
+    const int k = chain[chain_off[r]]->rank++;
+    row_uid[r] = leaves[r];
+    p->plan_leaf_tokens[r] = leaf_tokens_pre[r];
+    row_pos[r] = leaf_tokens_pre[r] + ((int64_t)k << 40);
   }
 
   // the work-list invariant: the KV tokens the kernels stream
@@ -1060,6 +1219,23 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     fprintf(stderr, "fk plan: %d rows, %lld private units, %lld chunks, partials %lld (private %lld), max slots %d\n",
             B, (long long)U, (long long)nchunks, (long long)parts, (long long)priv_parts, max_slots);
   }
+  if (plan_digest_on()) {
+    PlanDigest dg;
+    dg.scalars({batch_tokens, shared_tokens, private_tokens, streamed_tokens, (int64_t)shared.size(), num_mma, num_tc,
+                tc_units, tc_ctas, tc_nchunks, (int64_t)tc_l2_share, priv_base, NPT, U, nchunks, wpc, G, grid_ctas,
+                (int64_t)max_slots, (int64_t)n_items, w_active});
+    for (int i = 0; i < n_items; ++i) {
+      const PlanItem& it = items[i];
+      const PlanShared& sh = shared[it.sh];
+      dg.scalars({sh.page_off + it.page0, it.npages, it.ntok, sh.q_off + it.q0, it.nq, it.head, it_unit_off[i],
+                  it_qslot_off[i], it.units});
+    }
+    dg.vec(qrows); dg.vec(qslot); dg.vec(row_priv_off); dg.vec(row_priv_np); dg.vec(row_unit_off);
+    dg.vec(row_head_base); dg.vec(row_head_count); dg.vec(pages); dg.vec(page_ntok); dg.vec(row_uid); dg.vec(row_pos);
+    dg.vec(page_row); dg.span(chunk_start.data(), nchunks + 1); dg.vec(rh_chunk0); dg.vec(ch_item); dg.vec(ch_t0); dg.vec(ch_t1);
+    dg.vec(it_first_chunk); dg.vec(cta_chunk0);
+    p->plan_digest = dg.h;
+  }
   if (!p->on_device) {
     p->have_plan = true;
     return FK_OK;
@@ -1068,7 +1244,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   PT(T7);
   // ---- upload ---------------------------------------------------------------
   FK_ON_DEVICE(p->desc.device);
-  int rc = ensure_scratch(p, B, max_slots);
+  int rc = ensure_scratch(p, B, max_slots, st);
   if (rc != FK_OK) return rc;
   const size_t ni = (size_t)std::max(n_items, 1);
   const size_t nb = (size_t)std::max(B, 1);
@@ -1086,7 +1262,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_app = L.add(sizeof(int32_t) * 2 * nb);
   const size_t o_apos = L.add(sizeof(int64_t) * nb);
   const size_t o_prow = L.add(sizeof(int32_t) * page_row.size());
-  const size_t o_cs = L.add(sizeof(int32_t) * chunk_start.size());
+  const size_t o_cs = L.add(sizeof(int32_t) * (size_t)(nchunks + 1));
   const size_t o_rhc = L.add(sizeof(int32_t) * rh_chunk0.size());
   const size_t nchb = sizeof(int32_t) * std::max<size_t>(ch_item.size(), 1);
   const size_t o_chi = L.add(nchb);
@@ -1115,8 +1291,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   };
   int32_t* itb = (int32_t*)(h + o_it);
   for (int i = 0; i < n_items; ++i) {
-    const Item& it = items[i];
-    const Shared& sh = shared[it.sh];
+    const PlanItem& it = items[i];
+    const PlanShared& sh = shared[it.sh];
     itb[0 * ni + i] = sh.page_off + it.page0;
     itb[1 * ni + i] = it.npages;
     itb[2 * ni + i] = it.ntok;
@@ -1148,7 +1324,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   memset(h + o_apos, 0, nb * 8);
   put(o_prow, page_row.data(), page_row.size() * 4);
-  put(o_cs, chunk_start.data(), chunk_start.size() * 4);
+  put(o_cs, chunk_start.data(), (size_t)(nchunks + 1) * 4);
   put(o_rhc, rh_chunk0.data(), rh_chunk0.size() * 4);
   put(o_chi, ch_item.data(), ch_item.size() * 4);
   put(o_ch0, ch_t0.data(), ch_t0.size() * 4);
@@ -1177,6 +1353,14 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.qslot = (const int32_t*)(d + o_qs);
   pd.tc_units = (int)tc_units;
   pd.tc_ctas = (int)tc_ctas;
+  // The launched prefix grid only changes when the plan's CTA count leaves
+  // [grid - 16, grid]: CTAs past tc_ctas exit at once, and a step whose
+  // launches repeat the previous ones replays its CUDA graph without node
+  // updates (the running set, and with it tc_ctas, moves every step under
+  // a serving load).
+  if (tc_ctas > 0 && (tc_ctas > p->tc_grid || tc_ctas + 16 < p->tc_grid))
+    p->tc_grid = (int)std::min<int64_t>(std::max<int64_t>(p->num_sms, tc_ctas), (tc_ctas + 7) / 8 * 8);
+  pd.tc_grid = p->tc_grid;
   pd.tc_nchunks = (int)tc_nchunks;
   pd.tc_chunk_item = (const int32_t*)(d + o_chi);
   pd.tc_chunk_tile0 = (const int32_t*)(d + o_ch0);
@@ -1317,9 +1501,50 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   const double t0 = timing ? now_us() : 0.0;
+  const int par0 = p->launch_parity;
+  cudaStream_t st = (cudaStream_t)stream;
+  // One graph per (layer range, stream, plan slot, starting partial half):
+  // with the plan in __constant__ memory the kernel arguments then repeat
+  // from step to step, and a replay needs no parameter update at all.
+  GraphCache& G = p->graphs[std::make_tuple(layer0, nlayers, st, p->cur * 2 + par0)];
+  // 0. nothing the launches depend on changed: replay as is
+  ReplayKey key;
+  memset(&key, 0, sizeof(key));
+  key.kv = p->kv;
+  key.num_pages = p->num_pages;
+  key.part_o = p->part_o;
+  key.part_ml = p->part_ml;
+  key.tick = p->tick;
+  key.part_cap = p->part_cap;
+  key.q = q;
+  key.out = out;
+  key.out_f32 = out_f32;
+  key.q_stride = q_layer_stride;
+  key.out_stride = out_layer_stride;
+  key.f32_stride = f32_layer_stride;
+  key.tc_begin = p->plan.tc_begin;
+  key.num_items = p->plan.num_items;
+  key.tc_grid = p->plan.tc_grid;
+  key.tc_ctas = p->plan.tc_ctas;
+  key.priv_any = p->plan.priv_units > 0;
+  key.priv_wpc = p->plan.priv_wpc;
+  key.priv_grid = p->priv_grid;
+  key.num_sms = p->num_sms;
+  key.pdl = (int32_t)p->pdl;
+  key.launch_order = (int32_t)p->launch_order;
+  key.plan_slot = p->plan_base + p->cur;
+  const bool check = getenv("FK_DEBUG_GRAPH_CHECK") != nullptr;  // (read per call: tests set it)
+  const bool key_hit = G.exec && G.key_ok && G.stream == st && p->have_plan && p->plan.num_rows > 0 &&
+                       !p->skip_merge && memcmp(&G.key, &key, sizeof(key)) == 0;
+  if (key_hit && !check) {
+    FK_CUDA(cudaGraphLaunch(G.exec, st));
+    p->launch_parity = par0 ^ (nlayers & 1);  // as the recorded run would have left it
+    p->graph_replays += 1;
+    if (timing) fprintf(stderr, "fk graph: replay %.1f us\n", now_us() - t0);
+    return FK_OK;
+  }
   // 1. record the launches (same code path; the partial-half parity advances
   // before anything runs, and goes back if the graph is not launched)
-  const int par0 = p->launch_parity;
   struct Rollback {
     fk_pool* p;
     int par;
@@ -1338,15 +1563,19 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
     rollback.armed = false;
     return FK_OK;
   }
-  cudaStream_t st = (cudaStream_t)stream;
-  // One graph per (layer range, stream, plan slot, starting partial half):
-  // with the plan in __constant__ memory the kernel arguments then repeat
-  // from step to step, and a replay needs no parameter update at all.
-  GraphCache& G = p->graphs[std::make_tuple(layer0, nlayers, st, p->cur * 2 + par0)];
   bool same = G.exec && G.stream == st && G.shape.size() == recs.n;
   for (size_t i = 0; same && i < recs.n; ++i) {
     const fk::LaunchRec &a = G.shape[i], &b = recs.v[i];
     same = a.func == b.func && a.pdl == b.pdl && a.offs == b.offs;
+  }
+  if (key_hit) {  // FK_DEBUG_GRAPH_CHECK: the key said "unchanged" -- so must the launches
+    for (size_t i = 0; same && i < recs.n; ++i) {
+      const fk::LaunchRec &a = G.shape[i], &b = recs.v[i];
+      same = a.grid.x == b.grid.x && a.grid.y == b.grid.y && a.block.x == b.block.x && a.smem == b.smem &&
+             a.bytes == b.bytes;
+    }
+    if (!same) return fail(FK_INVALID_ARGUMENT, "graph replay key missed a launch change");
+    p->graph_replays += 1;  // (checked: counted as the replay it would have been)
   }
   const double t1 = timing ? now_us() : 0.0;
   int updated = 0;
@@ -1419,6 +1648,8 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   const double t2 = timing ? now_us() : 0.0;
   FK_CUDA(cudaGraphLaunch(G.exec, st));
   rollback.armed = false;
+  G.key = key;
+  G.key_ok = true;
   if (timing)
     fprintf(stderr, "fk graph: %zu launches, record %.1f us, %s %.1f us (%d nodes), launch %.1f us\n", recs.n,
             t1 - t0, same ? "update" : "capture", t2 - t1, updated, now_us() - t2);
@@ -1608,13 +1839,15 @@ int fk_ctx_copy_kv(fk_pool* dst, int64_t dst_ctx, const fk_pool* src, int64_t sr
   return FK_OK;
 }
 
-int fk_synth_queries(fk_pool* p, uint64_t seed, void* q_all, void* stream) {
+int fk_synth_queries(fk_pool* p, uint64_t seed, void* q_all, int32_t rows_cap, void* stream) {
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   if (p->plan.num_rows == 0) return FK_OK;
   FK_ON_DEVICE(p->desc.device);
-  FK_CUDA(launch_synth_queries(p->arena(), p->plan, p->plan_base + p->cur, seed, q_all, (cudaStream_t)stream));
+  if (rows_cap != 0 && rows_cap < p->plan.num_rows) return fail(FK_INVALID_ARGUMENT, "rows_cap %d < %d rows", rows_cap, p->plan.num_rows);
+  FK_CUDA(launch_synth_queries(p->arena(), p->plan, p->plan_base + p->cur, seed, q_all,
+                               rows_cap ? rows_cap : p->plan.num_rows, (cudaStream_t)stream));
   return FK_OK;
 }
 
@@ -1627,6 +1860,8 @@ int fk_synth_append(fk_pool* p, uint64_t seed, float k_scale, void* stream) {
   FK_CUDA(launch_synth_append(p->arena(), p->plan, p->plan_base + p->cur, seed, k_scale, (cudaStream_t)stream));
   return FK_OK;
 }
+
+uint64_t fk_debug_plan_digest(const fk_pool* p) { return p ? p->plan_digest : 0; }
 
 // ---- hashing (tokenizer.py:36-49) -------------------------------------------
 

@@ -662,7 +662,7 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int ps, int la
     }
   }
   if (p.tc_ctas == 0) return cudaSuccess;
-  return launch_k(fk_prefix_tc_kernel, dim3(p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, ps, layer,
+  return launch_k(fk_prefix_tc_kernel, dim3(p.tc_grid > p.tc_ctas ? p.tc_grid : p.tc_ctas), dim3(kTcThreads), kTcSmem, s, pdl, a, ps, layer,
                   (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_run, after_private ? 1 : 0);
 }
 

@@ -941,16 +941,25 @@ class GpuEngine(_EngineBase):
         # (set_stream instead of the context managers: this is the per-step
         # host path.)
         torch.cuda.set_stream(st)
+        # Engine-owned buffers hold `cap` >= B rows per layer (B rounded up to
+        # a power of two): the pointers and layer strides the kernels get stay
+        # the same while the batch moves, so the step's CUDA graph replays
+        # without node updates (under a serving load B changes every step).
+        cap = self._row_cap(B)
+        row_bytes = geo.num_heads * geo.head_dim * 2
         try:
             if tensor_model:
                 q = model.q
                 if q.device.type != "cuda":
                     q = q.to(self._dev, non_blocking=True)
+                q_stride = B * row_bytes
             else:  # synthetic queries into an engine-owned buffer (only the engine stream touches it)
                 q = self.__dict__.get("_synth_q")
-                if q is None or tuple(q.shape) != shape:
-                    q = self._synth_q = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
-                _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed, q.data_ptr(), self._spv))
+                if q is None or q.shape[1] != cap:
+                    q = self._synth_q = torch.empty((geo.num_layers, cap, geo.num_heads, geo.head_dim),
+                                                    dtype=torch.bfloat16, device=self._dev)
+                _lib.check(_lib.lib.fk_synth_queries(self._pool.handle, self.model_seed, q.data_ptr(), cap, self._spv))
+                q_stride = cap * row_bytes
             out = model.out if tensor_model else None
             if out is None or tuple(out.shape) != shape or out.dtype != torch.bfloat16 or out.device != self._dev:
                 # engine-owned outputs: a ring of two, alternating with the
@@ -960,16 +969,19 @@ class GpuEngine(_EngineBase):
                 # to own the buffer)
                 ring = self.__dict__.setdefault("_out_ring", [None, None])
                 i = self._ring_i = self.__dict__.get("_ring_i", 1) ^ 1
-                out = ring[i]
-                if out is None or tuple(out.shape) != shape:
-                    out = ring[i] = torch.empty(shape, dtype=torch.bfloat16, device=self._dev)
+                full = ring[i]
+                if full is None or full.shape[1] != cap:
+                    full = ring[i] = torch.empty((geo.num_layers, cap, geo.num_heads, geo.head_dim),
+                                                 dtype=torch.bfloat16, device=self._dev)
+                out, out_stride = full[:, :B], cap * row_bytes
+            else:
+                out_stride = B * row_bytes
             f32 = torch.empty(shape, dtype=torch.float32, device=self._dev) if self.capture_f32 else None
             # every layer's queries are already on the device: one C call
             # replays the layers' kernels (fk_attn_decode_layers, a CUDA graph)
-            layer_bytes = B * geo.num_heads * geo.head_dim * 2
             _lib.check(_lib.lib.fk_attn_decode_layers(
-                self._pool.handle, 0, geo.num_layers, q.data_ptr(), layer_bytes, out.data_ptr(), layer_bytes,
-                f32.data_ptr() if f32 is not None else None, layer_bytes * 2, self._spv))
+                self._pool.handle, 0, geo.num_layers, q.data_ptr(), q_stride, out.data_ptr(), out_stride,
+                f32.data_ptr() if f32 is not None else None, B * row_bytes * 2, self._spv))
             self.last_output = out
             self.last_output_f32 = f32
             if tensor_model and model.copy_out:
@@ -979,6 +991,16 @@ class GpuEngine(_EngineBase):
         finally:
             torch.cuda.set_stream(caller)
         self._last_running = running
+
+    def _row_cap(self, B: int) -> int:
+        """Rows of the engine-owned q/out buffers: B rounded up to a power of
+        two, at least 64 (a batch that builds up request by request then
+        never reallocates -- a reallocation costs milliseconds under a
+        serving load), shrunk only when B falls below a quarter of it."""
+        cap = self.__dict__.get("_cap", 0)
+        if B > cap or 4 * B < cap:
+            cap = self._cap = max(64, 1 << (B - 1).bit_length())
+        return cap
 
     @property
     def last_rows(self) -> List[str]:
@@ -1066,6 +1088,8 @@ class GpuEngine(_EngineBase):
     def step(self) -> Optional[StepReport]:
         if not self.has_work():
             return None
+        if _PHASES:
+            tm = [time.perf_counter()]
         started_ns = self.clock_ns
         emitted: Dict[str, int] = {}
         finished: List[str] = []
@@ -1092,7 +1116,7 @@ class GpuEngine(_EngineBase):
 
         running = self._running_rows()
         if _PHASES:
-            tm = [time.perf_counter()]
+            tm.append(time.perf_counter())
         batch_tokens = self._plan(running) if running else 0
         if _PHASES:
             tm.append(time.perf_counter())
@@ -1140,11 +1164,6 @@ class GpuEngine(_EngineBase):
 
         if _PHASES:
             tm.append(time.perf_counter())
-            acc = self.__dict__.setdefault("phase_us", {"plan": 0.0, "attention": 0.0, "grow_append": 0.0, "n": 0})
-            acc["plan"] += (tm[1] - tm[0]) * 1e6
-            acc["attention"] += (tm[2] - tm[1]) * 1e6
-            acc["grow_append"] += (tm[3] - tm[2]) * 1e6
-            acc["n"] += 1
         for rid in fill_completed:  # fills done this step decode next step
             g = self.gens.get(rid)
             if g is not None and not g.started:
@@ -1160,6 +1179,10 @@ class GpuEngine(_EngineBase):
         if snapshot is not None:
             positions = [int(self._pos_buf[i]) for i in range(len(running))]
             self.history.append(self._history_record(running, snapshot, batch_tokens, positions))
+        if _PHASES:  # per-step host microseconds of each phase (the plan includes its GPU wait)
+            tm.append(time.perf_counter())
+            self.__dict__.setdefault("phase_steps", []).append(
+                {k: (tm[i + 1] - tm[i]) * 1e6 for i, k in enumerate(("pre", "plan", "attention", "grow_append", "post"))})
         return report
 
     def _running_rows(self) -> List[GenerationTask]:

@@ -65,9 +65,9 @@ def direct(args):
     torch.cuda.synchronize()
     out = {"mode": "direct", "config": args.config, "rows": rows, "steps": args.steps,
            "step_host_us_median": statistics.median(us), "step_host_us_mean": statistics.mean(us)}
-    ph = eng.__dict__.get("phase_us")
+    ph = eng.__dict__.get("phase_steps")
     if ph:
-        out["phase_us"] = {k: ph[k] / ph["n"] for k in ("plan", "attention", "grow_append")}
+        out["phase_us_median"] = {k: statistics.median(x[k] for x in ph) for k in ph[0]}
     print(json.dumps(out))
 
 
@@ -104,7 +104,7 @@ def main():
         apps += [dataclasses.replace(a, app_id=f"g{g}.{a.app_id}") for a in wl.apps]
     work = Workload("GroupsPerEngine", 7, {"groups": args.engines}, apps)
 
-    step_us, full = [], []
+    step_us, full, slow = [], [], []
     orig_step = P.GpuEngine.step
 
     def timed_step(self):
@@ -116,6 +116,8 @@ def main():
         # host CPU time of the step: wall time minus the time the plan waited
         # for the GPU to release a plan slot (the host runs <= 1 step ahead)
         step_us.append((t1 - t0) * 1e6 - (w1 - w0) / 1e3)
+        if step_us[-1] > 1000:  # where the slow steps happen (engine, its step, rows)
+            slow.append((round(step_us[-1]), self.engine_id, len(self.reports), self.last_plan.num_rows))
         full.append(r is not None and r.batch_tokens > 0 and self.last_plan.num_rows == args.users)
         return r
 
@@ -160,18 +162,21 @@ def main():
         "full_batch_steps": sum(full),
         "full_batch_step_host_us_median": statistics.median([u for u, f in zip(step_us, full) if f] or [0.0]),
         "full_batch_step_host_us_mean": statistics.mean([u for u, f in zip(step_us, full) if f] or [0.0]),
+        "step_host_us_p90": sorted(steady)[int(0.9 * (len(steady) - 1))],
+        "step_host_us_p99": sorted(steady)[int(0.99 * (len(steady) - 1))],
+        "step_host_us_max": max(step_us), "steps_over_1ms": sum(u > 1000 for u in step_us),
+        "slow_steps": slow[:60],
         "manager_loop_us_per_engine_step": wall / max(len(step_us), 1) * 1e6,
         "wall_s": wall, "wall_with_gpu_drain_s": gpu_wall, "virtual_end_ms": end_ns / 1e6,
         "max_batch": max(max((r.batch_tokens for r in e.reports), default=0) for e in mgr.engines.values()),
     }
     del decode
-    ph = [e.__dict__.get("phase_us") for e in mgr.engines.values()]
-    ph = [x for x in ph if x]
-    if ph:  # FK_DEBUG_TIMING=1: per-phase host us per step (plan includes its GPU wait)
-        n = sum(x["n"] for x in ph)
-        out["phase_us"] = {k: sum(x[k] for x in ph) / n for k in ("plan", "attention", "grow_append")}
+    ph = [x for e in mgr.engines.values() for x in e.__dict__.get("phase_steps", [])]
+    if ph:  # FK_DEBUG_TIMING=1: per-phase host us per step, medians (plan includes its GPU wait)
+        out["phase_us_median"] = {k: statistics.median(x[k] for x in ph) for k in ph[0]}
+        n = len(ph)
         waits = sum(e.pool_stats().host_wait_ns for e in mgr.engines.values() if e.device is not None)
-        out["phase_us"]["plan_gpu_wait"] = waits / 1e3 / n
+        out["plan_gpu_wait_us_mean"] = waits / 1e3 / n
     print(json.dumps(out))
 
 

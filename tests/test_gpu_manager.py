@@ -110,3 +110,24 @@ def test_shared_ctx_fallback_migrates_the_prefix(cuda_device):
         alias = {dst: src for dst, (_, src, _) in eng.migrated.items()}
         kv = O.KVCache(eng.model_seed, eng.geometry.num_heads, eng.model_k_scale, alias=alias)
         check_history(eng, kv=kv)
+
+
+def test_graph_replay_key_under_a_serving_load(cuda_device, monkeypatch):
+    """Under the manager the batch changes from step to step (requests join
+    and finish).  The engine-owned q/out buffers keep their pointers (row
+    capacity), the prefix grid its size (hysteresis), so most steps replay
+    the cached CUDA graph without recording (fk_attn_decode_layers' replay
+    key).  FK_DEBUG_GRAPH_CHECK=1 records every step anyway and fails if a
+    replayed step's launches would have differed; outputs (bf16, no f32
+    capture, which would change a pointer every step) match the oracle."""
+    monkeypatch.setenv("FK_DEBUG_GRAPH_CHECK", "1")
+    want = manager_view(*run_manager(None, 1))
+    factory = P.engine_factory(P.ModelGeometry(2, 8, 128), keep_history=True)
+    mgr, end_ns = run_manager(factory, 1)
+    assert manager_view(mgr, end_ns) == want
+    (eng,) = mgr.engines.values()
+    eng.stream.synchronize()
+    steps = len(eng.history)
+    replays = eng.pool_stats().graph_replays
+    assert steps >= 8 and replays >= steps // 2, (steps, replays)
+    check_history(eng, f32=False)

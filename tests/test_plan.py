@@ -78,3 +78,18 @@ def test_nested_plan_counts_every_level_once():
     running = list(eng.gens.values())
     assert eng._plan(running) == 4096 + 8 * 1024 + 64 * 256
     assert eng.last_plan.num_shared_ctx == 9
+
+
+def test_plan_digests_pinned():
+    """Every array and scalar the planner uploads, for 558 (forest, options,
+    dedup) cases x 3 steps, equals the digests the round-1 planner wrote
+    (tests/golden/make_plan_digests.py): the host-speed rewrite of
+    fk_step_plan changed no plan."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "golden", "make_plan_digests.py"), "--check"],
+                       env={**os.environ, "FK_DEBUG_PLAN_DIGEST": "1"}, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
