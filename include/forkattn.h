@@ -132,6 +132,9 @@ enum {
                                  runs fk_attn_decode.  fk_plan_info.batch_tokens stays the
                                  reference's pre-growth count.  0 (default): the reference's span
                                  (chain tokens at step start, engine.py:416-434), append after */
+  FK_OPT_GROUP_FANOUT = 18,   /* shared contexts read by <= this many rows (0..64) are streamed by the
+                                 private kernel once per group of up to 8 rows -- the rows are the N of
+                                 its transposed m16n8 products -- instead of by a prefix kernel */
   FK_OPT_DEBUG_SKIP_MERGE = 90 /* diagnostic only: 1 = do not launch the LSE merge (outputs are NOT
                                  written); bounds the time the merge adds to a layer */
 };

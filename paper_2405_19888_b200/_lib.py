@@ -39,6 +39,7 @@ FK_OPT_PRIV_WARPS = 11
 FK_OPT_GRAPH = 12
 FK_OPT_TC_BOUNDARY_COST = 14
 FK_OPT_APPEND_FIRST = 16
+FK_OPT_GROUP_FANOUT = 18
 FK_OPT_DEBUG_SKIP_MERGE = 90
 
 

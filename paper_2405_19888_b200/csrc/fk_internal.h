@@ -19,6 +19,8 @@ constexpr int kTcMaxChunk = 24;   // largest tcgen05 chunk (tiles)
 constexpr int kPrivWarpsPerCta = 10;  // private kernel default shape: 10 warps per CTA x 2 stages (measured best)
 constexpr int kPrivMinChunk = 2;     // private guided schedule: smallest chunk (pages), default
 constexpr int kPrivMaxChunk = 32;    // largest chunk (one lane-parallel metadata load)
+constexpr int kWideSlots = 32;       // plans with more partials per (row, head) merge with a CTA per item
+constexpr int kGroupRows = 8;        // rows per private-kernel item (the N of its m16n8 products)
 
 // Device view of one step plan.  All arrays live in one device buffer.
 // Partials of (row, head) live at slots [0, row_head_count): shared-prefix
@@ -51,18 +53,24 @@ struct PlanDev {
   const int* tc_cta_chunk0;       // [tc_ctas + 1]
   int tc_l2_share;                // CTAs b, b + X/k stream the same tiles together: default L2 policy
   // rows
-  const int* row_priv_off;     // offset into pages[] / page_ntok[]
-  const int* row_priv_npages;
-  const int* row_unit_off;     // row's first entry in the flat private list
-  const int* row_head_base;    // [rows][H] slot of private piece 0
+  const int* row_head_base;    // [rows][H] first slot after the row's prefix-kernel pieces
   const int* row_head_count;   // [rows][H] partials the merge combines
   const int* pages;            // physical page ids
   const int* page_ntok;        // valid tokens per page entry
   // private schedule: units u in [0, H * priv_np) = (head, flat private page
   // entry e): head = u / priv_np, entry = priv_base + u % priv_np, cut into
   // chunks [priv_chunk_start[c], priv_chunk_start[c + 1]) that warps grab
-  // from a ticket counter.
-  const int* page_row;         // row of each flat private entry
+  // from a ticket counter.  Entries belong to items: a run of pages streamed
+  // once for up to kGroupRows rows (a small-fan-out shared context, or one
+  // row's private chain).
+  const int* page_item;        // item of each flat private entry
+  const int* item_nrows;       // rows of each item (1..kGroupRows)
+  const int* item_roff;        // its rows at item_rows[item_roff[k] ..]
+  const int* item_rows;
+  const int* item_slot;        // [(item_roff[k] + j) * H + head]: slot of the (item, head) run's first piece for row j
+  const int* item_chunk0;      // [item][H] first chunk of the (item, head) run
+  int n_gitems;                // items [0, n_gitems) are grouped; item n_gitems + r is row r's private chain
+  int n_grows;                 // rows listed by the grouped items (row r's private item lists its row at n_grows + r)
   int priv_base;               // offset of the private entries in pages[]
   int priv_np;                 // number of private page entries (NPT)
   int priv_units;              // U = H * NPT
@@ -71,7 +79,6 @@ struct PlanDev {
   int priv_warps;              // grid warps (grid = priv_warps / priv_wpc)
   int priv_static;             // warps that start on chunk = warp index (the ones that start at once)
   const int* priv_chunk_start; // [priv_nchunks + 1]
-  const int* priv_rh_chunk0;   // [rows][H] first chunk of each (row, head) item
   // synthetic keys per row
   const long long* row_uid;    // leaf context uid
   const long long* row_pos;    // leaf tokens at plan time + (rank << 40)
@@ -154,7 +161,7 @@ cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int ps, int la
                              float scale_log2, const CUtensorMap* tmap, const CUtensorMap* tmap_run,
                              bool pdl, bool after_private, cudaStream_t s);
 cudaError_t launch_merge(const ArenaDev& a, int ps, void* out, float* out_f32, int layer, int grid, bool pdl,
-                         cudaStream_t s);
+                         bool wide, cudaStream_t s);
 cudaError_t launch_append(const ArenaDev& a, const PlanDev& p, int ps, int layer0, int nlayers,
                           const void* k, const void* v, cudaStream_t s);
 cudaError_t launch_synth_fill(const ArenaDev& a, const int* pages_dev, int npages_first,

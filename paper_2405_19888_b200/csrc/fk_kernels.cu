@@ -48,7 +48,7 @@ __device__ __forceinline__ uint32_t sw_page(int row, int c16) {
 }
 
 struct UnitMeta {
-  int pg, ntok, row, head;
+  int pg, ntok, item, head, nr;  // nr: rows of the item (1 = a private chain)
 };
 
 CTA_TL_DECL(fk_tl_cta_priv);
@@ -62,7 +62,9 @@ struct PdlTail {
     if (threadIdx.x == 0) pdl_wait_primary();
   }
 };
-template <int STAGES, int WARPS>
+// GROUPED: the plan has row-group items (small-fan-out shared contexts);
+// without them the single-row path is the whole kernel.
+template <int STAGES, int WARPS, bool GROUPED>
 __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, int ps, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
                                                                    float scale_log2,
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
 
   // unit metadata of a chunk (<= 32 units) held lane-parallel in registers
   auto load_chunk = [&](int c, int& len) {
-    UnitMeta m{0, 0, 0, 0};
+    UnitMeta m{0, 0, 0, 0, 1};
     len = 0;
     if (c < nch) {
       const int u0 = p.priv_chunk_start[c];
@@ -119,7 +121,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
         m.head = u / NPT;
         m.pg = p.pages[p.priv_base + e];
         m.ntok = p.page_ntok[p.priv_base + e];
-        m.row = p.page_row[e];
+        m.item = p.page_item[e];
+        m.nr = (!GROUPED || m.item >= p.n_gitems) ? 1 : p.item_nrows[m.item];
       }
     }
     return m;
@@ -128,8 +131,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
     UnitMeta r;
     r.pg = __shfl_sync(0xffffffffu, m.pg, i);
     r.ntok = __shfl_sync(0xffffffffu, m.ntok, i);
-    r.row = __shfl_sync(0xffffffffu, m.row, i);
+    r.item = __shfl_sync(0xffffffffu, m.item, i);
     r.head = __shfl_sync(0xffffffffu, m.head, i);
+    r.nr = __shfl_sync(0xffffffffu, m.nr, i);
     return r;
   };
   auto issue = [&](int s, const UnitMeta& m) {  // lane 0 only
@@ -165,23 +169,34 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
   };
   issue_ahead();
 
-  // q^T as the B operand of S^T = K . q^T: column 0 of a 128 x 8 tile
-  // (lanes 0-3 hold it); the next piece's q is prefetched one page ahead into qn
+  // row j of an item: a private item's row follows from its index, a grouped
+  // item lists its rows
+  auto item_row = [&](int item, int j) -> int {
+    return item >= p.n_gitems ? item - p.n_gitems : p.item_rows[p.item_roff[item] + j];
+  };
+  // q^T as the B operand of S^T = K . q^T: column n of the 128 x 8 tile is the
+  // item's row n (lanes 4n .. 4n + 3 hold it; a private item has column 0
+  // only); the next piece's q is prefetched one page ahead into qn
   uint32_t qa[8][2], qn[8][2];
-  auto fetch_q = [&](uint32_t (&dst)[8][2], int row, int head) {
-    const uint32_t* Q = reinterpret_cast<const uint32_t*>(q + ((long long)row * H + head) * kHeadDim);
+  auto fetch_q = [&](uint32_t (&dst)[8][2], int item, int nr, int head) {
+    const int row = g < nr ? item_row(item, g) : -1;
+    const uint32_t* Q = reinterpret_cast<const uint32_t*>(q + ((long long)max(row, 0) * H + head) * kHeadDim);
 #pragma unroll
     for (int kt = 0; kt < 8; ++kt) {
-      dst[kt][0] = g == 0 ? Q[kt * 8 + t4] : 0u;
-      dst[kt][1] = g == 0 ? Q[kt * 8 + 4 + t4] : 0u;
+      dst[kt][0] = row >= 0 ? Q[kt * 8 + t4] : 0u;
+      dst[kt][1] = row >= 0 ? Q[kt * 8 + 4 + t4] : 0u;
     }
   };
   UnitMeta cur = sh(ma, 0);
-  fetch_q(qa, cur.row, cur.head);
-  float o[8][4];  // o^T tiles, lanes t4 == 0: dims 16 mt + g (c0 hi, c1 lo) and 16 mt + g + 8 (c2, c3)
+  fetch_q(qa, cur.item, cur.nr, cur.head);
+  // o^T tiles: dims 16 mt + g (c0, c1) and 16 mt + g + 8 (c2, c3) x columns
+  // 2 t4, 2 t4 + 1.  Private item: lanes t4 == 0, column 0 = P hi, column 1 =
+  // P lo.  Grouped item: the columns are its rows (P hi and lo in two MMAs).
+  float o[8][4];
 #pragma unroll
   for (int k = 0; k < 8; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
-  float m = -INFINITY, l = 0.f;
+  float m = -INFINITY, l = 0.f;    // private: the row; grouped: column 2 t4
+  float m2 = -INFINITY, l2 = 0.f;  // grouped: column 2 t4 + 1
   const int mi = lane >> 3, ri = lane & 7;
 
   while (true) {
@@ -189,8 +204,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
     const bool chunk_last = i + 1 == la;
     const bool have_next = !chunk_last || lb > 0;
     const UnitMeta nxt = !chunk_last ? sh(ma, i + 1) : (lb > 0 ? sh(mb, 0) : cur);
-    const bool piece_end = chunk_last || nxt.row != cur.row || nxt.head != cur.head;
-    if (piece_end && have_next) fetch_q(qn, nxt.row, nxt.head);
+    const bool piece_end = chunk_last || nxt.item != cur.item || nxt.head != cur.head;
+    if (piece_end && have_next) fetch_q(qn, nxt.item, nxt.nr, nxt.head);
     const int s = (int)(seq % STAGES);
     mbar_wait(&full[warp][s], (seq / STAGES) & 1);
     const uint32_t Ks = smem_u32(ring + s * kPwStageBytes);
@@ -207,68 +222,147 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
       const uint32_t af[4] = {r0, r2, r1, r3};
       mma_bf16(st, af, qa[kt][0], qa[kt][1]);
     }
-    const bool real = t4 == 0;
-    const float v0 = real && g < cur.ntok ? st[0] * scale_log2 : -INFINITY;
-    const float v1 = real && g + 8 < cur.ntok ? st[2] * scale_log2 : -INFINITY;
-    float mx = fmaxf(v0, v1);
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-    mx = __shfl_sync(0xffffffffu, mx, 0);
-    const float m_new = fmaxf(m, mx);
-    const float alpha = ex2(m - m_new);
-    m = m_new;
-    const float p0 = real ? ex2(v0 - m_new) : 0.f, p1 = real ? ex2(v1 - m_new) : 0.f;
-    l = l * alpha + (p0 + p1);
-    // p^T as the B operand: lane (g, t4) takes tokens 2 t4, 2 t4 + 1 (b0) and
-    // 2 t4 + 8, 2 t4 + 9 (b1); token t sits in lane 4 (t & 7)
-    const float x0 = __shfl_sync(0xffffffffu, p0, 8 * t4), x1 = __shfl_sync(0xffffffffu, p0, 8 * t4 + 4);
-    const float y0 = __shfl_sync(0xffffffffu, p1, 8 * t4), y1 = __shfl_sync(0xffffffffu, p1, 8 * t4 + 4);
-    const uint32_t ph0 = pack_bf16(x0, x1), ph1 = pack_bf16(y0, y1);
-    const uint32_t pl0 = pack_bf16(x0 - bf_lo(ph0), x1 - bf_hi(ph0));
-    const uint32_t pl1 = pack_bf16(y0 - bf_lo(ph1), y1 - bf_hi(ph1));
-    // P hi in column 0 and P lo in column 1 of one B operand (lanes g = 0 and
-    // g = 1): one MMA per 16-dim slice; o = column 0 + column 1 at the end
-    const uint32_t pb0 = g == 1 ? pl0 : ph0, pb1 = g == 1 ? pl1 : ph1;
+    if (!GROUPED || cur.nr == 1) {
+      const bool real = t4 == 0;
+      const float v0 = real && g < cur.ntok ? st[0] * scale_log2 : -INFINITY;
+      const float v1 = real && g + 8 < cur.ntok ? st[2] * scale_log2 : -INFINITY;
+      float mx = fmaxf(v0, v1);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      mx = __shfl_sync(0xffffffffu, mx, 0);
+      const float m_new = fmaxf(m, mx);
+      const float alpha = ex2(m - m_new);
+      m = m_new;
+      const float p0 = real ? ex2(v0 - m_new) : 0.f, p1 = real ? ex2(v1 - m_new) : 0.f;
+      l = l * alpha + (p0 + p1);
+      // p^T as the B operand: lane (g, t4) takes tokens 2 t4, 2 t4 + 1 (b0) and
+      // 2 t4 + 8, 2 t4 + 9 (b1); token t sits in lane 4 (t & 7)
+      const float x0 = __shfl_sync(0xffffffffu, p0, 8 * t4), x1 = __shfl_sync(0xffffffffu, p0, 8 * t4 + 4);
+      const float y0 = __shfl_sync(0xffffffffu, p1, 8 * t4), y1 = __shfl_sync(0xffffffffu, p1, 8 * t4 + 4);
+      const uint32_t ph0 = pack_bf16(x0, x1), ph1 = pack_bf16(y0, y1);
+      const uint32_t pl0 = pack_bf16(x0 - bf_lo(ph0), x1 - bf_hi(ph0));
+      const uint32_t pl1 = pack_bf16(y0 - bf_lo(ph1), y1 - bf_hi(ph1));
+      // P hi in column 0 and P lo in column 1 of one B operand (lanes g = 0 and
+      // g = 1): one MMA per 16-dim slice; o = column 0 + column 1 at the end
+      const uint32_t pb0 = g == 1 ? pl0 : ph0, pb1 = g == 1 ? pl1 : ph1;
+  #pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        o[k][0] *= alpha;
+        o[k][1] *= alpha;
+        o[k][2] *= alpha;
+        o[k][3] *= alpha;
+      }
+  #pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4_t(Vs + sw_page((mi >> 1) * 8 + ri, 2 * mt + (mi & 1)), r0, r1, r2, r3);
+        const uint32_t af[4] = {r0, r1, r2, r3};
+        mma_bf16(o[mt], af, pb0, pb1);
+      }
+    } else {
+      // grouped item: columns a = 2 t4 and b = 2 t4 + 1 of S^T are rows of the
+      // item (the columns past its rows hold q = 0 and are never written)
+      const float sa0 = g < cur.ntok ? st[0] * scale_log2 : -INFINITY;
+      const float sb0 = g < cur.ntok ? st[1] * scale_log2 : -INFINITY;
+      const float sa1 = g + 8 < cur.ntok ? st[2] * scale_log2 : -INFINITY;
+      const float sb1 = g + 8 < cur.ntok ? st[3] * scale_log2 : -INFINITY;
+      float mxa = fmaxf(sa0, sa1), mxb = fmaxf(sb0, sb1);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      o[k][0] *= alpha;
-      o[k][1] *= alpha;
-      o[k][2] *= alpha;
-      o[k][3] *= alpha;
-    }
+      for (int x = 4; x < 32; x <<= 1) {
+        mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, x));
+        mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, x));
+      }
+      const float mna = fmaxf(m, mxa), mnb = fmaxf(m2, mxb);
+      const float ala = ex2(m - mna), alb = ex2(m2 - mnb);
+      m = mna;
+      m2 = mnb;
+      const float pa0 = ex2(sa0 - mna), pb0 = ex2(sb0 - mnb), pa1 = ex2(sa1 - mna), pb1 = ex2(sb1 - mnb);
+      l = l * ala + (pa0 + pa1);
+      l2 = l2 * alb + (pb0 + pb1);
+      // P^T as the B operand: lane (g, t4) needs P(token 2 t4 [+1] [+8], row g);
+      // P(token j, row c) sits in lane 4 (j & 7) + (c >> 1), half c & 1 of
+      // the (a, b) pair of its token row j (< 8: X, >= 8: Y)
+      const uint32_t X = pack_bf16(pa0, pb0), Y = pack_bf16(pa1, pb1);
+      const uint32_t Xl = pack_bf16(pa0 - bf_lo(X), pb0 - bf_hi(X));
+      const uint32_t Yl = pack_bf16(pa1 - bf_lo(Y), pb1 - bf_hi(Y));
+      const int srcA = 8 * t4 + (g >> 1), srcB = srcA + 4;
+      const int hs = (g & 1) * 16;
+      auto pair = [&](uint32_t v) {
+        const uint32_t lo = (__shfl_sync(0xffffffffu, v, srcA) >> hs) & 0xFFFFu;
+        const uint32_t hi = (__shfl_sync(0xffffffffu, v, srcB) >> hs) & 0xFFFFu;
+        return lo | (hi << 16);
+      };
+      const uint32_t bh0 = pair(X), bh1 = pair(Y), bl0 = pair(Xl), bl1 = pair(Yl);
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      uint32_t r0, r1, r2, r3;
-      ldsm_x4_t(Vs + sw_page((mi >> 1) * 8 + ri, 2 * mt + (mi & 1)), r0, r1, r2, r3);
-      const uint32_t af[4] = {r0, r1, r2, r3};
-      mma_bf16(o[mt], af, pb0, pb1);
+      for (int k = 0; k < 8; ++k) {
+        o[k][0] *= ala;
+        o[k][1] *= alb;
+        o[k][2] *= ala;
+        o[k][3] *= alb;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4_t(Vs + sw_page((mi >> 1) * 8 + ri, 2 * mt + (mi & 1)), r0, r1, r2, r3);
+        const uint32_t af[4] = {r0, r1, r2, r3};
+        mma_bf16(o[mt], af, bh0, bh1);
+        mma_bf16(o[mt], af, bl0, bl1);
+      }
     }
     __syncwarp();  // every lane is done reading stage s
     ++i;
     ++seq;
     issue_ahead();
     if (piece_end) {
-      // partial of (row, head) from this chunk
-      const int row = cur.row, head = cur.head;
-      const long long rh = (long long)row * H + head;
-      const int slot = p.row_head_base[rh] + (ca - p.priv_rh_chunk0[rh]);
-      const long long pi = part_index(p, H, row, slot, head);
+      // partial of each of the item's rows at this head from this chunk: slot
+      // = the (item, head) run's first slot for the row + its piece index
+      const int item = cur.item, head = cur.head;
+      const int piece = ca - p.item_chunk0[item * H + head];
+      auto slot_of = [&](int j) {
+        const int roff = item >= p.n_gitems ? p.n_grows + item - p.n_gitems : p.item_roff[item];
+        return p.item_slot[(roff + j) * H + head] + piece;
+      };
       float lsum = l;
       lsum += __shfl_xor_sync(0xffffffffu, lsum, 4);
       lsum += __shfl_xor_sync(0xffffffffu, lsum, 8);
       lsum += __shfl_xor_sync(0xffffffffu, lsum, 16);
-      if (t4 == 0) {
-        float* po = a.part_o + pi * kHeadDim;
+      if (!GROUPED || cur.nr == 1) {
+        if (t4 == 0) {
+          const int row = item_row(item, 0);
+          const long long pi = part_index(p, H, row, slot_of(0), head);
+          float* po = a.part_o + pi * kHeadDim;
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          po[mt * 16 + g] = o[mt][0] + o[mt][1];
-          po[mt * 16 + g + 8] = o[mt][2] + o[mt][3];
+          for (int mt = 0; mt < 8; ++mt) {
+            po[mt * 16 + g] = o[mt][0] + o[mt][1];
+            po[mt * 16 + g + 8] = o[mt][2] + o[mt][3];
+          }
+          if (g == 0) a.part_ml[pi] = make_float2(m, lsum);
         }
-        if (g == 0) a.part_ml[pi] = make_float2(m, lsum);
+      } else {
+        float lsum2 = l2;
+        lsum2 += __shfl_xor_sync(0xffffffffu, lsum2, 4);
+        lsum2 += __shfl_xor_sync(0xffffffffu, lsum2, 8);
+        lsum2 += __shfl_xor_sync(0xffffffffu, lsum2, 16);
+#pragma unroll
+        for (int cb2 = 0; cb2 < 2; ++cb2) {
+          const int col = 2 * t4 + cb2;
+          if (col < cur.nr) {
+            const long long pi = part_index(p, H, item_row(item, col), slot_of(col), head);
+            float* po = a.part_o + pi * kHeadDim;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              po[mt * 16 + g] = o[mt][cb2];
+              po[mt * 16 + g + 8] = o[mt][2 + cb2];
+            }
+            if (g == 0) a.part_ml[pi] = cb2 ? make_float2(m2, lsum2) : make_float2(m, lsum);
+          }
+        }
       }
       m = -INFINITY;
       l = 0.f;
+      m2 = -INFINITY;
+      l2 = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) o[k][0] = o[k][1] = o[k][2] = o[k][3] = 0.f;
 #pragma unroll
@@ -533,6 +627,107 @@ __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, int ps, __nv_
   CTA_TL_END(fk_tl_cta_merge, layer);
 }
 
+// K4 for plans with many partials per (row, head) -- small batches, where the
+// private stream of one row is cut into ~U / W chunks (a single 6k-token
+// request has ~200 pieces per head) -- one CTA per (row, head): warp w
+// combines slots w, w + 8, ... (their (m, l) lane-parallel, 32 per round, and
+// their o 8 loads at a time), then warp 0 combines the 8 warp results through
+// shared memory.  A warp per item would walk ~200 slots one load round after
+// another.
+constexpr int kWideWarps = 8;
+__global__ void __launch_bounds__(kWideWarps * 32) fk_merge_wide_kernel(ArenaDev a, int ps,
+                                                                       __nv_bfloat16* __restrict__ out,
+                                                                       float* __restrict__ out_f32, int layer) {
+  const PlanDev& p = fk_plan_c[ps];
+  __shared__ float s_m[kWideWarps], s_l[kWideWarps];
+  __shared__ float4 s_o[kWideWarps][32];
+  CTA_TL_START(fk_tl_cta_merge, layer);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = a.num_heads, nrh = p.num_rows * H;
+  pdl_wait_primary();       // partials of the prefix and private grids are complete
+  pdl_launch_dependents();  // the next layer's first kernel may start (other partial half)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.tick = 0u;  // (as fk_merge_kernel)
+  for (int w = blockIdx.x; w < nrh; w += gridDim.x) {
+    const int row = w / H, head = w % H;
+    const int ns = partial_count(p, H, row, head);
+    const long long base = part_index(p, H, row, 0, head);  // slot stride is H
+    float M = -INFINITY, L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    // this warp's slots k = warp + kWideWarps * j, 32 per round (online across rounds)
+    for (int j0 = 0; warp + kWideWarps * j0 < ns; j0 += 32) {
+      const int kl = warp + kWideWarps * (j0 + lane);
+      const float2 ml = kl < ns ? __ldcg(&a.part_ml[base + (long long)kl * H]) : make_float2(-INFINITY, 0.f);
+      float mr = ml.x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+      const float mn = fmaxf(M, mr);
+      if (mn == -INFINITY) continue;
+      const float sc = ex2(M - mn);  // (M == -inf: 0, nothing accumulated yet)
+      acc.x *= sc;
+      acc.y *= sc;
+      acc.z *= sc;
+      acc.w *= sc;
+      L *= sc;
+      M = mn;
+      const float wl = kl < ns ? ex2(ml.x - M) : 0.f;
+      float lsum = ml.y * wl;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+      L += lsum;
+      const int cnt = min(32, (ns - warp + kWideWarps - 1) / kWideWarps - j0);
+      for (int g0 = 0; g0 < cnt; g0 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int kk = warp + kWideWarps * (j0 + g0 + k);
+          v[k] = g0 + k < cnt ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)kk * H) * kHeadDim) + lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float wk = __shfl_sync(0xffffffffu, wl, (g0 + k) & 31);
+          acc.x = fmaf(v[k].x, wk, acc.x);
+          acc.y = fmaf(v[k].y, wk, acc.y);
+          acc.z = fmaf(v[k].z, wk, acc.z);
+          acc.w = fmaf(v[k].w, wk, acc.w);
+        }
+      }
+    }
+    if (lane == 0) {
+      s_m[warp] = M;
+      s_l[warp] = L;
+    }
+    s_o[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      float Mc = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kWideWarps; ++k) Mc = fmaxf(Mc, s_m[k]);
+      float Lc = 0.f;
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (Mc != -INFINITY) {
+#pragma unroll
+        for (int k = 0; k < kWideWarps; ++k) {
+          const float wk = s_m[k] == -INFINITY ? 0.f : ex2(s_m[k] - Mc);
+          Lc = fmaf(s_l[k], wk, Lc);
+          const float4 v = s_o[k][lane];
+          r.x = fmaf(v.x, wk, r.x);
+          r.y = fmaf(v.y, wk, r.y);
+          r.z = fmaf(v.z, wk, r.z);
+          r.w = fmaf(v.w, wk, r.w);
+        }
+      }
+      const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
+      r = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
+      const long long oi = ((long long)row * H + head) * kHeadDim + lane * 4;
+      *reinterpret_cast<uint2*>(out + oi) = make_uint2(pack_bf16(r.x, r.y), pack_bf16(r.z, r.w));
+      if (out_f32) *reinterpret_cast<float4*>(out_f32 + oi) = r;
+    }
+    __syncthreads();
+  }
+  CTA_TL_END(fk_tl_cta_merge, layer);
+}
+
 extern "C" int fk_debug_cta_timeline_merge(unsigned long long* out, int n) {
 #ifdef FK_TIMELINE
   if (cudaDeviceSynchronize() != cudaSuccess) return 6;
@@ -686,17 +881,17 @@ cudaError_t upload_plan_main(int ps, const PlanDev* host_pinned, cudaStream_t s)
                                  cudaMemcpyHostToDevice, s);
 }
 
-template <int STAGES, int WARPS>
+template <int STAGES, int WARPS, bool GROUPED>
 static cudaError_t launch_private_shape(const ArenaDev& a, int ps, int layer, const void* q, float scale_log2,
                                        const CUtensorMap* tmap, int grid_ctas, bool pdl, cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   constexpr int smem = priv_smem<STAGES, WARPS>();
   if (!attr_set_on_device(attr_devices)) {
-    cudaError_t e = cudaFuncSetAttribute(fk_private_kernel<STAGES, WARPS>,
+    cudaError_t e = cudaFuncSetAttribute(fk_private_kernel<STAGES, WARPS, GROUPED>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_k(fk_private_kernel<STAGES, WARPS>, dim3(grid_ctas), dim3(WARPS * 32), smem, s, pdl, a, ps, layer,
+  return launch_k(fk_private_kernel<STAGES, WARPS, GROUPED>, dim3(grid_ctas), dim3(WARPS * 32), smem, s, pdl, a, ps, layer,
                   (const __nv_bfloat16*)q, scale_log2, *tmap);
 }
 
@@ -706,14 +901,20 @@ cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int ps, int laye
   // ring shapes: per-warp stages x warps per CTA (8 KiB stages): 10 x 2 = 160 KiB
   // (the default, measured best), 8 x 3 and 12 x 2 = 192 KiB
   switch (p.priv_wpc) {
-    case 8: return launch_private_shape<3, 8>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
-    case 12: return launch_private_shape<2, 12>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
-    default: return launch_private_shape<2, 10>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+    case 8: return launch_private_shape<3, 8, false>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+    case 12: return launch_private_shape<2, 12, false>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+    default:
+      // (row groups: the default shape only -- the planner keeps them off for the others)
+      if (p.n_gitems > 0) return launch_private_shape<2, 10, true>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+      return launch_private_shape<2, 10, false>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
   }
 }
 
 cudaError_t launch_merge(const ArenaDev& a, int ps, void* out, float* out_f32, int layer, int grid, bool pdl,
-                         cudaStream_t s) {
+                         bool wide, cudaStream_t s) {
+  if (wide)
+    return launch_k(fk_merge_wide_kernel, dim3(grid), dim3(kWideWarps * 32), 0, s, pdl, a, ps, (__nv_bfloat16*)out,
+                    out_f32, layer);
   return launch_k(fk_merge_kernel, dim3(grid), dim3(256), 0, s, pdl, a, ps, (__nv_bfloat16*)out, out_f32, layer);
 }
 

@@ -56,6 +56,7 @@ struct Ctx {
   uint32_t mark = 0;
   int32_t fan = 0;      // rows whose chain holds this context
   int32_t sidx = -1;    // index among the step's shared contexts, or -1
+  int32_t gidx = -1;    // index among the step's grouped (small fan-out) contexts, or -1
   int32_t rank = 0;     // rows planned so far with this context as their leaf
   bool shared = false;  // fan-out >= 2 with tokens (dedup mode)
 };
@@ -78,7 +79,8 @@ struct PlanScratch {
   std::vector<Ctx*> chain, order;
   std::vector<int32_t> chain_off, srows, pages, page_ntok, qrows, it_unit_off, ch_item, ch_t0, ch_t1, cta_chunk0,
       it_first_chunk, pieces_of, rs_off, rs_sh, rs_qb, row_head_base, base_at, it_qslot_off, qslot, row_priv_off,
-      row_priv_np, row_unit_off, page_row, chunk_start, row_head_count, rh_chunk0, srow_e, acc;
+      row_priv_np, row_unit_off, page_item, chunk_start, row_head_count, item_chunk0, srow_e, acc, pit_e0, pit_np,
+      pit_roff, pit_nrows, pit_rows, grow_cnt, grows, gfill, item_slot, item_pieces;
   std::vector<int64_t> leaf_tokens_pre, cut, cut0, qb_off, row_uid, row_pos;
   int64_t n_chunks = 0;  // chunk_start holds n_chunks + 1 entries in use
   std::vector<PlanShared> shared;
@@ -138,7 +140,7 @@ struct ReplayKey {
   const void *q, *out, *out_f32;
   int64_t q_stride, out_stride, f32_stride;
   int32_t tc_begin, num_items, tc_grid, tc_ctas, priv_any, priv_wpc, priv_grid, num_sms, pdl, launch_order, plan_slot;
-  int32_t pad;
+  int32_t wide_merge;
 };
 static_assert(sizeof(ReplayKey) % 8 == 0, "ReplayKey is compared bytewise");
 
@@ -217,6 +219,8 @@ struct fk_pool {
   int64_t graph_replays = 0; // fk_attn_decode_layers calls replayed without recording
   int64_t skip_merge = 0;    // FK_OPT_DEBUG_SKIP_MERGE (diagnostic)
   int64_t append_first = 0;  // FK_OPT_APPEND_FIRST: fk_step_plan grows the rows first (attend own token)
+  int64_t group_fanout = 8;  // FK_OPT_GROUP_FANOUT: shared contexts with <= this many rows go to the private kernel
+                             // (measured: faster than tcgen05 up to 8 forks, slower at 16)
   bool plan_grew = false;    // the current plan already did the step's growth (fk_step_grow returns it)
   std::vector<int64_t> grow_pos, grow_ids;
   unsigned* tick = nullptr;  // device: private chunk tickets, one counter per partial half
@@ -534,6 +538,10 @@ int fk_pool_set_option(fk_pool* p, int32_t option, int64_t value) {
     case FK_OPT_CORUN: p->corun = value; break;
     case FK_OPT_PREFIX_RATE_PCT: p->prefix_rate_pct = std::max<int64_t>(1, value); break;
     case FK_OPT_APPEND_FIRST: p->append_first = value != 0; break;
+    case FK_OPT_GROUP_FANOUT:
+      if (value < 0 || value > 64) return fail(FK_INVALID_ARGUMENT, "group fan-out must be 0..64");
+      p->group_fanout = value;
+      break;
     case FK_OPT_DEBUG_SKIP_MERGE: p->skip_merge = value != 0; break;
     default: return fail(FK_INVALID_ARGUMENT, "unknown option %d", option);
   }
@@ -692,6 +700,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
         c->mark = epoch;
         c->fan = 1;
         c->sidx = -1;
+        c->gidx = -1;
         c->rank = 0;
         order.push_back(c);
       } else {
@@ -735,7 +744,22 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   const int64_t streamed_tokens = p->append_first ? count_tokens() : batch_tokens;
   // (after the growth: a leaf two generations share becomes shared once it has a token)
-  for (Ctx* c : order) c->shared = dedup && c->fan >= 2 && c->tokens > 0;
+  // Shared contexts with a small fan-out (<= FK_OPT_GROUP_FANOUT rows) are
+  // streamed by the private kernel for groups of up to 8 rows (one K/V read
+  // serves the group: the rows are the N of its transposed products); larger
+  // ones go to the prefix kernels.
+  int n_grouped = 0;
+  int64_t grouped_tokens = 0, grouped_tok_heads = 0;
+  for (Ctx* c : order) {
+    c->shared = dedup && c->fan >= 2 && c->tokens > 0;
+    if (c->shared && p->group_fanout > 0 && c->fan <= p->group_fanout && p->priv_wpc == kPrivWarpsPerCta) {
+      c->shared = false;
+      c->gidx = n_grouped++;
+      grouped_tokens += c->tokens;
+      grouped_tok_heads += c->tokens * H * ((c->fan + kGroupRows - 1) / kGroupRows);
+    }
+  }
+  shared_tokens += grouped_tokens;  // (streamed once per group: the dedup count holds them once)
 
   PT(T1);
   // ---- shared contexts (K2 work) --------------------------------------------
@@ -851,7 +875,8 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // the SMs in proportion to each side's bytes over its per-SM rate.
   int64_t priv_tok_heads = 0;
   for (const Ctx* c : chain)
-    if (!c->shared) priv_tok_heads += c->tokens * H;
+    if (!c->shared && c->gidx < 0) priv_tok_heads += c->tokens * H;
+  priv_tok_heads += grouped_tok_heads;
   // a 128-query block costs the softmax ~4/3 of a <= 64-query block per tile
   // (the 16-lane layout only covers fan-outs <= 64; measured 2.5 vs 1.9 us)
   double tc_tok_heads = 0.0;
@@ -1067,16 +1092,70 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
 
   PT(T4);
-  // ---- private streams (K3 work) ----------------------------------------------
-  std::vector<int32_t>& row_priv_off = S.row_priv_off;
-  std::vector<int32_t>& row_priv_np = S.row_priv_np;
-  row_priv_off.resize(B);
-  row_priv_np.resize(B);
+  // ---- private-kernel items (K3 work) -------------------------------------------
+  // An item is a run of page entries streamed once for a group of rows: the
+  // pages of a small-fan-out shared context (FK_OPT_GROUP_FANOUT, up to 8 rows
+  // per item; a context with more rows gets one item per 8) or one row's
+  // private chain (root -> leaf, contexts with fan-out 1).  Grouped items come
+  // first, then one item per row in row order (item B_g + r = row r).
+  std::vector<int32_t>& it_e0 = S.pit_e0;      // first entry (relative to the private base)
+  std::vector<int32_t>& it_np = S.pit_np;      // entries
+  std::vector<int32_t>& it_roff = S.pit_roff;  // rows at it_rows[it_roff ..]
+  std::vector<int32_t>& it_nrows = S.pit_nrows;
+  std::vector<int32_t>& it_rows = S.pit_rows;
+  it_e0.clear();
+  it_np.clear();
+  it_roff.clear();
+  it_nrows.clear();
+  it_rows.clear();
+  const int64_t priv_base = (int64_t)pages.size();
+  if (n_grouped > 0) {
+    // rows of each grouped context, row order
+    std::vector<int32_t>& grow_cnt = S.grow_cnt;
+    std::vector<int32_t>& grows = S.grows;
+    grow_cnt.assign(n_grouped + 1, 0);
+    for (const Ctx* c : chain)
+      if (c->gidx >= 0) grow_cnt[c->gidx + 1] += 1;
+    for (int gi = 0; gi < n_grouped; ++gi) grow_cnt[gi + 1] += grow_cnt[gi];
+    grows.resize(grow_cnt[n_grouped]);
+    std::vector<int32_t>& gfill = S.gfill;
+    gfill.assign(grow_cnt.begin(), grow_cnt.end() - 1);
+    for (int r = 0; r < B; ++r)
+      for (int32_t k = chain_off[r]; k < chain_off[r + 1]; ++k) {
+        const int32_t gi = chain[k]->gidx;
+        if (gi >= 0) grows[gfill[gi]++] = r;
+      }
+    for (const Ctx* c : order) {
+      if (c->gidx < 0) continue;
+      const int32_t r0 = grow_cnt[c->gidx], r1 = grow_cnt[c->gidx + 1];
+      const int32_t e0 = (int32_t)(pages.size() - priv_base);
+      for (size_t j = 0; j < c->phys.size(); ++j) {
+        const int64_t nt = std::min<int64_t>(kPage, c->tokens - (int64_t)j * kPage);
+        if (nt <= 0) break;
+        pages.push_back(c->phys[j]);
+        page_ntok.push_back((int32_t)nt);
+      }
+      const int32_t np = (int32_t)(pages.size() - priv_base) - e0;
+      for (int32_t a = r0; a < r1; a += kGroupRows) {
+        if (a > r0) {  // the next group streams the same pages again (L2)
+          for (int32_t j = 0; j < np; ++j) {
+            pages.push_back(pages[priv_base + e0 + j]);
+            page_ntok.push_back(page_ntok[priv_base + e0 + j]);
+          }
+        }
+        it_e0.push_back(a > r0 ? (int32_t)(pages.size() - priv_base) - np : e0);
+        it_np.push_back(np);
+        it_roff.push_back((int32_t)it_rows.size());
+        it_nrows.push_back(std::min<int32_t>(kGroupRows, r1 - a));
+        for (int32_t b = a; b < std::min<int32_t>(r1, a + kGroupRows); ++b) it_rows.push_back(grows[b]);
+      }
+    }
+  }
   for (int r = 0; r < B; ++r) {
-    row_priv_off[r] = (int32_t)pages.size();
+    const int32_t e0 = (int32_t)(pages.size() - priv_base);
     for (int32_t k = chain_off[r + 1] - 1; k >= chain_off[r]; --k) {  // root -> leaf
       const Ctx& c = *chain[k];
-      if (c.shared || c.tokens <= 0) continue;
+      if (c.shared || c.gidx >= 0 || c.tokens <= 0) continue;
       private_tokens += c.tokens;
       for (size_t j = 0; j < c.phys.size(); ++j) {
         const int64_t nt = std::min<int64_t>(kPage, c.tokens - (int64_t)j * kPage);
@@ -1085,20 +1164,19 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
         page_ntok.push_back((int32_t)nt);
       }
     }
-    row_priv_np[r] = (int32_t)pages.size() - row_priv_off[r];
+    it_e0.push_back(e0);
+    it_np.push_back((int32_t)(pages.size() - priv_base) - e0);
+    it_roff.push_back((int32_t)it_rows.size());
+    it_nrows.push_back(1);
+    it_rows.push_back(r);
   }
+  const int32_t n_pitems = (int32_t)it_e0.size();
   // private units (head, flat private entry), head-major
-  const int64_t priv_base = B > 0 ? row_priv_off[0] : (int64_t)pages.size();
   const int64_t NPT = (int64_t)pages.size() - priv_base;
-  std::vector<int32_t>& row_unit_off = S.row_unit_off;
-  std::vector<int32_t>& page_row = S.page_row;
-  row_unit_off.assign(std::max(B, 1), 0);
-  page_row.resize(std::max<int64_t>(NPT, 1));
-  page_row[0] = 0;
-  for (int r = 0; r < B; ++r) {
-    row_unit_off[r] = (int32_t)(row_priv_off[r] - priv_base);
-    std::fill_n(page_row.begin() + row_unit_off[r], row_priv_np[r], r);
-  }
+  std::vector<int32_t>& page_item = S.page_item;
+  page_item.resize(std::max<int64_t>(NPT, 1));
+  page_item[0] = 0;
+  for (int32_t k = 0; k < n_pitems; ++k) std::fill_n(page_item.begin() + it_e0[k], it_np[k], k);
   const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
   PT(T5);
@@ -1142,34 +1220,48 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // once), so its launch stays the same from step to step.
   const int64_t grid_ctas = (corun && p->launch_order == 1) ? priv_sms : p->num_sms;
   const int64_t G = grid_ctas * wpc;
-  // items (row, head) are contiguous unit ranges in unit order (head-major,
-  // rows in row order: their offsets only grow), so one forward sweep finds
-  // every item's chunks
+  // (item, head) runs are contiguous unit ranges in unit order (head-major,
+  // items in entry order), so one forward sweep finds every run's chunks; each
+  // row of an item gets that run's pieces as consecutive partial slots, after
+  // its tcgen05 / mma prefix pieces and its earlier items' pieces
   std::vector<int32_t>& row_head_count = S.row_head_count;
-  std::vector<int32_t>& rh_chunk0 = S.rh_chunk0;
-  row_head_count.assign(std::max<int64_t>((int64_t)B * H, 1), 0);
-  rh_chunk0.assign(std::max<int64_t>((int64_t)B * H, 1), 0);
-  int max_slots = 1;
+  std::vector<int32_t>& item_chunk0 = S.item_chunk0;
+  std::vector<int32_t>& item_slot = S.item_slot;  // [(it_roff[k] + j) * H + h]
+  std::vector<int32_t>& run_pieces = S.item_pieces;  // [item][H]
+  row_head_count.assign(row_head_base.begin(), row_head_base.end());
+  item_chunk0.assign(std::max<int64_t>((int64_t)n_pitems * H, 1), 0);
+  run_pieces.assign(std::max<int64_t>((int64_t)n_pitems * H, 1), 0);
+  item_slot.resize(std::max<size_t>(it_rows.size() * (size_t)H, 1));
   {
     const int32_t* cs = chunk_start.data();
     int64_t c = 0;  // chunk holding the current unit
     for (int64_t h = 0; h < H; ++h)
-      for (int r = 0; r < B; ++r) {
-        const int64_t np = row_priv_np[r];
-        int pieces = 0;
+      for (int32_t k = 0; k < n_pitems; ++k) {
+        const int64_t np = it_np[k];
         if (np > 0) {
-          const int64_t a0 = h * NPT + row_unit_off[r], b0 = a0 + np;
+          const int64_t a0 = h * NPT + it_e0[k], b0 = a0 + np;
           while (cs[c + 1] <= a0) ++c;
           const int64_t c0 = c;
           while (cs[c + 1] <= b0 - 1) ++c;
-          rh_chunk0[r * H + h] = (int32_t)c0;
-          pieces = (int)(c - c0 + 1);
+          item_chunk0[k * H + h] = (int32_t)c0;
+          run_pieces[k * H + h] = (int32_t)(c - c0 + 1);
         }
-        const int cnt = row_head_base[r * H + h] + pieces;
-        row_head_count[r * H + h] = cnt;
-        max_slots = std::max(max_slots, cnt);
       }
+    // slots, item by item in entry order (each row's runs follow one another)
+    for (int32_t k = 0; k < n_pitems; ++k) {
+      const int32_t* pc = run_pieces.data() + (size_t)k * H;
+      for (int32_t j = 0; j < it_nrows[k]; ++j) {
+        int32_t* cnt = row_head_count.data() + (size_t)it_rows[it_roff[k] + j] * H;
+        int32_t* sl = item_slot.data() + (size_t)(it_roff[k] + j) * H;
+        for (int64_t h = 0; h < H; ++h) {
+          sl[h] = cnt[h];
+          cnt[h] += pc[h];
+        }
+      }
+    }
   }
+  int max_slots = 1;
+  for (int32_t v : row_head_count) max_slots = std::max(max_slots, v);
   PT(T6);
   // synthetic keys: (leaf uid, leaf tokens at plan time + rank << 40)
   std::vector<int64_t>& row_uid = S.row_uid;
@@ -1197,7 +1289,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     info->shared_tokens = shared_tokens;
     info->private_tokens = private_tokens;
     info->num_rows = B;
-    info->num_shared_ctx = (int32_t)shared.size();
+    info->num_shared_ctx = (int32_t)shared.size() + n_grouped;  // (grouped: streamed by the private kernel)
     info->num_prefix_ctas = (int32_t)(num_mma + tc_ctas);
     info->max_slots = max_slots;
     info->num_tc_items = num_tc;
@@ -1230,9 +1322,25 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       dg.scalars({sh.page_off + it.page0, it.npages, it.ntok, sh.q_off + it.q0, it.nq, it.head, it_unit_off[i],
                   it_qslot_off[i], it.units});
     }
+    // (the round-1 per-row private layout, from the private items)
+    std::vector<int32_t>& row_priv_off = S.row_priv_off;
+    std::vector<int32_t>& row_priv_np = S.row_priv_np;
+    std::vector<int32_t>& row_unit_off = S.row_unit_off;
+    row_priv_off.resize(B);
+    row_priv_np.resize(B);
+    row_unit_off.assign(std::max(B, 1), 0);
+    for (int r = 0; r < B; ++r) {
+      const int32_t k = n_pitems - B + r;
+      row_priv_off[r] = (int32_t)priv_base + it_e0[k];
+      row_priv_np[r] = it_np[k];
+      row_unit_off[r] = it_e0[k];
+    }
     dg.vec(qrows); dg.vec(qslot); dg.vec(row_priv_off); dg.vec(row_priv_np); dg.vec(row_unit_off);
     dg.vec(row_head_base); dg.vec(row_head_count); dg.vec(pages); dg.vec(page_ntok); dg.vec(row_uid); dg.vec(row_pos);
-    dg.vec(page_row); dg.span(chunk_start.data(), nchunks + 1); dg.vec(rh_chunk0); dg.vec(ch_item); dg.vec(ch_t0); dg.vec(ch_t1);
+    dg.vec(page_item); dg.span(chunk_start.data(), nchunks + 1); dg.vec(item_chunk0);
+    if (n_pitems > B) {  // grouped items (not in the round-1 planner)
+      dg.vec(it_e0); dg.vec(it_np); dg.vec(it_nrows); dg.vec(it_rows); dg.vec(item_slot);
+    } dg.vec(ch_item); dg.vec(ch_t0); dg.vec(ch_t1);
     dg.vec(it_first_chunk); dg.vec(cta_chunk0);
     p->plan_digest = dg.h;
   }
@@ -1253,7 +1361,6 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_it = L.add(sizeof(int32_t) * 9 * ni);
   const size_t o_q = L.add(sizeof(int32_t) * std::max<size_t>(qrows.size(), 1));
   const size_t o_qs = L.add(sizeof(int32_t) * std::max<size_t>(qslot.size(), 1));
-  const size_t o_rows = L.add(sizeof(int32_t) * 3 * nb);
   const size_t o_rh = L.add(sizeof(int32_t) * 2 * nbh);
   const size_t o_pages = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
   const size_t o_pnt = L.add(sizeof(int32_t) * std::max<size_t>(pages.size(), 1));
@@ -1261,9 +1368,13 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const size_t o_pos = L.add(sizeof(int64_t) * nb);
   const size_t o_app = L.add(sizeof(int32_t) * 2 * nb);
   const size_t o_apos = L.add(sizeof(int64_t) * nb);
-  const size_t o_prow = L.add(sizeof(int32_t) * page_row.size());
+  const size_t o_prow = L.add(sizeof(int32_t) * page_item.size());
   const size_t o_cs = L.add(sizeof(int32_t) * (size_t)(nchunks + 1));
-  const size_t o_rhc = L.add(sizeof(int32_t) * rh_chunk0.size());
+  const size_t o_rhc = L.add(sizeof(int32_t) * item_chunk0.size());
+  const size_t npi = (size_t)std::max(n_pitems, 1);
+  const size_t o_pit = L.add(sizeof(int32_t) * 2 * npi);  // nrows, roff
+  const size_t o_pir = L.add(sizeof(int32_t) * std::max<size_t>(it_rows.size(), 1));
+  const size_t o_pis = L.add(sizeof(int32_t) * item_slot.size());
   const size_t nchb = sizeof(int32_t) * std::max<size_t>(ch_item.size(), 1);
   const size_t o_chi = L.add(nchb);
   const size_t o_ch0 = L.add(nchb);
@@ -1305,12 +1416,6 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   }
   put(o_q, qrows.data(), qrows.size() * 4);
   put(o_qs, qslot.data(), qslot.size() * 4);
-  int32_t* rb = (int32_t*)(h + o_rows);
-  for (int r = 0; r < B; ++r) {
-    rb[0 * nb + r] = row_priv_off[r];
-    rb[1 * nb + r] = row_priv_np[r];
-    rb[2 * nb + r] = row_unit_off[r];
-  }
   put(o_rh, row_head_base.data(), row_head_base.size() * 4);
   put(o_rh + nbh * 4, row_head_count.data(), row_head_count.size() * 4);
   put(o_pages, pages.data(), pages.size() * 4);
@@ -1323,9 +1428,13 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
     ab[nb + r] = 0;
   }
   memset(h + o_apos, 0, nb * 8);
-  put(o_prow, page_row.data(), page_row.size() * 4);
+  put(o_prow, page_item.data(), page_item.size() * 4);
   put(o_cs, chunk_start.data(), (size_t)(nchunks + 1) * 4);
-  put(o_rhc, rh_chunk0.data(), rh_chunk0.size() * 4);
+  put(o_rhc, item_chunk0.data(), item_chunk0.size() * 4);
+  put(o_pit, it_nrows.data(), (size_t)n_pitems * 4);
+  put(o_pit + npi * 4, it_roff.data(), (size_t)n_pitems * 4);
+  put(o_pir, it_rows.data(), it_rows.size() * 4);
+  put(o_pis, item_slot.data(), item_slot.size() * 4);
   put(o_chi, ch_item.data(), ch_item.size() * 4);
   put(o_ch0, ch_t0.data(), ch_t0.size() * 4);
   put(o_ch1, ch_t1.data(), ch_t1.size() * 4);
@@ -1368,10 +1477,6 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.it_first_chunk = (const int32_t*)(d + o_ifc);
   pd.tc_cta_chunk0 = (const int32_t*)(d + o_cc0);
   pd.tc_l2_share = tc_l2_share ? 1 : 0;
-  const int32_t* drb = (const int32_t*)(d + o_rows);
-  pd.row_priv_off = drb;
-  pd.row_priv_npages = drb + nb;
-  pd.row_unit_off = drb + 2 * nb;
   pd.row_head_base = (const int32_t*)(d + o_rh);
   pd.row_head_count = (const int32_t*)(d + o_rh) + nbh;
   pd.pages = (const int32_t*)(d + o_pages);
@@ -1381,7 +1486,11 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.app_page = (const int32_t*)(d + o_app);
   pd.app_slot = (const int32_t*)(d + o_app) + nb;
   pd.app_pos = (const long long*)(d + o_apos);
-  pd.page_row = (const int32_t*)(d + o_prow);
+  pd.page_item = (const int32_t*)(d + o_prow);
+  pd.item_nrows = (const int32_t*)(d + o_pit);
+  pd.item_roff = (const int32_t*)(d + o_pit) + npi;
+  pd.item_rows = (const int32_t*)(d + o_pir);
+  pd.item_slot = (const int32_t*)(d + o_pis);
   pd.priv_base = (int)priv_base;
   pd.priv_np = (int)NPT;
   pd.priv_units = (int)U;
@@ -1390,7 +1499,9 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   pd.priv_warps = (int)G;
   pd.priv_static = p->priv_static_first ? (int)std::min<int64_t>(std::min<int64_t>(w_active, G), nchunks) : 0;
   pd.priv_chunk_start = (const int32_t*)(d + o_cs);
-  pd.priv_rh_chunk0 = (const int32_t*)(d + o_rhc);
+  pd.item_chunk0 = (const int32_t*)(d + o_rhc);
+  pd.n_gitems = n_pitems - B;
+  pd.n_grows = (int)it_rows.size() - B;
   p->off_app_page = o_app;
   p->off_app_slot = o_app + nb * 4;
   p->off_app_pos = o_apos;
@@ -1474,7 +1585,11 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
     FK_CUDA(cudaMemsetAsync(a.tick, 0, sizeof(unsigned), st));
     return FK_OK;
   }
-  FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, 4 * p->num_sms, p->pdl != 0, st), "merge");
+  // (plans with many partials per (row, head): one CTA of 8 warps per item;
+  // the grid stays fixed either way, so the launch does not change per step)
+  const bool wide = p->plan.max_slots > kWideSlots;
+  FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, wide ? 2 * p->num_sms : 4 * p->num_sms, p->pdl != 0, wide, st),
+            "merge");
 #undef FK_LAUNCH
   return FK_OK;
 }
@@ -1533,6 +1648,7 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   key.pdl = (int32_t)p->pdl;
   key.launch_order = (int32_t)p->launch_order;
   key.plan_slot = p->plan_base + p->cur;
+  key.wide_merge = p->plan.max_slots > kWideSlots;
   const bool check = getenv("FK_DEBUG_GRAPH_CHECK") != nullptr;  // (read per call: tests set it)
   const bool key_hit = G.exec && G.key_ok && G.stream == st && p->have_plan && p->plan.num_rows > 0 &&
                        !p->skip_merge && memcmp(&G.key, &key, sizeof(key)) == 0;

@@ -8,6 +8,8 @@ the one-token growth in between.
 Written once with the round-1 planner (plan_digests.json); the planner was
 then rewritten for host speed and must reproduce every digest
 (tests/test_plan.py::test_plan_digests_pinned runs --check in a subprocess).
+The FK_OPT_GROUP_FANOUT option sets (opt9, opt10) were added afterwards by the
+grouped planner (--add: writes only keys the file does not have).
 """
 
 import ctypes
@@ -33,6 +35,9 @@ OPTION_SETS = [
     {_lib.FK_OPT_PRIV_STATIC_FIRST: 0, _lib.FK_OPT_TC_BOUNDARY_COST: 0},
     {_lib.FK_OPT_APPEND_FIRST: 1},
     {_lib.FK_OPT_MIN_SPLIT_PAGES: 16, _lib.FK_OPT_TC_MIN_FANOUT: 0, _lib.FK_OPT_LAUNCH_ORDER: 1},
+    # (round 2, written by the grouped planner: regression pins, not round-1 parity)
+    {_lib.FK_OPT_GROUP_FANOUT: 8},
+    {_lib.FK_OPT_GROUP_FANOUT: 16, _lib.FK_OPT_TC_MIN_FANOUT: 0, _lib.FK_OPT_APPEND_FIRST: 1},
 ]
 
 
@@ -89,15 +94,17 @@ def run():
     lib.fk_debug_plan_digest.restype = ctypes.c_uint64
     lib.fk_debug_plan_digest.argtypes = [ctypes.c_void_p]
     out = {}
-    for name, H, build in forest_cases():
+    for ci, (name, H, build) in enumerate(forest_cases()):
         for oi, opts in enumerate(OPTION_SETS):
-            for dedup in (1, 0):
-                rng = random.Random(len(out) + 17)
+            for di, dedup in enumerate((1, 0)):
+                # (the seeds of the 9 round-1 option sets are their original enumeration index)
+                rng = random.Random((ci * 9 + oi) * 2 + di + 17 if oi < 9 else 100000 + (ci * 100 + oi) * 2 + di)
                 ctxs, leaves = build(rng)
                 desc = _lib.PoolDesc(2, H, 128, 16, 1 << 22, 0, -1, 0)
                 pool = ctypes.c_void_p()
                 _lib.check(lib.fk_pool_create(ctypes.byref(desc), ctypes.byref(pool)))
-                for k, v in opts.items():
+                # (the round-1 planner had no row groups: its sets run with them off)
+                for k, v in ({_lib.FK_OPT_GROUP_FANOUT: 0, **opts} if oi < 9 else opts).items():
                     _lib.check(lib.fk_pool_set_option(pool, k, v))
                 ids = (ctypes.c_int64 * 4096)()
                 n = ctypes.c_int64()
@@ -130,6 +137,10 @@ def main():
         for k in bad[:10]:
             print("MISMATCH", k, want[k], got.get(k))
         sys.exit(1 if bad else 0)
+    if "--add" in sys.argv:
+        want = json.load(open(OUT))
+        assert all(want[k] == got[k] for k in want), "existing digests changed"
+        got = {**got, **want}
     with open(OUT, "w") as f:
         json.dump(got, f, indent=0, sort_keys=True)
     print(f"wrote {len(got)} digests to {OUT}")

@@ -25,10 +25,12 @@ pytestmark = pytest.mark.gpu
 PATH = {"path": "mma"}
 
 
-@pytest.fixture(params=["mma", "tc"], autouse=True)
+@pytest.fixture(params=["mma", "tc", "grp"], autouse=True)
 def prefix_path(request):
     """Every case runs with the shared prefixes on the warp-level mma.sync
-    kernel and again on the tcgen05 kernel (fan-out threshold 2)."""
+    kernel, on the tcgen05 kernel (fan-out threshold 2), and with shared
+    contexts of fan-out <= 16 streamed by the private kernel for groups of up
+    to 8 rows (FK_OPT_GROUP_FANOUT=16; larger fan-outs on tcgen05)."""
     PATH["path"] = request.param
     yield request.param
 
@@ -37,7 +39,8 @@ def make_engine(cuda_device, H, L=1, shared=True, k_scale=1.0, seed=0x5EED, kv_t
     eng = P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=kv_tokens, device=cuda_device,
                       geometry=P.ModelGeometry(L, H, 128), model=P.SyntheticDecodeModel(seed, k_scale),
                       capture_f32=True, keep_history=True, **kw)
-    eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, 2 if PATH["path"] == "tc" else 0)
+    eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, 0 if PATH["path"] == "mma" else 2)
+    eng.set_option(_lib.FK_OPT_GROUP_FANOUT, 16 if PATH["path"] == "grp" else 0)
     return eng
 
 

@@ -32,10 +32,13 @@ def random_forest(seed, shared=True):
     return eng, twin, leaves
 
 
-@pytest.mark.parametrize("shared", [True, False])
-def test_plan_batch_tokens_matches_walk_and_twin(shared):
+@pytest.mark.parametrize("shared,group", [(True, 0), (False, 0), (True, 8), (True, 16)])
+def test_plan_batch_tokens_matches_walk_and_twin(shared, group):
+    """(group > 0: small-fan-out shared contexts go to the private kernel as
+    row groups -- FK_OPT_GROUP_FANOUT -- and still count once)"""
     for seed in range(60):
         eng, twin, leaves = random_forest(seed, shared)
+        eng.set_option(P._lib.FK_OPT_GROUP_FANOUT, group)
         running = [g for g in eng.gens.values() if g.started and not g.done]
         bt = eng._plan(running)
         info = eng.last_plan
@@ -81,10 +84,11 @@ def test_nested_plan_counts_every_level_once():
 
 
 def test_plan_digests_pinned():
-    """Every array and scalar the planner uploads, for 558 (forest, options,
-    dedup) cases x 3 steps, equals the digests the round-1 planner wrote
-    (tests/golden/make_plan_digests.py): the host-speed rewrite of
-    fk_step_plan changed no plan."""
+    """Every array and scalar the planner uploads, for 682 (forest, options,
+    dedup) cases x 3 steps, equals the pinned digests
+    (tests/golden/make_plan_digests.py): 558 were written by the round-1
+    planner, so the host-speed rewrite of fk_step_plan changed no plan; the
+    124 FK_OPT_GROUP_FANOUT cases pin the grouped planner."""
     import os
     import subprocess
     import sys
