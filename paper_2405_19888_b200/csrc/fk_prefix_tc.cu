@@ -124,7 +124,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
   TL(160);
   CTA_TL_START(fk_tl_cta_prefix, layer);
 
-  if (threadIdx.x == 0) {
+  // The producer's first chunk metadata and page window (three dependent
+  // global loads) are fetched while warps 1 and 2 set up TMEM and the
+  // barriers, so the first TMA load goes out right after the CTA barrier.
+  int sidx = 0, send = 0, f_item = 0, f_tile0 = 0, f_tile1 = 0, f_head = 0, f_npi = 0, f_poff = 0, f_win = 0, f_nwin = 0;
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      prefetch_tmap(&tmap_run);
+    }
+    sidx = p.tc_cta_chunk0[blockIdx.x];
+    send = p.tc_cta_chunk0[blockIdx.x + 1];
+    f_item = p.tc_chunk_item[sidx];
+    f_tile0 = p.tc_chunk_tile0[sidx];
+    f_tile1 = p.tc_chunk_tile1[sidx];
+    f_head = p.it_head[f_item];
+    f_npi = p.it_npages[f_item];
+    f_poff = p.it_page_off[f_item];
+    const int wb = f_tile0 * kTcTilePages;
+    f_win = wb + lane < f_npi ? p.pages[f_poff + wb + lane] : 0;
+    f_nwin = wb + 32 + lane < f_npi ? p.pages[f_poff + wb + 32 + lane] : 0;
+  }
+  if (threadIdx.x == 64) {  // (warp 2: warp 0 is busy with the loads above)
     for (int s = 0; s < kTcKStages; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -160,12 +181,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     // into a 2 x 32-entry register window; the next chunk's item metadata and
     // first window are fetched over the following two tiles, so a chunk
     // switch never waits on a dependent global load.  Lane 0 issues the TMA.
-    if (lane == 0) {
-      prefetch_tmap(&tmap);
-      prefetch_tmap(&tmap_run);
-    }
-    int sidx = p.tc_cta_chunk0[blockIdx.x];
-    const int send = p.tc_cta_chunk0[blockIdx.x + 1];
     auto grab = [&]() -> int { return sidx < send ? sidx++ : -1; };
     auto post = [&](int i, int chunk) {
       if (lane == 0) {
@@ -175,14 +190,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) fk_prefix_tc_kernel(ArenaDev a,
     };
     TcCursor c;
     c.qi = 0;
-    tc_load_chunk(p, c, grab());  // every CTA has at least one static chunk
+    c.chunk = grab();  // every CTA has at least one static chunk (prefetched above)
+    c.item = f_item;
+    c.tile = f_tile0;
+    c.tile1 = f_tile1;
     post(0, c.chunk);
     int nxt = grab();  // the chunk after the current one, posted right away
     post(1, nxt);
-    int head = p.it_head[c.item], npi = p.it_npages[c.item], poff = p.it_page_off[c.item];
+    int head = f_head, npi = f_npi, poff = f_poff;
     int wbase = c.tile * kTcTilePages;
-    int win = wbase + lane < npi ? p.pages[poff + wbase + lane] : 0;
-    int nwin = wbase + 32 + lane < npi ? p.pages[poff + wbase + 32 + lane] : 0;
+    int win = f_win, nwin = f_nwin;
     int n_item = 0, n_tile0 = 0, n_tile1 = 0, n_head = 0, n_npi = 0, n_poff = 0, n_win = 0, n_nwin = 0;
     int n_stage = 0;  // 0 nothing, 1 metadata, 2 metadata + first window of chunk `nxt`
     for (int t = 0;; ++t) {
