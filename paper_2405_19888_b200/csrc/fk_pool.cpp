@@ -6,6 +6,7 @@
 #include "fk_internal.h"
 
 #include <cuda_bf16.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -243,6 +244,27 @@ struct fk_pool {
 };
 
 namespace {
+
+// NVTX ranges around the host entry points of the step (SURVEY §5 tracing):
+// `ncu --nvtx --nvtx-include "fk_attn_decode_layers/"` selects one call's
+// kernels, a timeline tool shows plan / attention / growth / append per step.
+// (Push/pop cost a few ns without a tool attached.)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* name, int64_t payload) {
+    nvtxEventAttributes_t e = {};
+    e.version = NVTX_VERSION;
+    e.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    e.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    e.message.ascii = name;
+    e.payloadType = NVTX_PAYLOAD_TYPE_INT64;
+    e.payload.llValue = payload;
+    nvtxRangePushEx(&e);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 int64_t blocks_for(int64_t tokens, int64_t bs) { return (tokens + bs - 1) / bs; }
 
@@ -669,6 +691,7 @@ int fk_ctx_blocks(const fk_pool* p, int64_t ctx, int64_t* logical, int32_t* phys
 
 int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, void* stream,
                  fk_plan_info* info) {
+  NvtxRange nvtx("fk_step_plan", B);
   static const bool plan_timing = getenv("FK_DEBUG_TIMING") != nullptr;
   double pt[8] = {0};
 #define PT(n) do { if (plan_timing) pt[#n[1] - '0'] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); } while (0)
@@ -1522,6 +1545,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
 
 int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* out_f32,
                    void* stream) {
+  NvtxRange nvtx("fk_attn_decode", layer);
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan: call fk_step_plan first");
@@ -1602,6 +1626,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
 int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void* q, int64_t q_layer_stride,
                           void* out, int64_t out_layer_stride, float* out_f32, int64_t f32_layer_stride,
                           void* stream) {
+  NvtxRange nvtx("fk_attn_decode_layers", nlayers);
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (nlayers < 0 || layer0 < 0 || layer0 + nlayers > p->desc.num_layers)
     return fail(FK_INVALID_ARGUMENT, "bad layer range [%d, %d)", layer0, layer0 + nlayers);
@@ -1778,6 +1803,7 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
 }
 
 int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids, int32_t* n_failed) {
+  NvtxRange nvtx("fk_step_grow");
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   const int B = (int)p->plan_leaves.size();
@@ -1814,6 +1840,7 @@ int fk_step_grow(fk_pool* p, int64_t* positions, int64_t* new_ids, int32_t* n_fa
 }
 
 int fk_step_commit(fk_pool* p, const int64_t* positions, void* stream) {
+  NvtxRange nvtx("fk_step_commit");
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->have_plan) return fail(FK_INVALID_ARGUMENT, "no plan");
   const int B = (int)p->plan_leaves.size();
@@ -1858,6 +1885,7 @@ int fk_append_kv(fk_pool* p, int32_t layer, const void* k, const void* v, void* 
 
 int fk_append_kv_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void* k, const void* v,
                         void* stream) {
+  NvtxRange nvtx("fk_append_kv_layers", nlayers);
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (!p->committed) return fail(FK_INVALID_ARGUMENT, "fk_step_commit not called for this plan");
@@ -1872,6 +1900,7 @@ int fk_append_kv_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const void*
 
 int fk_synth_fill(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, uint64_t seed,
                   float k_scale, void* stream) {
+  NvtxRange nvtx("fk_synth_fill", pos1 - pos0);
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   auto it = p->ctxs.find(ctx);
@@ -1895,6 +1924,7 @@ int fk_synth_fill(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, uint64_t 
 
 int fk_fill_kv(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, int32_t layer0, int32_t nlayers,
                const void* k, const void* v, void* stream) {
+  NvtxRange nvtx("fk_fill_kv", pos1 - pos0);
   if (!p) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!p->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   auto it = p->ctxs.find(ctx);
@@ -1922,6 +1952,7 @@ int fk_fill_kv(fk_pool* p, int64_t ctx, int64_t pos0, int64_t pos1, int32_t laye
 
 int fk_ctx_copy_kv(fk_pool* dst, int64_t dst_ctx, const fk_pool* src, int64_t src_ctx, int64_t ntok,
                    void* stream) {
+  NvtxRange nvtx("fk_ctx_copy_kv", ntok);
   if (!dst || !src) return fail(FK_INVALID_ARGUMENT, "null pool");
   if (!dst->on_device || !src->on_device) return fail(FK_NO_DEVICE, "host-only pool has no device arena");
   if (dst->desc.num_layers != src->desc.num_layers || dst->desc.num_heads != src->desc.num_heads ||

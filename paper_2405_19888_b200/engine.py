@@ -35,6 +35,7 @@ from .errors import ContextBusy, OutOfMemory, UnknownContext, UnknownParentConte
 
 MS = 1_000_000  # ns per millisecond
 _PHASES = bool(os.environ.get("FK_DEBUG_TIMING"))  # per-phase host time of step() (profiles/host_step.py)
+_NVTX = bool(os.environ.get("FK_NVTX"))  # an NVTX range per GpuEngine.step (the C++ entry points always emit theirs)
 FNV64_EMPTY = 0xCBF29CE484222325
 
 
@@ -1096,6 +1097,15 @@ class GpuEngine(_EngineBase):
     def step(self) -> Optional[StepReport]:
         if not self.has_work():
             return None
+        if _NVTX and self.device is not None:
+            self._torch.cuda.nvtx.range_push(f"GpuEngine.step {self.engine_id}")
+            try:
+                return self._step()
+            finally:
+                self._torch.cuda.nvtx.range_pop()
+        return self._step()
+
+    def _step(self) -> Optional[StepReport]:
         if _PHASES:
             tm = [time.perf_counter()]
         started_ns = self.clock_ns
