@@ -19,7 +19,16 @@ constexpr int kTcMaxChunk = 24;   // largest tcgen05 chunk (tiles)
 constexpr int kPrivWarpsPerCta = 10;  // private kernel default shape: 10 warps per CTA x 2 stages (measured best)
 constexpr int kPrivMinChunk = 2;     // private guided schedule: smallest chunk (pages), default
 constexpr int kPrivMaxChunk = 32;    // largest chunk (one lane-parallel metadata load)
-constexpr int kWideSlots = 32;       // plans with more partials per (row, head) merge with a CTA per item
+constexpr int kWideSlots = 32;       // plans with more partials per (row, head) and few (row, head) items
+                                     // merge with a CTA per item (fk_merge_wide_kernel)
+constexpr int kNarrowMaxSlots = 128; // the warp-per-item merge's register rounds
+// The merge kernel for a plan: a CTA per (row, head) when items are many
+// partials each and few (a few rows: ~200 pieces per head), a warp per item
+// otherwise -- thousands of items (map-reduce: 2560 with ~40 pieces) keep all
+// of the fixed grid's warps busy in one pass.
+inline bool wide_merge(int max_slots, int rows, int heads, int num_sms) {
+  return max_slots > kNarrowMaxSlots || (max_slots > kWideSlots && rows * heads <= 4 * num_sms);
+}
 constexpr int kGroupRows = 8;        // rows per private-kernel item (the N of its m16n8 products)
 
 // Device view of one step plan.  All arrays live in one device buffer.

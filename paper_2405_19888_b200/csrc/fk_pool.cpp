@@ -1616,7 +1616,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   }
   // (plans with many partials per (row, head): one CTA of 8 warps per item;
   // the grid stays fixed either way, so the launch does not change per step)
-  const bool wide = p->plan.max_slots > kWideSlots;
+  const bool wide = wide_merge(p->plan.max_slots, p->plan.num_rows, p->desc.num_heads, p->num_sms);
   FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, wide ? 2 * p->num_sms : 4 * p->num_sms, p->pdl != 0, wide, st),
             "merge");
 #undef FK_LAUNCH
@@ -1678,7 +1678,7 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   key.pdl = (int32_t)p->pdl;
   key.launch_order = (int32_t)p->launch_order;
   key.plan_slot = p->plan_base + p->cur;
-  key.wide_merge = p->plan.max_slots > kWideSlots;
+  key.wide_merge = wide_merge(p->plan.max_slots, p->plan.num_rows, p->desc.num_heads, p->num_sms);
   const bool check = getenv("FK_DEBUG_GRAPH_CHECK") != nullptr;  // (read per call: tests set it)
   const bool key_hit = G.exec && G.key_ok && G.stream == st && p->have_plan && p->plan.num_rows > 0 &&
                        !p->skip_merge && memcmp(&G.key, &key, sizeof(key)) == 0;
