@@ -141,7 +141,7 @@ struct ReplayKey {
   const void *q, *out, *out_f32;
   int64_t q_stride, out_stride, f32_stride;
   int32_t tc_begin, num_items, tc_grid, tc_ctas, priv_any, priv_wpc, priv_grid, num_sms, pdl, launch_order, plan_slot;
-  int32_t wide_merge;
+  int32_t wide_merge, grouped;  // (grouped: the private kernel's row-group instantiation)
 };
 static_assert(sizeof(ReplayKey) % 8 == 0, "ReplayKey is compared bytewise");
 
@@ -1669,8 +1669,11 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   key.f32_stride = f32_layer_stride;
   key.tc_begin = p->plan.tc_begin;
   key.num_items = p->plan.num_items;
-  key.tc_grid = p->plan.tc_grid;
-  key.tc_ctas = p->plan.tc_ctas;
+  // (the prefix launch depends on the plan's CTA count only through its grid,
+  // max(tc_grid, tc_ctas), and whether there is one: the count itself lives in
+  // the __constant__ plan and may move from step to step under a serving load)
+  key.tc_grid = p->plan.tc_ctas > 0 ? std::max(p->plan.tc_grid, p->plan.tc_ctas) : 0;
+  key.tc_ctas = p->plan.tc_ctas > 0;
   key.priv_any = p->plan.priv_units > 0;
   key.priv_wpc = p->plan.priv_wpc;
   key.priv_grid = p->priv_grid;
@@ -1679,6 +1682,7 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   key.launch_order = (int32_t)p->launch_order;
   key.plan_slot = p->plan_base + p->cur;
   key.wide_merge = wide_merge(p->plan.max_slots, p->plan.num_rows, p->desc.num_heads, p->num_sms);
+  key.grouped = p->plan.n_gitems > 0;
   const bool check = getenv("FK_DEBUG_GRAPH_CHECK") != nullptr;  // (read per call: tests set it)
   const bool key_hit = G.exec && G.key_ok && G.stream == st && p->have_plan && p->plan.num_rows > 0 &&
                        !p->skip_merge && memcmp(&G.key, &key, sizeof(key)) == 0;
