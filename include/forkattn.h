@@ -115,7 +115,8 @@ enum {
                                  start under the previous layer's merge -- only when q is not
                                  written by the kernel launched right before fk_attn_decode */
   FK_OPT_PRIV_MIN_CHUNK = 8,  /* smallest chunk (pages) of the private kernel's guided dynamic
-                                 schedule, 1..32 (default 2): the granularity of its tail */
+                                 schedule, 1..32: the granularity of its tail; 0 (default): 2, or
+                                 4 for plans under 32K (head, page) units (a few rows) */
   FK_OPT_PRIV_STATIC_FIRST = 9, /* 1 (default): the private warps that start at once take their
                                  first chunk by warp index instead of a ticket */
   FK_OPT_PRIV_WARPS = 11,     /* private CTA shape: 10 warps x 2 stages (default), 8 x 3 or 12 x 2 */
@@ -132,9 +133,10 @@ enum {
                                  runs fk_attn_decode.  fk_plan_info.batch_tokens stays the
                                  reference's pre-growth count.  0 (default): the reference's span
                                  (chain tokens at step start, engine.py:416-434), append after */
-  FK_OPT_GROUP_FANOUT = 18,   /* shared contexts read by <= this many rows (0..64) are streamed by the
-                                 private kernel once per group of up to 8 rows -- the rows are the N of
-                                 its transposed m16n8 products -- instead of by a prefix kernel */
+  FK_OPT_GROUP_FANOUT = 18,   /* shared contexts read by <= this many rows (0..64, default 8) are
+                                 streamed by the private kernel once per group of up to 8 rows -- the
+                                 rows are the N of its transposed m16n8 products -- instead of by a
+                                 prefix kernel (default CTA shape only); 0 = off */
   FK_OPT_DEBUG_SKIP_MERGE = 90 /* diagnostic only: 1 = do not launch the LSE merge (outputs are NOT
                                  written); bounds the time the merge adds to a layer */
 };

@@ -26,8 +26,12 @@ def main():
     ap.add_argument("--opt", action="append", default=[])
     ap.add_argument("--isolated", action="store_true",
                     help="stamps of bench.time_layers_isolated (direct launches, a foreign kernel between layers)")
+    ap.add_argument("--shape", default=None, help="P,B,S[,L,H]: fork group shape instead of --config")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
+    if args.shape:
+        v = [int(x) for x in args.shape.split(",")]
+        cfg = dict(model="custom", P=v[0], B=v[1], S=v[2], L=v[3] if len(v) > 3 else 40, H=v[4] if len(v) > 4 else 40)
     eng, rows = bench.build_engine(cfg, 0, torch, out_len=32)
     for kv in args.opt:
         k, v = kv.split("=")
