@@ -57,8 +57,11 @@ def main():
     t0 = None
     for par in pars:
         pre = [x for x in out["prefix"][par][:info.num_prefix_ctas] if x[0]]
-        t_last = max(s for s, _ in pre)
-        pre = [x for x in pre if x[0] >= t_last - 20000]
+        if pre:
+            t_last = max(s for s, _ in pre)
+            pre = [x for x in pre if x[0] >= t_last - 20000]
+        else:  # (no prefix kernel: small fan-outs stream in the private kernel)
+            t_last = max(s for s, _ in out["priv"][par] if s)
         priv = [x for x in out["priv"][par] if x[0] and abs(x[0] - t_last) < 60000 and x[1] >= x[0]]
         if t0 is None:
             t0 = min(s for s, _ in pre + priv)
@@ -75,7 +78,7 @@ def main():
     par = pars[-1]
     print("last layer prefix CTAs (tiles, pieces, duration us):")
     print(" ".join("%d/%d/%.0f" % (notes[par][i][0], notes[par][i][1], (out["prefix"][par][i][1] - out["prefix"][par][i][0]) / 1e3)
-                   for i in range(info.num_prefix_ctas)))
+                   for i in range(info.num_prefix_ctas)) or "-")
     print("plan:", info.num_rows, "rows", info.num_prefix_ctas, "prefix CTAs", info.max_slots, "slots")
 
 
