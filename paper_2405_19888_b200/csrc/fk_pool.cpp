@@ -1666,7 +1666,7 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   key.out_f32 = out_f32;
   key.q_stride = q_layer_stride;
   key.out_stride = out_layer_stride;
-  key.f32_stride = f32_layer_stride;
+  key.f32_stride = out_f32 ? f32_layer_stride : 0;  // (no f32 output: the stride is never used)
   key.tc_begin = p->plan.tc_begin;
   key.num_items = p->plan.num_items;
   // (the prefix launch depends on the plan's CTA count only through its grid,
@@ -1686,6 +1686,14 @@ int fk_attn_decode_layers(fk_pool* p, int32_t layer0, int32_t nlayers, const voi
   const bool check = getenv("FK_DEBUG_GRAPH_CHECK") != nullptr;  // (read per call: tests set it)
   const bool key_hit = G.exec && G.key_ok && G.stream == st && p->have_plan && p->plan.num_rows > 0 &&
                        !p->skip_merge && memcmp(&G.key, &key, sizeof(key)) == 0;
+  static const bool key_debug = getenv("FK_DEBUG_GRAPH_KEY") != nullptr;
+  if (key_debug && G.exec && G.key_ok && !key_hit) {  // which 8-byte word of the key moved
+    const uint64_t *a = (const uint64_t*)&G.key, *b = (const uint64_t*)&key;
+    fprintf(stderr, "fk graph key miss: words");
+    for (size_t w = 0; w < sizeof(key) / 8; ++w)
+      if (a[w] != b[w]) fprintf(stderr, " %zu", w);
+    fprintf(stderr, "\n");
+  }
   if (key_hit && !check) {
     FK_CUDA(cudaGraphLaunch(G.exec, st));
     p->launch_parity = par0 ^ (nlayers & 1);  // as the recorded run would have left it

@@ -990,7 +990,7 @@ class GpuEngine(_EngineBase):
             # replays the layers' kernels (fk_attn_decode_layers, a CUDA graph)
             _lib.check(_lib.lib.fk_attn_decode_layers(
                 self._pool.handle, 0, geo.num_layers, q.data_ptr(), q_stride, out.data_ptr(), out_stride,
-                f32.data_ptr() if f32 is not None else None, B * row_bytes * 2, self._spv))
+                f32.data_ptr() if f32 is not None else None, B * row_bytes * 2 if f32 is not None else 0, self._spv))
             self.last_output = out
             self.last_output_f32 = f32
             if tensor_model and model.copy_out:
