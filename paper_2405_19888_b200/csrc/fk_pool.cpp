@@ -1608,7 +1608,9 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
     int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;
   }
-  // fixed merge grid (warps loop over (row, head)): 4 CTAs of 8 warps per SM
+  // fixed merge grid (warps loop over (row, head)): 3 CTAs of 8 warps per SM -- as many as
+  // its registers let be resident at once (a 4th wave measured 0.5-0.8 % slower per step, 2
+  // per SM slower still)
   if (p->skip_merge) {  // diagnostic: no merge (and the ticket half reset by a memset)
     if (fk::g_launch_rec) return fail(FK_INVALID_ARGUMENT, "FK_OPT_DEBUG_SKIP_MERGE needs FK_OPT_GRAPH=0");
     FK_CUDA(cudaMemsetAsync(a.tick, 0, sizeof(unsigned), st));
@@ -1617,7 +1619,7 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   // (plans with many partials per (row, head): one CTA of 8 warps per item;
   // the grid stays fixed either way, so the launch does not change per step)
   const bool wide = wide_merge(p->plan.max_slots, p->plan.num_rows, p->desc.num_heads, p->num_sms);
-  FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, wide ? 2 * p->num_sms : 4 * p->num_sms, p->pdl != 0, wide, st),
+  FK_LAUNCH(launch_merge(a, ps, out, out_f32, layer, wide ? 2 * p->num_sms : 3 * p->num_sms, p->pdl != 0, wide, st),
             "merge");
 #undef FK_LAUNCH
   return FK_OK;
