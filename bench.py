@@ -140,6 +140,10 @@ def rank_units(cfg, rank=0, world=1):
     return rank_groups(rank, n, world) if cfg.get("strong") else list(range(n))
 
 
+class DoesNotFit(RuntimeError):
+    """The config's share for this rank does not fit one GPU's memory."""
+
+
 def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=4096, rank=0, world=1):
     import paper_2405_19888_b200 as P
     from paper_2405_19888_b200.workloads import drain_fills, fork_group, nested_forest
@@ -159,6 +163,12 @@ def build_engine(cfg, device, torch, host_inputs=False, seed=0x5EED, out_len=409
         pages = len(units) * (pg(cfg["P"]) + cfg["B"] * (pg(1024) + grow))
     else:
         pages = pg(cfg["P"]) + cfg["B"] * (pg(cfg["S"]) + grow)
+    need = pages * L * 2 * H * 16 * 128 * 2
+    free = torch.cuda.mem_get_info(device)[0]
+    if need > 0.9 * free:  # (the strong-scaling configs hold the BASELINE totals: several GPUs)
+        eng.close()
+        raise DoesNotFit(f"KV arena {need / 1e9:.0f} GB for this rank's {len(units)} of {cfg.get('groups') or cfg.get('apps') or 1} "
+                         f"group(s) > {free / 1e9:.0f} GB free on the GPU: run it over more GPUs (torchrun)")
     eng.reserve_pages(pages)
     if "app" in cfg:
         nested_forest(eng, cfg["P"], cfg["app"], len(units), cfg["S"], cfg["B"], out_len=out_len, seed=seed)
@@ -452,7 +462,21 @@ def main():
     from paper_2405_19888_b200.cluster import max_over_ranks, sum_over_ranks
 
     out_len = 2 * (args.steps + args.warmup) + 64
-    eng, rows = build_engine(cfg, device, torch, out_len=out_len, rank=rank, world=world)
+    why = None
+    try:
+        eng, rows = build_engine(cfg, device, torch, out_len=out_len, rank=rank, world=world)
+    except DoesNotFit as e:
+        why = str(e)
+    if dist is not None:  # every rank stops when one cannot hold its share
+        flag = torch.tensor([0 if why else 1], dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not flag.item() and why is None:
+            why = "another rank's share does not fit its GPU"
+            eng.close()
+    if why:
+        if rank == 0:
+            print(json.dumps({"metric": metric, "config": workload, "n_gpus": args.gpus, "unavailable": why}))
+        return
 
     def apply_options(e):
         if args.tc_min_fanout is not None:
