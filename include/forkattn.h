@@ -166,7 +166,12 @@ int fk_ctx_blocks(const fk_pool* pool, int64_t ctx, int64_t* logical,
 /* Engine.step decode half (engine.py:416-417, 470-484): build the work list
  * for the running leaves (gens order) and upload it on `stream`.  dedup=1 is
  * CostModel.shared_kernel=True (shared contexts streamed once for all their
- * descendants); dedup=0 streams every request's whole chain. */
+ * descendants); dedup=0 streams every request's whole chain.
+ * Stream order: `stream` must be the stream the plan's attention runs on (or
+ * be ordered before it): the upload, and any growth of the partial buffers
+ * (stream-ordered allocation, no device sync), are enqueued there.  The host
+ * runs at most one plan ahead: the call blocks until the GPU has finished
+ * with the plan slot it reuses (two slots, host_wait_ns). */
 int fk_step_plan(fk_pool* pool, const int64_t* leaves, int32_t num_rows,
                  int32_t dedup, void* stream, fk_plan_info* info);
 /* Decode attention for one layer over the current plan.
@@ -180,7 +185,11 @@ int fk_attn_decode(fk_pool* pool, int32_t layer, const void* q, void* out,
 /* fk_attn_decode for layers [layer0, layer0 + nlayers) in one call, when the
  * queries of several layers are ready at once (layer i reads
  * q + i * q_layer_stride bytes, writes out + i * out_layer_stride); the
- * kernels and their ordering are exactly those of the per-layer calls. */
+ * kernels and their ordering are exactly those of the per-layer calls.
+ * Replayed as a CUDA graph (FK_OPT_GRAPH): a call whose pointers, strides,
+ * plan slot and launch shapes repeat relaunches the cached graph without
+ * recording; keeping q/out buffers and strides stable from step to step is
+ * what makes that happen. */
 int fk_attn_decode_layers(fk_pool* pool, int32_t layer0, int32_t nlayers, const void* q,
                           int64_t q_layer_stride, void* out, int64_t out_layer_stride, float* out_f32,
                           int64_t f32_layer_stride, void* stream);
