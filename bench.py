@@ -405,6 +405,8 @@ def main():
     ap.add_argument("--tc-min-fanout", type=int, default=None)
     ap.add_argument("--corun", type=int, default=None, help="FK_OPT_CORUN (default: library default, 1)")
     ap.add_argument("--prefix-rate-pct", type=int, default=None)
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=V",
+                    help="any FK_OPT_<NAME> (repeatable; A/B experiments)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -485,6 +487,9 @@ def main():
             e.set_option(_lib.FK_OPT_CORUN, args.corun)
         if args.prefix_rate_pct is not None:
             e.set_option(_lib.FK_OPT_PREFIX_RATE_PCT, args.prefix_rate_pct)
+        for kv in args.opt:
+            k, v = kv.split("=")
+            e.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
 
     apply_options(eng)
     L, H = cfg["L"], cfg["H"]

@@ -3,6 +3,7 @@ runs bench.py alternately with FK_LIB_PATH = A and B and prints each run's
 tokens/s, layer us and isolated fraction, then the medians.
 
     python profiles/lib_ab.py --a .ab/libforkattn_old.so --b paper_2405_19888_b200/libforkattn.so [--config ...]
+    python profiles/lib_ab.py --a L --b L --opt-b PREFIX_JOINS=1     (an option A/B on one build)
 """
 import argparse
 import json
@@ -21,6 +22,8 @@ def main():
     ap.add_argument("--config", default=None)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--opt-a", action="append", default=[], help="bench.py --opt for arm A (NAME=V)")
+    ap.add_argument("--opt-b", action="append", default=[], help="bench.py --opt for arm B (NAME=V)")
     args = ap.parse_args()
     res = {"A": [], "B": []}
     for r in range(args.rounds):
@@ -29,6 +32,8 @@ def main():
                    "--no-cpu-baseline", "--no-e2e", "--no-check"]
             if args.config:
                 cmd += ["--config", args.config]
+            for kv in args.opt_a if name == "A" else args.opt_b:
+                cmd += ["--opt", kv]
             out = subprocess.run(cmd, env={**os.environ, "FK_LIB_PATH": os.path.abspath(lib)}, capture_output=True,
                                  text=True, timeout=600)
             line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
