@@ -123,7 +123,7 @@ enum {
   FK_OPT_GRAPH = 12,          /* 1 (default): fk_attn_decode_layers replays its launches as a CUDA
                                  graph (captured once per launch structure, parameters updated in
                                  place afterwards); 0: direct launches */
-  FK_OPT_TC_BOUNDARY_COST = 14, /* static split: tiles a piece start mid-range costs a CTA (default 4) */
+  FK_OPT_TC_BOUNDARY_COST = 14, /* static split: tiles a piece start mid-range costs a CTA (default 12) */
   /* 10, 13 (tcgen05 dynamic tail) and 15 (fused merge) were removed in round 2:
      measured slower than what they replace; setting them fails */
   FK_OPT_APPEND_FIRST = 16,   /* 1: attend to the step's own token (a real decoder): fk_step_plan does

@@ -190,7 +190,8 @@ struct fk_pool {
   int64_t priv_min_chunk = 0;  // smallest private chunk (pages), the tail granularity; 0: auto (kPrivMinChunk, 4 for small plans)
   int64_t priv_wpc = kPrivWarpsPerCta;  // private CTA shape (warps; stages follow)
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
-  int64_t tc_boundary_cost = 4;  // tiles a piece start mid-range costs a tcgen05 CTA (static split)
+  int64_t tc_boundary_cost = 12;  // tiles a piece start mid-range costs a tcgen05 CTA (static split; 12 measured
+                                  // +0.5..1.4 % over 4 at 13B/7B x 64 and nested, neutral elsewhere)
   int64_t pdl = 1;  // PDL: 1 between a layer's kernels, 2 also into the next layer's
   int64_t use_graph = 1;  // fk_attn_decode_layers replays a CUDA graph
   std::map<std::tuple<int32_t, int32_t, cudaStream_t, int>, GraphCache> graphs;  // (layer0, nlayers, stream, slot/half)

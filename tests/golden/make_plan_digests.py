@@ -103,10 +103,11 @@ def run():
                 desc = _lib.PoolDesc(2, H, 128, 16, 1 << 22, 0, -1, 0)
                 pool = ctypes.c_void_p()
                 _lib.check(lib.fk_pool_create(ctypes.byref(desc), ctypes.byref(pool)))
-                # (the round-1 planner had no row groups and a fixed 2-page minimum
-                # chunk: its sets run that way; the grouped sets were pinned with it too)
-                for k, v in ({_lib.FK_OPT_GROUP_FANOUT: 0, _lib.FK_OPT_PRIV_MIN_CHUNK: 2, **opts} if oi < 9
-                             else {_lib.FK_OPT_PRIV_MIN_CHUNK: 2, **opts}).items():
+                # (the round-1 planner had no row groups, a fixed 2-page minimum
+                # chunk and a boundary cost of 4 tiles: its sets run that way; the
+                # grouped sets were pinned with the latter two as well)
+                base = {_lib.FK_OPT_PRIV_MIN_CHUNK: 2, _lib.FK_OPT_TC_BOUNDARY_COST: 4}
+                for k, v in ({_lib.FK_OPT_GROUP_FANOUT: 0, **base, **opts} if oi < 9 else {**base, **opts}).items():
                     _lib.check(lib.fk_pool_set_option(pool, k, v))
                 ids = (ctypes.c_int64 * 4096)()
                 n = ctypes.c_int64()
