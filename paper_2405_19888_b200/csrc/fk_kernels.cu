@@ -629,12 +629,14 @@ __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, int ps, __nv_
 
 // K4 for plans with many partials per (row, head) -- small batches, where the
 // private stream of one row is cut into ~U / W chunks (a single 6k-token
-// request has ~200 pieces per head) -- one CTA per (row, head): warp w
-// combines slots w, w + 8, ... (their (m, l) lane-parallel, 32 per round, and
-// their o 8 loads at a time), then warp 0 combines the 8 warp results through
-// shared memory.  A warp per item would walk ~200 slots one load round after
-// another.
+// request has ~100 pieces per head) -- one CTA per (row, head): warp w
+// combines slots w, w + 8, ...: the first kWidePre of them (128 slots per
+// item) with their (m, l) and o all loaded in one memory round trip, any
+// further ones 32 (m, l) / 8 o at a time; then warp 0 combines the 8 warp
+// results through shared memory.  A warp per item would walk ~100 slots one
+// load round after another.
 constexpr int kWideWarps = 8;
+constexpr int kWidePre = 16;
 __global__ void __launch_bounds__(kWideWarps * 32) fk_merge_wide_kernel(ArenaDev a, int ps,
                                                                        __nv_bfloat16* __restrict__ out,
                                                                        float* __restrict__ out_f32, int layer) {
@@ -653,8 +655,35 @@ __global__ void __launch_bounds__(kWideWarps * 32) fk_merge_wide_kernel(ArenaDev
     const long long base = part_index(p, H, row, 0, head);  // slot stride is H
     float M = -INFINITY, L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    // this warp's slots k = warp + kWideWarps * j, 32 per round (online across rounds)
-    for (int j0 = 0; warp + kWideWarps * j0 < ns; j0 += 32) {
+    {  // slots warp + kWideWarps * j, j < kWidePre: o and (m, l) loads issued together
+      float4 v[kWidePre];
+#pragma unroll
+      for (int j = 0; j < kWidePre; ++j) {
+        const int kk = warp + kWideWarps * j;
+        v[j] = kk < ns ? __ldcg(reinterpret_cast<const float4*>(a.part_o + (base + (long long)kk * H) * kHeadDim) + lane)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      const int kl = warp + kWideWarps * lane;
+      const bool mine = lane < kWidePre && kl < ns;
+      const float2 ml = mine ? __ldcg(&a.part_ml[base + (long long)kl * H]) : make_float2(-INFINITY, 0.f);
+      M = ml.x;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      const float wl = mine && M != -INFINITY ? ex2(ml.x - M) : 0.f;
+      L = ml.y * wl;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+#pragma unroll
+      for (int j = 0; j < kWidePre; ++j) {
+        const float wk = __shfl_sync(0xffffffffu, wl, j);
+        acc.x = fmaf(v[j].x, wk, acc.x);
+        acc.y = fmaf(v[j].y, wk, acc.y);
+        acc.z = fmaf(v[j].z, wk, acc.z);
+        acc.w = fmaf(v[j].w, wk, acc.w);
+      }
+    }
+    // any further slots, 32 per round (online across rounds)
+    for (int j0 = kWidePre; warp + kWideWarps * j0 < ns; j0 += 32) {
       const int kl = warp + kWideWarps * (j0 + lane);
       const float2 ml = kl < ns ? __ldcg(&a.part_ml[base + (long long)kl * H]) : make_float2(-INFINITY, 0.f);
       float mr = ml.x;

@@ -74,7 +74,12 @@ def main():
             en = sorted((e - t0) / 1e3 for _, e in xs)
             print(f"layer%2 {par} {name:8s} ctas={len(xs):4d} start min/med/max {st[0]:7.2f} {statistics.median(st):7.2f} "
                   f"{st[-1]:7.2f}   end min/med/max {en[0]:7.2f} {statistics.median(en):7.2f} {en[-1]:7.2f}")
-    print("(merge* start = after its griddepcontrol.wait)")
+    print("(merge* start = after its griddepcontrol.wait; the wide merge stamps its launch)")
+    par = pars[-1]
+    late = sorted(((e, s, i) for i, (s, e) in enumerate(out["merge"][par]) if s and e >= s and abs(s - t_last) < 200000),
+                  reverse=True)[:6]
+    print("last layer, latest merge CTAs (index: start, end us):",
+          " ".join("%d: %.2f, %.2f" % (i, (s - t0) / 1e3, (e - t0) / 1e3) for e, s, i in late))
     par = pars[-1]
     print("last layer prefix CTAs (tiles, pieces, duration us):")
     print(" ".join("%d/%d/%.0f" % (notes[par][i][0], notes[par][i][1], (out["prefix"][par][i][1] - out["prefix"][par][i][0]) / 1e3)
