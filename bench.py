@@ -108,7 +108,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lines = [ln for t, ln in self.lines if self.t_mark is None or t >= self.t_mark]
         if not lines:  # timed region shorter than one sample period
@@ -122,11 +122,18 @@ class ClockSampler:
                 smax = float(parts[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[3]))
+            except ValueError:
+                pass
             for n, v in zip(names, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
+        # (board power: nvidia-smi's averaged reading, it trails the load by
+        # ~1 s; sustained runs settle at the 1000 W cap, profiles/r02/power/)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(pw) if pw else None}
 
 
 # ------------------------------------------------------------------ workload
