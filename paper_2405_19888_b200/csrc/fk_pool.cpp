@@ -1215,12 +1215,43 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   // run: one division per distinct size, then plain stores (this runs every step)
   std::vector<int32_t>& chunk_start = S.chunk_start;
   {
-    // (auto: plans under 32K units -- a few rows -- cut every (item, head) run
-    // into ~U / W pieces whatever the chunk size; 4-page chunks halve the
-    // partials there and measured +3 % (1 row) to +4.5 % (8 forks); the
-    // headline's 43K units keep 2, measured better for them in round 1)
-    const int64_t w2 = 2 * w_active,
-                  mc = p->priv_min_chunk > 0 ? p->priv_min_chunk : (U < 32768 ? 4 : kPrivMinChunk);
+    const int64_t w2 = 2 * w_active;
+    // chunk count of the guided schedule for a minimum size (the generator
+    // below without its stores)
+    auto count_chunks = [&](int64_t mc) {
+      int64_t n = 0, pos = 0;
+      while (pos < U) {
+        const int64_t R = U - pos;
+        const int64_t sz = std::min<int64_t>(std::max<int64_t>((R + w2 - 1) / w2, mc), kPrivMaxChunk);
+        const int64_t floor_r = sz > mc ? (sz - 1) * w2 : 0;
+        int64_t k = sz > mc ? (R - floor_r + sz - 1) / sz : (R + sz - 1) / sz;
+        k = std::min<int64_t>(k, (R + sz - 1) / sz);
+        n += k;
+        pos = std::min<int64_t>(U, pos + k * sz);
+      }
+      return n;
+    };
+    // Minimum chunk (auto): the headline's 43K units keep 2 (measured better
+    // in round 1).  Plans under 32K units -- a few rows -- cut every (item,
+    // head) run into ~U / W pieces whatever the size, so bigger chunks pay:
+    // with a prefix grid 4; without one every warp starts at once and takes
+    // ~n / W chunks, the last round leaves ceil(n/W) - n/W of the warps idle
+    // for one chunk of mc pages, and each chunk costs about two pages of time
+    // (ticket, metadata, pipeline refill, one more partial to merge), so mc in
+    // 4..8 minimises idle * mc + 2 n / W (fan-outs 1-8: +1.5..6 % over a fixed
+    // 4, profiles/r02/tune/).
+    int64_t mc = p->priv_min_chunk > 0 ? p->priv_min_chunk : (U < 32768 ? 4 : kPrivMinChunk);
+    if (p->priv_min_chunk == 0 && U < 32768 && tc_ctas == 0 && U > 0) {
+      double best = 1e300;
+      for (int64_t m = 8; m >= 4; --m) {  // (ties keep the larger chunk)
+        const double f = (double)count_chunks(m) / (double)w_active;
+        const double cost = (std::ceil(f - 1e-9) - f) * (double)m + 2.0 * f;
+        if (cost < best - 1e-9) {
+          best = cost;
+          mc = m;
+        }
+      }
+    }
     // upper bound of the chunk count: every chunk but the last has >= mc
     // units (grown only: a resize down and up again would zero-fill)
     const size_t bound = (size_t)(U / std::max<int64_t>(mc, 1) + 2);

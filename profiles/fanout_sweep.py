@@ -16,17 +16,22 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from paper_2405_19888_b200 import _lib  # noqa: E402
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--fanouts", default="2,4,8,16,32,64")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=V", help="FK_OPT_<NAME> on every engine")
     args = ap.parse_args()
     peak, kind = bench.load_peaks()
     for b in [int(x) for x in args.fanouts.split(",")]:
         cfg = dict(model="LLaMA-13B", L=40, H=40, P=6000, B=b, S=256)
         eng, rows = bench.build_engine(cfg, 0, torch, out_len=2 * args.steps + 32)
+        for kv in args.opt:
+            k, v = kv.split("=")
+            eng.set_option(getattr(_lib, "FK_OPT_" + k), int(v))
         for _ in range(3):
             eng.step()
         t = bench.time_steps(eng, args.steps, torch)
