@@ -1231,16 +1231,17 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
       }
       return n;
     };
-    // Minimum chunk (auto): the headline's 43K units keep 2 (measured better
-    // in round 1).  Plans under 32K units -- a few rows -- cut every (item,
-    // head) run into ~U / W pieces whatever the size, so bigger chunks pay:
-    // with a prefix grid 4; without one every warp starts at once and takes
-    // ~n / W chunks, the last round leaves ceil(n/W) - n/W of the warps idle
-    // for one chunk of mc pages, and each chunk costs about two pages of time
-    // (ticket, metadata, pipeline refill, one more partial to merge), so mc in
-    // 4..8 minimises idle * mc + 2 n / W (fan-outs 1-8: +1.5..6 % over a fixed
-    // 4, profiles/r02/tune/).
-    int64_t mc = p->priv_min_chunk > 0 ? p->priv_min_chunk : (U < 32768 ? 4 : kPrivMinChunk);
+    // Minimum chunk (auto): 2 pages beside a prefix grid (the private CTAs
+    // past the free SMs start as prefix CTAs retire, so there is no last
+    // round to fit; 2 measured best from 16 to 64 forks, profiles/r02/tune/).
+    // Small plans without one (under 32K units: a few rows, every (item, head)
+    // run cut into ~U / W pieces) start every warp at once and take ~n / W
+    // chunks: the last round leaves ceil(n/W) - n/W of the warps idle for one
+    // chunk of mc pages, and each chunk costs about two pages of time (ticket,
+    // metadata, pipeline refill, one more partial to merge), so mc in 4..8
+    // minimises idle * mc + 2 n / W (fan-outs 1-8: +2.8..6.9 % over a fixed 4,
+    // profiles/r02/min_chunk/).
+    int64_t mc = p->priv_min_chunk > 0 ? p->priv_min_chunk : kPrivMinChunk;
     if (p->priv_min_chunk == 0 && U < 32768 && tc_ctas == 0 && U > 0) {
       double best = 1e300;
       for (int64_t m = 8; m >= 4; --m) {  // (ties keep the larger chunk)
