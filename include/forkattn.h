@@ -116,7 +116,8 @@ enum {
                                  written by the kernel launched right before fk_attn_decode */
   FK_OPT_PRIV_MIN_CHUNK = 8,  /* smallest chunk (pages) of the private kernel's guided dynamic
                                  schedule, 1..32: the granularity of its tail; 0 (default): 2, or
-                                 4 for plans under 32K (head, page) units (a few rows) */
+                                 for plans under 32K (head, page) units with no prefix grid (a
+                                 few rows) 4..8, fitted to the last round of chunks */
   FK_OPT_PRIV_STATIC_FIRST = 9, /* 1 (default): the private warps that start at once take their
                                  first chunk by warp index instead of a ticket */
   FK_OPT_PRIV_WARPS = 11,     /* private CTA shape: 10 warps x 2 stages (default), 8 x 3 or 12 x 2 */

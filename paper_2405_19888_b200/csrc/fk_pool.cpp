@@ -187,7 +187,7 @@ struct fk_pool {
   int64_t tc_min_fanout = 2;  // tcgen05 for every shared context (measured faster than mma.sync at fan-out 2..32)
   int64_t prefix_target_ctas = 0;  // 0 -> num_sms
   int64_t launch_order = 0;
-  int64_t priv_min_chunk = 0;  // smallest private chunk (pages), the tail granularity; 0: auto (kPrivMinChunk, 4 for small plans)
+  int64_t priv_min_chunk = 0;  // smallest private chunk (pages), the tail granularity; 0: auto (see the planner)
   int64_t priv_wpc = kPrivWarpsPerCta;  // private CTA shape (warps; stages follow)
   int64_t priv_static_first = 1;  // private warps that start at once take chunk = warp index (no ticket)
   int64_t tc_boundary_cost = 12;  // tiles a piece start mid-range costs a tcgen05 CTA (static split; 12 measured
