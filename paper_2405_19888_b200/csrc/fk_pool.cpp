@@ -1204,7 +1204,7 @@ int fk_step_plan(fk_pool* p, const int64_t* leaves, int32_t B, int32_t dedup, vo
   const int64_t U = NPT * H;
   if (U > INT32_MAX) return fail(FK_INVALID_ARGUMENT, "private work too large (%lld units)", (long long)U);
   PT(T5);
-  // Guided dynamic schedule: chunks shrink from ~U / (2 W) pages to 4 as the
+  // Guided dynamic schedule: chunks shrink from ~U / (2 W) pages to mc as the
   // list drains (W = warps that start at once), warps grab them from a ticket
   // counter.  The grid covers every SM: in co-run the CTAs beyond the free
   // SMs start when tcgen05 prefix CTAs retire and take the leftovers.
