@@ -97,3 +97,17 @@ def test_plan_digests_pinned():
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "golden", "make_plan_digests.py"), "--check"],
                        env={**os.environ, "FK_DEBUG_PLAN_DIGEST": "1"}, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_auto_min_chunk():
+    """Small plans without a prefix grid: the automatic minimum private chunk
+    is the one the last-round rule predicts (tests/plan_min_chunk_check.py
+    restates it and compares plan digests against the explicit option)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "plan_min_chunk_check.py")],
+                       env={**os.environ, "FK_DEBUG_PLAN_DIGEST": "1"}, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
