@@ -206,7 +206,16 @@ class _Pool:
             reserved=0,
         )
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib.fk_pool_create(ctypes.byref(desc), ctypes.byref(h)))
+        rc = _lib.lib.fk_pool_create(ctypes.byref(desc), ctypes.byref(h))
+        if rc == _lib.FK_INVALID_ARGUMENT and device is not None:
+            # A process holds at most 64 device pools (two __constant__ plan
+            # slots each).  Engines dropped without close() inside reference
+            # cycles keep theirs until the cycle collector runs: run it, retry.
+            import gc
+
+            gc.collect()
+            rc = _lib.lib.fk_pool_create(ctypes.byref(desc), ctypes.byref(h))
+        _lib.check(rc)
         self.handle = h
         self._ids = (ctypes.c_int64 * 64)()
         self._stats = _lib.PoolStats()
