@@ -89,7 +89,10 @@ typedef struct {
 } fk_plan_info;
 
 /* ---- pool ---------------------------------------------------------------- */
-/* Replaces PagedKvStore.__init__ (engine.py:69-74) + the device KV arena. */
+/* Replaces PagedKvStore.__init__ (engine.py:69-74) + the device KV arena.
+ * A process holds at most 64 device pools at a time (each owns two
+ * __constant__ plan slots); the 65th fails with FK_INVALID_ARGUMENT until
+ * one is destroyed.  Host-only pools (device -1) are unlimited. */
 int fk_pool_create(const fk_pool_desc* desc, fk_pool** out);
 int fk_pool_destroy(fk_pool* pool);
 /* manager.py:138 writes store.total_blocks after construction. */
