@@ -35,12 +35,27 @@ def prefix_path(request):
     yield request.param
 
 
+_OPEN = []
+
+
+@pytest.fixture(autouse=True)
+def close_engines():
+    """Engines are closed when their test ends: a process holds at most 64
+    device pools, and under compute-sanitizer the interpreter's frames (held
+    from C) keep finished tests' engines alive, so release cannot wait for
+    garbage collection (profiles/sanitize_full.sh runs this whole file)."""
+    yield
+    while _OPEN:
+        _OPEN.pop().close()
+
+
 def make_engine(cuda_device, H, L=1, shared=True, k_scale=1.0, seed=0x5EED, kv_tokens=1 << 20, **kw):
     eng = P.GpuEngine("e0", P.CostModel(shared_kernel=shared), kv_tokens=kv_tokens, device=cuda_device,
                       geometry=P.ModelGeometry(L, H, 128), model=P.SyntheticDecodeModel(seed, k_scale),
                       capture_f32=True, keep_history=True, **kw)
     eng.set_option(_lib.FK_OPT_TC_MIN_FANOUT, 0 if PATH["path"] == "mma" else 2)
     eng.set_option(_lib.FK_OPT_GROUP_FANOUT, 16 if PATH["path"] == "grp" else 0)
+    _OPEN.append(eng)
     return eng
 
 
