@@ -1,11 +1,11 @@
 #!/bin/bash
-# compute-sanitizer memcheck and racecheck over the whole GPU parity file
+# compute-sanitizer memcheck, racecheck and synccheck over the whole GPU parity file
 # (every case, all four prefix paths: mma.sync, tcgen05, row groups, and the
 # shapes each path's tests build).  Output: gpurun_out/san_full/
 set -u
 cd "$(dirname "$0")/.."
 O=gpurun_out/san_full; mkdir -p $O
-for tool in memcheck racecheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck}; do
   extra=""
   [ "$tool" = racecheck ] && extra="--racecheck-report analysis"
   timeout 3000 compute-sanitizer --tool $tool $extra --target-processes all --print-limit 200 \
