@@ -524,12 +524,12 @@ def main():
                  "max_slots": info.max_slots, "tc_items": info.num_tc_items, "mma_items": info.num_mma_items}
     # per-layer attention alone for the roofline (same plan as the last step);
     # the isolated-layer figure is measured in alternation with it (the
-    # part's clock moves under its power cap), medians of three rounds each
+    # part's clock moves under its power cap), medians of five rounds each
     t_layers, t_isos, t_foreign = [], [], 0.0
-    for _ in range(3):
+    for _ in range(5):
         t_layers.append(time_layers(eng, max(args.steps // 6, 3), torch))
         if not args.no_isolated:
-            ti, t_foreign = time_layers_isolated(eng, 2, torch)
+            ti, t_foreign = time_layers_isolated(eng, 3, torch)
             t_isos.append(ti)
     t_layer = statistics.median(t_layers)
     barrier()
