@@ -611,7 +611,10 @@ __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, int ps, __nv_
   const int lane = threadIdx.x & 31;
   const int H = a.num_heads, nrh = p.num_rows * H, stride = gridDim.x * 8;
   int w = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int ns = w < nrh ? partial_count(p, H, w / H, w % H) : 0;  // plan data: before the wait
+  // plan data, read before the wait: the partial counts of this warp's first
+  // two (row, head) items (more rows than warps: x 128 / x 256 forks)
+  const int ns = w < nrh ? partial_count(p, H, w / H, w % H) : 0;
+  const int ns2 = w + stride < nrh ? partial_count(p, H, (w + stride) / H, (w + stride) % H) : 0;
   pdl_wait_primary();       // partials of the prefix and private grids are complete
   pdl_launch_dependents();  // the next layer's first kernel may start (other partial half)
   // Every CTA of this launch's prefix and private grids has finished, so
@@ -623,6 +626,8 @@ __global__ void __launch_bounds__(256) fk_merge_kernel(ArenaDev a, int ps, __nv_
   if (threadIdx.x == 0 && blockIdx.x < 1024) fk_tl_cta_merge[layer & 1][blockIdx.x][0] = global_ns();
 #endif
   if (w < nrh) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane, ns);  // (8 early slots: 12 / 16 measured slower)
+  w += stride;
+  if (w < nrh) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane, ns2);
   for (w += stride; w < nrh; w += stride) merge_row_head_warp(a, p, w / H, w % H, out, out_f32, lane);
   CTA_TL_END(fk_tl_cta_merge, layer);
 }
