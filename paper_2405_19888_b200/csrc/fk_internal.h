@@ -163,7 +163,8 @@ extern thread_local RecBuf* g_launch_rec;
 cudaError_t upload_plan_main(int ps, const PlanDev* host_pinned, cudaStream_t s);  // fk_kernels.cu
 cudaError_t upload_plan_tc(int ps, const PlanDev* host_pinned, cudaStream_t s);    // fk_prefix_tc.cu
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,
-                           float scale_log2, const CUtensorMap* tmap, int grid, bool pdl, cudaStream_t s);
+                           float scale_log2, const CUtensorMap* tmap, const CUtensorMap* tmap_half, int grid, bool pdl,
+                           cudaStream_t s);
 cudaError_t launch_prefix_mma(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,
                               float scale_log2, const CUtensorMap* tmap, cudaStream_t s);
 cudaError_t launch_prefix_tc(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q,

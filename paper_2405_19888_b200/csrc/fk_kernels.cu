@@ -68,7 +68,8 @@ template <int STAGES, int WARPS, bool GROUPED>
 __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, int ps, int layer,
                                                                    const __nv_bfloat16* __restrict__ q,
                                                                    float scale_log2,
-                                                                   const __grid_constant__ CUtensorMap tmap) {
+                                                                   const __grid_constant__ CUtensorMap tmap,
+                                                                   const __grid_constant__ CUtensorMap tmap_h) {
   const PlanDev& p = fk_plan_c[ps];
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -103,9 +104,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
   uint8_t* ring = smem + warp * STAGES * kPwStageBytes;
   if (lane == 0) {
     prefetch_tmap(&tmap);
+    prefetch_tmap(&tmap_h);
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[warp][s], 1);
     fence_mbar_init();
   }
+  // A chain's last page with <= 8 tokens loads only its first 8 rows; rows
+  // 8..15 of the stage keep an earlier page's (finite) bytes, which meet
+  // p = 0.  Zero them once so the first use of a stage sees no NaN bits.
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s)
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      uint4* z = reinterpret_cast<uint4*>(ring + s * kPwStageBytes + x * 2048 + 1024);
+      z[lane] = z[lane + 32] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  fence_proxy_async();  // before the TMA (async proxy) writes the same stages
   __syncwarp();
 
   // unit metadata of a chunk (<= 32 units) held lane-parallel in registers
@@ -139,10 +152,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) fk_private_kernel(ArenaDev a, i
   auto issue = [&](int s, const UnitMeta& m) {  // lane 0 only
     uint8_t* st = ring + s * kPwStageBytes;
     const int pk = (int)plane_index(layer, 0, m.head, H), pv = (int)plane_index(layer, 1, m.head, H);
-    mbar_expect_tx(&full[warp][s], kPwStageBytes);
     // every private page is read once per layer: evict-first keeps L2 for the
     // partials and the prefix tiles
     const uint64_t pol = l2_policy_evict_first();
+    if (m.ntok <= kPage / 2) {  // a chain's short last page: its first 8 rows only
+      mbar_expect_tx(&full[warp][s], kPwStageBytes / 2);
+      tma_load_3d_hint(st, &tmap_h, 0, m.pg * kPage, pk, &full[warp][s], pol);
+      tma_load_3d_hint(st + 2048, &tmap_h, 64, m.pg * kPage, pk, &full[warp][s], pol);
+      tma_load_3d_hint(st + 4096, &tmap_h, 0, m.pg * kPage, pv, &full[warp][s], pol);
+      tma_load_3d_hint(st + 6144, &tmap_h, 64, m.pg * kPage, pv, &full[warp][s], pol);
+      return;
+    }
+    mbar_expect_tx(&full[warp][s], kPwStageBytes);
     tma_load_3d_hint(st, &tmap, 0, m.pg * kPage, pk, &full[warp][s], pol);
     tma_load_3d_hint(st + 2048, &tmap, 64, m.pg * kPage, pk, &full[warp][s], pol);
     tma_load_3d_hint(st + 4096, &tmap, 0, m.pg * kPage, pv, &full[warp][s], pol);
@@ -917,7 +938,8 @@ cudaError_t upload_plan_main(int ps, const PlanDev* host_pinned, cudaStream_t s)
 
 template <int STAGES, int WARPS, bool GROUPED>
 static cudaError_t launch_private_shape(const ArenaDev& a, int ps, int layer, const void* q, float scale_log2,
-                                       const CUtensorMap* tmap, int grid_ctas, bool pdl, cudaStream_t s) {
+                                       const CUtensorMap* tmap, const CUtensorMap* tmap_h, int grid_ctas, bool pdl,
+                                       cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   constexpr int smem = priv_smem<STAGES, WARPS>();
   if (!attr_set_on_device(attr_devices)) {
@@ -926,21 +948,21 @@ static cudaError_t launch_private_shape(const ArenaDev& a, int ps, int layer, co
     if (e != cudaSuccess) return e;
   }
   return launch_k(fk_private_kernel<STAGES, WARPS, GROUPED>, dim3(grid_ctas), dim3(WARPS * 32), smem, s, pdl, a, ps, layer,
-                  (const __nv_bfloat16*)q, scale_log2, *tmap);
+                  (const __nv_bfloat16*)q, scale_log2, *tmap, *tmap_h);
 }
 
 cudaError_t launch_private(const ArenaDev& a, const PlanDev& p, int ps, int layer, const void* q, float scale_log2,
-                           const CUtensorMap* tmap, int grid, bool pdl, cudaStream_t s) {
+                           const CUtensorMap* tmap, const CUtensorMap* tmap_h, int grid, bool pdl, cudaStream_t s) {
   if (p.priv_units == 0) return cudaSuccess;
   // ring shapes: per-warp stages x warps per CTA (8 KiB stages): 10 x 2 = 160 KiB
   // (the default, measured best), 8 x 3 and 12 x 2 = 192 KiB
   switch (p.priv_wpc) {
-    case 8: return launch_private_shape<3, 8, false>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
-    case 12: return launch_private_shape<2, 12, false>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+    case 8: return launch_private_shape<3, 8, false>(a, ps, layer, q, scale_log2, tmap, tmap_h, grid, pdl, s);
+    case 12: return launch_private_shape<2, 12, false>(a, ps, layer, q, scale_log2, tmap, tmap_h, grid, pdl, s);
     default:
       // (row groups: the default shape only -- the planner keeps them off for the others)
-      if (p.n_gitems > 0) return launch_private_shape<2, 10, true>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
-      return launch_private_shape<2, 10, false>(a, ps, layer, q, scale_log2, tmap, grid, pdl, s);
+      if (p.n_gitems > 0) return launch_private_shape<2, 10, true>(a, ps, layer, q, scale_log2, tmap, tmap_h, grid, pdl, s);
+      return launch_private_shape<2, 10, false>(a, ps, layer, q, scale_log2, tmap, tmap_h, grid, pdl, s);
   }
 }
 

@@ -180,6 +180,7 @@ struct fk_pool {
   size_t arena_bytes = 0;
   alignas(64) CUtensorMap tmap;      // box {64 dims, 16 rows}: one page
   alignas(64) CUtensorMap tmap_run;  // box {64 dims, 128 rows}: 8 contiguous pages
+  alignas(64) CUtensorMap tmap_half; // box {64 dims, 8 rows}: the first half of a page
   bool tmap_ok = false;
   int num_sms = 148;
 
@@ -322,6 +323,11 @@ int encode_tmap(fk_pool* p) {
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FK_CUDA_ERROR, "cuTensorMapEncodeTiled (run) failed (%d)", (int)r);
+  cuuint32_t box_half[3] = {64, (cuuint32_t)(kPage / 2), 1};
+  r = fn(&p->tmap_half, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, p->kv, dims, strides, box_half, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FK_CUDA_ERROR, "cuTensorMapEncodeTiled (half) failed (%d)", (int)r);
   p->tmap_ok = true;
   return FK_OK;
 }
@@ -1633,10 +1639,10 @@ int fk_attn_decode(fk_pool* p, int32_t layer, const void* q, void* out, float* o
   if (p->launch_order == 0) {
     int rc = run_prefix(xl, false);
     if (rc != FK_OK) return rc;
-    FK_LAUNCH(launch_private(a, p->plan, ps, layer, q, scale_log2, &p->tmap, p->priv_grid,
+    FK_LAUNCH(launch_private(a, p->plan, ps, layer, q, scale_log2, &p->tmap, &p->tmap_half, p->priv_grid,
                              (p->pdl && (has_mma || has_tc)) || (xl && !has_tc), st), "private");
   } else {
-    FK_LAUNCH(launch_private(a, p->plan, ps, layer, q, scale_log2, &p->tmap, p->priv_grid, xl, st), "private");
+    FK_LAUNCH(launch_private(a, p->plan, ps, layer, q, scale_log2, &p->tmap, &p->tmap_half, p->priv_grid, xl, st), "private");
     const bool chained = p->pdl && has_tc && !has_mma && p->plan.priv_units > 0;
     int rc = run_prefix(chained, chained);
     if (rc != FK_OK) return rc;

@@ -36,7 +36,8 @@ def parse(path):
 
 def main(d):
     out_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
-    data = {}
+    # configs not captured in this run keep their earlier entry
+    data = json.load(open(out_path)) if os.path.exists(out_path) else {}
     for path in sorted(glob.glob(os.path.join(d, "*.csv"))):
         cfg = os.path.basename(path)[:-4]
         meta = json.load(open(path[:-4] + ".json"))
