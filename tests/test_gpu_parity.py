@@ -97,7 +97,10 @@ def test_tiny_config1(cuda_device):
 def test_ragged_suffixes_cross_pages(cuda_device):
     rng = random.Random(1)
     eng = make_engine(cuda_device, H=4, L=2)
-    lens = [rng.randint(0, 70) for _ in range(13)] + [0, 1, 15, 16, 17]
+    # 7, 8, 9, 24, 25: last pages on either side of the private kernel's
+    # half-page load (<= 8 tokens: rows 0..7 only); 20 steps move each
+    # chain's last page through both forms
+    lens = [rng.randint(0, 70) for _ in range(13)] + [0, 1, 7, 8, 9, 15, 16, 17, 24, 25]
     fork_group(eng, 100, lens, out_len=20, seed=3)  # 100 = partial last prefix page
     run_steps(eng, 20)
     check_history(eng)
